@@ -1,0 +1,170 @@
+"""Generate the golden fixtures by running the UNMODIFIED reference (mselast).
+
+Run in the build container, where /root/reference exists:
+
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden.py
+
+Everything here calls the reference's own public functions (plus, for the
+BASELINE configs, the composition seam SURVEY.md §A.3 describes:
+``build_coarse_space`` + ``assemble_coarse_operator`` +
+``_subdomain_elasticity_solvers`` on delta-extended blocks, combined through
+``TwoLevelPreconditioner``).  The outputs pin the oracle
+(tests/test_oracle_pins.py) and, on the GPU box, the CUDA path.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+import scipy.sparse as sp  # noqa: E402
+
+REF = Path("/root/reference/pkg/src")
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(HERE.parents[1]))
+
+from mselast import assembly, cli, coefficients, grid, krylov, schwarz, spectral  # noqa: E402
+from mselast.grid import Patch  # noqa: E402
+
+from paper_2006_13387_b200 import configs  # noqa: E402
+
+
+def eigenvalues_per_center(mesh, part, coeff, dirichlet, n_max=6):
+    out = []
+    for patch in part.neighborhoods:
+        prob = spectral.build_local_eigproblem(mesh, coeff, patch, "diffusion", dirichlet)
+        k = min(n_max + 1, prob.dim)
+        out.append(spectral.solve_local_eig_dense(prob, k).eigenvalues)
+    return np.array(out)
+
+
+def save(name, **arrays):
+    path = HERE / name
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, f"{path.stat().st_size/1024:.0f} KiB")
+
+
+def elements():
+    save("ref_elements.npz",
+         Ke0_nu03=assembly.element_stiffness_elasticity(1.0, 0.3),
+         Ke0_nu025=assembly.element_stiffness_elasticity(1.0, 0.25),
+         lap=assembly.laplace_element_scalar(),
+         mass_h001=assembly.mass_element_scalar(0.01))
+
+
+def bench100(eta):
+    """The reference's own benchmark cell, 100^2 / 10^2, EH+Rot (cli.py:63-105)."""
+    out = {}
+    for tol in (1e-6, 1e-8):
+        cfg = cli.BenchmarkConfig(tol=tol)
+        res = cli.run_single(cfg, eta, "EH+Rot")
+        op, rep = res["operator"], res["report"]
+        out[f"iters_{tol:g}"] = rep.iterations
+        out[f"x_{tol:g}"] = res["solution"]
+        out[f"res_{tol:g}"] = np.array(rep.residuals)
+        out[f"cond_{tol:g}"] = rep.cond_estimate
+        out["coarse_dim"] = res["coarse_dim"]
+    mesh = grid.build_fine_mesh(100, 100)
+    part = grid.build_coarse_partition(mesh, 10, 10)
+    coeff = coefficients.generate_coefficient(cfg.layout, mesh, eta, nu=cfg.nu)
+    dirichlet = mesh.boundary_nodes()
+    pre = schwarz.build_preconditioner("EH+Rot", op, mesh, part, coeff, dirichlet)
+    rng = np.random.default_rng(7)
+    r = rng.standard_normal(op.n_free)
+    save(f"ref_bench100_eta{eta:g}.npz", E=coeff.values, dirichlet_nodes=dirichlet,
+         free_dofs=op.free_dofs, b=res["rhs"], mode_counts=np.array(pre.info["mode_counts"]),
+         eigenvalues=eigenvalues_per_center(mesh, part, coeff, dirichlet),
+         apply_r=r, apply_z=pre.apply(r), nu=0.3, **out)
+
+
+class _KeptPatch(Patch):
+    """Patch whose kept nodes follow the frozen block rule."""
+
+    def interior_node_ids(self, mesh):
+        a0, a1 = self.ex0 + 1, self.ex1 - 1
+        b0, b1 = self.ey0 + 1, self.ey1 - 1
+        if self.ex0 == 0:
+            a0 = 0
+        if self.ex1 == mesh.nx:
+            a1 = mesh.nx
+        if self.ey0 == 0:
+            b0 = 0
+        if self.ey1 == mesh.ny:
+            b1 = mesh.ny
+        a = np.arange(a0, a1 + 1)
+        b = np.arange(b0, b1 + 1)
+        return (b[:, None] * (mesh.nx + 1) + a[None, :]).ravel()
+
+
+class _Blocks:
+    def __init__(self, mesh, H, delta):
+        self.neighborhoods = [
+            _KeptPatch(max(0, I * H - delta), min(mesh.nx, (I + 1) * H + delta),
+                       max(0, J * H - delta), min(mesh.ny, (J + 1) * H + delta))
+            for J in range(mesh.ny // H) for I in range(mesh.nx // H)
+        ]
+
+
+def adapter_case(spec, fname, tol=1e-8, maxit=5000):
+    """BASELINE config through reference functions."""
+    mesh = grid.build_fine_mesh(spec.nx, spec.ny)
+    coeff = assembly.CoefficientField(spec.E, spec.nu, spec.E_min, spec.E_max)
+    free = np.setdiff1d(np.arange(mesh.n_dofs), spec.constrained_dofs)
+    Ke = assembly.element_stiffness_elasticity(1.0, spec.nu)
+    op = assembly._assemble(mesh.element_dofs(), coeff.values[:, None, None] * Ke[None], mesh.n_dofs, free)
+    part = grid.build_coarse_partition(mesh, spec.nx // spec.H, spec.ny // spec.H)
+    pou = grid.build_partition_of_unity(part)
+    variant = schwarz.get_variant("EH+Rot")
+    basis, modes, _ = schwarz.build_coarse_space(variant, op, mesh, part, coeff,
+                                                 spec.heat_dirichlet_nodes, schwarz.EigOptions(), pou)
+    from mselast import coarse
+    cop = coarse.assemble_coarse_operator(op, basis)
+    level1 = schwarz._subdomain_elasticity_solvers(op, mesh, _Blocks(mesh, spec.H, spec.delta))
+    pre = schwarz.TwoLevelPreconditioner(variant, level1, cop, op.n_free, {})
+    b = spec.load_full[free]
+    x, rep = krylov.pcg_solve(op.matrix, b, pre, tol=tol, maxit=maxit)
+    rng = np.random.default_rng(11)
+    r = rng.standard_normal(op.n_free)
+    z = pre.apply(r)
+    # jitter band: reversed level-1 order and b scaled by (1 + 2^-52)
+    pre_rev = schwarz.TwoLevelPreconditioner(variant, level1[::-1], cop, op.n_free, {})
+    x_rev, rep_rev = krylov.pcg_solve(op.matrix, b, pre_rev, tol=tol, maxit=maxit)
+    x_sc, rep_sc = krylov.pcg_solve(op.matrix, b * (1 + 2.0 ** -52), pre, tol=tol, maxit=maxit)
+    nx_ = np.linalg.norm(x)
+    save(fname, E=spec.E, constrained_dofs=spec.constrained_dofs,
+         heat_dirichlet_nodes=spec.heat_dirichlet_nodes, load_full=spec.load_full,
+         nx=spec.nx, ny=spec.ny, H=spec.H, delta=spec.delta, nu=spec.nu, tol=tol,
+         iters=rep.iterations, x=x, residuals=np.array(rep.residuals), cond=rep.cond_estimate,
+         coarse_dim=basis.N_c, mode_counts=np.array(modes),
+         eigenvalues=eigenvalues_per_center(mesh, part, coeff, spec.heat_dirichlet_nodes),
+         K0=cop.K0, apply_r=r, apply_z=z,
+         jitter_iters=np.array([rep_rev.iterations, rep_sc.iterations]),
+         jitter_x=np.array([np.linalg.norm(x_rev - x) / nx_, np.linalg.norm(x_sc - x) / nx_]))
+    print(fname, "iters", rep.iterations, "N_c", basis.N_c, "modes", np.bincount(modes),
+          "jitter", rep_rev.iterations, rep_sc.iterations)
+
+
+def main():
+    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s"}
+    if "elements" in which:
+        elements()
+    if "bench" in which:
+        bench100(1.0)
+        bench100(1e6)
+    if "cfg1" in which:
+        adapter_case(configs.config1(seed=0), "ref_config1.npz")
+    if "mbb" in which:
+        adapter_case(configs.config4(seed=0, nx=64, ny=32, H=16, delta=2, eta=1e9), "ref_mbb_64x32.npz")
+    if "cfg3s" in which:
+        adapter_case(configs.config3(seed=0, n=128, H=32, delta=2), "ref_config3_n128.npz")
+    if "cfg2s" in which:
+        adapter_case(configs.config2(seed=0, eta=1e4, n=128, H=32, delta=2), "ref_config2_n128.npz")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,93 @@
+"""Pin the CPU oracle against outputs of the unmodified reference.
+
+The fixtures in tests/golden/ were produced by tests/golden/make_golden.py,
+which runs the reference package itself.  These tests need no GPU.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import mselast_oracle as O
+from paper_2006_13387_b200 import configs
+
+
+def test_element_matrices_bitwise():
+    g = load_golden("ref_elements.npz")
+    assert np.array_equal(O.elasticity_element(0.3), g["Ke0_nu03"])
+    assert np.array_equal(O.elasticity_element(0.25), g["Ke0_nu025"])
+    assert np.array_equal(O.laplace_element(), g["lap"])
+    assert np.array_equal(O.mass_element(0.01), g["mass_h001"])
+
+
+def _bench_problem(g):
+    mesh = O.mesh_for(100, 100)
+    op = O.elasticity_operator(mesh, g["E"], 0.3, O.whole_node_dofs(mesh, g["dirichlet_nodes"]))
+    assert np.array_equal(op.free_dofs, g["free_dofs"])
+    return O.OracleProblem(mesh, op, g["E"], 0.3, g["b"], g["dirichlet_nodes"])
+
+
+@pytest.mark.parametrize("eta", ["1", "1e+06"])
+def test_reference_benchmark_cell(eta):
+    """Reference semantics (subdomains = omega_j), 100^2/10^2, EH+Rot."""
+    g = load_golden(f"ref_bench100_eta{eta}.npz")
+    prob = _bench_problem(g)
+    P = O.build_two_level(prob, H=10, level1_mode="neighborhoods")
+    assert P.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(P.info["mode_counts"]), g["mode_counts"])
+    lam = np.array(P.coarse_space.eigenvalues)
+    assert np.allclose(lam, g["eigenvalues"], rtol=1e-12, atol=1e-12 * np.abs(g["eigenvalues"]).max())
+    z = P.apply(g["apply_r"])
+    assert np.linalg.norm(z - g["apply_z"]) <= 1e-13 * np.linalg.norm(g["apply_z"])
+    for tol in ("1e-06", "1e-08"):
+        x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=float(tol), maxit=2000)
+        assert rep.iterations == int(g[f"iters_{tol}"])
+        xr = g[f"x_{tol}"]
+        assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+        assert rep.cond_estimate == pytest.approx(float(g[f"cond_{tol}"]), rel=1e-8)
+
+
+def _adapter_check(name, apply_only=False):
+    g = load_golden(name)
+    spec = configs.ProblemSpec(
+        name=name, nx=int(g["nx"]), ny=int(g["ny"]), E=g["E"], E_min=float(g["E"].min()),
+        E_max=1.0, constrained_dofs=g["constrained_dofs"],
+        heat_dirichlet_nodes=g["heat_dirichlet_nodes"], load_full=g["load_full"],
+        H=int(g["H"]), delta=int(g["delta"]), nu=float(g["nu"]))
+    prob = O.problem_from_spec(spec)
+    P = O.build_two_level(prob, H=spec.H, delta=spec.delta, level1_mode="blocks")
+    assert P.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(P.info["mode_counts"]), g["mode_counts"])
+    assert np.allclose(P.coarse.K0, g["K0"], rtol=0, atol=1e-13 * np.abs(g["K0"]).max())
+    z = P.apply(g["apply_r"])
+    assert np.linalg.norm(z - g["apply_z"]) <= 1e-12 * np.linalg.norm(g["apply_z"])
+    if apply_only:
+        return
+    x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=float(g["tol"]), maxit=5000)
+    assert rep.iterations == int(g["iters"])
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+
+
+def test_config1_adapter_matches_reference_composition():
+    _adapter_check("ref_config1.npz")
+
+
+def test_mbb_componentwise_adapter_matches_reference_composition():
+    _adapter_check("ref_mbb_64x32.npz")
+
+
+def test_gap_rule_examples():
+    # spectral.py:161-186 semantics
+    assert O.gap_count([0.0, 1.0, 1.1, 2.0, 3.0, 4.0, 5.0], 6) == 1
+    assert O.gap_count([1e-6, 2e-6, 1.0, 2.0, 3.0, 4.0, 5.0], 6) == 2
+    assert O.gap_count([1e-8, 1e-6, 1e-4, 1e-2, 1.0, 1e2, 1e4], 6) == 6
+    assert O.gap_count([1.0, 2.0], 6) == 1
+
+
+def test_configs_are_deterministic():
+    a = configs.config1(seed=3)
+    b = configs.config1(seed=3)
+    assert np.array_equal(a.E, b.E)
+    c = configs.config3(seed=0, n=64, H=16)
+    assert abs(c.meta["volume"] - 0.4) < 1e-6
+    assert c.E.min() >= 1e-6 - 1e-18 and c.E.max() <= 1.0
