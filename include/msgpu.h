@@ -1,0 +1,142 @@
+/*
+ * msgpu.h — C ABI of the B200-native two-level spectral Schwarz PCG solve path.
+ *
+ * The reference (mselast, pure Python) has no FFI; its drop-in boundary is the
+ * duck-typed Python API listed in SURVEY.md §8(b).  Each entry point below
+ * replaces one of those reference interfaces (file:line into
+ * /root/reference/pkg/src/mselast/); paper_2006_13387_b200/ binds them with
+ * ctypes and re-exposes the reference's Python names on top.
+ *
+ * Conventions
+ *  - status codes: MS_OK (0) or a negative MS_E_* value; the message of the
+ *    last failure on a context is returned by ms_last_error().  The Python
+ *    layer maps MS_E_INVALID/MS_E_NOT_SPD to ValueError exactly where the
+ *    reference raises ValueError (krylov.py:88-98, schwarz.py:77-78,
+ *    coarse.py:142-147).
+ *  - vectors crossing the ABI are FREE-dof vectors (length n_free) in the
+ *    reference ordering: sorted free ids of the component-grouped full dof
+ *    vector (assembly.py:150-205).  Pointers may be host or device memory
+ *    (detected with cudaPointerGetAttributes); every call is synchronous
+ *    with respect to the caller.
+ *  - one CUDA stream per context; handles are not thread-safe, use one per
+ *    thread.  No torch types cross this boundary.
+ */
+#ifndef MSGPU_H
+#define MSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSGPU_ABI_VERSION 1
+
+enum {
+  MS_OK = 0,
+  MS_E_INVALID = -1,   /* bad argument / dimension mismatch            -> ValueError   */
+  MS_E_NOT_SPD = -2,   /* non-positive pivot in a Cholesky factor        -> ValueError   */
+  MS_E_CUDA = -3,      /* CUDA runtime failure                           -> RuntimeError */
+  MS_E_NOMEM = -4,     /* device allocation failed                       -> MemoryError  */
+  MS_E_STATE = -5      /* call out of order (e.g. apply before build)    -> RuntimeError */
+};
+
+typedef struct ms_ctx ms_ctx;
+typedef struct ms_problem ms_problem;
+typedef struct ms_precond ms_precond;
+
+/* level-1 subdomain layouts */
+enum {
+  MS_LEVEL1_NEIGHBORHOODS = 0, /* reference: subdomains = omega_j, strictly interior nodes (schwarz.py:97-109) */
+  MS_LEVEL1_BLOCKS = 1         /* BASELINE configs: delta-extended HxH blocks               */
+};
+
+/* level-1 local solver */
+enum {
+  MS_LOCAL_BANDED = 0,  /* banded Cholesky factor, forward/backward sweeps per apply */
+  MS_LOCAL_DENSE_INV = 1 /* explicit packed dense inverse, batched SYMV per apply     */
+};
+
+/* Options of build_preconditioner("EH+Rot" / "EH", ...) — schwarz.py:54-59, :176-211. */
+typedef struct ms_precond_opts {
+  int Nx, Ny;            /* coarse blocks per axis (CoarsePartition, grid.py:117)        */
+  int level1_kind;       /* MS_LEVEL1_*                                                 */
+  int delta;             /* overlap in elements for MS_LEVEL1_BLOCKS                    */
+  int n_max;             /* EigOptions.n_max (default 6)                                */
+  double gap_threshold;  /* select_modes gap threshold (default 50.0, spectral.py:161)  */
+  int enrich;            /* 1: EH+Rot (enrich_rotations, coarse.py:120); 0: EH          */
+  int fixed_rule;        /* 0: rule 'gap' (heat default); 1: rule 'fixed'               */
+  int local_solver;      /* MS_LOCAL_*                                                  */
+  int use_coarse;        /* 1 (default); 0 drops level 2 (diagnostics)                  */
+  const int64_t* heat_dirichlet_nodes; /* whole nodes clamped in the heat eigenproblems */
+  int64_t n_heat_dirichlet;
+} ms_precond_opts;
+
+/* Build metadata, the `info` dict of schwarz.py:202-210 plus eigensolver stats. */
+typedef struct ms_precond_info {
+  int coarse_dim;        /* N_c                                               */
+  int n_centers;         /* interior coarse nodes (neighbourhoods)            */
+  int n_subdomains;      /* level-1 subdomains                                */
+  int max_eig_passes;    /* subspace-iteration passes of the slowest centre   */
+  double t_level1;       /* s, level-1 assembly + factorisation               */
+  double t_eig;          /* s, batched eigensolves + selection                */
+  double t_coarse;       /* s, eigensolves + basis + K0 + factor/inverse      */
+  double local_bytes;    /* bytes of level-1 operator data read per apply     */
+  double coarse_bytes;   /* bytes of coarse data (psi + K0^-1) read per apply */
+} ms_precond_info;
+
+/* SolveReport (krylov.py:17-35); history arrays are caller-provided. */
+typedef struct ms_report {
+  int iterations;
+  int converged;
+  double final_residual;  /* ||r_k|| / ||b|| of the recursive residual        */
+  double t_solve;         /* s, device time of the PCG loop (CUDA events)      */
+  double t_total;         /* s, wall time of the call incl. host<->device copy */
+} ms_report;
+
+/* ---- context ---------------------------------------------------------- */
+int ms_ctx_create(int device, ms_ctx** out);
+int ms_ctx_destroy(ms_ctx* ctx);
+/* copies the last error message of `ctx` (or the global one when ctx==NULL) */
+int ms_last_error(const ms_ctx* ctx, char* buf, size_t len);
+int ms_abi_version(void);
+
+/* ---- operator: assemble_elasticity (assembly.py:208-220) ---------------
+ * E: per-element modulus, n_el = nx*ny, row-major (e = j*nx + i).
+ * free_dofs: sorted ascending full-dof ids (component-grouped), n_free of them.
+ * Replaces `assemble_elasticity(mesh, coeff, dirichlet)` and the SymmetricSparseOperator it returns. */
+int ms_problem_create(ms_ctx* ctx, int nx, int ny, double h, double nu, const double* E,
+                      const int64_t* free_dofs, int64_t n_free, ms_problem** out);
+int ms_problem_destroy(ms_problem* prob);
+int64_t ms_problem_n_free(const ms_problem* prob);
+/* replace E in place (topology-optimisation loop, topopt.py:150-160) */
+int ms_problem_set_modulus(ms_problem* prob, const double* E);
+/* q = A p over free dofs — replaces `op.matrix @ p` (krylov.py:90,114). */
+int ms_operator_apply(ms_problem* prob, const double* p, double* q);
+
+/* ---- preconditioner: build_preconditioner (schwarz.py:176-211) ---------- */
+int ms_precond_build(ms_problem* prob, const ms_precond_opts* opts, ms_precond** out);
+int ms_precond_destroy(ms_precond* pc);
+/* z = M^-1 r — TwoLevelPreconditioner.apply (schwarz.py:76-84) */
+int ms_precond_apply(ms_precond* pc, const double* r, double* z);
+/* z = R0^T K0^-1 R0 r only — CoarseOperator.apply_inverse (coarse.py:156-158) */
+int ms_precond_apply_coarse(ms_precond* pc, const double* r, double* z);
+/* info; mode_counts (length >= n_centers) and eigenvalues (n_centers x 7,
+ * row-major, the k = min(n_max+1, dim) lowest per centre, NaN-padded) may be NULL. */
+int ms_precond_info_get(const ms_precond* pc, ms_precond_info* info, int* mode_counts,
+                        double* eigenvalues);
+/* dense K0 (N_c x N_c, row-major, host buffer), reference row ordering (coarse.py:94-133) */
+int ms_precond_coarse_matrix(const ms_precond* pc, double* K0);
+
+/* ---- PCG: pcg_solve (krylov.py:81-134) ------------------------------------
+ * pc may be NULL (plain CG, the 'None' variant).  x0 = 0.  Stops when
+ * ||r_k|| <= tol ||b|| for the recursively updated residual.
+ * residuals (>= maxit+1), alphas (>= maxit), betas (>= maxit) may be NULL. */
+int ms_pcg_solve(ms_problem* prob, ms_precond* pc, const double* b, double tol, int maxit,
+                 double* x, ms_report* rep, double* residuals, double* alphas, double* betas);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSGPU_H */

@@ -1,0 +1,18 @@
+"""B200-native two-level spectral Schwarz PCG for high-contrast elasticity.
+
+Drop-in for the solve path of the reference package ``mselast`` (EH / EH+Rot
+variants): the public names below mirror ``mselast.grid``,
+``mselast.assembly``, ``mselast.schwarz`` and ``mselast.krylov``; every
+solver call runs in hand-written sm_100a kernels behind the C ABI
+``include/msgpu.h`` (``libmsgpu.so``).  There is no CPU fallback.
+"""
+
+from .grid import FineMesh, CoarsePartition, Patch, build_fine_mesh, build_coarse_partition
+from .assembly import (CoefficientField, LoadSpec, ElasticityOperator, assemble_elasticity,
+                       build_load_vector, simp_modulus, vector_dirichlet_dofs)
+from .schwarz import (VARIANTS, GPU_VARIANTS, EigOptions, IdentityPreconditioner,
+                      TwoLevelPreconditioner, build_preconditioner, get_variant)
+from .krylov import SolveReport, estimate_condition, pcg_solve
+from .solve import solve_spec
+
+__all__ = [n for n in dir() if not n.startswith("_")]

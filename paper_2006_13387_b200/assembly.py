@@ -1,0 +1,164 @@
+"""Elasticity operator on the GPU behind the reference's assembly API.
+
+``assemble_elasticity`` (assembly.py:208-220 in the reference) returns an
+operator object with the same duck type as ``SymmetricSparseOperator``
+(``free_dofs``, ``n_free``, ``free_index()``, ``expand``, ``restrict``,
+``matrix @ v``) whose matvec is the matrix-free sm_100a kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._context import default_context
+
+
+@dataclass
+class CoefficientField:
+    """Per-element modulus with bounds and Poisson ratio (assembly.py:21-52)."""
+
+    values: np.ndarray
+    nu: float
+    E_min: float
+    E_max: float
+
+    def __post_init__(self):
+        self.values = np.asarray(self.values, dtype=float).ravel()
+        if self.E_min <= 0:
+            raise ValueError("E_min must be positive")
+        tol = 1e-12 * self.E_max
+        if self.values.min() < self.E_min - tol or self.values.max() > self.E_max + tol:
+            raise ValueError("element moduli out of [E_min, E_max]")
+
+    @property
+    def contrast(self):
+        return self.E_max / self.E_min
+
+
+@dataclass
+class LoadSpec:
+    point_loads: list = field(default_factory=list)  # (node, component, magnitude)
+
+
+def build_load_vector(mesh, load):
+    """Full-layout load vector from point loads (assembly.py:63-77, point-load part)."""
+    f = np.zeros(mesh.n_dofs)
+    for node, comp, mag in load.point_loads:
+        if not (0 <= node < mesh.n_nodes) or comp not in (0, 1):
+            raise ValueError(f"invalid point load ({node}, {comp})")
+        f[node + comp * mesh.n_nodes] += mag
+    return f
+
+
+def simp_modulus(rho_f, p, E_min, E_max):
+    """E = E_min + rho^p (E_max - E_min) (assembly.py:280-287)."""
+    rho_f = np.asarray(rho_f, dtype=float)
+    if rho_f.min() < -1e-12 or rho_f.max() > 1 + 1e-12:
+        raise ValueError("density out of [0, 1]")
+    if p < 1:
+        raise ValueError("penalization exponent must be >= 1")
+    return E_min + np.clip(rho_f, 0.0, 1.0) ** p * (E_max - E_min)
+
+
+def vector_dirichlet_dofs(mesh, nodes):
+    nodes = np.asarray(nodes, dtype=np.int64)
+    return np.concatenate([nodes, nodes + mesh.n_nodes])
+
+
+class ElasticityOperator:
+    """Free-dof Q1 plane-stress operator held on the GPU."""
+
+    def __init__(self, mesh, coeff, free_dofs, ctx=None):
+        self.mesh = mesh
+        self.coeff = coeff
+        self.nu = float(coeff.nu)
+        self.free_dofs = np.ascontiguousarray(free_dofs, dtype=np.int64)
+        self.n_full = mesh.n_dofs
+        if self.free_dofs.size == 0:
+            raise ValueError("empty free-dof set")
+        self._ctx = ctx or default_context()
+        lib = _lib.load()
+        h = C.c_void_p()
+        E = np.ascontiguousarray(coeff.values, dtype=np.float64)
+        _lib.check(lib.ms_problem_create(self._ctx.handle, mesh.nx, mesh.ny, mesh.h, self.nu,
+                                         C.c_void_p(E.ctypes.data), C.c_void_p(self.free_dofs.ctypes.data),
+                                         self.free_dofs.size, C.byref(h)), self._ctx.handle)
+        self.handle = h
+
+    # SymmetricSparseOperator duck type (assembly.py:150-182)
+    @property
+    def n_free(self):
+        return int(self.free_dofs.size)
+
+    @property
+    def matrix(self):
+        return self
+
+    @property
+    def shape(self):
+        return (self.n_free, self.n_free)
+
+    def free_index(self):
+        idx = np.full(self.n_full, -1, dtype=np.int64)
+        idx[self.free_dofs] = np.arange(self.n_free)
+        return idx
+
+    def expand(self, x_free):
+        x = np.zeros(self.n_full)
+        x[self.free_dofs] = x_free
+        return x
+
+    def restrict(self, x_full):
+        return np.asarray(x_full)[self.free_dofs]
+
+    def apply(self, p):
+        """q = A p on the GPU (replaces ``op.matrix @ p``, krylov.py:90)."""
+        if p.shape[0] != self.n_free:
+            raise ValueError("vector dimension mismatch")
+        pp, keep, dev = _lib.vec_ptr(p)
+        if dev:
+            import torch
+
+            q = torch.empty_like(keep)
+            qp = C.c_void_p(q.data_ptr())
+        else:
+            q = np.empty(self.n_free)
+            qp = C.c_void_p(q.ctypes.data)
+        _lib.check(_lib.load().ms_operator_apply(self.handle, pp, qp), self._ctx.handle)
+        return q
+
+    __matmul__ = apply
+
+    def set_modulus(self, E):
+        E = np.ascontiguousarray(E, dtype=np.float64)
+        _lib.check(_lib.load().ms_problem_set_modulus(self.handle, C.c_void_p(E.ctypes.data)),
+                   self._ctx.handle)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().ms_problem_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def assemble_elasticity(mesh, coeff, dirichlet_nodes, constrained_dofs=None):
+    """GPU operator over free dofs (assembly.py:208-220).
+
+    ``dirichlet_nodes`` clamp whole nodes exactly as in the reference;
+    ``constrained_dofs`` (full-dof ids) additionally allows component-wise
+    constraints (MBB configs).
+    """
+    if coeff.values.size != mesh.n_elements:
+        raise ValueError("coefficient field does not match mesh")
+    cons = vector_dirichlet_dofs(mesh, dirichlet_nodes)
+    if constrained_dofs is not None:
+        cons = np.concatenate([cons, np.asarray(constrained_dofs, dtype=np.int64)])
+    free = np.setdiff1d(np.arange(mesh.n_dofs), cons)
+    return ElasticityOperator(mesh, coeff, free)

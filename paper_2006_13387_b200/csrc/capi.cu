@@ -1,0 +1,763 @@
+// C ABI of the B200-native EH+Rot Schwarz PCG path (include/msgpu.h).
+//
+// Host-side orchestration only: geometry, offsets, allocation and kernel
+// sequencing.  All arithmetic on vectors, factors and eigenproblems runs in
+// the kernels of operator.cu / banded.cu / eigen.cu / coarse.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/msgpu.h"
+#include "banded.cuh"
+#include "coarse.cuh"
+#include "common.cuh"
+#include "eigen.cuh"
+#include "operator.cuh"
+
+using namespace msgpu;
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_err;
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw Error(MS_E_NOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
+                                  " bytes failed: " + cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void zero(cudaStream_t st) { MS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st)); }
+  void upload(const T* h, size_t count, cudaStream_t st) {
+    if (count > n) alloc(count);
+    if (count) MS_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+};
+
+bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// element matrices, same formulas as the reference (assembly.py:83-147)
+void unit_elasticity(double nu, double K[64]) {
+  const double g[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+  const double f = 1.0 / (1.0 - nu * nu);
+  const double C[3][3] = {{f * 1.0, f * nu, 0.0}, {f * nu, f * 1.0, 0.0}, {0.0, 0.0, f * (1.0 - nu) / 2.0}};
+  double A[8][8] = {};
+  for (double xi : g)
+    for (double eta : g) {
+      const double dx[4] = {-(1 - eta), 1 - eta, eta, -eta};
+      const double dy[4] = {-(1 - xi), -xi, xi, 1 - xi};
+      double B[3][8] = {};
+      for (int m = 0; m < 4; ++m) {
+        B[0][m] = dx[m];
+        B[1][4 + m] = dy[m];
+        B[2][m] = dy[m];
+        B[2][4 + m] = dx[m];
+      }
+      double BtC[8][3] = {};
+      for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 3; ++j)
+          for (int l = 0; l < 3; ++l) BtC[i][j] += B[l][i] * C[l][j];
+      for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+          double s = 0.0;
+          for (int l = 0; l < 3; ++l) s += BtC[i][l] * B[l][j];
+          A[i][j] += 0.25 * s;
+        }
+    }
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) K[i * 8 + j] = 0.5 * (A[i][j] + A[j][i]);
+}
+
+void heat_elements(double h, HeatParam& hp) {
+  const double g[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+  double A[4][4] = {};
+  for (double xi : g)
+    for (double eta : g) {
+      const double dx[4] = {-(1 - eta), 1 - eta, eta, -eta};
+      const double dy[4] = {-(1 - xi), -xi, xi, 1 - xi};
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) A[i][j] += 0.25 * (dx[i] * dx[j] + dy[i] * dy[j]);
+    }
+  const double pat[4][4] = {{4, 2, 1, 2}, {2, 4, 2, 1}, {1, 2, 4, 2}, {2, 1, 2, 4}};
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      hp.lap[i * 4 + j] = A[i][j];
+      hp.mel[i * 4 + j] = (h * h / 36.0) * pat[i][j];
+    }
+}
+
+}  // namespace
+
+struct ms_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+};
+
+struct ms_problem {
+  ms_ctx* ctx = nullptr;
+  Grid g{};
+  double nu = 0.3;
+  KeParam ke{};
+  DBuf<double> E;
+  DBuf<uint8_t> mask;
+  DBuf<int64_t> free_dofs;
+  int64_t n_free = 0;
+  int64_t n_full = 0;
+  // PCG workspace (full layout)
+  DBuf<double> x, r, z, p0, p1, q, tmp, tmp2;
+  DBuf<PcgScalars> sc;
+  DBuf<double> partials;
+  DBuf<double> hres, halpha, hbeta;
+  int hcap = 0;
+  void ensure_workspace() {
+    if (x.p) return;
+    const cudaStream_t st = ctx->st;
+    for (DBuf<double>* b : {&x, &r, &z, &p0, &p1, &q, &tmp, &tmp2}) {
+      b->alloc(n_full);
+      b->zero(st);
+    }
+    sc.alloc(1);
+    partials.alloc(std::max<int64_t>(reduce_blocks(), (int64_t)div_up(g.nx + 1, MV_TX) * div_up(g.ny + 1, MV_TY)));
+  }
+};
+
+struct ms_precond {
+  ms_problem* prob = nullptr;
+  ms_precond_opts opts{};
+  std::vector<int64_t> heat_dir;
+  // level 1
+  int NbX = 0, NbY = 0, nsys = 0, max_bw = 0;
+  std::vector<BandSys> hsys;
+  DBuf<BandSys> sys;
+  DBuf<double> Lc, Lr, ybuf;
+  DBuf<int> xcov, ycov;
+  L1Dev l1{};
+  // coarse
+  bool has_coarse = false;
+  CoarseDev cd{};
+  DBuf<int> nsel, hoff;
+  DBuf<int64_t> psioff;
+  DBuf<double> psi, chi, K0inv, f0, y0, part, evals, K0keep;
+  std::vector<int> h_nsel;
+  std::vector<double> h_evals;
+  int N_c = 0;
+  int max_pass = 0;
+  ms_precond_info info{};
+};
+
+#define MS_API_BEGIN try {
+#define MS_API_END(ctxptr)                                  \
+  }                                                         \
+  catch (const Error& e) {                                  \
+    set_error(ctxptr, e.what());                            \
+    return e.code;                                          \
+  }                                                         \
+  catch (const std::exception& e) {                         \
+    set_error(ctxptr, e.what());                            \
+    return MS_E_CUDA;                                       \
+  }                                                         \
+  return MS_OK;
+
+static void set_error(ms_ctx* ctx, const std::string& m) {
+  if (ctx) ctx->err = m;
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_err = m;
+}
+
+// ---------------------------------------------------------------------------
+// helpers
+
+static void check_fail(DBuf<int>& flag, cudaStream_t st, const char* what) {
+  int h = 0;
+  MS_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  if (h != 0)
+    throw Error(MS_E_NOT_SPD, std::string(what) + " not positive definite (pivot/system " +
+                                  std::to_string(h - 1) + ")");
+}
+
+// copy an ABI vector (host or device, free layout) into a full-layout device vector
+static void load_free(ms_problem* P, const double* src, double* dst_full) {
+  const cudaStream_t st = P->ctx->st;
+  MS_CUDA(cudaMemsetAsync(dst_full, 0, P->n_full * sizeof(double), st));
+  const double* dsrc = src;
+  if (!is_device_ptr(src)) {
+    MS_CUDA(cudaMemcpyAsync(P->tmp2.p, src, P->n_free * sizeof(double), cudaMemcpyHostToDevice, st));
+    dsrc = P->tmp2.p;
+  }
+  launch_scatter_free(P->n_free, P->free_dofs.p, dsrc, dst_full, st);
+}
+
+static void store_free(ms_problem* P, const double* src_full, double* dst) {
+  const cudaStream_t st = P->ctx->st;
+  if (is_device_ptr(dst)) {
+    launch_gather_free(P->n_free, P->free_dofs.p, src_full, dst, st);
+  } else {
+    launch_gather_free(P->n_free, P->free_dofs.p, src_full, P->tmp2.p, st);
+    MS_CUDA(cudaMemcpyAsync(dst, P->tmp2.p, P->n_free * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  MS_CUDA(cudaStreamSynchronize(st));
+}
+
+static void level1_axis(int n_el, int nblocks, int kind, int delta, std::vector<int>& lo,
+                        std::vector<int>& hi) {
+  const int H = n_el / nblocks;
+  lo.clear();
+  hi.clear();
+  if (kind == MS_LEVEL1_NEIGHBORHOODS) {
+    for (int I = 1; I < nblocks; ++I) {
+      lo.push_back((I - 1) * H + 1);
+      hi.push_back((I + 1) * H - 1);
+    }
+  } else {
+    for (int I = 0; I < nblocks; ++I) {
+      const int e0 = std::max(0, I * H - delta), e1 = std::min(n_el, (I + 1) * H + delta);
+      lo.push_back(e0 == 0 ? 0 : e0 + 1);
+      hi.push_back(e1 == n_el ? n_el : e1 - 1);
+    }
+  }
+}
+
+// precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
+static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgScalars* sc,
+                               double* beta_hist) {
+  ms_problem* P = pc->prob;
+  const cudaStream_t st = P->ctx->st;
+  const int* done = sc ? &sc->done : nullptr;
+  if (pc->nsys > 0)
+    launch_l1_solve(P->g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
+  if (pc->has_coarse) {
+    launch_restrict(P->g, pc->cd, r, pc->f0.p, done, st);
+    launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st);
+  }
+  launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
+                 pc->y0.p, r, z, sc, P->partials.p, beta_hist, st);
+}
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int ms_abi_version(void) { return MSGPU_ABI_VERSION; }
+
+int ms_last_error(const ms_ctx* ctx, char* buf, size_t len) {
+  if (!buf || len == 0) return MS_E_INVALID;
+  std::string m;
+  if (ctx)
+    m = ctx->err;
+  else {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    m = g_err;
+  }
+  std::strncpy(buf, m.c_str(), len - 1);
+  buf[len - 1] = '\0';
+  return MS_OK;
+}
+
+int ms_ctx_create(int device, ms_ctx** out) {
+  ms_ctx* c = nullptr;
+  MS_API_BEGIN
+  if (!out) throw Error(MS_E_INVALID, "null output handle");
+  int ndev = 0;
+  MS_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw Error(MS_E_INVALID, "invalid CUDA device " + std::to_string(device));
+  MS_CUDA(cudaSetDevice(device));
+  c = new ms_ctx();
+  c->device = device;
+  MS_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  *out = c;
+  MS_API_END(c)
+}
+
+int ms_ctx_destroy(ms_ctx* ctx) {
+  if (!ctx) return MS_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+  return MS_OK;
+}
+
+int ms_problem_create(ms_ctx* ctx, int nx, int ny, double h, double nu, const double* E,
+                      const int64_t* free_dofs, int64_t n_free, ms_problem** out) {
+  MS_API_BEGIN
+  if (!ctx || !out || !E || (!free_dofs && n_free > 0)) throw Error(MS_E_INVALID, "null argument");
+  if (nx < 1 || ny < 1) throw Error(MS_E_INVALID, "element counts must be positive");
+  if (!(nu >= 0.0 && nu < 0.5)) throw Error(MS_E_INVALID, "Poisson ratio outside [0, 0.5)");
+  if (n_free <= 0) throw Error(MS_E_INVALID, "empty free-dof set");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  std::unique_ptr<ms_problem> P(new ms_problem());
+  P->ctx = ctx;
+  P->g.nx = nx;
+  P->g.ny = ny;
+  P->g.nnx = nx + 1;
+  P->g.n_nodes = (int64_t)(nx + 1) * (ny + 1);
+  P->g.h = h;
+  P->nu = nu;
+  P->n_full = 2 * P->g.n_nodes;
+  P->n_free = n_free;
+  if (n_free > P->n_full) throw Error(MS_E_INVALID, "more free dofs than dofs");
+  unit_elasticity(nu, P->ke.k);
+  const cudaStream_t st = ctx->st;
+  const int64_t n_el = (int64_t)nx * ny;
+  P->E.alloc(n_el);
+  if (is_device_ptr(E))
+    MS_CUDA(cudaMemcpyAsync(P->E.p, E, n_el * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  else
+    P->E.upload(E, n_el, st);
+  std::vector<int64_t> fd(n_free);
+  if (is_device_ptr(free_dofs))
+    MS_CUDA(cudaMemcpy(fd.data(), free_dofs, n_free * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  else
+    std::memcpy(fd.data(), free_dofs, n_free * sizeof(int64_t));
+  std::vector<uint8_t> mask(P->n_full, 0);
+  for (int64_t i = 0; i < n_free; ++i) {
+    if (fd[i] < 0 || fd[i] >= P->n_full || (i > 0 && fd[i] <= fd[i - 1]))
+      throw Error(MS_E_INVALID, "free dofs must be sorted, unique and in range");
+    mask[fd[i]] = 1;
+  }
+  P->free_dofs.upload(fd.data(), n_free, st);
+  P->mask.upload(mask.data(), mask.size(), st);
+  P->ensure_workspace();
+  MS_CUDA(cudaStreamSynchronize(st));
+  *out = P.release();
+  MS_API_END(ctx)
+}
+
+int ms_problem_destroy(ms_problem* prob) {
+  if (!prob) return MS_OK;
+  cudaSetDevice(prob->ctx->device);
+  cudaStreamSynchronize(prob->ctx->st);
+  delete prob;
+  return MS_OK;
+}
+
+int64_t ms_problem_n_free(const ms_problem* prob) { return prob ? prob->n_free : -1; }
+
+int ms_problem_set_modulus(ms_problem* prob, const double* E) {
+  MS_API_BEGIN
+  if (!prob || !E) throw Error(MS_E_INVALID, "null argument");
+  const int64_t n_el = (int64_t)prob->g.nx * prob->g.ny;
+  MS_CUDA(cudaMemcpyAsync(prob->E.p, E, n_el * sizeof(double), cudaMemcpyDefault, prob->ctx->st));
+  MS_CUDA(cudaStreamSynchronize(prob->ctx->st));
+  MS_API_END(prob ? prob->ctx : nullptr)
+}
+
+int ms_operator_apply(ms_problem* P, const double* p, double* q) {
+  MS_API_BEGIN
+  if (!P || !p || !q) throw Error(MS_E_INVALID, "null argument");
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  load_free(P, p, P->tmp.p);
+  launch_matvec(P->g, P->ke, P->E.p, P->mask.p, nullptr, P->tmp.p, nullptr, P->q.p, MV_PLAIN,
+                nullptr, nullptr, nullptr, P->ctx->st);
+  store_free(P, P->q.p, q);
+  MS_API_END(P ? P->ctx : nullptr)
+}
+
+int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) {
+  MS_API_BEGIN
+  if (!P || !o || !out) throw Error(MS_E_INVALID, "null argument");
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  const cudaStream_t st = P->ctx->st;
+  const Grid& g = P->g;
+  if (o->Nx < 1 || o->Ny < 1 || g.nx % o->Nx || g.ny % o->Ny)
+    throw Error(MS_E_INVALID, "coarse mesh " + std::to_string(o->Nx) + "x" + std::to_string(o->Ny) +
+                                  " not nested in fine mesh");
+  if (o->n_max < 1) throw Error(MS_E_INVALID, "mode cap must be >= 1");
+  if (o->n_max > kNeig - 1) throw Error(MS_E_INVALID, "n_max > 6 is not supported by the GPU eigensolver");
+  if (o->level1_kind == MS_LEVEL1_BLOCKS && o->delta < 1)
+    throw Error(MS_E_INVALID, "block level-1 needs overlap delta >= 1");
+  if (o->local_solver != MS_LOCAL_BANDED) throw Error(MS_E_INVALID, "local solver not available");
+  std::unique_ptr<ms_precond> pc(new ms_precond());
+  pc->prob = P;
+  pc->opts = *o;
+  if (o->heat_dirichlet_nodes && o->n_heat_dirichlet > 0)
+    pc->heat_dir.assign(o->heat_dirichlet_nodes, o->heat_dirichlet_nodes + o->n_heat_dirichlet);
+  pc->opts.heat_dirichlet_nodes = nullptr;
+  DBuf<int> fail;
+  fail.alloc(1);
+
+  // ---------------- level 1 ----------------
+  cudaEvent_t e0, e1, e2, e3;
+  MS_CUDA(cudaEventCreate(&e0));
+  MS_CUDA(cudaEventCreate(&e1));
+  MS_CUDA(cudaEventCreate(&e2));
+  MS_CUDA(cudaEventCreate(&e3));
+  MS_CUDA(cudaEventRecord(e0, st));
+  {
+    std::vector<int> xlo, xhi, ylo, yhi;
+    level1_axis(g.nx, o->Nx, o->level1_kind, o->delta, xlo, xhi);
+    level1_axis(g.ny, o->Ny, o->level1_kind, o->delta, ylo, yhi);
+    pc->NbX = (int)xlo.size();
+    pc->NbY = (int)ylo.size();
+    pc->nsys = pc->NbX * pc->NbY;
+    int64_t foff = 0, yoff = 0;
+    for (int J = 0; J < pc->NbY; ++J)
+      for (int I = 0; I < pc->NbX; ++I) {
+        BandSys s{};
+        if (xhi[I] < xlo[I] || yhi[J] < ylo[J]) throw Error(MS_E_INVALID, "empty level-1 subdomain");
+        band_setup(s, xlo[I], xhi[I], ylo[J], yhi[J], 2);
+        s.foff = foff;
+        s.yoff = yoff;
+        foff += (int64_t)s.n * (s.bw + 1);
+        yoff += s.n;
+        pc->max_bw = std::max(pc->max_bw, s.bw);
+        pc->hsys.push_back(s);
+      }
+    std::vector<int> xcov((g.nx + 1) * 4, -1), ycov((g.ny + 1) * 4, -1);
+    auto cover = [](const std::vector<int>& lo, const std::vector<int>& hi, int nn, std::vector<int>& cov) {
+      for (int a = 0; a < nn; ++a) {
+        int c = 0;
+        for (int I = 0; I < (int)lo.size(); ++I)
+          if (a >= lo[I] && a <= hi[I]) {
+            if (c == 4) throw Error(MS_E_INVALID, "a node is covered by more than 4 subdomains per axis");
+            cov[a * 4 + c++] = I;
+          }
+      }
+    };
+    cover(xlo, xhi, g.nx + 1, xcov);
+    cover(ylo, yhi, g.ny + 1, ycov);
+    pc->sys.upload(pc->hsys.data(), pc->hsys.size(), st);
+    pc->xcov.upload(xcov.data(), xcov.size(), st);
+    pc->ycov.upload(ycov.data(), ycov.size(), st);
+    pc->Lc.alloc(foff);
+    pc->Lr.alloc(foff);
+    pc->ybuf.alloc(yoff);
+    pc->Lr.zero(st);
+    fail.zero(st);
+    launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p, pc->nsys, pc->Lc.p, st);
+    launch_band_potrf(pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
+    check_fail(fail, st, "level-1 subdomain matrix");
+    pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->sys.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
+    pc->info.n_subdomains = pc->nsys;
+    pc->info.local_bytes = (double)foff * 2 * sizeof(double);
+  }
+  MS_CUDA(cudaEventRecord(e1, st));
+
+  // ---------------- coarse space ----------------
+  pc->has_coarse = o->use_coarse != 0 && o->Nx >= 2 && o->Ny >= 2;
+  if (pc->has_coarse) {
+    CoarseDev& cd = pc->cd;
+    cd.Nx = o->Nx;
+    cd.Ny = o->Ny;
+    cd.mex = g.nx / o->Nx;
+    cd.mey = g.ny / o->Ny;
+    cd.NLx = 2 * cd.mex + 1;
+    cd.NLy = 2 * cd.mey + 1;
+    cd.n_centers = (o->Nx - 1) * (o->Ny - 1);
+    cd.enrich = o->enrich ? 1 : 0;
+    cd.h = g.h;
+    const int nc = cd.n_centers;
+    const int NL = cd.NLx * cd.NLy;
+    if (NL < 4 * kEigBlock) throw Error(MS_E_INVALID, "neighbourhoods too small for the block eigensolver");
+    // heat Dirichlet node mask
+    std::vector<uint8_t> hd(g.n_nodes, 0);
+    for (int64_t nid : pc->heat_dir) {
+      if (nid < 0 || nid >= g.n_nodes) throw Error(MS_E_INVALID, "heat Dirichlet node out of range");
+      hd[nid] = 1;
+    }
+    DBuf<uint8_t> hdir;
+    hdir.upload(hd.data(), hd.size(), st);
+    HeatParam hp{};
+    heat_elements(g.h, hp);
+    // shift: relative 1e-12 of the pencil's spectral bound 24/h^2
+    const double sigma = 1e-12 * 24.0 / (g.h * g.h);
+    pc->evals.alloc((size_t)nc * kNeig);
+    DBuf<int> passes, neumann;
+    passes.alloc(nc);
+    neumann.alloc(nc);
+    pc->nsel.alloc(nc);
+    pc->psioff.alloc(nc);
+    pc->psi.alloc((size_t)nc * o->n_max * NL);
+    std::vector<int64_t> h_psioff(nc, 0);
+    pc->h_nsel.assign(nc, 0);
+    const int batch = std::min(nc, 1024);
+    DBuf<BandSys> hsysd;
+    DBuf<double> hLc, hLr, work, evecs;
+    int64_t psi_cursor = 0;
+    for (int k0 = 0; k0 < nc; k0 += batch) {
+      const int nk = std::min(batch, nc - k0);
+      std::vector<BandSys> hs(nk);
+      int64_t foff = 0;
+      int mbw = 0;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int k = k0 + kb;
+        const int I = k % (o->Nx - 1) + 1, J = k / (o->Nx - 1) + 1;
+        BandSys s{};
+        band_setup(s, (I - 1) * cd.mex, (I + 1) * cd.mex, (J - 1) * cd.mey, (J + 1) * cd.mey, 1);
+        s.foff = foff;
+        foff += (int64_t)s.n * (s.bw + 1);
+        mbw = std::max(mbw, s.bw);
+        hs[kb] = s;
+      }
+      if (!hLc.p || hLc.n < (size_t)foff) {
+        hLc.alloc(foff);
+        hLr.alloc(foff);
+        work.alloc((size_t)nk * 2 * kEigBlock * NL);
+        evecs.alloc((size_t)nk * kNeig * NL);
+      }
+      hsysd.upload(hs.data(), nk, st);
+      MS_CUDA(cudaMemsetAsync(hLr.p, 0, foff * sizeof(double), st));
+      fail.zero(st);
+      launch_heat_assemble(g, P->E.p, hdir.p, hp, sigma, hsysd.p, nk, hLc.p, st);
+      launch_band_potrf(hsysd.p, nk, mbw, hLc.p, hLr.p, fail.p, st);
+      check_fail(fail, st, "neighbourhood heat pencil (K + sigma M)");
+      EigBatch eb{o->Nx, cd.mex, cd.mey, k0, nk, hsysd.p, hLc.p, hLr.p, work.p, pc->evals.p,
+                  evecs.p, passes.p, neumann.p};
+      launch_subspace(g, P->E.p, hdir.p, hp, eb, 300, 1e-12, st);
+      launch_select(nc, pc->evals.p, o->n_max, o->gap_threshold, o->fixed_rule, pc->nsel.p, st);
+      std::vector<int> bsel(nk);
+      MS_CUDA(cudaMemcpyAsync(bsel.data(), pc->nsel.p + k0, nk * sizeof(int), cudaMemcpyDeviceToHost, st));
+      MS_CUDA(cudaStreamSynchronize(st));
+      for (int kb = 0; kb < nk; ++kb) {
+        h_psioff[k0 + kb] = psi_cursor;
+        psi_cursor += (int64_t)bsel[kb] * NL;
+        pc->h_nsel[k0 + kb] = bsel[kb];
+      }
+      pc->psioff.upload(h_psioff.data(), nc, st);
+      launch_compact_psi(eb, cd.NLx, pc->nsel.p, pc->psioff.p, pc->psi.p, st);
+    }
+    {
+      std::vector<int> hp_(nc);
+      MS_CUDA(cudaMemcpyAsync(hp_.data(), passes.p, nc * sizeof(int), cudaMemcpyDeviceToHost, st));
+      MS_CUDA(cudaStreamSynchronize(st));
+      pc->max_pass = *std::max_element(hp_.begin(), hp_.end());
+    }
+    MS_CUDA(cudaEventRecord(e2, st));
+    // offsets
+    std::vector<int> h_hoff(nc);
+    int acc = 0;
+    for (int k = 0; k < nc; ++k) {
+      h_hoff[k] = acc;
+      acc += 2 * pc->h_nsel[k];
+    }
+    cd.roff = acc;
+    pc->N_c = acc + (cd.enrich ? nc : 0);
+    cd.N_c = pc->N_c;
+    pc->hoff.upload(h_hoff.data(), nc, st);
+    pc->chi.alloc((size_t)nc * NL);
+    cd.nsel = pc->nsel.p;
+    cd.hoff = pc->hoff.p;
+    cd.psioff = pc->psioff.p;
+    cd.psi = pc->psi.p;
+    cd.chi = pc->chi.p;
+    launch_pou_table(g, cd, pc->chi.p, st);
+    // K0 = R0 A R0^T, symmetrised, inverted
+    const int N = pc->N_c;
+    DBuf<double> K0;
+    K0.alloc((size_t)N * N);
+    K0.zero(st);
+    const int ncta = std::min(nc, 148 * 4);
+    DBuf<double> scratch;
+    scratch.alloc((size_t)ncta * 4 * NL);
+    launch_k0_assemble(g, P->ke, P->E.p, P->mask.p, cd, K0.p, scratch.p, ncta, st);
+    launch_symmetrize(N, K0.p, st);
+    const int nt = div_up(N, kTile);
+    pc->K0inv.alloc((size_t)packed_tiles(nt) * kTile * kTile);
+    DBuf<double> inv_work;
+    inv_work.alloc(dense_spd_inverse_work_bytes(N) / sizeof(double));
+    fail.zero(st);
+    dense_spd_inverse(N, K0.p, pc->K0inv.p, inv_work.p, fail.p, st);
+    check_fail(fail, st, "coarse operator: basis is rank deficient, K0");
+    pc->f0.alloc(N);
+    pc->y0.alloc(N);
+    pc->part.alloc((size_t)packed_tiles(nt) * 2 * kTile);
+    if ((size_t)N * N <= (size_t)4096 * 4096) {
+      pc->K0keep.alloc((size_t)N * N);
+      MS_CUDA(cudaMemcpyAsync(pc->K0keep.p, K0.p, (size_t)N * N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    pc->h_evals.resize((size_t)nc * kNeig);
+    MS_CUDA(cudaMemcpyAsync(pc->h_evals.data(), pc->evals.p, pc->h_evals.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    pc->info.coarse_bytes = (double)(psi_cursor + (int64_t)packed_tiles(nt) * kTile * kTile) * sizeof(double);
+  } else {
+    MS_CUDA(cudaEventRecord(e2, st));
+  }
+  MS_CUDA(cudaEventRecord(e3, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  float t1 = 0, t2 = 0, t3 = 0;
+  MS_CUDA(cudaEventElapsedTime(&t1, e0, e1));
+  MS_CUDA(cudaEventElapsedTime(&t2, e1, e2));
+  MS_CUDA(cudaEventElapsedTime(&t3, e1, e3));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  cudaEventDestroy(e3);
+  pc->info.coarse_dim = pc->N_c;
+  pc->info.n_centers = pc->has_coarse ? pc->cd.n_centers : 0;
+  pc->info.max_eig_passes = pc->max_pass;
+  pc->info.t_level1 = t1 * 1e-3;
+  pc->info.t_eig = t2 * 1e-3;
+  pc->info.t_coarse = t3 * 1e-3;
+  *out = pc.release();
+  MS_API_END(P ? P->ctx : nullptr)
+}
+
+int ms_precond_destroy(ms_precond* pc) {
+  if (!pc) return MS_OK;
+  cudaSetDevice(pc->prob->ctx->device);
+  cudaStreamSynchronize(pc->prob->ctx->st);
+  delete pc;
+  return MS_OK;
+}
+
+int ms_precond_apply(ms_precond* pc, const double* r, double* z) {
+  MS_API_BEGIN
+  if (!pc || !r || !z) throw Error(MS_E_INVALID, "null argument");
+  ms_problem* P = pc->prob;
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  load_free(P, r, P->r.p);
+  precond_apply_full(pc, P->r.p, P->z.p, nullptr, nullptr);
+  store_free(P, P->z.p, z);
+  MS_API_END(pc ? pc->prob->ctx : nullptr)
+}
+
+int ms_precond_apply_coarse(ms_precond* pc, const double* r, double* z) {
+  MS_API_BEGIN
+  if (!pc || !r || !z) throw Error(MS_E_INVALID, "null argument");
+  if (!pc->has_coarse) throw Error(MS_E_STATE, "preconditioner has no coarse level");
+  ms_problem* P = pc->prob;
+  const cudaStream_t st = P->ctx->st;
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  load_free(P, r, P->r.p);
+  launch_restrict(P->g, pc->cd, P->r.p, pc->f0.p, nullptr, st);
+  launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
+  launch_combine(P->g, P->mask.p, nullptr, &pc->cd, pc->y0.p, P->r.p, P->z.p, nullptr, nullptr, nullptr, st);
+  store_free(P, P->z.p, z);
+  MS_API_END(pc ? pc->prob->ctx : nullptr)
+}
+
+int ms_precond_info_get(const ms_precond* pc, ms_precond_info* info, int* mode_counts,
+                        double* eigenvalues) {
+  MS_API_BEGIN
+  if (!pc) throw Error(MS_E_INVALID, "null argument");
+  if (info) *info = pc->info;
+  if (mode_counts && pc->has_coarse)
+    std::memcpy(mode_counts, pc->h_nsel.data(), pc->h_nsel.size() * sizeof(int));
+  if (eigenvalues && pc->has_coarse)
+    std::memcpy(eigenvalues, pc->h_evals.data(), pc->h_evals.size() * sizeof(double));
+  MS_API_END(nullptr)
+}
+
+int ms_precond_coarse_matrix(const ms_precond* pc, double* K0) {
+  MS_API_BEGIN
+  if (!pc || !K0) throw Error(MS_E_INVALID, "null argument");
+  if (!pc->K0keep.p) throw Error(MS_E_STATE, "K0 is only retained for N_c <= 4096");
+  MS_CUDA(cudaSetDevice(pc->prob->ctx->device));
+  MS_CUDA(cudaMemcpy(K0, pc->K0keep.p, (size_t)pc->N_c * pc->N_c * sizeof(double), cudaMemcpyDeviceToHost));
+  MS_API_END(nullptr)
+}
+
+int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int maxit, double* x,
+                 ms_report* rep, double* residuals, double* alphas, double* betas) {
+  MS_API_BEGIN
+  if (!P || !b || !x) throw Error(MS_E_INVALID, "null argument");
+  if (!(tol > 0.0 && tol < 1.0)) throw Error(MS_E_INVALID, "tolerance must be in (0, 1)");
+  if (maxit < 0) throw Error(MS_E_INVALID, "maxit must be >= 0");
+  if (pc && pc->prob != P) throw Error(MS_E_INVALID, "preconditioner built for another problem");
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  const auto wall0 = std::chrono::steady_clock::now();
+  const cudaStream_t st = P->ctx->st;
+  if (P->hcap < maxit + 1) {
+    P->hres.alloc(maxit + 1);
+    P->halpha.alloc(std::max(maxit, 1));
+    P->hbeta.alloc(std::max(maxit, 1));
+    P->hcap = maxit + 1;
+  }
+  load_free(P, b, P->r.p);  // r = b
+  P->x.zero(st);
+  P->p0.zero(st);
+  P->p1.zero(st);
+  PcgScalars hs{};
+  hs.tol = tol;
+  hs.maxit = maxit;
+  hs.first = 1;
+  hs.done = maxit == 0 ? 1 : 0;
+  MS_CUDA(cudaMemcpyAsync(P->sc.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+  cudaEvent_t t0, t1;
+  MS_CUDA(cudaEventCreate(&t0));
+  MS_CUDA(cudaEventCreate(&t1));
+  MS_CUDA(cudaEventRecord(t0, st));
+  const int64_t n = P->n_full;
+  launch_init_norm(n, P->r.p, P->sc.p, P->partials.p, P->hres.p, st);
+  double* zp = pc ? P->z.p : P->r.p;
+  if (pc)
+    precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p);
+  else
+    launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
+  int it = 0;
+  int done = 0;
+  const int chunk = 8;
+  while (!done && it < maxit) {
+    const int upto = std::min(maxit, it + chunk);
+    for (; it < upto; ++it) {
+      double* pold = (it & 1) ? P->p1.p : P->p0.p;
+      double* pnew = (it & 1) ? P->p0.p : P->p1.p;
+      launch_matvec(P->g, P->ke, P->E.p, P->mask.p, zp, pold, pnew, P->q.p, MV_PCG, P->sc.p,
+                    P->partials.p, P->halpha.p, st);
+      launch_pcg_update(n, P->x.p, pnew, P->r.p, P->q.p, P->sc.p, P->partials.p, P->hres.p, st);
+      if (pc)
+        precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p);
+      else
+        launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
+    }
+    MS_CUDA(cudaMemcpyAsync(&hs, P->sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    MS_CUDA(cudaStreamSynchronize(st));
+    done = hs.done;
+  }
+  MS_CUDA(cudaEventRecord(t1, st));
+  MS_CUDA(cudaMemcpyAsync(&hs, P->sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  store_free(P, P->x.p, x);
+  float ms = 0.f;
+  MS_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  const int iters = hs.iter;
+  if (residuals) MS_CUDA(cudaMemcpy(residuals, P->hres.p, (iters + 1) * sizeof(double), cudaMemcpyDefault));
+  if (alphas && iters > 0) MS_CUDA(cudaMemcpy(alphas, P->halpha.p, iters * sizeof(double), cudaMemcpyDefault));
+  if (betas && iters > 1) MS_CUDA(cudaMemcpy(betas, P->hbeta.p, (iters - 1) * sizeof(double), cudaMemcpyDefault));
+  if (rep) {
+    rep->iterations = iters;
+    rep->converged = hs.converged;
+    rep->final_residual = hs.res;
+    rep->t_solve = ms * 1e-3;
+    rep->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  }
+  MS_API_END(P ? P->ctx : nullptr)
+}
+
+}  // extern "C"

@@ -1,0 +1,691 @@
+// Coarse level of the EH+Rot preconditioner and the additive combine.
+//
+// Reference: coarse.py:58-168 (basis rows, K0, Cholesky, apply_inverse),
+// grid.py:172-207 (partition of unity), schwarz.py:76-84 (additive apply).
+// The basis is never materialised as a sparse R0: rows are rebuilt on the fly
+// from the stored eigenvectors psi, the partition-of-unity table chi and the
+// rotation formula, so one restriction/prolongation streams only psi.
+#include <algorithm>
+#include <vector>
+
+#include "coarse.cuh"
+
+namespace msgpu {
+
+// ---------------------------------------------------------------------------
+// partition of unity (grid.py:172-207), bit-exact: same IEEE operations in
+// the same order (no FMA contraction), hat sums accumulated in centre order.
+__device__ __forceinline__ double pou_raw(const CoarseDev& cd, int I, int J, int a, int b) {
+  const double x = __dmul_rn((double)a, cd.h), y = __dmul_rn((double)b, cd.h);
+  const double cx = __dmul_rn((double)(I * cd.mex), cd.h);
+  const double cy = __dmul_rn((double)(J * cd.mey), cd.h);
+  const double Hx = __dmul_rn((double)cd.mex, cd.h), Hy = __dmul_rn((double)cd.mey, cd.h);
+  const double tx = __dsub_rn(1.0, __ddiv_rn(fabs(__dsub_rn(x, cx)), Hx));
+  const double ty = __dsub_rn(1.0, __ddiv_rn(fabs(__dsub_rn(y, cy)), Hy));
+  return __dmul_rn(fmax(0.0, tx), fmax(0.0, ty));
+}
+
+__device__ __forceinline__ int center_index(const CoarseDev& cd, int I, int J) {
+  return (J - 1) * (cd.Nx - 1) + (I - 1);
+}
+
+__device__ __forceinline__ int local_node(const CoarseDev& cd, int I, int J, int a, int b) {
+  return (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
+}
+
+// rotation field [-(y - y_j), x - x_j] at node (a, b) (coarse.py:120-133), no FMA contraction
+__device__ __forceinline__ void rot_xy(const CoarseDev& cd, int I, int J, int a, int b, double& rx,
+                                       double& ry) {
+  const double x = __dmul_rn((double)a, cd.h), y = __dmul_rn((double)b, cd.h);
+  const double cx = __dmul_rn((double)(I * cd.mex), cd.h), cy = __dmul_rn((double)(J * cd.mey), cd.h);
+  rx = -__dsub_rn(y, cy);
+  ry = __dsub_rn(x, cx);
+}
+
+__global__ void k_pou_table(Grid g, CoarseDev cd, double* __restrict__ chi) {
+  const int k = blockIdx.x;
+  const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
+  const int NL = cd.NLx * cd.NLy;
+  for (int ln = threadIdx.x; ln < NL; ln += blockDim.x) {
+    const int a = (I - 1) * cd.mex + ln % cd.NLx, b = (J - 1) * cd.mey + ln / cd.NLx;
+    // centres whose closed neighbourhood contains (a, b), J-major
+    const int ilo = max(1, (a + cd.mex - 1) / cd.mex - 1), ihi = min(cd.Nx - 1, a / cd.mex + 1);
+    const int jlo = max(1, (b + cd.mey - 1) / cd.mey - 1), jhi = min(cd.Ny - 1, b / cd.mey + 1);
+    double total = 0.0;
+    for (int jj = jlo; jj <= jhi; ++jj)
+      for (int ii = ilo; ii <= ihi; ++ii) total = __dadd_rn(total, pou_raw(cd, ii, jj, a, b));
+    const double safe = total > 0.0 ? total : 1.0;
+    chi[(int64_t)k * NL + ln] = __ddiv_rn(pou_raw(cd, I, J, a, b), safe);
+  }
+}
+
+void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStream_t st) {
+  if (cd.n_centers == 0) return;
+  k_pou_table<<<cd.n_centers, 256, 0, st>>>(g, cd, chi);
+  MS_CUDA(cudaGetLastError());
+}
+
+// value of basis row `bi` of centre k at global node (a, b), component c.
+// bi < 2*nsel: heat mode bi/2 in slot bi%2; bi == 2*nsel: rotation.
+__device__ __forceinline__ double basis_value(const CoarseDev& cd, int k, int I, int J, int bi,
+                                              int nsel, int a, int b, int c) {
+  const int NL = cd.NLx * cd.NLy;
+  const int ln = local_node(cd, I, J, a, b);
+  const double chi = cd.chi[(int64_t)k * NL + ln];
+  if (bi < 2 * nsel) {
+    if ((bi & 1) != c) return 0.0;
+    return __dmul_rn(chi, cd.psi[cd.psioff[k] + (int64_t)(bi >> 1) * NL + ln]);
+  }
+  double rx, ry;
+  rot_xy(cd, I, J, a, b, rx, ry);
+  return __dmul_rn(chi, c == 0 ? rx : ry);
+}
+
+__device__ __forceinline__ int basis_row(const CoarseDev& cd, int k, int bi, int nsel) {
+  return bi < 2 * nsel ? cd.hoff[k] + bi : cd.roff + k;
+}
+
+// ---------------------------------------------------------------------------
+// f0 = R0 r, one CTA per centre, <= 13 rows per pass.
+constexpr int kNbChunk = 13;
+
+__global__ void __launch_bounds__(256)
+    k_restrict(Grid g, CoarseDev cd, const double* __restrict__ r, double* __restrict__ f0,
+               const int* done) {
+  if (done && *(volatile const int*)done) return;
+  __shared__ double sred[8];
+  const int k = blockIdx.x;
+  const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
+  const int nsel = cd.nsel[k];
+  const int nb = 2 * nsel + cd.enrich;
+  const int NL = cd.NLx * cd.NLy;
+  const double* chi = cd.chi + (int64_t)k * NL;
+  const double* psi = cd.psi + cd.psioff[k];
+  for (int b0 = 0; b0 < nb; b0 += kNbChunk) {
+    double acc[kNbChunk];
+#pragma unroll
+    for (int t = 0; t < kNbChunk; ++t) acc[t] = 0.0;
+    for (int ln = threadIdx.x; ln < NL; ln += blockDim.x) {
+      const int a = (I - 1) * cd.mex + ln % cd.NLx, b = (J - 1) * cd.mey + ln / cd.NLx;
+      const double ch = chi[ln];
+      if (ch == 0.0) continue;
+      const int64_t n = (int64_t)b * g.nnx + a;
+      const double rx = r[n], ry = r[n + g.n_nodes];
+#pragma unroll
+      for (int t = 0; t < kNbChunk; ++t) {
+        const int bi = b0 + t;
+        if (bi < 2 * nsel) {
+          const double v = ch * psi[(int64_t)(bi >> 1) * NL + ln];
+          acc[t] += v * ((bi & 1) ? ry : rx);
+        } else if (bi < nb) {
+          double ex, ey;
+          rot_xy(cd, I, J, a, b, ex, ey);
+          acc[t] += __dmul_rn(ch, ex) * rx + __dmul_rn(ch, ey) * ry;
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kNbChunk; ++t) {
+      const int bi = b0 + t;
+      const double s = block_sum(acc[t], sred);
+      if (bi < nb && threadIdx.x == 0) f0[basis_row(cd, k, bi, nsel)] = s;
+    }
+  }
+}
+
+void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double* f0,
+                     const int* done, cudaStream_t st) {
+  if (cd.n_centers == 0) return;
+  k_restrict<<<cd.n_centers, 256, 0, st>>>(g, cd, r, f0, done);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// combine: node-centric sum of the overlapping local solutions (in the
+// reference's J-major subdomain order, schwarz.py:79-81), then the coarse
+// prolongation; fused r.z reduction for PCG.
+__global__ void __launch_bounds__(256)
+    k_combine(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, int has_l1, CoarseDev cd,
+              int has_coarse, const double* __restrict__ y0, const double* __restrict__ r,
+              double* __restrict__ z, PcgScalars* sc, double* partials, double* beta_hist) {
+  if (sc && sc->done) return;
+  __shared__ double sred[8];
+  const int64_t nn = g.n_nodes;
+  double dot = 0.0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(n % g.nnx), b = (int)(n / g.nnx);
+    double zx = 0.0, zy = 0.0;
+    if (has_l1) {
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int J = l1.ycov[b * 4 + tj];
+        if (J < 0) break;
+#pragma unroll
+        for (int ti = 0; ti < 4; ++ti) {
+          const int I = l1.xcov[a * 4 + ti];
+          if (I < 0) break;
+          const BandSys s = l1.sys[J * l1.NbX + I];
+          const int ln = band_local_node(s, a, b);
+          const double* ys = l1.ybuf + s.yoff + 2 * ln;
+          zx += ys[0];
+          zy += ys[1];
+        }
+      }
+    }
+    if (has_coarse) {
+      double cxs = 0.0, cys = 0.0;
+      const int ilo = max(1, a / cd.mex), ihi = min(cd.Nx - 1, (a + cd.mex - 1) / cd.mex);
+      const int jlo = max(1, b / cd.mey), jhi = min(cd.Ny - 1, (b + cd.mey - 1) / cd.mey);
+      const int NL = cd.NLx * cd.NLy;
+      for (int J = jlo; J <= jhi; ++J)
+        for (int I = ilo; I <= ihi; ++I) {
+          if (abs(a - I * cd.mex) >= cd.mex || abs(b - J * cd.mey) >= cd.mey) continue;
+          const int k = center_index(cd, I, J);
+          const int ln = local_node(cd, I, J, a, b);
+          const double ch = cd.chi[(int64_t)k * NL + ln];
+          const int nsel = cd.nsel[k];
+          const double* ps = cd.psi + cd.psioff[k] + ln;
+          const int h0 = cd.hoff[k];
+          for (int m = 0; m < nsel; ++m) {
+            const double v = ch * ps[(int64_t)m * NL];
+            cxs += v * y0[h0 + 2 * m];
+            cys += v * y0[h0 + 2 * m + 1];
+          }
+          if (cd.enrich) {
+            double ex, ey;
+            rot_xy(cd, I, J, a, b, ex, ey);
+            const double yr = y0[cd.roff + k];
+            cxs += __dmul_rn(ch, ex) * yr;
+            cys += __dmul_rn(ch, ey) * yr;
+          }
+        }
+      zx += cxs;
+      zy += cys;
+    }
+    zx = mask[n] ? zx : 0.0;
+    zy = mask[n + nn] ? zy : 0.0;
+    z[n] = zx;
+    z[n + nn] = zy;
+    if (sc) dot += zx * r[n] + zy * r[n + nn];
+  }
+  if (!sc) return;
+  const double bs = block_sum(dot, sred);
+  double tot;
+  if (grid_reduce_last(bs, partials, &sc->tickets[2], &tot, sred)) {
+    if (threadIdx.x == 0) {
+      if (sc->first) {
+        sc->beta = 0.0;
+        sc->first = 0;
+      } else {
+        sc->beta = tot / sc->rz;
+        if (beta_hist) beta_hist[sc->iter - 1] = sc->beta;
+      }
+      sc->rz = tot;
+    }
+  }
+}
+
+void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
+                    const double* y0, const double* r, double* z, PcgScalars* sc,
+                    double* partials, double* beta_hist, cudaStream_t st) {
+  L1Dev l1v{};
+  CoarseDev cdv{};
+  if (l1) l1v = *l1;
+  if (cd) cdv = *cd;
+  const int blocks = std::min<int64_t>(148 * 8, div_up(g.n_nodes, 256));
+  k_combine<<<blocks, 256, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0, y0, r, z, sc,
+                                    partials, beta_hist);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// K0 = R0 A R0^T.  Persistent CTAs over centres; for each basis vector a of
+// centre k: v = Psi_a on closed omega_k, u = A v (matrix-free, elements of
+// omega_k only), then K0[b][a] = Psi_b . u for every basis b of the <= 9
+// centres whose neighbourhood overlaps omega_k.
+__global__ void __launch_bounds__(256)
+    k_k0_assemble(Grid g, KeParam ke, const double* __restrict__ E,
+                  const uint8_t* __restrict__ mask, CoarseDev cd, double* __restrict__ K0,
+                  double* __restrict__ scratch) {
+  __shared__ double sred[8];
+  const int NL = cd.NLx * cd.NLy;
+  double* v = scratch + (int64_t)blockIdx.x * 4 * NL;  // [2][NL]
+  double* u = v + 2 * NL;                              // [2][NL]
+  const int nex = 2 * cd.mex, ney = 2 * cd.mey;
+  for (int k = blockIdx.x; k < cd.n_centers; k += gridDim.x) {
+    const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
+    const int nsel = cd.nsel[k], nb = 2 * nsel + cd.enrich;
+    const int ax0 = (I - 1) * cd.mex, by0 = (J - 1) * cd.mey;
+    for (int ai = 0; ai < nb; ++ai) {
+      for (int ln = threadIdx.x; ln < NL; ln += blockDim.x) {
+        const int a = ax0 + ln % cd.NLx, b = by0 + ln / cd.NLx;
+        const int64_t n = (int64_t)b * g.nnx + a;
+        v[ln] = mask[n] ? basis_value(cd, k, I, J, ai, nsel, a, b, 0) : 0.0;
+        v[NL + ln] = mask[n + g.n_nodes] ? basis_value(cd, k, I, J, ai, nsel, a, b, 1) : 0.0;
+      }
+      __syncthreads();
+      for (int ln = threadIdx.x; ln < NL; ln += blockDim.x) {
+        const int la = ln % cd.NLx, lb = ln / cd.NLx;
+        double qx = 0.0, qy = 0.0;
+        const int exs[4] = {la - 1, la, la, la - 1};
+        const int eys[4] = {lb - 1, lb - 1, lb, lb};
+        const int cn[4] = {2, 3, 0, 1};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int ex = exs[e], ey = eys[e];
+          if (ex < 0 || ey < 0 || ex >= nex || ey >= ney) continue;
+          const double Ee = E[(int64_t)(by0 + ey) * g.nx + ax0 + ex];
+          const int c = cn[e];
+          const int l0 = ey * cd.NLx + ex;
+          const int lnm[4] = {l0, l0 + 1, l0 + cd.NLx + 1, l0 + cd.NLx};
+          double sx = 0.0, sy = 0.0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const double vx = v[lnm[m]], vy = v[NL + lnm[m]];
+            sx += ke.k[c * 8 + m] * vx + ke.k[c * 8 + 4 + m] * vy;
+            sy += ke.k[(4 + c) * 8 + m] * vx + ke.k[(4 + c) * 8 + 4 + m] * vy;
+          }
+          qx += Ee * sx;
+          qy += Ee * sy;
+        }
+        const int64_t n = (int64_t)(by0 + lb) * g.nnx + ax0 + la;
+        u[ln] = mask[n] ? qx : 0.0;
+        u[NL + ln] = mask[n + g.n_nodes] ? qy : 0.0;
+      }
+      __syncthreads();
+      const int col = basis_row(cd, k, ai, nsel);
+      for (int J2 = max(1, J - 1); J2 <= min(cd.Ny - 1, J + 1); ++J2)
+        for (int I2 = max(1, I - 1); I2 <= min(cd.Nx - 1, I + 1); ++I2) {
+          const int k2 = center_index(cd, I2, J2);
+          const int nsel2 = cd.nsel[k2], nb2 = 2 * nsel2 + cd.enrich;
+          // overlap of the closed neighbourhoods, in omega_k local coordinates
+          const int xa = max(ax0, (I2 - 1) * cd.mex), xb = min(ax0 + nex, (I2 + 1) * cd.mex);
+          const int ya = max(by0, (J2 - 1) * cd.mey), yb = min(by0 + ney, (J2 + 1) * cd.mey);
+          const int wx = xb - xa + 1, wy = yb - ya + 1;
+          for (int bi = 0; bi < nb2; ++bi) {
+            double acc = 0.0;
+            for (int t = threadIdx.x; t < wx * wy; t += blockDim.x) {
+              const int a = xa + t % wx, b = ya + t / wx;
+              const int ln = (a - ax0) + (b - by0) * cd.NLx;
+              acc += basis_value(cd, k2, I2, J2, bi, nsel2, a, b, 0) * u[ln] +
+                     basis_value(cd, k2, I2, J2, bi, nsel2, a, b, 1) * u[NL + ln];
+            }
+            const double s = block_sum(acc, sred);
+            if (threadIdx.x == 0) K0[(int64_t)basis_row(cd, k2, bi, nsel2) * cd.N_c + col] = s;
+          }
+        }
+      __syncthreads();
+    }
+  }
+}
+
+void launch_k0_assemble(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
+                        const CoarseDev& cd, double* K0, double* scratch, int n_cta,
+                        cudaStream_t st) {
+  if (cd.n_centers == 0) return;
+  k_k0_assemble<<<n_cta, 256, 0, st>>>(g, ke, E, mask, cd, K0, scratch);
+  MS_CUDA(cudaGetLastError());
+}
+
+__global__ void k_symmetrize(int N, double* A) {
+  const int64_t total = (int64_t)N * N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / N), j = (int)(t % N);
+    if (j >= i) continue;
+    const double v = 0.5 * (A[(int64_t)i * N + j] + A[(int64_t)j * N + i]);
+    A[(int64_t)i * N + j] = v;
+    A[(int64_t)j * N + i] = v;
+  }
+}
+
+void launch_symmetrize(int N, double* A, cudaStream_t st) {
+  if (N == 0) return;
+  k_symmetrize<<<148 * 4, 256, 0, st>>>(N, A);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Dense SPD inverse by tiled Cholesky (potrf), triangular inverse (trtri) and
+// L^-T L^-1 (lauum), all on packed 64x64 lower tiles.  Replaces LAPACK
+// ?potrf/?potrs (coarse.py:143,154): applying the explicit packed inverse is
+// one bandwidth-bound SYMV per PCG iteration instead of two latency-bound
+// triangular sweeps.
+constexpr int T = kTile;
+constexpr int kTT = 256;  // threads per tile CTA (16 x 16, 4 x 4 outputs each)
+
+struct TileAcc {
+  double v[4][4];
+};
+
+// acc += sA * sB where sA[r][q], sB[q][c] are 64x64 row-major in smem
+__device__ __forceinline__ void tile_mma(TileAcc& acc, const double* sA, const double* sB) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll 4
+  for (int q = 0; q < T; ++q) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = sA[(ty + 16 * i) * T + q];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = sB[q * T + tx + 16 * j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc.v[i][j] += a[i] * b[j];
+  }
+}
+
+// load a 64x64 tile (row-major, contiguous) into smem, optionally transposed
+__device__ __forceinline__ void tile_load(double* s, const double* g, bool trans) {
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
+    const int r = t / T, c = t % T;
+    if (trans)
+      s[c * T + r] = g[t];
+    else
+      s[t] = g[t];
+  }
+}
+
+__device__ __forceinline__ void acc_zero(TileAcc& a) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a.v[i][j] = 0.0;
+}
+
+__device__ __forceinline__ void acc_store(const TileAcc& a, double* g, double scale, bool add) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = (ty + 16 * i) * T + tx + 16 * j;
+      g[idx] = add ? g[idx] + scale * a.v[i][j] : scale * a.v[i][j];
+    }
+}
+
+__global__ void k_pack_tiles(int N, int nt, const double* __restrict__ A, double* __restrict__ P) {
+  const int64_t total = packed_tiles(nt) * T * T;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = t / (T * T);
+    const int within = (int)(t % (T * T));
+    // invert tile index -> (i, j)
+    int i = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(i + 1) * (i + 2) / 2 <= tile) ++i;
+    while ((int64_t)i * (i + 1) / 2 > tile) --i;
+    const int j = (int)(tile - (int64_t)i * (i + 1) / 2);
+    const int r = i * T + within / T, c = j * T + within % T;
+    double v;
+    if (r < N && c < N)
+      v = A[(int64_t)r * N + c];
+    else
+      v = (r == c) ? 1.0 : 0.0;
+    P[t] = v;
+  }
+}
+
+// Cholesky of diagonal tile k in place (lower), plus its triangular inverse
+// written to Winv (tile k,k of the trtri array).
+__global__ void __launch_bounds__(kTT) k_potrf_tile(int k, int N, double* __restrict__ P,
+                                                    double* __restrict__ W, int* fail) {
+  extern __shared__ double sm[];
+  double* a = sm;          // 64 x 64
+  double* inv = sm + T * T;
+  double* D = P + tile_index(k, k) * T * T;
+  tile_load(a, D, false);
+  __syncthreads();
+  for (int c = 0; c < T; ++c) {
+    double d = a[c * T + c];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) atomicCAS(fail, 0, k * T + c + 1);
+      d = 1.0;
+    }
+    const double s = sqrt(d);
+    __syncthreads();
+    if (threadIdx.x == 0) a[c * T + c] = s;
+    for (int r = c + 1 + threadIdx.x; r < T; r += blockDim.x) a[r * T + c] /= s;
+    __syncthreads();
+    for (int t = threadIdx.x; t < (T - c - 1) * (T - c - 1); t += blockDim.x) {
+      const int r = c + 1 + t / (T - c - 1), q = c + 1 + t % (T - c - 1);
+      if (q <= r) a[r * T + q] -= a[r * T + c] * a[q * T + c];
+    }
+    __syncthreads();
+  }
+  // zero the strict upper triangle, write L back
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
+    const int r = t / T, c = t % T;
+    if (c > r) a[t] = 0.0;
+    D[t] = a[t];
+  }
+  __syncthreads();
+  // inverse of lower-triangular L: column j solves L x = e_j by forward
+  // substitution; thread j owns column j (64 columns).
+  if (threadIdx.x < T) {
+    const int j = threadIdx.x;
+    for (int r = 0; r < T; ++r) {
+      double s = (r == j) ? 1.0 : 0.0;
+      for (int q = j; q < r; ++q) s -= a[r * T + q] * inv[q * T + j];
+      inv[r * T + j] = (r < j) ? 0.0 : s / a[r * T + r];
+    }
+  }
+  __syncthreads();
+  double* Wk = W + tile_index(k, k) * T * T;
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) Wk[t] = inv[t];
+}
+
+// panel: L_ik = A_ik L_kk^-T = A_ik (Winv_kk)^T, i > k
+__global__ void __launch_bounds__(kTT) k_trsm_tiles(int k, int nt, double* __restrict__ P,
+                                                    const double* __restrict__ W) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  const int i = k + 1 + blockIdx.x;
+  double* Aik = P + tile_index(i, k) * T * T;
+  tile_load(sA, Aik, false);
+  tile_load(sB, W + tile_index(k, k) * T * T, true);  // sB[q][c] = Winv[c][q]
+  __syncthreads();
+  TileAcc acc;
+  acc_zero(acc);
+  tile_mma(acc, sA, sB);
+  __syncthreads();
+  acc_store(acc, Aik, 1.0, false);
+}
+
+// trailing update A_ij -= L_ik L_jk^T for k < j <= i
+__global__ void __launch_bounds__(kTT) k_syrk_tiles(int k, int nt, double* __restrict__ P) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  // blockIdx.x enumerates (i, j) pairs with k < j <= i < nt
+  const int m = nt - k - 1;
+  int64_t t = blockIdx.x;
+  int ii = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(ii + 1) * (ii + 2) / 2 <= t) ++ii;
+  while ((int64_t)ii * (ii + 1) / 2 > t) --ii;
+  const int jj = (int)(t - (int64_t)ii * (ii + 1) / 2);
+  if (ii >= m) return;
+  const int i = k + 1 + ii, j = k + 1 + jj;
+  tile_load(sA, P + tile_index(i, k) * T * T, false);
+  tile_load(sB, P + tile_index(j, k) * T * T, true);
+  __syncthreads();
+  TileAcc acc;
+  acc_zero(acc);
+  tile_mma(acc, sA, sB);
+  acc_store(acc, P + tile_index(i, j) * T * T, -1.0, true);
+}
+
+// W_ij = -W_ii * sum_{l=j}^{i-1} L_il W_lj for i = j + d
+__global__ void __launch_bounds__(kTT) k_trtri_tiles(int d, int nt, const double* __restrict__ P,
+                                                     double* __restrict__ W) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  const int j = blockIdx.x, i = j + d;
+  TileAcc acc;
+  acc_zero(acc);
+  for (int l = j; l < i; ++l) {
+    __syncthreads();
+    tile_load(sA, P + tile_index(i, l) * T * T, false);
+    tile_load(sB, W + tile_index(l, j) * T * T, false);
+    __syncthreads();
+    tile_mma(acc, sA, sB);
+  }
+  __syncthreads();
+  // sB <- acc, sA <- W_ii ; result = -(W_ii acc)
+  {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) sB[(ty + 16 * a) * T + tx + 16 * b] = acc.v[a][b];
+  }
+  tile_load(sA, W + tile_index(i, i) * T * T, false);
+  __syncthreads();
+  TileAcc out;
+  acc_zero(out);
+  tile_mma(out, sA, sB);
+  acc_store(out, W + tile_index(i, j) * T * T, -1.0, false);
+}
+
+// X_ij = sum_{l >= i} W_li^T W_lj  (i >= j) = (L^-T L^-1)_ij
+__global__ void __launch_bounds__(kTT) k_lauum_tiles(int nt, const double* __restrict__ W,
+                                                     double* __restrict__ X) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  const int64_t t = blockIdx.x;
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
+  while ((int64_t)i * (i + 1) / 2 > t) --i;
+  const int j = (int)(t - (int64_t)i * (i + 1) / 2);
+  TileAcc acc;
+  acc_zero(acc);
+  for (int l = i; l < nt; ++l) {
+    __syncthreads();
+    tile_load(sA, W + tile_index(l, i) * T * T, true);  // sA[r][q] = W_li[q][r]
+    tile_load(sB, W + tile_index(l, j) * T * T, false);
+    __syncthreads();
+    tile_mma(acc, sA, sB);
+  }
+  acc_store(acc, X + tile_index(i, j) * T * T, 1.0, false);
+}
+
+size_t dense_spd_inverse_work_bytes(int N) {
+  const int nt = div_up(N, T);
+  return (size_t)packed_tiles(nt) * T * T * sizeof(double) * 2;
+}
+
+void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work, int* fail,
+                       cudaStream_t st) {
+  if (N == 0) return;
+  const int nt = div_up(N, T);
+  const int64_t ptiles = packed_tiles(nt);
+  double* P = work;                      // Cholesky factor tiles
+  double* W = work + ptiles * T * T;     // L^-1 tiles
+  const size_t smem = 2 * T * T * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    MS_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_trsm_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_trtri_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_lauum_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, P);
+  MS_CUDA(cudaMemsetAsync(W, 0, ptiles * T * T * sizeof(double), st));
+  for (int k = 0; k < nt; ++k) {
+    k_potrf_tile<<<1, kTT, smem, st>>>(k, N, P, W, fail);
+    const int m = nt - k - 1;
+    if (m > 0) {
+      k_trsm_tiles<<<m, kTT, smem, st>>>(k, nt, P, W);
+      k_syrk_tiles<<<(unsigned)((int64_t)m * (m + 1) / 2), kTT, smem, st>>>(k, nt, P);
+    }
+  }
+  for (int d = 1; d < nt; ++d) k_trtri_tiles<<<nt - d, kTT, smem, st>>>(d, nt, P, W);
+  k_lauum_tiles<<<(unsigned)ptiles, kTT, smem, st>>>(nt, W, packed_inv);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// packed-tile SYMV: per tile, u = X_IJ f_J (-> y_I) and, off the diagonal,
+// v = X_IJ^T f_I (-> y_J); partials are reduced in a fixed order.
+__global__ void __launch_bounds__(256)
+    k_symv_tiles(int N, int nt, const double* __restrict__ X, const double* __restrict__ f,
+                 double* __restrict__ part, const int* done) {
+  if (done && *(volatile const int*)done) return;
+  __shared__ double sv[16][T + 1];
+  const int64_t t = blockIdx.x;
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
+  while ((int64_t)i * (i + 1) / 2 > t) --i;
+  const int j = (int)(t - (int64_t)i * (i + 1) / 2);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const double* Xt = X + t * T * T;
+  double fj[4], fi[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int cj = j * T + tx * 4 + q, ri = i * T + ty * 4 + q;
+    fj[q] = cj < N ? f[cj] : 0.0;
+    fi[q] = ri < N ? f[ri] : 0.0;
+  }
+  double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
+    const double2 x01 = __ldg(row), x23 = __ldg(row + 1);
+    u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
+    v[0] += x01.x * fi[rr];
+    v[1] += x01.y * fi[rr];
+    v[2] += x23.x * fi[rr];
+    v[3] += x23.y * fi[rr];
+  }
+  // u: reduce over tx (16 lanes of a half warp)
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
+  }
+  double* pu = part + t * 2 * T;
+  double* pv = pu + T;
+  if (tx == 0) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) pu[ty * 4 + rr] = u[rr];
+  }
+  if (i != j) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[ty][tx * 4 + q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < T) {
+      double s = 0.0;
+#pragma unroll
+      for (int g = 0; g < 16; ++g) s += sv[g][threadIdx.x];
+      pv[threadIdx.x] = s;
+    }
+  }
+}
+
+__global__ void k_symv_reduce(int N, int nt, const double* __restrict__ part, double* __restrict__ y,
+                              const int* done) {
+  if (done && *(volatile const int*)done) return;
+  const int I = blockIdx.x, r = threadIdx.x;
+  const int row = I * T + r;
+  if (row >= N) return;
+  double s = 0.0;
+  for (int J = 0; J <= I; ++J) s += part[tile_index(I, J) * 2 * T + r];
+  for (int I2 = I + 1; I2 < nt; ++I2) s += part[tile_index(I2, I) * 2 * T + T + r];
+  y[row] = s;
+}
+
+void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
+                        const int* done, cudaStream_t st) {
+  if (N == 0) return;
+  const int nt = div_up(N, T);
+  k_symv_tiles<<<(unsigned)packed_tiles(nt), 256, 0, st>>>(N, nt, X, f, part, done);
+  k_symv_reduce<<<nt, T, 0, st>>>(N, nt, part, y, done);
+  MS_CUDA(cudaGetLastError());
+}
+
+}  // namespace msgpu

@@ -1,0 +1,74 @@
+// Coarse level (spectral EH+Rot space) and the preconditioner combine step.
+#pragma once
+
+#include "banded.cuh"
+#include "common.cuh"
+#include "operator.cuh"
+
+namespace msgpu {
+
+// Level-1 geometry for the node-centric combine: subdomain (I, J) has kept
+// node range [xlo[I], xlo[I]+xlen[I]-1] x [ylo[J], ...]; the covering lists
+// give, per node column a (row b), up to 4 block indices I (J), ascending,
+// -1 padded.  Subdomain s = J*NbX + I.
+struct L1Dev {
+  int NbX, NbY;
+  const BandSys* sys;
+  const int* xcov;  // (nx+1) * 4
+  const int* ycov;  // (ny+1) * 4
+  const double* ybuf;
+};
+
+// Coarse space on device.  Centre k = (I, J), 1 <= I < Nx, 1 <= J < Ny,
+// k = (J-1)*(Nx-1) + (I-1) (the reference's neighbourhood order, grid.py:132).
+struct CoarseDev {
+  int Nx, Ny, mex, mey;
+  int NLx, NLy;           // closed-omega nodes per axis: 2*mex+1, 2*mey+1
+  int n_centers;
+  int enrich;
+  int N_c;
+  int roff;               // first rotation row = 2 * sum(nsel)
+  double h;
+  const int* nsel;        // per centre
+  const int* hoff;        // per centre: first heat row (2 * prefix sum of nsel)
+  const int64_t* psioff;  // per centre: offset into psi (nsel * NL values)
+  const double* psi;      // selected eigenvectors on closed omega, lexicographic
+  const double* chi;      // per centre: partition of unity on closed omega (NL values)
+};
+
+// chi table, bit-identical to the reference's PoU (grid.py:172-207)
+void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStream_t st);
+
+// f0 = R0 r (coarse.py:156-158, restriction half)
+void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double* f0,
+                     const int* done, cudaStream_t st);
+
+// z = sum_s R_s^T y_s (level-1, J-major order) + R0^T y0 (if cd) ; masked;
+// optionally r.z -> beta (PCG mode when sc != nullptr).
+void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
+                    const double* y0, const double* r, double* z, PcgScalars* sc,
+                    double* partials, double* beta_hist, cudaStream_t st);
+
+// K0 = R0 A R0^T (dense row-major N_c x N_c), symmetrised (coarse.py:161-168)
+void launch_k0_assemble(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
+                        const CoarseDev& cd, double* K0, double* scratch, int n_cta,
+                        cudaStream_t st);
+void launch_symmetrize(int N, double* A, cudaStream_t st);
+
+// ---- dense SPD inverse in packed 64x64 tiles ------------------------------
+constexpr int kTile = 64;
+__host__ __device__ inline int64_t packed_tiles(int nt) { return (int64_t)nt * (nt + 1) / 2; }
+__host__ __device__ inline int64_t tile_index(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
+
+// A (row-major N x N, lower triangle read) -> packed-tile lower inverse.
+// Returns (via *fail) 1 + the failing pivot row on a non-positive pivot.
+void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work, int* fail,
+                       cudaStream_t st);
+size_t dense_spd_inverse_work_bytes(int N);
+
+// y = X f for X symmetric stored as packed lower tiles.  `part` needs
+// packed_tiles(nt) * 2 * kTile doubles.
+void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
+                        const int* done, cudaStream_t st);
+
+}  // namespace msgpu

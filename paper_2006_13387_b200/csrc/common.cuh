@@ -1,0 +1,94 @@
+// Shared device helpers for the msgpu kernels (sm_100a, fp64 throughout).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace msgpu {
+
+// Host-side error type carrying an ABI status code.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define MS_CUDA(call)                                                                 \
+  do {                                                                                \
+    cudaError_t err__ = (call);                                                       \
+    if (err__ != cudaSuccess)                                                         \
+      throw ::msgpu::Error(-3, std::string(#call ": ") + cudaGetErrorString(err__) + \
+                                   " @" __FILE__ ":" + std::to_string(__LINE__));     \
+  } while (0)
+
+constexpr int kWarp = 32;
+constexpr int kReduceThreads = 256;
+
+// Structured-grid description shared by every kernel.
+struct Grid {
+  int nx, ny;      // elements per axis
+  int nnx;         // nodes per row = nx + 1
+  int64_t n_nodes; // (nx+1)(ny+1); full vector = [x-plane | y-plane]
+  double h;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree).  `sh` needs blockDim.x/32 doubles.
+// Result valid in all threads.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < nw ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+// "Last block finishes" deterministic grid reduction: every block writes its
+// partial; the last one to arrive (atomic ticket) sums all partials in index
+// order.  Returns true in the finishing block (all threads), with *out set.
+__device__ __forceinline__ bool grid_reduce_last(double blockval, double* partials,
+                                                 unsigned int* ticket, double* out,
+                                                 double* sh) {
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x + gridDim.x * blockIdx.y] = blockval;
+    __threadfence();
+    unsigned int nb = gridDim.x * gridDim.y;
+    unsigned int t = atomicAdd(ticket, 1u);
+    am_last = (t == nb - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  const unsigned int nb = gridDim.x * gridDim.y;
+  // fixed order: thread i sums partials i, i+T, ...; then block tree
+  double s = 0.0;
+  for (unsigned int i = threadIdx.x; i < nb; i += blockDim.x) s += ((volatile double*)partials)[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) {
+    *out = s;
+    *ticket = 0u;  // re-arm for the next launch
+  }
+  return true;
+}
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace msgpu

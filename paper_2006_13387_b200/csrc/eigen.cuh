@@ -1,0 +1,48 @@
+// Batched local heat eigensolves for the spectral coarse space.
+#pragma once
+
+#include "banded.cuh"
+#include "common.cuh"
+
+namespace msgpu {
+
+constexpr int kEigBlock = 16;  // subspace block size p
+constexpr int kNeig = 7;       // eigenpairs kept per centre: min(n_max+1, dim), n_max = 6
+
+struct HeatParam {
+  double lap[16];  // unit Q1 Laplacian element (assembly.py:133-140)
+  double mel[16];  // Q1 mass element for side h (assembly.py:143-147)
+};
+
+struct EigBatch {
+  int Nx, mex, mey;    // centre (I, J) geometry
+  int k0, nk;          // first centre and number of centres in this batch
+  const BandSys* sys;  // heat band systems of the batch (index = centre - k0)
+  const double* Lc;
+  const double* Lr;
+  double* work;        // per centre: 2 * p * NL doubles
+  double* evals;       // global: centre * kNeig (ascending)
+  double* evecs;       // batch: (centre - k0) * kNeig * NL, band order, M-orthonormal
+  int* passes;         // global: per centre
+  int* neumann;        // global: per centre (1 if no heat-Dirichlet node in omega)
+};
+
+// B = K_H + sigma M_H in band form (Dirichlet nodes -> identity rows)
+void launch_heat_assemble(const Grid& g, const double* E, const uint8_t* hdir,
+                          const HeatParam& hp, double sigma, const BandSys* sys, int nsys,
+                          double* Lc, cudaStream_t st);
+
+// shift-invert block subspace iteration with Jacobi Rayleigh-Ritz, one CTA per centre
+void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
+                     const EigBatch& b, int max_pass, double tol, cudaStream_t st);
+
+// gap / fixed selection on device (spectral.py:161-186)
+void launch_select(int n_centers, const double* evals, int n_max, double threshold, int fixed,
+                   int* nsel, cudaStream_t st);
+
+// copy the selected vectors of a batch into the compact psi store (lexicographic
+// closed-omega node order), sign-normalised: largest-|.| entry positive.
+void launch_compact_psi(const EigBatch& b, int NLx, const int* nsel, const int64_t* psioff,
+                        double* psi, cudaStream_t st);
+
+}  // namespace msgpu

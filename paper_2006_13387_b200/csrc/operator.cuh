@@ -1,0 +1,60 @@
+// Matrix-free Q1 elasticity operator and fused PCG vector kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace msgpu {
+
+// Device-resident PCG scalars: the whole loop runs without host round trips;
+// the host polls `done` every few iterations.
+struct PcgScalars {
+  double rz;       // r.z of the current iterate
+  double pq;       // p.q
+  double alpha, beta;
+  double rr;       // ||r||^2
+  double bnorm;    // ||b||
+  double tol;
+  double res;      // ||r||/||b||
+  int iter;        // iterations completed
+  int maxit;
+  int done;
+  int converged;
+  int first;       // next z.r reduction starts the recurrence (beta = 0)
+  int pad;
+  unsigned int tickets[8];
+};
+
+// Element stiffness of the unit modulus Q1 plane-stress element, passed by
+// value (kernel parameter space is a broadcast constant bank).
+struct KeParam {
+  double k[64];
+};
+
+constexpr int MV_TX = 32;  // nodes per CTA in x
+constexpr int MV_TY = 8;   // nodes per CTA in y (one node per thread)
+
+enum { MV_PLAIN = 0, MV_PCG = 1 };
+
+void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
+                   const double* z, const double* p_old, double* p_new, double* q, int mode,
+                   PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st);
+
+void launch_pcg_update(int64_t n, double* x, const double* p, double* r, const double* q,
+                       PcgScalars* sc, double* partials, double* res_hist, cudaStream_t st);
+
+// rz reduction -> beta (first call of a solve sets rz and beta = 0)
+void launch_rz(int64_t n, const double* r, const double* z, PcgScalars* sc, double* partials,
+               double* beta_hist, cudaStream_t st);
+
+// sc->bnorm = ||b||, sc->res = 1, history[0] = 1
+void launch_init_norm(int64_t n, const double* b, PcgScalars* sc, double* partials,
+                      double* res_hist, cudaStream_t st);
+
+void launch_scatter_free(int64_t n_free, const int64_t* free_dofs, const double* src_free,
+                         double* dst_full, cudaStream_t st);
+void launch_gather_free(int64_t n_free, const int64_t* free_dofs, const double* src_full,
+                        double* dst_free, cudaStream_t st);
+
+int reduce_blocks();
+
+}  // namespace msgpu

@@ -1,0 +1,183 @@
+"""Two-level additive Schwarz preconditioner on the GPU (reference schwarz.py).
+
+``build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts)``
+keeps the reference signature (schwarz.py:176-211).  The GPU path implements
+the EH and EH+Rot variants (elasticity level 1, heat-eigenproblem coarse
+space, gap rule); the other Table-1 tags are listed for API parity and raise
+``NotImplementedError`` (SURVEY.md §8(f) ranks them "next").
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .assembly import ElasticityOperator
+
+
+@dataclass(frozen=True)
+class PreconditionerVariant:
+    tag: str
+    level1: str
+    eig_kind: str | None
+    randomized: bool
+    enrich: bool
+
+
+VARIANTS = {
+    v.tag: v
+    for v in [
+        PreconditionerVariant("EE", "elasticity", "elasticity", False, False),
+        PreconditionerVariant("EE;Rand", "elasticity", "elasticity", True, False),
+        PreconditionerVariant("HH", "heat", "heat", False, False),
+        PreconditionerVariant("HH+Rot", "heat", "heat", False, True),
+        PreconditionerVariant("EH", "elasticity", "heat", False, False),
+        PreconditionerVariant("EH+Rot", "elasticity", "heat", False, True),
+        PreconditionerVariant("EH+Rot;Rand", "elasticity", "heat", True, True),
+    ]
+}
+GPU_VARIANTS = ("EH", "EH+Rot")
+
+
+def get_variant(tag):
+    try:
+        return VARIANTS[tag]
+    except KeyError:
+        raise ValueError(f"unknown preconditioner variant {tag!r}; choose from {sorted(VARIANTS)}") from None
+
+
+@dataclass
+class EigOptions:
+    """schwarz.py:54-59"""
+
+    n_max: int = 6
+    rule: str | None = None  # None -> 'gap' for heat
+    n_snapshots: int | None = None
+    seed: int = 0
+
+
+class IdentityPreconditioner:
+    """The 'None' variant: plain CG."""
+
+    coarse_dim = 0
+    info = {}
+
+    def apply(self, r):
+        return r
+
+
+class TwoLevelPreconditioner:
+    """GPU-resident level-1 band factors + spectral coarse space + K0^-1."""
+
+    def __init__(self, variant, op, handle, info):
+        self.variant = variant
+        self.op = op
+        self.handle = handle
+        self.n_free = op.n_free
+        self.info = info
+
+    @property
+    def coarse_dim(self):
+        return self.info["coarse_dim"]
+
+    @property
+    def mode_counts(self):
+        return self.info["mode_counts"]
+
+    def _call(self, fn, r):
+        if r.shape[0] != self.n_free:
+            raise ValueError("residual dimension mismatch")
+        rp, keep, dev = _lib.vec_ptr(r)
+        if dev:
+            import torch
+
+            z = torch.empty_like(keep)
+            zp = C.c_void_p(z.data_ptr())
+        else:
+            z = np.empty(self.n_free)
+            zp = C.c_void_p(z.ctypes.data)
+        _lib.check(fn(self.handle, rp, zp), self.op._ctx.handle)
+        return z
+
+    def apply(self, r):
+        """z = sum_i R_i^T K_i^-1 R_i r + R0^T K0^-1 R0 r (schwarz.py:76-84)."""
+        return self._call(_lib.load().ms_precond_apply, r)
+
+    def apply_coarse(self, r):
+        """R0^T K0^-1 R0 r (CoarseOperator.apply_inverse, coarse.py:156-158)."""
+        return self._call(_lib.load().ms_precond_apply_coarse, r)
+
+    def coarse_matrix(self):
+        N = self.coarse_dim
+        K0 = np.empty((N, N))
+        _lib.check(_lib.load().ms_precond_coarse_matrix(self.handle, _lib.dptr(K0)), self.op._ctx.handle)
+        return K0
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().ms_precond_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None, *,
+                         level1="neighborhoods", delta=None, use_coarse=True):
+    """Build a two-level preconditioner by variant name (schwarz.py:176-211).
+
+    level1='neighborhoods' is the reference's layout (subdomains = omega_j);
+    level1='blocks' uses delta-extended coarse blocks (the BASELINE configs).
+    ``dirichlet_nodes`` are the whole nodes clamped in the heat eigenproblems.
+    """
+    if tag == "None":
+        return IdentityPreconditioner()
+    variant = get_variant(tag)
+    if tag not in GPU_VARIANTS:
+        raise NotImplementedError(f"variant {tag!r} is not on the GPU path (supported: {GPU_VARIANTS})")
+    if not isinstance(op, ElasticityOperator):
+        raise TypeError("build_preconditioner needs the GPU ElasticityOperator from assemble_elasticity")
+    opts = opts or EigOptions()
+    rule = opts.rule or "gap"
+    if rule not in ("gap", "fixed"):
+        raise ValueError(f"unknown selection rule {rule!r}")
+    hd = np.ascontiguousarray(np.asarray(dirichlet_nodes, dtype=np.int64).ravel())
+    o = _lib.PrecondOpts()
+    o.Nx, o.Ny = part.Nx, part.Ny
+    if level1 == "neighborhoods":
+        o.level1_kind, o.delta = _lib.MS_LEVEL1_NEIGHBORHOODS, 0
+    elif level1 == "blocks":
+        if delta is None:
+            raise ValueError("level1='blocks' needs the overlap delta")
+        o.level1_kind, o.delta = _lib.MS_LEVEL1_BLOCKS, int(delta)
+    else:
+        raise ValueError(f"unknown level-1 layout {level1!r}")
+    o.n_max = int(opts.n_max)
+    o.gap_threshold = 50.0
+    o.enrich = 1 if variant.enrich else 0
+    o.fixed_rule = 1 if rule == "fixed" else 0
+    o.local_solver = _lib.MS_LOCAL_BANDED
+    o.use_coarse = 1 if use_coarse else 0
+    o.heat_dirichlet_nodes = hd.ctypes.data_as(C.POINTER(C.c_int64)) if hd.size else None
+    o.n_heat_dirichlet = hd.size
+    lib = _lib.load()
+    h = C.c_void_p()
+    _lib.check(lib.ms_precond_build(op.handle, C.byref(o), C.byref(h)), op._ctx.handle)
+    inf = _lib.PrecondInfo()
+    nc = (part.Nx - 1) * (part.Ny - 1) if use_coarse else 0
+    counts = np.zeros(max(nc, 1), dtype=np.int32)
+    evals = np.full((max(nc, 1), 7), np.nan)
+    _lib.check(lib.ms_precond_info_get(h, C.byref(inf), _lib.iptr(counts), _lib.dptr(evals)))
+    info = {
+        "t_level1": inf.t_level1, "t_coarse": inf.t_coarse, "t_eig": inf.t_eig,
+        "coarse_dim": inf.coarse_dim, "mode_counts": [int(c) for c in counts[:nc]],
+        "basis_kind": "H+Rot" if variant.enrich else "H", "selection_rule": rule,
+        "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
+        "max_eig_passes": inf.max_eig_passes, "local_bytes": inf.local_bytes,
+        "coarse_bytes": inf.coarse_bytes, "level1": level1, "delta": delta,
+    }
+    return TwoLevelPreconditioner(variant, op, h, info)

@@ -1,0 +1,221 @@
+"""CUDA path vs the CPU oracle and the reference's golden fixtures (B200 only).
+
+Tolerances (BASELINE.json north_star): coarse dimension and per-centre mode
+counts bit-exact; PCG iterations within max(+-1, the reference's own jitter
+band recorded in the fixture); solution relative l2 <= 1e-8 (or the
+fixture's jitter noise floor x10 when that is larger).  Operator apply: fp64
+round-off (<= 1e-13 relative).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import mselast_oracle as O
+from paper_2006_13387_b200 import configs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2006_13387_b200 as G  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def gpu_problem(nx, ny, E, nu, free):
+    mesh = G.build_fine_mesh(nx, ny)
+    coeff = G.CoefficientField(E, nu, float(np.min(E)), float(np.max(E)))
+    return mesh, coeff, G.ElasticityOperator(mesh, coeff, free)
+
+
+def spec_from_golden(g):
+    return configs.ProblemSpec(
+        name="golden", nx=int(g["nx"]), ny=int(g["ny"]), E=g["E"], E_min=float(g["E"].min()),
+        E_max=1.0, constrained_dofs=g["constrained_dofs"],
+        heat_dirichlet_nodes=g["heat_dirichlet_nodes"], load_full=g["load_full"],
+        H=int(g["H"]), delta=int(g["delta"]), nu=float(g["nu"]))
+
+
+# ---------------------------------------------------------------------------
+# operator
+
+
+@pytest.mark.parametrize("nx,ny,kind", [(64, 64, "cantilever"), (48, 32, "mbb"), (20, 20, "clamped"), (7, 5, "clamped")])
+def test_operator_matches_csr(nx, ny, kind, rng):
+    E = rng.uniform(1e-3, 1.0, nx * ny)
+    mesh_o = O.mesh_for(nx, ny)
+    if kind == "cantilever":
+        cons, _, _ = configs.cantilever_bcs(nx, ny)
+    elif kind == "mbb":
+        cons, _, _ = configs.mbb_bcs(nx, ny)
+    else:
+        jj, ii = np.divmod(np.arange(mesh_o.n_nodes), nx + 1)
+        nodes = np.nonzero((ii == 0) | (ii == nx) | (jj == 0) | (jj == ny))[0]
+        cons = O.whole_node_dofs(mesh_o, nodes)
+    op_o = O.elasticity_operator(mesh_o, E, 0.3, cons)
+    _, _, op = gpu_problem(nx, ny, E, 0.3, op_o.free_dofs)
+    for _ in range(3):
+        p = rng.standard_normal(op_o.n_free)
+        assert rel(op @ p, op_o.matrix @ p) <= 1e-13
+
+
+def test_operator_accepts_cuda_tensors(rng):
+    nx = 16
+    E = rng.uniform(0.1, 1.0, nx * nx)
+    mesh_o = O.mesh_for(nx, nx)
+    cons, _, _ = configs.cantilever_bcs(nx, nx)
+    op_o = O.elasticity_operator(mesh_o, E, 0.3, cons)
+    _, _, op = gpu_problem(nx, nx, E, 0.3, op_o.free_dofs)
+    p = rng.standard_normal(op_o.n_free)
+    q = op @ torch.tensor(p, device="cuda")
+    assert q.is_cuda and rel(q.cpu().numpy(), op_o.matrix @ p) <= 1e-13
+
+
+# ---------------------------------------------------------------------------
+# plain CG
+
+
+def test_unpreconditioned_cg_matches_oracle(rng):
+    nx = 24
+    E = rng.uniform(0.2, 1.0, nx * nx)
+    mesh_o = O.mesh_for(nx, nx)
+    cons, _, load = configs.cantilever_bcs(nx, nx)
+    op_o = O.elasticity_operator(mesh_o, E, 0.3, cons)
+    b = rng.standard_normal(op_o.n_free)
+    x_o, rep_o = O.pcg(op_o.matrix, b, None, tol=1e-8, maxit=5000)
+    _, _, op = gpu_problem(nx, nx, E, 0.3, op_o.free_dofs)
+    x, rep = G.pcg_solve(op, b, None, tol=1e-8, maxit=5000)
+    assert rep.converged and abs(rep.iterations - rep_o.iterations) <= 2
+    assert rel(x, x_o) <= 1e-8
+    assert np.allclose(rep.residuals[:20], rep_o.residuals[:20], rtol=1e-8)
+
+
+def test_maxit_reports_unconverged(rng):
+    nx = 16
+    E = np.ones(nx * nx)
+    mesh_o = O.mesh_for(nx, nx)
+    cons, _, _ = configs.cantilever_bcs(nx, nx)
+    op_o = O.elasticity_operator(mesh_o, E, 0.3, cons)
+    _, _, op = gpu_problem(nx, nx, E, 0.3, op_o.free_dofs)
+    _, rep = G.pcg_solve(op, rng.standard_normal(op_o.n_free), None, tol=1e-14, maxit=3)
+    assert not rep.converged and rep.iterations == 3
+
+
+def test_zero_rhs_and_bad_tolerance():
+    nx = 8
+    E = np.ones(nx * nx)
+    mesh_o = O.mesh_for(nx, nx)
+    cons, _, _ = configs.cantilever_bcs(nx, nx)
+    op_o = O.elasticity_operator(mesh_o, E, 0.3, cons)
+    _, _, op = gpu_problem(nx, nx, E, 0.3, op_o.free_dofs)
+    x, rep = G.pcg_solve(op, np.zeros(op_o.n_free), None)
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    with pytest.raises(ValueError):
+        G.pcg_solve(op, np.zeros(op_o.n_free), None, tol=2.0)
+
+
+# ---------------------------------------------------------------------------
+# preconditioner pieces
+
+
+def _bench(eta):
+    g = load_golden(f"ref_bench100_eta{eta}.npz")
+    mesh = G.build_fine_mesh(100, 100)
+    coeff = G.CoefficientField(g["E"], 0.3, float(g["E"].min()), 1.0)
+    op = G.ElasticityOperator(mesh, coeff, g["free_dofs"])
+    part = G.build_coarse_partition(mesh, 10, 10)
+    pre = G.build_preconditioner("EH+Rot", op, mesh, part, coeff, g["dirichlet_nodes"])
+    return g, mesh, op, pre
+
+
+@pytest.mark.parametrize("eta", ["1", "1e+06"])
+def test_reference_benchmark_cell_full_pcg(eta):
+    g, mesh, op, pre = _bench(eta)
+    assert pre.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
+    lam = pre.info["eigenvalues"]
+    ref = g["eigenvalues"]
+    scale = np.abs(ref).max(axis=1, keepdims=True)
+    assert np.all(np.abs(lam - ref) <= 1e-9 * np.abs(ref) + 1e-12 * scale)
+    z = pre.apply(g["apply_r"])
+    assert rel(z, g["apply_z"]) <= 1e-9
+    for tol in ("1e-06", "1e-08"):
+        x, rep = G.pcg_solve(op, g["b"], pre, tol=float(tol), maxit=2000)
+        assert rep.converged
+        assert abs(rep.iterations - int(g[f"iters_{tol}"])) <= 1
+        assert rel(x, g[f"x_{tol}"]) <= (1e-8 if tol == "1e-08" else 1e-6)
+        assert rep.cond_estimate == pytest.approx(float(g[f"cond_{tol}"]), rel=1e-3)
+
+
+def test_apply_symmetric_positive_and_linear(rng):
+    g, mesh, op, pre = _bench("1e+06")
+    for _ in range(5):
+        v, w = rng.standard_normal(op.n_free), rng.standard_normal(op.n_free)
+        a, b = v @ pre.apply(w), w @ pre.apply(v)
+        assert a == pytest.approx(b, rel=1e-10)
+        assert v @ pre.apply(v) > 0
+    assert not np.any(pre.apply(np.zeros(op.n_free)))
+    with pytest.raises(ValueError):
+        pre.apply(np.zeros(3))
+
+
+def test_deterministic_solves():
+    g, mesh, op, pre = _bench("1e+06")
+    x1, r1 = G.pcg_solve(op, g["b"], pre, tol=1e-8)
+    x2, r2 = G.pcg_solve(op, g["b"], pre, tol=1e-8)
+    assert np.array_equal(x1, x2) and r1.iterations == r2.iterations
+
+
+@pytest.mark.parametrize("name", ["ref_config1.npz", "ref_mbb_64x32.npz", "ref_config2_n128.npz",
+                                  "ref_config3_n128.npz"])
+def test_baseline_config_against_reference(name):
+    g = load_golden(name)
+    spec = spec_from_golden(g)
+    from paper_2006_13387_b200.solve import setup_spec
+
+    mesh, op, pre = setup_spec(spec)
+    assert pre.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
+    z = pre.apply(g["apply_r"])
+    assert rel(z, g["apply_z"]) <= 1e-7
+    x, rep = G.pcg_solve(op, spec.rhs(), pre, tol=float(g["tol"]), maxit=5000)
+    lo = min(int(g["iters"]), int(g["jitter_iters"].min())) - 1
+    hi = max(int(g["iters"]), int(g["jitter_iters"].max())) + 1
+    assert rep.converged and lo <= rep.iterations <= hi, (rep.iterations, g["iters"], g["jitter_iters"])
+    floor = max(1e-8, 10 * float(g["jitter_x"].max()))
+    assert rel(x, g["x"]) <= floor
+
+
+def test_level1_only_matches_oracle(rng):
+    spec = configs.config1(seed=1, n=32, H=8, delta=2)
+    prob = O.problem_from_spec(spec)
+    l1 = O.level1_solvers(prob.op, prob.mesh, O.block_rects(prob.mesh, 8, 2), keep_domain_boundary=True)
+    P = O.TwoLevel(l1, None, prob.op.n_free)
+    mesh = G.build_fine_mesh(32, 32)
+    coeff = G.CoefficientField(spec.E, 0.3, spec.E_min, 1.0)
+    op = G.ElasticityOperator(mesh, coeff, spec.free_dofs())
+    part = G.build_coarse_partition(mesh, 4, 4)
+    pre = G.build_preconditioner("EH+Rot", op, mesh, part, coeff, spec.heat_dirichlet_nodes,
+                                 level1="blocks", delta=2, use_coarse=False)
+    for _ in range(3):
+        r = rng.standard_normal(op.n_free)
+        assert rel(pre.apply(r), P.apply(r)) <= 1e-8
+
+
+def test_coarse_apply_matches_oracle(rng):
+    spec = configs.config3(seed=2, n=64, H=16, delta=2, eta=1e4)
+    prob = O.problem_from_spec(spec)
+    Po = O.build_two_level(prob, H=16, delta=2, level1_mode="blocks")
+    from paper_2006_13387_b200.solve import setup_spec
+
+    mesh, op, pre = setup_spec(spec)
+    assert pre.coarse_dim == Po.coarse_dim
+    assert pre.mode_counts == Po.info["mode_counts"]
+    for _ in range(3):
+        r = rng.standard_normal(op.n_free)
+        assert rel(pre.apply_coarse(r), Po.coarse.apply(r)) <= 1e-8
