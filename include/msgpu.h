@@ -79,6 +79,7 @@ typedef struct ms_precond_info {
   int n_centers;         /* interior coarse nodes (neighbourhoods)            */
   int n_subdomains;      /* level-1 subdomains                                */
   int max_eig_passes;    /* subspace-iteration passes of the slowest centre   */
+  double mean_eig_passes; /* mean passes over centres                          */
   double t_level1;       /* s, level-1 assembly + factorisation               */
   double t_eig;          /* s, batched eigensolves + selection                */
   double t_coarse;       /* s, eigensolves + basis + K0 + factor/inverse      */
@@ -88,6 +89,7 @@ typedef struct ms_precond_info {
 
 /* SolveReport (krylov.py:17-35); history arrays are caller-provided. */
 typedef struct ms_report {
+  int64_t kernel_launches; /* msgpu kernels launched by the solve (incl. init)  */
   int iterations;
   int converged;
   double final_residual;  /* ||r_k|| / ||b|| of the recursive residual        */
@@ -101,6 +103,23 @@ int ms_ctx_destroy(ms_ctx* ctx);
 /* copies the last error message of `ctx` (or the global one when ctx==NULL) */
 int ms_last_error(const ms_ctx* ctx, char* buf, size_t len);
 int ms_abi_version(void);
+
+/* Per-kernel CUDA-event profiling of the PCG hot path (bench.py's roofline):
+ * device milliseconds and launch counts accumulated per component, launches
+ * issued after convergence excluded.  Components: */
+enum {
+  MS_PROF_MATVEC = 0,       /* matrix-free operator + p update + p.q         */
+  MS_PROF_UPDATE = 1,       /* x, r update + ||r||                            */
+  MS_PROF_LEVEL1 = 2,       /* batched level-1 banded forward/backward sweeps */
+  MS_PROF_RESTRICT = 3,     /* R0 r                                           */
+  MS_PROF_COARSE_SOLVE = 4, /* K0^-1 f0 packed SYMV (2 kernels)               */
+  MS_PROF_COMBINE = 5,      /* level-1 overlap sum + prolongation + r.z       */
+  MS_PROF_N = 8
+};
+int ms_ctx_set_profiling(ms_ctx* ctx, int on); /* also resets the counters */
+int ms_ctx_profile_get(const ms_ctx* ctx, double* ms, long long* counts); /* MS_PROF_N each */
+/* the context's cudaStream_t (for event timing by callers) */
+void* ms_ctx_stream(const ms_ctx* ctx);
 
 /* ---- operator: assemble_elasticity (assembly.py:208-220) ---------------
  * E: per-element modulus, n_el = nx*ny, row-major (e = j*nx + i).

@@ -256,6 +256,25 @@ def lowest_eigenpairs(K, M, k):
     return sla.eigh(K.matrix.toarray(), M.matrix.toarray(), subset_by_index=[0, k - 1])
 
 
+def lowest_eigenpairs_arpack(K, M, k):
+    """Shift-invert ARPACK alternative to ?sygvx, same pencil and k.
+
+    Used where the dense solve is too slow (the bench's bounded CPU sample and
+    large parity cases); tests check it against ``lowest_eigenpairs`` on the
+    golden neighbourhoods.  Vectors are M-orthonormal like eigh's.
+    """
+    A, B = K.matrix.tocsc(), M.matrix.tocsc()
+    n = A.shape[0]
+    if n <= 4 * k + 20:
+        return lowest_eigenpairs(K, M, k)
+    sigma = -1e-10 * A.diagonal().sum() / B.diagonal().sum()
+    w, v = spla.eigsh(A, k, B, sigma=sigma, which="LM")
+    order = np.argsort(w)
+    w, v = w[order], v[:, order]
+    v = v / np.sqrt(np.einsum("ij,ij->j", v, B @ v))
+    return w, v
+
+
 def gap_count(lam, n_max, threshold=50.0):
     """Gap rule (spectral.py:161-186): largest i<=n_max with l[i]/max(l[i-1],eps)>=thr."""
     if n_max < 1:
@@ -456,6 +475,9 @@ class TwoLevel:
         if self.coarse is not None:
             z += self.coarse.apply(r)
         return z
+
+    def level1_only(self, r):
+        return self.level1_apply(r)
 
     def level1_apply(self, r):
         z = np.zeros_like(r)

@@ -6,6 +6,7 @@ CUDA device is usable, every solver entry point raises.
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 from pathlib import Path
@@ -24,7 +25,10 @@ EXPORTS = (
     "ms_problem_create", "ms_problem_destroy", "ms_problem_n_free", "ms_problem_set_modulus",
     "ms_operator_apply", "ms_precond_build", "ms_precond_destroy", "ms_precond_apply",
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
+    "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream",
 )
+PROF_NAMES = ("matvec", "update", "level1", "restrict", "coarse_solve", "combine")
+MS_PROF_N = 8
 
 
 class PrecondOpts(C.Structure):
@@ -39,14 +43,14 @@ class PrecondOpts(C.Structure):
 class PrecondInfo(C.Structure):
     _fields_ = [
         ("coarse_dim", C.c_int), ("n_centers", C.c_int), ("n_subdomains", C.c_int),
-        ("max_eig_passes", C.c_int), ("t_level1", C.c_double), ("t_eig", C.c_double),
+        ("max_eig_passes", C.c_int), ("mean_eig_passes", C.c_double), ("t_level1", C.c_double), ("t_eig", C.c_double),
         ("t_coarse", C.c_double), ("local_bytes", C.c_double), ("coarse_bytes", C.c_double),
     ]
 
 
 class Report(C.Structure):
     _fields_ = [
-        ("iterations", C.c_int), ("converged", C.c_int), ("final_residual", C.c_double),
+        ("kernel_launches", C.c_int64), ("iterations", C.c_int), ("converged", C.c_int), ("final_residual", C.c_double),
         ("t_solve", C.c_double), ("t_total", C.c_double),
     ]
 
@@ -56,6 +60,20 @@ class MsError(RuntimeError):
 
 
 _lib = None
+_SHUTDOWN = False
+
+
+def _mark_shutdown():
+    global _SHUTDOWN
+    _SHUTDOWN = True
+
+
+atexit.register(_mark_shutdown)
+
+
+def alive():
+    """False once the interpreter is exiting: handles are leaked, not freed."""
+    return _lib is not None and not _SHUTDOWN
 
 
 def load(path: str | os.PathLike | None = None):
@@ -87,6 +105,9 @@ def load(path: str | os.PathLike | None = None):
         "ms_precond_info_get": (C.c_int, [vp, C.POINTER(PrecondInfo), ip, dp]),
         "ms_precond_coarse_matrix": (C.c_int, [vp, dp]),
         "ms_pcg_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, vp, C.POINTER(Report), dp, dp, dp]),
+        "ms_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
+        "ms_ctx_profile_get": (C.c_int, [vp, dp, C.POINTER(C.c_longlong)]),
+        "ms_ctx_stream": (C.c_void_p, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -140,7 +140,7 @@ class ElasticityOperator:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib.alive():
             try:
                 _lib.load().ms_problem_destroy(h)
             except Exception:

@@ -140,150 +140,142 @@ void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, dou
 }
 
 // ---------------------------------------------------------------------------
-// Level-1 sweeps, one warp per subdomain.  Column-oriented (axpy) forward
-// sweep over Lc, and the same over Lr for the backward sweep, so neither
-// needs a reduction: the only loop-carried chain is the window slot of the
-// next row.  Band columns are software-pipelined PD steps ahead in
-// registers; lane l owns band offsets j = l+1+32t.
+// Level-1 sweeps, one warp per subdomain, window held in registers.
+//
+// Column-oriented (axpy) substitution: after w_k is known, rows k+1..k+bw
+// receive  acc[k+j] -= L[k+j][k] * w_k.  Row r's accumulator lives in lane
+// r % 32, register slot (r/32 - current block) -- slots rotate every 32
+// steps, so all register indices are compile-time constants inside the
+// unrolled 32-step block.  Per step the only cross-lane traffic is one
+// shuffle broadcasting w_k from its owner lane; there is no shared memory and
+// no warp barrier, so the band columns, prefetched PD steps ahead, stay in
+// flight.  The backward sweep is the same recurrence on the row band Lr in
+// reversed numbering (row' = n-1-row).
 constexpr int kSolveWarps = 4;
-constexpr int kPD = 8;
+constexpr int kPD = 4;
 
-template <int JPL>
+template <int T, bool REV>
+__device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, int bw,
+                                           double* __restrict__ y, int lane) {
+  constexpr int R = T + 1;  // register slots (blocks of 32 rows) per lane
+  const int S = bw + 1;
+  auto lcol = [&](int k) -> const double* {
+    return REV ? L + (int64_t)(n - 1 - k) * S : L + (int64_t)k * S;
+  };
+  auto yat = [&](int r) -> double* { return REV ? y + (n - 1 - r) : y + r; };
+
+  double acc[R];
+#pragma unroll
+  for (int s = 0; s < R - 1; ++s) {
+    const int r = 32 * s + lane;
+    acc[s] = r < n ? *yat(r) : 0.0;
+  }
+  acc[R - 1] = 0.0;
+  double rnext = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane) : 0.0;
+
+  // prefetch ring: band values of the next PD steps
+  double lv[kPD][T], dv[kPD];
+  auto load = [&](int k, int u, double(&l)[T], double& d) {
+    const int base = ((lane - u - 1) & 31) + 1;
+    const bool ok = k < n;
+    const double* col = lcol(ok ? k : 0);
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int j = base + 32 * t;
+      l[t] = (ok && j <= bw) ? __ldg(col + j) : 0.0;
+    }
+    d = ok ? __ldg(col) : 0.0;
+  };
+#pragma unroll
+  for (int u = 0; u < kPD; ++u) load(u, u, lv[u], dv[u]);
+
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    // rows of block (k0/32 + R-1) enter the window
+    acc[R - 1] = rnext;
+    {
+      const int r = k0 + 32 * R + lane;
+      rnext = r < n ? *yat(r) : 0.0;
+    }
+    double wout = 0.0;
+#pragma unroll 1
+    for (int u0 = 0; u0 < 32; u0 += kPD) {
+#pragma unroll
+     for (int q = 0; q < kPD; ++q) {
+      const int u = u0 + q;
+      const int k = k0 + u;
+      if (k < n) {
+        const double wloc = acc[0] * dv[q];
+        const double wk = __shfl_sync(0xffffffffu, wloc, u);
+        if (lane == u) wout = wk;
+        const int base = ((lane - u - 1) & 31) + 1;
+        const bool hi = lane <= u;  // row k+base lies in the next block
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const double upd = lv[q][t] * wk;  // zero when k+j is outside the band
+          if (hi) {
+            if (t + 1 < R) acc[t + 1] -= upd;
+          } else {
+            acc[t] -= upd;
+          }
+          (void)base;
+        }
+        load(k + kPD, (u + kPD) & 31, lv[q], dv[q]);
+      }
+     }
+    }
+    if (k0 + lane < n) *yat(k0 + lane) = wout;
+    // rotate the register window by one block
+#pragma unroll
+    for (int s = 0; s < R - 1; ++s) acc[s] = acc[s + 1];
+    acc[R - 1] = 0.0;
+  }
+}
+
+template <int T>
 __global__ void __launch_bounds__(kSolveWarps * 32)
     k_l1_solve(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                const double* __restrict__ Lr, const double* __restrict__ r,
                double* __restrict__ ybuf, const int* done) {
   if (done && *(volatile const int*)done) return;
-  extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sid = blockIdx.x * kSolveWarps + warp;
   if (sid >= nsys) return;
   const BandSys s = sys[sid];
-  const int S = s.bw + 1, n = s.n, bw = s.bw;
-  double* acc = smem + warp * (JPL * 32 + 1);
   double* y = ybuf + s.yoff;
-
   // gather R_s r (node-interleaved local order)
-  for (int i = lane; i < n; i += 32) {
+  for (int i = lane; i < s.n; i += 32) {
     const int ln = s.ncomp == 2 ? (i >> 1) : i, c = s.ncomp == 2 ? (i & 1) : 0;
     int a, b;
     band_node_of(s, ln, a, b);
     y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
   }
   __syncwarp();
-
-  double lv[kPD][JPL], dv[kPD], rv[kPD];
-  // ---- forward: L w = rhs ----
-  {
-    const double* L = Lc + s.foff;
-    for (int i = lane; i < S && i < n; i += 32) acc[i] = y[i];
-    __syncwarp();
-    auto load = [&](int k, double(&l)[JPL], double& d, double& rr) {
-#pragma unroll
-      for (int t = 0; t < JPL; ++t) {
-        const int j = lane + 1 + 32 * t;
-        l[t] = (k < n && j <= bw) ? __ldg(L + (int64_t)k * S + j) : 0.0;
-      }
-      d = (k < n) ? __ldg(L + (int64_t)k * S) : 0.0;
-      rr = (k + S < n) ? y[k + S] : 0.0;
-    };
-#pragma unroll
-    for (int u = 0; u < kPD; ++u) load(u, lv[u], dv[u], rv[u]);
-    for (int k0 = 0; k0 < n; k0 += kPD) {
-#pragma unroll
-      for (int u = 0; u < kPD; ++u) {
-        const int k = k0 + u;
-        if (k < n) {
-          const int sk = k % S;
-          const double wk = acc[sk] * dv[u];
-#pragma unroll
-          for (int t = 0; t < JPL; ++t) {
-            const int j = lane + 1 + 32 * t;
-            if (j <= bw) {
-              const int sl = (sk + j) >= S ? sk + j - S : sk + j;
-              acc[sl] -= lv[u][t] * wk;
-            }
-          }
-          if (lane == 0) {
-            y[k] = wk;
-            if (k + S < n) acc[sk] = rv[u];
-          }
-          __syncwarp();
-          load(k + kPD, lv[u], dv[u], rv[u]);
-        }
-      }
-    }
-  }
+  band_sweep<T, false>(Lc + s.foff, s.n, s.bw, y, lane);
   __syncwarp();
-  // ---- backward: L^T y = w ----
-  {
-    const double* L = Lr + s.foff;
-    for (int i = lane; i < S && i < n; i += 32) {
-      const int row = n - 1 - i;
-      acc[row % S] = y[row];
-    }
-    __syncwarp();
-    auto load = [&](int k, double(&l)[JPL], double& d, double& rr) {
-#pragma unroll
-      for (int t = 0; t < JPL; ++t) {
-        const int j = lane + 1 + 32 * t;
-        l[t] = (k >= 0 && j <= bw) ? __ldg(L + (int64_t)k * S + j) : 0.0;
-      }
-      d = (k >= 0) ? __ldg(L + (int64_t)k * S) : 0.0;
-      rr = (k - S >= 0) ? y[k - S] : 0.0;
-    };
-#pragma unroll
-    for (int u = 0; u < kPD; ++u) load(n - 1 - u, lv[u], dv[u], rv[u]);
-    for (int k0 = 0; k0 < n; k0 += kPD) {
-#pragma unroll
-      for (int u = 0; u < kPD; ++u) {
-        const int k = n - 1 - (k0 + u);
-        if (k >= 0) {
-          const int sk = k % S;
-          const double yk = acc[sk] * dv[u];
-#pragma unroll
-          for (int t = 0; t < JPL; ++t) {
-            const int j = lane + 1 + 32 * t;
-            if (j <= bw && k - j >= 0) {
-              const int sl = (sk - j) < 0 ? sk - j + S : sk - j;
-              acc[sl] -= lv[u][t] * yk;
-            }
-          }
-          if (lane == 0) {
-            y[k] = yk;
-            if (k - S >= 0) acc[sk] = rv[u];
-          }
-          __syncwarp();
-          load(k - kPD, lv[u], dv[u], rv[u]);
-        }
-      }
-    }
-  }
+  band_sweep<T, true>(Lr + s.foff, s.n, s.bw, y, lane);
 }
 
-template <int JPL>
-static void solve_jpl(const Grid& g, const BandSys* sys, int nsys, const double* Lc,
-                      const double* Lr, const double* r, double* ybuf, const int* done,
-                      cudaStream_t st) {
-  const size_t smem = (size_t)kSolveWarps * (JPL * 32 + 1) * sizeof(double);
-  k_l1_solve<JPL><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, smem, st>>>(g, sys, nsys, Lc, Lr,
-                                                                             r, ybuf, done);
+template <int T>
+static void solve_t(const Grid& g, const BandSys* sys, int nsys, const double* Lc, const double* Lr,
+                    const double* r, double* ybuf, const int* done, cudaStream_t st) {
+  k_l1_solve<T><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, 0, st>>>(g, sys, nsys, Lc, Lr, r,
+                                                                        ybuf, done);
 }
 
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                      const double* Lr, const double* r, double* ybuf, const int* done,
                      cudaStream_t st) {
   if (nsys == 0) return;
-  const int jpl = std::max(1, div_up(max_bw, 32));
-  switch (jpl) {
-    case 1: solve_jpl<1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 2: solve_jpl<2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 3: solve_jpl<3>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 4: solve_jpl<4>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 5: solve_jpl<5>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 6: solve_jpl<6>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 7: solve_jpl<7>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 8: solve_jpl<8>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+  const int T = std::max(1, div_up(max_bw, 32));
+  switch (T) {
+    case 1: solve_t<1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 2: solve_t<2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 3: solve_t<3>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 4: solve_t<4>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 5: solve_t<5>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 6: solve_t<6>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 7: solve_t<7>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+    case 8: solve_t<8>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
     default: throw Error(-1, "level-1 band wider than 256 unsupported");
   }
   MS_CUDA(cudaGetLastError());

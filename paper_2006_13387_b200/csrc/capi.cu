@@ -123,10 +123,61 @@ void heat_elements(double h, HeatParam& hp) {
 
 }  // namespace
 
+// Optional CUDA-event profiling of every hot-path kernel launch, tagged with
+// the PCG iteration it belongs to (launches after convergence are dropped).
+struct Prof {
+  bool on = false;
+  double ms[MS_PROF_N] = {};
+  long long cnt[MS_PROF_N] = {};
+  std::vector<cudaEvent_t> pool;
+  struct Rec {
+    int comp, it;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      MS_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t begin(cudaStream_t st) {
+    if (!on) return nullptr;
+    cudaEvent_t a = get();
+    MS_CUDA(cudaEventRecord(a, st));
+    return a;
+  }
+  void end(int comp, int it, cudaStream_t st, cudaEvent_t a) {
+    if (!on) return;
+    cudaEvent_t b = get();
+    MS_CUDA(cudaEventRecord(b, st));
+    pending.push_back({comp, it, a, b});
+  }
+  // call after a stream sync; keep records of iterations < valid_iters
+  void flush(int valid_iters) {
+    for (const Rec& r : pending) {
+      if (r.it < valid_iters) {
+        float t = 0.f;
+        MS_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.comp] += t;
+        cnt[r.comp] += 1;
+      }
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+};
+
 struct ms_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   std::string err;
+  Prof prof;
 };
 
 struct ms_problem {
@@ -159,6 +210,8 @@ struct ms_problem {
 
 struct ms_precond {
   ms_problem* prob = nullptr;
+  int device = 0;
+  cudaStream_t st = nullptr;  // copies: destroy must not touch prob
   ms_precond_opts opts{};
   std::vector<int64_t> heat_dir;
   // level 1
@@ -256,18 +309,34 @@ static void level1_axis(int n_el, int nblocks, int kind, int delta, std::vector<
 
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
 static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgScalars* sc,
-                               double* beta_hist) {
+                               double* beta_hist, int it = -1) {
   ms_problem* P = pc->prob;
   const cudaStream_t st = P->ctx->st;
+  Prof& pf = P->ctx->prof;
   const int* done = sc ? &sc->done : nullptr;
-  if (pc->nsys > 0)
+  cudaEvent_t a;
+  if (pc->nsys > 0) {
+    a = pf.begin(st);
     launch_l1_solve(P->g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
-  if (pc->has_coarse) {
-    launch_restrict(P->g, pc->cd, r, pc->f0.p, done, st);
-    launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st);
+    pf.end(MS_PROF_LEVEL1, it, st, a);
   }
+  if (pc->has_coarse) {
+    a = pf.begin(st);
+    launch_restrict(P->g, pc->cd, r, pc->f0.p, done, st);
+    pf.end(MS_PROF_RESTRICT, it, st, a);
+    a = pf.begin(st);
+    launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st);
+    pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
+  }
+  a = pf.begin(st);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
                  pc->y0.p, r, z, sc, P->partials.p, beta_hist, st);
+  pf.end(MS_PROF_COMBINE, it, st, a);
+}
+
+static int precond_launches(const ms_precond* pc) {
+  if (!pc) return 1;  // rz
+  return (pc->nsys > 0 ? 1 : 0) + (pc->has_coarse ? 3 : 0) + 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -303,6 +372,28 @@ int ms_ctx_create(int device, ms_ctx** out) {
   *out = c;
   MS_API_END(c)
 }
+
+int ms_ctx_set_profiling(ms_ctx* ctx, int on) {
+  MS_API_BEGIN
+  if (!ctx) throw Error(MS_E_INVALID, "null context");
+  ctx->prof.on = on != 0;
+  for (int i = 0; i < MS_PROF_N; ++i) {
+    ctx->prof.ms[i] = 0.0;
+    ctx->prof.cnt[i] = 0;
+  }
+  MS_API_END(ctx)
+}
+
+int ms_ctx_profile_get(const ms_ctx* ctx, double* ms, long long* counts) {
+  if (!ctx || !ms || !counts) return MS_E_INVALID;
+  for (int i = 0; i < MS_PROF_N; ++i) {
+    ms[i] = ctx->prof.ms[i];
+    counts[i] = ctx->prof.cnt[i];
+  }
+  return MS_OK;
+}
+
+void* ms_ctx_stream(const ms_ctx* ctx) { return ctx ? (void*)ctx->st : nullptr; }
 
 int ms_ctx_destroy(ms_ctx* ctx) {
   if (!ctx) return MS_OK;
@@ -404,6 +495,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
   if (o->local_solver != MS_LOCAL_BANDED) throw Error(MS_E_INVALID, "local solver not available");
   std::unique_ptr<ms_precond> pc(new ms_precond());
   pc->prob = P;
+  pc->device = P->ctx->device;
+  pc->st = P->ctx->st;
   pc->opts = *o;
   if (o->heat_dirichlet_nodes && o->n_heat_dirichlet > 0)
     pc->heat_dir.assign(o->heat_dirichlet_nodes, o->heat_dirichlet_nodes + o->n_heat_dirichlet);
@@ -537,7 +630,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       launch_band_potrf(hsysd.p, nk, mbw, hLc.p, hLr.p, fail.p, st);
       check_fail(fail, st, "neighbourhood heat pencil (K + sigma M)");
       EigBatch eb{o->Nx, cd.mex, cd.mey, k0, nk, hsysd.p, hLc.p, hLr.p, work.p, pc->evals.p,
-                  evecs.p, passes.p, neumann.p};
+                  evecs.p, passes.p, neumann.p, o->n_max, o->gap_threshold, o->fixed_rule};
       launch_subspace(g, P->E.p, hdir.p, hp, eb, 300, 1e-12, st);
       launch_select(nc, pc->evals.p, o->n_max, o->gap_threshold, o->fixed_rule, pc->nsel.p, st);
       std::vector<int> bsel(nk);
@@ -556,6 +649,9 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       MS_CUDA(cudaMemcpyAsync(hp_.data(), passes.p, nc * sizeof(int), cudaMemcpyDeviceToHost, st));
       MS_CUDA(cudaStreamSynchronize(st));
       pc->max_pass = *std::max_element(hp_.begin(), hp_.end());
+      double sum = 0;
+      for (int v : hp_) sum += v;
+      pc->info.mean_eig_passes = sum / std::max(1, nc);
     }
     MS_CUDA(cudaEventRecord(e2, st));
     // offsets
@@ -629,8 +725,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
 
 int ms_precond_destroy(ms_precond* pc) {
   if (!pc) return MS_OK;
-  cudaSetDevice(pc->prob->ctx->device);
-  cudaStreamSynchronize(pc->prob->ctx->st);
+  cudaSetDevice(pc->device);
+  cudaStreamSynchronize(pc->st);
   delete pc;
   return MS_OK;
 }
@@ -727,17 +823,27 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     for (; it < upto; ++it) {
       double* pold = (it & 1) ? P->p1.p : P->p0.p;
       double* pnew = (it & 1) ? P->p0.p : P->p1.p;
+      Prof& pf = P->ctx->prof;
+      cudaEvent_t a = pf.begin(st);
       launch_matvec(P->g, P->ke, P->E.p, P->mask.p, zp, pold, pnew, P->q.p, MV_PCG, P->sc.p,
                     P->partials.p, P->halpha.p, st);
+      pf.end(MS_PROF_MATVEC, it, st, a);
+      a = pf.begin(st);
       launch_pcg_update(n, P->x.p, pnew, P->r.p, P->q.p, P->sc.p, P->partials.p, P->hres.p, st);
-      if (pc)
-        precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p);
-      else
+      pf.end(MS_PROF_UPDATE, it, st, a);
+      if (pc) {
+        precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, it);
+      } else {
+        a = pf.begin(st);
         launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
+        pf.end(MS_PROF_COMBINE, it, st, a);
+      }
     }
     MS_CUDA(cudaMemcpyAsync(&hs, P->sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     MS_CUDA(cudaStreamSynchronize(st));
     done = hs.done;
+    // the iteration that converged keeps its launches; later ones were no-ops
+    P->ctx->prof.flush(done ? hs.iter : it);
   }
   MS_CUDA(cudaEventRecord(t1, st));
   MS_CUDA(cudaMemcpyAsync(&hs, P->sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -751,6 +857,7 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   if (alphas && iters > 0) MS_CUDA(cudaMemcpy(alphas, P->halpha.p, iters * sizeof(double), cudaMemcpyDefault));
   if (betas && iters > 1) MS_CUDA(cudaMemcpy(betas, P->hbeta.p, (iters - 1) * sizeof(double), cudaMemcpyDefault));
   if (rep) {
+    rep->kernel_launches = 1 + precond_launches(pc) + (int64_t)iters * (2 + precond_launches(pc));
     rep->iterations = iters;
     rep->converged = hs.converged;
     rep->final_residual = hs.res;

@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(kEigThreads)
     X[t] = dir[i] ? 0.0 : hash_unif(((uint64_t)k << 32) ^ ((uint64_t)c << 24) ^ (uint64_t)i);
   }
   if (threadIdx.x < P) ritz_old[threadIdx.x] = 0.0;
+  if (threadIdx.x == 0) misc[3] = -1.0;
   __syncthreads();
   const int need = kNeig - (neumann ? 1 : 0);
   int pass = 0;
@@ -436,13 +437,34 @@ __global__ void __launch_bounds__(kEigThreads)
       X = W;
       W = t;
     }
-    // (7) convergence of the wanted Ritz values
+    // (7) stopping rule.  Only the selection needs the 7 eigenvalues, and only
+    // the selected modes' vectors enter the coarse space: the selected Ritz
+    // values must be converged to `tol` (their subspace sits below a gap of
+    // >= threshold, so it converges fast), the remaining ones to 1e-8 relative
+    // (enough to certify the gap tests), and the provisional selection must be
+    // the same as in the previous pass.
     if (threadIdx.x == 0) {
       const double scale = fabs(ritz[P - 1]);
-      bool conv = pass >= 3;
-      for (int i = 0; i < need; ++i)
-        if (fabs(ritz[i] - ritz_old[i]) > tol * fabs(ritz[i]) + 1e-15 * scale) conv = false;
+      const int off = neumann ? 1 : 0;
+      double lam[kNeig];
+      if (neumann) lam[0] = 0.0;
+      for (int i = 0; i < kNeig - off; ++i) lam[i + off] = ritz[i];
+      int sel = eb.fixed ? eb.n_max : 1;
+      if (!eb.fixed) {
+        const int wn = min(eb.n_max + 1, kNeig);
+        const double last = lam[wn - 1];
+        const double eps = last != 0.0 ? 1e-14 * fabs(last) : 1e-300;
+        for (int i = 1; i < wn; ++i)
+          if (lam[i] / fmax(lam[i - 1], eps) >= eb.gap) sel = i;
+        sel = min(sel, eb.n_max);
+      }
+      bool conv = pass >= 3 && sel == (int)misc[3];
+      for (int i = 0; i < need; ++i) {
+        const double t = (i + off < sel) ? tol : 1e-8;
+        if (fabs(ritz[i] - ritz_old[i]) > t * fabs(ritz[i]) + 1e-15 * scale) conv = false;
+      }
       for (int i = 0; i < P; ++i) ritz_old[i] = ritz[i];
+      misc[3] = (double)sel;
       misc[2] = conv ? 1.0 : 0.0;
     }
     __syncthreads();

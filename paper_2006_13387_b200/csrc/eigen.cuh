@@ -25,6 +25,9 @@ struct EigBatch {
   double* evecs;       // batch: (centre - k0) * kNeig * NL, band order, M-orthonormal
   int* passes;         // global: per centre
   int* neumann;        // global: per centre (1 if no heat-Dirichlet node in omega)
+  int n_max;           // selection parameters, used by the stopping rule
+  double gap;
+  int fixed;
 };
 
 // B = K_H + sigma M_H in band form (Dirichlet nodes -> identity rows)

@@ -118,7 +118,7 @@ class TwoLevelPreconditioner:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib.alive():
             try:
                 _lib.load().ms_precond_destroy(h)
             except Exception:
@@ -177,7 +177,7 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "coarse_dim": inf.coarse_dim, "mode_counts": [int(c) for c in counts[:nc]],
         "basis_kind": "H+Rot" if variant.enrich else "H", "selection_rule": rule,
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
-        "max_eig_passes": inf.max_eig_passes, "local_bytes": inf.local_bytes,
+        "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,
         "coarse_bytes": inf.coarse_bytes, "level1": level1, "delta": delta,
     }
     return TwoLevelPreconditioner(variant, op, h, info)
