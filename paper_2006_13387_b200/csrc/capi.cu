@@ -219,7 +219,8 @@ struct ms_precond {
   std::vector<BandSys> hsys;
   DBuf<BandSys> sys;
   DBuf<double> Lc, Lr, ybuf;
-  DBuf<int> xcov, ycov;
+  DBuf<int> xcov, ycov, xlo_d, xlen_d, ylo_d, ylen_d;
+  DBuf<int64_t> yoff_d;
   L1Dev l1{};
   // coarse
   bool has_coarse = false;
@@ -555,7 +556,20 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p, pc->nsys, pc->Lc.p, st);
     launch_band_potrf(pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
     check_fail(fail, st, "level-1 subdomain matrix");
-    pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->sys.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
+    {
+      std::vector<int> xl(pc->NbX), yl(pc->NbY);
+      for (int I = 0; I < pc->NbX; ++I) xl[I] = xhi[I] - xlo[I] + 1;
+      for (int J = 0; J < pc->NbY; ++J) yl[J] = yhi[J] - ylo[J] + 1;
+      std::vector<int64_t> yo(pc->nsys);
+      for (int s2 = 0; s2 < pc->nsys; ++s2) yo[s2] = pc->hsys[s2].yoff;
+      pc->xlo_d.upload(xlo.data(), xlo.size(), st);
+      pc->ylo_d.upload(ylo.data(), ylo.size(), st);
+      pc->xlen_d.upload(xl.data(), xl.size(), st);
+      pc->ylen_d.upload(yl.data(), yl.size(), st);
+      pc->yoff_d.upload(yo.data(), yo.size(), st);
+    }
+    pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->xlo_d.p, pc->xlen_d.p, pc->ylo_d.p, pc->ylen_d.p,
+                   pc->yoff_d.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
     pc->info.n_subdomains = pc->nsys;
     pc->info.local_bytes = (double)foff * 2 * sizeof(double);
   }

@@ -86,50 +86,72 @@ __device__ __forceinline__ int basis_row(const CoarseDev& cd, int k, int bi, int
 }
 
 // ---------------------------------------------------------------------------
-// f0 = R0 r, one CTA per centre, <= 13 rows per pass.
-constexpr int kNbChunk = 13;
+// f0 = R0 r, one CTA per centre.  The centre's NM selected modes are a
+// template parameter (dispatched per CTA), so the 2*NM+1 accumulators live in
+// registers and are reduced together: one shuffle tree per value and a
+// single shared-memory pass.  Node rows map onto lanes (coalesced r/psi/chi).
+constexpr int kMaxModes = 6;
+
+template <int NM>
+__device__ __forceinline__ void restrict_center(const Grid& g, const CoarseDev& cd, int k, int I,
+                                                int J, const double* __restrict__ r,
+                                                double* __restrict__ f0, double* sred) {
+  constexpr int NB = 2 * NM + 1;
+  const int NL = cd.NLx * cd.NLy;
+  const double* chi = cd.chi + (int64_t)k * NL;
+  const double* psi = cd.psi + cd.psioff[k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double acc[NB];
+#pragma unroll
+  for (int t = 0; t < NB; ++t) acc[t] = 0.0;
+  const int ax0 = (I - 1) * cd.mex, by0 = (J - 1) * cd.mey;
+  for (int lb = warp; lb < cd.NLy; lb += nw) {
+    const int b = by0 + lb;
+    const double* rrow = r + (int64_t)b * g.nnx + ax0;
+    for (int la = lane; la < cd.NLx; la += 32) {
+      const int ln = lb * cd.NLx + la;
+      const double ch = chi[ln];
+      const double rx = rrow[la], ry = rrow[la + g.n_nodes];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const double v = ch * psi[(int64_t)m * NL + ln];
+        acc[2 * m] += v * rx;
+        acc[2 * m + 1] += v * ry;
+      }
+      double ex, ey;
+      rot_xy(cd, I, J, ax0 + la, b, ex, ey);
+      acc[NB - 1] += __dmul_rn(ch, ex) * rx + __dmul_rn(ch, ey) * ry;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NB; ++t) {
+    const double v = warp_sum(acc[t]);
+    if (lane == 0) sred[t * 8 + warp] = v;
+  }
+  __syncthreads();
+  const int nb = 2 * NM + cd.enrich;
+  if (threadIdx.x < nb) {
+    const int t = threadIdx.x < 2 * NM ? threadIdx.x : NB - 1;
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += sred[t * 8 + w];
+    f0[basis_row(cd, k, threadIdx.x, NM)] = s;
+  }
+}
 
 __global__ void __launch_bounds__(256)
     k_restrict(Grid g, CoarseDev cd, const double* __restrict__ r, double* __restrict__ f0,
                const int* done) {
   if (done && *(volatile const int*)done) return;
-  __shared__ double sred[8];
+  __shared__ double sred[(2 * kMaxModes + 1) * 8];
   const int k = blockIdx.x;
   const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
-  const int nsel = cd.nsel[k];
-  const int nb = 2 * nsel + cd.enrich;
-  const int NL = cd.NLx * cd.NLy;
-  const double* chi = cd.chi + (int64_t)k * NL;
-  const double* psi = cd.psi + cd.psioff[k];
-  for (int b0 = 0; b0 < nb; b0 += kNbChunk) {
-    double acc[kNbChunk];
-#pragma unroll
-    for (int t = 0; t < kNbChunk; ++t) acc[t] = 0.0;
-    for (int ln = threadIdx.x; ln < NL; ln += blockDim.x) {
-      const int a = (I - 1) * cd.mex + ln % cd.NLx, b = (J - 1) * cd.mey + ln / cd.NLx;
-      const double ch = chi[ln];
-      if (ch == 0.0) continue;
-      const int64_t n = (int64_t)b * g.nnx + a;
-      const double rx = r[n], ry = r[n + g.n_nodes];
-#pragma unroll
-      for (int t = 0; t < kNbChunk; ++t) {
-        const int bi = b0 + t;
-        if (bi < 2 * nsel) {
-          const double v = ch * psi[(int64_t)(bi >> 1) * NL + ln];
-          acc[t] += v * ((bi & 1) ? ry : rx);
-        } else if (bi < nb) {
-          double ex, ey;
-          rot_xy(cd, I, J, a, b, ex, ey);
-          acc[t] += __dmul_rn(ch, ex) * rx + __dmul_rn(ch, ey) * ry;
-        }
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < kNbChunk; ++t) {
-      const int bi = b0 + t;
-      const double s = block_sum(acc[t], sred);
-      if (bi < nb && threadIdx.x == 0) f0[basis_row(cd, k, bi, nsel)] = s;
-    }
+  switch (cd.nsel[k]) {
+    case 1: restrict_center<1>(g, cd, k, I, J, r, f0, sred); break;
+    case 2: restrict_center<2>(g, cd, k, I, J, r, f0, sred); break;
+    case 3: restrict_center<3>(g, cd, k, I, J, r, f0, sred); break;
+    case 4: restrict_center<4>(g, cd, k, I, J, r, f0, sred); break;
+    case 5: restrict_center<5>(g, cd, k, I, J, r, f0, sred); break;
+    default: restrict_center<6>(g, cd, k, I, J, r, f0, sred); break;
   }
 }
 
@@ -144,53 +166,54 @@ void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double
 // combine: node-centric sum of the overlapping local solutions (in the
 // reference's J-major subdomain order, schwarz.py:79-81), then the coarse
 // prolongation; fused r.z reduction for PCG.
-__global__ void __launch_bounds__(256)
+constexpr int CB_X = 32, CB_Y = 8;
+
+__global__ void __launch_bounds__(CB_X* CB_Y)
     k_combine(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, int has_l1, CoarseDev cd,
               int has_coarse, const double* __restrict__ y0, const double* __restrict__ r,
               double* __restrict__ z, PcgScalars* sc, double* partials, double* beta_hist) {
   if (sc && sc->done) return;
   __shared__ double sred[8];
   const int64_t nn = g.n_nodes;
+  const int a = blockIdx.x * CB_X + threadIdx.x % CB_X, b = blockIdx.y * CB_Y + threadIdx.x / CB_X;
   double dot = 0.0;
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn;
-       n += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(n % g.nnx), b = (int)(n / g.nnx);
+  if (a <= g.nx && b <= g.ny) {
+    const int64_t n = (int64_t)b * g.nnx + a;
     double zx = 0.0, zy = 0.0;
     if (has_l1) {
-#pragma unroll
       for (int tj = 0; tj < 4; ++tj) {
         const int J = l1.ycov[b * 4 + tj];
         if (J < 0) break;
-#pragma unroll
+        const int y0_ = l1.ylo[J], hy = l1.ylen[J];
         for (int ti = 0; ti < 4; ++ti) {
           const int I = l1.xcov[a * 4 + ti];
           if (I < 0) break;
-          const BandSys s = l1.sys[J * l1.NbX + I];
-          const int ln = band_local_node(s, a, b);
-          const double* ys = l1.ybuf + s.yoff + 2 * ln;
-          zx += ys[0];
-          zy += ys[1];
+          const int x0_ = l1.xlo[I], wx = l1.xlen[I];
+          const int ln = (wx <= hy) ? (b - y0_) * wx + (a - x0_) : (a - x0_) * hy + (b - y0_);
+          const double2 v = *reinterpret_cast<const double2*>(l1.ybuf + l1.yoff[J * l1.NbX + I] + 2 * ln);
+          zx += v.x;
+          zy += v.y;
         }
       }
     }
     if (has_coarse) {
       double cxs = 0.0, cys = 0.0;
-      const int ilo = max(1, a / cd.mex), ihi = min(cd.Nx - 1, (a + cd.mex - 1) / cd.mex);
-      const int jlo = max(1, b / cd.mey), jhi = min(cd.Ny - 1, (b + cd.mey - 1) / cd.mey);
       const int NL = cd.NLx * cd.NLy;
+      const int ia = a / cd.mex, jb = b / cd.mey;
+      const int ilo = max(1, ia), ihi = min(cd.Nx - 1, a - ia * cd.mex ? ia + 1 : ia);
+      const int jlo = max(1, jb), jhi = min(cd.Ny - 1, b - jb * cd.mey ? jb + 1 : jb);
       for (int J = jlo; J <= jhi; ++J)
         for (int I = ilo; I <= ihi; ++I) {
-          if (abs(a - I * cd.mex) >= cd.mex || abs(b - J * cd.mey) >= cd.mey) continue;
           const int k = center_index(cd, I, J);
           const int ln = local_node(cd, I, J, a, b);
           const double ch = cd.chi[(int64_t)k * NL + ln];
           const int nsel = cd.nsel[k];
           const double* ps = cd.psi + cd.psioff[k] + ln;
-          const int h0 = cd.hoff[k];
+          const double* yk = y0 + cd.hoff[k];
           for (int m = 0; m < nsel; ++m) {
             const double v = ch * ps[(int64_t)m * NL];
-            cxs += v * y0[h0 + 2 * m];
-            cys += v * y0[h0 + 2 * m + 1];
+            cxs += v * yk[2 * m];
+            cys += v * yk[2 * m + 1];
           }
           if (cd.enrich) {
             double ex, ey;
@@ -207,7 +230,7 @@ __global__ void __launch_bounds__(256)
     zy = mask[n + nn] ? zy : 0.0;
     z[n] = zx;
     z[n + nn] = zy;
-    if (sc) dot += zx * r[n] + zy * r[n + nn];
+    if (sc) dot = zx * r[n] + zy * r[n + nn];
   }
   if (!sc) return;
   const double bs = block_sum(dot, sred);
@@ -233,9 +256,9 @@ void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const C
   CoarseDev cdv{};
   if (l1) l1v = *l1;
   if (cd) cdv = *cd;
-  const int blocks = std::min<int64_t>(148 * 8, div_up(g.n_nodes, 256));
-  k_combine<<<blocks, 256, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0, y0, r, z, sc,
-                                    partials, beta_hist);
+  dim3 grid(div_up(g.nx + 1, CB_X), div_up(g.ny + 1, CB_Y));
+  k_combine<<<grid, CB_X * CB_Y, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0, y0, r, z, sc,
+                                          partials, beta_hist);
   MS_CUDA(cudaGetLastError());
 }
 

@@ -13,9 +13,13 @@ namespace msgpu {
 // -1 padded.  Subdomain s = J*NbX + I.
 struct L1Dev {
   int NbX, NbY;
-  const BandSys* sys;
-  const int* xcov;  // (nx+1) * 4
-  const int* ycov;  // (ny+1) * 4
+  const int* xlo;       // per block column I: first kept node, kept count
+  const int* xlen;
+  const int* ylo;       // per block row J
+  const int* ylen;
+  const int64_t* yoff;  // per subdomain: offset of its local vector in ybuf
+  const int* xcov;      // (nx+1) * 4
+  const int* ycov;      // (ny+1) * 4
   const double* ybuf;
 };
 
