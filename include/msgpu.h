@@ -147,6 +147,19 @@ int ms_precond_info_get(const ms_precond* pc, ms_precond_info* info, int* mode_c
                         double* eigenvalues);
 /* dense K0 (N_c x N_c, row-major, host buffer), reference row ordering (coarse.py:94-133) */
 int ms_precond_coarse_matrix(const ms_precond* pc, double* K0);
+/* Component microbenchmark: each hot-path kernel alone, `reps` launches
+ * timed with CUDA events on the context stream; ms[MS_BENCH_N] = mean ms. */
+enum {
+  MS_BENCH_MATVEC = 0,
+  MS_BENCH_LEVEL1 = 1,
+  MS_BENCH_RESTRICT = 2,
+  MS_BENCH_COARSE_SOLVE = 3,
+  MS_BENCH_COMBINE = 4,
+  MS_BENCH_COMBINE_L1 = 5,     /* level-1 overlap sum only  */
+  MS_BENCH_COMBINE_COARSE = 6, /* coarse prolongation only  */
+  MS_BENCH_N = 8
+};
+int ms_precond_bench(ms_precond* pc, int reps, double* ms);
 
 /* ---- PCG: pcg_solve (krylov.py:81-134) ------------------------------------
  * pc may be NULL (plain CG, the 'None' variant).  x0 = 0.  Stops when

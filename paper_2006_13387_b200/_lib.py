@@ -25,8 +25,9 @@ EXPORTS = (
     "ms_problem_create", "ms_problem_destroy", "ms_problem_n_free", "ms_problem_set_modulus",
     "ms_operator_apply", "ms_precond_build", "ms_precond_destroy", "ms_precond_apply",
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
-    "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream",
+    "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
 )
+BENCH_NAMES = ("matvec", "level1", "restrict", "coarse_solve", "combine", "combine_l1", "combine_coarse")
 PROF_NAMES = ("matvec", "update", "level1", "restrict", "coarse_solve", "combine")
 MS_PROF_N = 8
 
@@ -108,6 +109,7 @@ def load(path: str | os.PathLike | None = None):
         "ms_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
         "ms_ctx_profile_get": (C.c_int, [vp, dp, C.POINTER(C.c_longlong)]),
         "ms_ctx_stream": (C.c_void_p, [vp]),
+        "ms_precond_bench": (C.c_int, [vp, C.c_int, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

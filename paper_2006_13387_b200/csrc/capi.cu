@@ -331,7 +331,7 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
   }
   a = pf.begin(st);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
-                 pc->y0.p, r, z, sc, P->partials.p, beta_hist, st);
+                 pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st);
   pf.end(MS_PROF_COMBINE, it, st, a);
 }
 
@@ -538,7 +538,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
         int c = 0;
         for (int I = 0; I < (int)lo.size(); ++I)
           if (a >= lo[I] && a <= hi[I]) {
-            if (c == 4) throw Error(MS_E_INVALID, "a node is covered by more than 4 subdomains per axis");
+            if (c == 2) throw Error(MS_E_INVALID, "a node is covered by more than 2 subdomains per axis (overlap too large)");
             cov[a * 4 + c++] = I;
           }
       }
@@ -590,7 +590,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     cd.h = g.h;
     const int nc = cd.n_centers;
     const int NL = cd.NLx * cd.NLy;
-    if (NL < 4 * kEigBlock) throw Error(MS_E_INVALID, "neighbourhoods too small for the block eigensolver");
+    if (NL < 4 * kEigBlock || cd.mex < 4 || cd.mey < 4)
+      throw Error(MS_E_INVALID, "coarse blocks must be >= 4 elements per side (block eigensolver)");
     // heat Dirichlet node mask
     std::vector<uint8_t> hd(g.n_nodes, 0);
     for (int64_t nid : pc->heat_dir) {
@@ -766,7 +767,8 @@ int ms_precond_apply_coarse(ms_precond* pc, const double* r, double* z) {
   load_free(P, r, P->r.p);
   launch_restrict(P->g, pc->cd, P->r.p, pc->f0.p, nullptr, st);
   launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
-  launch_combine(P->g, P->mask.p, nullptr, &pc->cd, pc->y0.p, P->r.p, P->z.p, nullptr, nullptr, nullptr, st);
+  launch_combine(P->g, P->mask.p, nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, P->r.p, P->z.p,
+                 nullptr, nullptr, nullptr, st);
   store_free(P, P->z.p, z);
   MS_API_END(pc ? pc->prob->ctx : nullptr)
 }
@@ -781,6 +783,60 @@ int ms_precond_info_get(const ms_precond* pc, ms_precond_info* info, int* mode_c
   if (eigenvalues && pc->has_coarse)
     std::memcpy(eigenvalues, pc->h_evals.data(), pc->h_evals.size() * sizeof(double));
   MS_API_END(nullptr)
+}
+
+int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
+  MS_API_BEGIN
+  if (!pc || !ms || reps < 1) throw Error(MS_E_INVALID, "bad argument");
+  ms_problem* P = pc->prob;
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  const cudaStream_t st = P->ctx->st;
+  cudaEvent_t e0, e1;
+  MS_CUDA(cudaEventCreate(&e0));
+  MS_CUDA(cudaEventCreate(&e1));
+  auto timeit = [&](auto&& fn) {
+    fn();  // warm
+    MS_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < reps; ++i) fn();
+    MS_CUDA(cudaEventRecord(e1, st));
+    MS_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    MS_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    return (double)t / reps;
+  };
+  const Grid& g = P->g;
+  double* r = P->r.p;
+  for (int i = 0; i < MS_BENCH_N; ++i) ms[i] = 0.0;
+  ms[MS_BENCH_MATVEC] = timeit([&] {
+    launch_matvec(g, P->ke, P->E.p, P->mask.p, nullptr, r, nullptr, P->q.p, MV_PLAIN, nullptr, nullptr,
+                  nullptr, st);
+  });
+  if (pc->nsys > 0)
+    ms[MS_BENCH_LEVEL1] = timeit([&] {
+      launch_l1_solve(g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, nullptr, st);
+    });
+  if (pc->has_coarse) {
+    ms[MS_BENCH_RESTRICT] = timeit([&] { launch_restrict(g, pc->cd, r, pc->f0.p, nullptr, st); });
+    ms[MS_BENCH_COARSE_SOLVE] = timeit([&] {
+      launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
+    });
+    ms[MS_BENCH_COMBINE_COARSE] = timeit([&] {
+      launch_combine(g, P->mask.p, nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, P->z.p,
+                     nullptr, nullptr, nullptr, st);
+    });
+  }
+  if (pc->nsys > 0)
+    ms[MS_BENCH_COMBINE_L1] = timeit([&] {
+      launch_combine(g, P->mask.p, &pc->l1, nullptr, pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, P->z.p,
+                     nullptr, nullptr, nullptr, st);
+    });
+  ms[MS_BENCH_COMBINE] = timeit([&] {
+    launch_combine(g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
+                   pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, P->z.p, nullptr, nullptr, nullptr, st);
+  });
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  MS_API_END(pc ? pc->prob->ctx : nullptr)
 }
 
 int ms_precond_coarse_matrix(const ms_precond* pc, double* K0) {

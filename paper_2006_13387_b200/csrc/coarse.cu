@@ -166,63 +166,107 @@ void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double
 // combine: node-centric sum of the overlapping local solutions (in the
 // reference's J-major subdomain order, schwarz.py:79-81), then the coarse
 // prolongation; fused r.z reduction for PCG.
-constexpr int CB_X = 32, CB_Y = 8;
+// One CTA per coarse cell [ci*mex, (ci+1)*mex) x [cj*mey, (cj+1)*mey) (the last
+// cell row/column also owns the domain's far boundary nodes).  Every node of
+// the cell sees the same <= 4 coarse centres (ci..ci+1, cj..cj+1), so their
+// metadata and y0 entries are CTA-uniform registers; the per-node work is the
+// chi / psi loads and FMAs.  Level-1 covers: <= 2 per axis, unrolled 2x2 with
+// predicated loads.  Summation order: level-1 in J-major subdomain order,
+// coarse part in J-major centre order, then their sum.
+constexpr int kCombineThreads = 256;
 
-__global__ void __launch_bounds__(CB_X* CB_Y)
+__global__ void __launch_bounds__(kCombineThreads)
     k_combine(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, int has_l1, CoarseDev cd,
-              int has_coarse, const double* __restrict__ y0, const double* __restrict__ r,
-              double* __restrict__ z, PcgScalars* sc, double* partials, double* beta_hist) {
+              int has_coarse, int Nx, int Ny, const double* __restrict__ y0,
+              const double* __restrict__ r, double* __restrict__ z, PcgScalars* sc,
+              double* partials, double* beta_hist) {
   if (sc && sc->done) return;
-  __shared__ double sred[8];
+  __shared__ double sred[kCombineThreads / 32];
   const int64_t nn = g.n_nodes;
-  const int a = blockIdx.x * CB_X + threadIdx.x % CB_X, b = blockIdx.y * CB_Y + threadIdx.x / CB_X;
+  const int ci = blockIdx.x, cj = blockIdx.y;
+  const int mx = g.nx / Nx, my = g.ny / Ny;
+  const int a_lo = ci * mx, a_hi = (ci == Nx - 1) ? g.nx : a_lo + mx - 1;
+  const int b_lo = cj * my, b_hi = (cj == Ny - 1) ? g.ny : b_lo + my - 1;
+  const int w = a_hi - a_lo + 1, hgt = b_hi - b_lo + 1;
+  // the cell's coarse centres, J-major: (ci,cj) (ci+1,cj) (ci,cj+1) (ci+1,cj+1)
+  bool cok[4];
+  int ck[4], cns[4];
+  int64_t cpo[4];
+  __shared__ double cy[4][2 * kMaxModes + 1];
+  const int NL = has_coarse ? cd.NLx * cd.NLy : 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int I = ci + (c & 1), J = cj + (c >> 1);
+    cok[c] = has_coarse && I >= 1 && I <= Nx - 1 && J >= 1 && J <= Ny - 1;
+    ck[c] = cok[c] ? (J - 1) * (Nx - 1) + (I - 1) : 0;
+    cns[c] = cok[c] ? __ldg(cd.nsel + ck[c]) : 0;
+    cpo[c] = cok[c] ? __ldg(cd.psioff + ck[c]) : 0;
+  }
+  if (threadIdx.x < 4 * (2 * kMaxModes + 1)) {
+    const int c = threadIdx.x / (2 * kMaxModes + 1), m = threadIdx.x % (2 * kMaxModes + 1);
+    double v = 0.0;
+    if (cok[c]) {
+      if (m < 2 * cns[c])
+        v = y0[__ldg(cd.hoff + ck[c]) + m];
+      else if (m == 2 * kMaxModes && cd.enrich)
+        v = y0[cd.roff + ck[c]];
+    }
+    cy[c][m] = v;
+  }
+  __syncthreads();
   double dot = 0.0;
-  if (a <= g.nx && b <= g.ny) {
+  for (int t = threadIdx.x; t < w * hgt; t += kCombineThreads) {
+    const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
     const int64_t n = (int64_t)b * g.nnx + a;
     double zx = 0.0, zy = 0.0;
     if (has_l1) {
-      for (int tj = 0; tj < 4; ++tj) {
-        const int J = l1.ycov[b * 4 + tj];
-        if (J < 0) break;
-        const int y0_ = l1.ylo[J], hy = l1.ylen[J];
-        for (int ti = 0; ti < 4; ++ti) {
-          const int I = l1.xcov[a * 4 + ti];
-          if (I < 0) break;
-          const int x0_ = l1.xlo[I], wx = l1.xlen[I];
-          const int ln = (wx <= hy) ? (b - y0_) * wx + (a - x0_) : (a - x0_) * hy + (b - y0_);
-          const double2 v = *reinterpret_cast<const double2*>(l1.ybuf + l1.yoff[J * l1.NbX + I] + 2 * ln);
-          zx += v.x;
-          zy += v.y;
+      const int Js[2] = {l1.ycov[b * 4], l1.ycov[b * 4 + 1]};
+      const int Is[2] = {l1.xcov[a * 4], l1.xcov[a * 4 + 1]};
+      double2 v[2][2];
+#pragma unroll
+      for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti) {
+          const int J = Js[tj], I = Is[ti];
+          v[tj][ti] = make_double2(0.0, 0.0);
+          if (J >= 0 && I >= 0) {
+            const int y0_ = l1.ylo[J], hy = l1.ylen[J], x0_ = l1.xlo[I], wx = l1.xlen[I];
+            const int ln = (wx <= hy) ? (b - y0_) * wx + (a - x0_) : (a - x0_) * hy + (b - y0_);
+            v[tj][ti] = __ldg(reinterpret_cast<const double2*>(l1.ybuf + l1.yoff[J * l1.NbX + I] + 2 * ln));
+          }
         }
-      }
+#pragma unroll
+      for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti) {
+          zx += v[tj][ti].x;
+          zy += v[tj][ti].y;
+        }
     }
     if (has_coarse) {
       double cxs = 0.0, cys = 0.0;
-      const int NL = cd.NLx * cd.NLy;
-      const int ia = a / cd.mex, jb = b / cd.mey;
-      const int ilo = max(1, ia), ihi = min(cd.Nx - 1, a - ia * cd.mex ? ia + 1 : ia);
-      const int jlo = max(1, jb), jhi = min(cd.Ny - 1, b - jb * cd.mey ? jb + 1 : jb);
-      for (int J = jlo; J <= jhi; ++J)
-        for (int I = ilo; I <= ihi; ++I) {
-          const int k = center_index(cd, I, J);
-          const int ln = local_node(cd, I, J, a, b);
-          const double ch = cd.chi[(int64_t)k * NL + ln];
-          const int nsel = cd.nsel[k];
-          const double* ps = cd.psi + cd.psioff[k] + ln;
-          const double* yk = y0 + cd.hoff[k];
-          for (int m = 0; m < nsel; ++m) {
-            const double v = ch * ps[(int64_t)m * NL];
-            cxs += v * yk[2 * m];
-            cys += v * yk[2 * m + 1];
-          }
-          if (cd.enrich) {
-            double ex, ey;
-            rot_xy(cd, I, J, a, b, ex, ey);
-            const double yr = y0[cd.roff + k];
-            cxs += __dmul_rn(ch, ex) * yr;
-            cys += __dmul_rn(ch, ey) * yr;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!cok[c]) continue;
+        const int I = ci + (c & 1), J = cj + (c >> 1);
+        const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
+        const double ch = __ldg(cd.chi + (int64_t)ck[c] * NL + ln);
+        const double* ps = cd.psi + cpo[c] + ln;
+#pragma unroll
+        for (int m = 0; m < kMaxModes; ++m) {
+          if (m < cns[c]) {
+            const double vv = ch * __ldg(ps + (int64_t)m * NL);
+            cxs += vv * cy[c][2 * m];
+            cys += vv * cy[c][2 * m + 1];
           }
         }
+        if (cd.enrich) {
+          double ex, ey;
+          rot_xy(cd, I, J, a, b, ex, ey);
+          cxs += __dmul_rn(ch, ex) * cy[c][2 * kMaxModes];
+          cys += __dmul_rn(ch, ey) * cy[c][2 * kMaxModes];
+        }
+      }
       zx += cxs;
       zy += cys;
     }
@@ -230,7 +274,7 @@ __global__ void __launch_bounds__(CB_X* CB_Y)
     zy = mask[n + nn] ? zy : 0.0;
     z[n] = zx;
     z[n + nn] = zy;
-    if (sc) dot = zx * r[n] + zy * r[n + nn];
+    if (sc) dot += zx * r[n] + zy * r[n + nn];
   }
   if (!sc) return;
   const double bs = block_sum(dot, sred);
@@ -250,15 +294,14 @@ __global__ void __launch_bounds__(CB_X* CB_Y)
 }
 
 void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
-                    const double* y0, const double* r, double* z, PcgScalars* sc,
+                    int Nx, int Ny, const double* y0, const double* r, double* z, PcgScalars* sc,
                     double* partials, double* beta_hist, cudaStream_t st) {
   L1Dev l1v{};
   CoarseDev cdv{};
   if (l1) l1v = *l1;
   if (cd) cdv = *cd;
-  dim3 grid(div_up(g.nx + 1, CB_X), div_up(g.ny + 1, CB_Y));
-  k_combine<<<grid, CB_X * CB_Y, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0, y0, r, z, sc,
-                                          partials, beta_hist);
+  k_combine<<<dim3(Nx, Ny), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0, Nx,
+                                                      Ny, y0, r, z, sc, partials, beta_hist);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -690,16 +733,28 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void k_symv_reduce(int N, int nt, const double* __restrict__ part, double* __restrict__ y,
-                              const int* done) {
+// y_I = sum_J u(I,J) + sum_{I'>I} v(I',I): 8 groups of 64 threads split the
+// tile list, then a fixed-order combine -> deterministic.
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(T* kRedGroups)
+    k_symv_reduce(int N, int nt, const double* __restrict__ part, double* __restrict__ y,
+                  const int* done) {
   if (done && *(volatile const int*)done) return;
-  const int I = blockIdx.x, r = threadIdx.x;
-  const int row = I * T + r;
-  if (row >= N) return;
-  double s = 0.0;
-  for (int J = 0; J <= I; ++J) s += part[tile_index(I, J) * 2 * T + r];
-  for (int I2 = I + 1; I2 < nt; ++I2) s += part[tile_index(I2, I) * 2 * T + T + r];
-  y[row] = s;
+  __shared__ double s[kRedGroups][T];
+  const int I = blockIdx.x, r = threadIdx.x % T, grp = threadIdx.x / T;
+  double acc = 0.0;
+  for (int t = grp; t < nt; t += kRedGroups) {
+    acc += (t <= I) ? part[tile_index(I, t) * 2 * T + r] : part[tile_index(t, I) * 2 * T + T + r];
+  }
+  s[grp][r] = acc;
+  __syncthreads();
+  const int row = I * T + threadIdx.x;
+  if (threadIdx.x < T && row < N) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRedGroups; ++q) v += s[q][threadIdx.x];
+    y[row] = v;
+  }
 }
 
 void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
@@ -707,7 +762,7 @@ void launch_symv_packed(int N, const double* X, const double* f, double* y, doub
   if (N == 0) return;
   const int nt = div_up(N, T);
   k_symv_tiles<<<(unsigned)packed_tiles(nt), 256, 0, st>>>(N, nt, X, f, part, done);
-  k_symv_reduce<<<nt, T, 0, st>>>(N, nt, part, y, done);
+  k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done);
   MS_CUDA(cudaGetLastError());
 }
 

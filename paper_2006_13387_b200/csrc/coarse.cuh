@@ -50,7 +50,7 @@ void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double
 // z = sum_s R_s^T y_s (level-1, J-major order) + R0^T y0 (if cd) ; masked;
 // optionally r.z -> beta (PCG mode when sc != nullptr).
 void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
-                    const double* y0, const double* r, double* z, PcgScalars* sc,
+                    int Nx, int Ny, const double* y0, const double* r, double* z, PcgScalars* sc,
                     double* partials, double* beta_hist, cudaStream_t st);
 
 // K0 = R0 A R0^T (dense row-major N_c x N_c), symmetrised (coarse.py:161-168)

@@ -15,27 +15,32 @@ int reduce_blocks() { return 148 * 8; }
 // q = K p (masked), optionally p = z + beta p_old first, with the p.q
 // reduction and alpha = rz / (p.q) fused into the last CTA.
 //
-// One CTA = 32x8 nodes, one node per thread.  p (both components) and E are
-// staged in shared memory with a one-node / one-element halo; out-of-domain
-// entries are zero so the 4-element gather needs no branches.
-__global__ void __launch_bounds__(MV_TX* MV_TY)
+// One CTA = 32x32 nodes, 256 threads, 4 vertically stacked nodes per thread.
+// p (both components) and E are staged in shared memory with a one-node /
+// one-element halo (out-of-domain entries are zero, so no branches).  The
+// gather loops over the 4 corner roles c of a node inside its elements: the
+// two Ke0 rows of corner c are read once per thread and reused for the
+// thread's 4 nodes.
+constexpr int MV_NY = 32;  // nodes per CTA in y
+constexpr int MV_RPT = MV_NY / MV_TY;  // nodes per thread
+
+__global__ void __launch_bounds__(MV_TX* MV_TY, 3)
     k_matvec(Grid g, KeParam ke, const double* __restrict__ E, const uint8_t* __restrict__ mask,
              const double* __restrict__ z, const double* __restrict__ p_old,
              double* __restrict__ p_new, double* __restrict__ q, int mode, PcgScalars* sc,
              double* partials, double* alpha_hist) {
   if (mode == MV_PCG && sc->done) return;
-  __shared__ double sp[2][MV_TY + 2][MV_TX + 2];
-  __shared__ double sE[MV_TY + 1][MV_TX + 1];
+  __shared__ double sp[2][MV_NY + 2][MV_TX + 2];
+  __shared__ double sE[MV_NY + 1][MV_TX + 1];
   __shared__ double sred[MV_TX * MV_TY / 32];
 
-  const int a0 = blockIdx.x * MV_TX, b0 = blockIdx.y * MV_TY;
+  const int a0 = blockIdx.x * MV_TX, b0 = blockIdx.y * MV_NY;
   const int tid = threadIdx.x;
   const double beta = (mode == MV_PCG) ? sc->beta : 0.0;
   const int64_t nn = g.n_nodes;
 
-  // stage p (nodes a0-1 .. a0+MV_TX, b0-1 .. b0+MV_TY)
-  for (int t = tid; t < (MV_TY + 2) * (MV_TX + 2); t += blockDim.x) {
-    const int ly = t / (MV_TX + 2), lx = t % (MV_TX + 2);
+  for (int t = tid; t < (MV_NY + 2) * (MV_TX + 2); t += blockDim.x) {
+    const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
     const int a = a0 + lx - 1, b = b0 + ly - 1;
     double px = 0.0, py = 0.0;
     if (a >= 0 && a <= g.nx && b >= 0 && b <= g.ny) {
@@ -51,51 +56,64 @@ __global__ void __launch_bounds__(MV_TX* MV_TY)
     sp[0][ly][lx] = px;
     sp[1][ly][lx] = py;
   }
-  // stage E (elements a0-1 .. a0+MV_TX-1, b0-1 .. b0+MV_TY-1)
-  for (int t = tid; t < (MV_TY + 1) * (MV_TX + 1); t += blockDim.x) {
-    const int ly = t / (MV_TX + 1), lx = t % (MV_TX + 1);
+  for (int t = tid; t < (MV_NY + 1) * (MV_TX + 1); t += blockDim.x) {
+    const int ly = t / (MV_TX + 1), lx = t - ly * (MV_TX + 1);
     const int i = a0 + lx - 1, j = b0 + ly - 1;
     sE[ly][lx] = (i >= 0 && i < g.nx && j >= 0 && j < g.ny) ? E[(int64_t)j * g.nx + i] : 0.0;
   }
   __syncthreads();
 
   const int tx = tid % MV_TX, ty = tid / MV_TX;
-  const int a = a0 + tx, b = b0 + ty;
-  double dot = 0.0;
-  if (a <= g.nx && b <= g.ny) {
-    // elements around the node by their lower-left p-tile corner, with the
-    // node's corner number inside each (0:(i,j) 1:(i+1,j) 2:(i+1,j+1) 3:(i,j+1))
-    const int ex[4] = {tx, tx + 1, tx + 1, tx};
-    const int ey[4] = {ty, ty, ty + 1, ty + 1};
-    const int cn[4] = {2, 3, 0, 1};
-    double qx = 0.0, qy = 0.0;
+  const int X = tx + 1;                 // node column in the p tile
+  const int Y0 = ty * MV_RPT + 1;       // first node row in the p tile
+  double qx[MV_RPT], qy[MV_RPT];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const double Ee = sE[ey[e]][ex[e]];
-      const int c = cn[e];
-      const double ux[4] = {sp[0][ey[e]][ex[e]], sp[0][ey[e]][ex[e] + 1], sp[0][ey[e] + 1][ex[e] + 1],
-                            sp[0][ey[e] + 1][ex[e]]};
-      const double uy[4] = {sp[1][ey[e]][ex[e]], sp[1][ey[e]][ex[e] + 1], sp[1][ey[e] + 1][ex[e] + 1],
-                            sp[1][ey[e] + 1][ex[e]]};
-      double sx = 0.0, sy = 0.0;
+  for (int r = 0; r < MV_RPT; ++r) qx[r] = qy[r] = 0.0;
+  // corner role c of the node in element E(X+dx, Y+dy)
+  const int dxs[4] = {0, -1, -1, 0};
+  const int dys[4] = {0, 0, -1, -1};
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        sx += ke.k[c * 8 + m] * ux[m] + ke.k[c * 8 + 4 + m] * uy[m];
-        sy += ke.k[(4 + c) * 8 + m] * ux[m] + ke.k[(4 + c) * 8 + 4 + m] * uy[m];
-      }
-      qx += Ee * sx;
-      qy += Ee * sy;
+  for (int c = 0; c < 4; ++c) {
+    double kx[8], ky[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      kx[m] = ke.k[c * 8 + m];
+      ky[m] = ke.k[(4 + c) * 8 + m];
     }
-    const int64_t n = (int64_t)b * g.nnx + a;
-    qx = mask[n] ? qx : 0.0;
-    qy = mask[n + nn] ? qy : 0.0;
-    q[n] = qx;
-    q[n + nn] = qy;
-    if (mode == MV_PCG) {
-      const double px = sp[0][ty + 1][tx + 1], py = sp[1][ty + 1][tx + 1];
-      p_new[n] = px;
-      p_new[n + nn] = py;
-      dot = px * qx + py * qy;
+    const int ex = X + dxs[c];
+#pragma unroll
+    for (int r = 0; r < MV_RPT; ++r) {
+      const int ey = Y0 + r + dys[c];
+      const double Ee = sE[ey][ex];
+      const double u0 = sp[0][ey][ex], u1 = sp[0][ey][ex + 1], u2 = sp[0][ey + 1][ex + 1],
+                   u3 = sp[0][ey + 1][ex];
+      const double v0 = sp[1][ey][ex], v1 = sp[1][ey][ex + 1], v2 = sp[1][ey + 1][ex + 1],
+                   v3 = sp[1][ey + 1][ex];
+      const double sx = kx[0] * u0 + kx[1] * u1 + kx[2] * u2 + kx[3] * u3 + kx[4] * v0 +
+                        kx[5] * v1 + kx[6] * v2 + kx[7] * v3;
+      const double sy = ky[0] * u0 + ky[1] * u1 + ky[2] * u2 + ky[3] * u3 + ky[4] * v0 +
+                        ky[5] * v1 + ky[6] * v2 + ky[7] * v3;
+      qx[r] += Ee * sx;
+      qy[r] += Ee * sy;
+    }
+  }
+  double dot = 0.0;
+  const int a = a0 + tx;
+#pragma unroll
+  for (int r = 0; r < MV_RPT; ++r) {
+    const int b = b0 + ty * MV_RPT + r;
+    if (a <= g.nx && b <= g.ny) {
+      const int64_t n = (int64_t)b * g.nnx + a;
+      const double ox = mask[n] ? qx[r] : 0.0;
+      const double oy = mask[n + nn] ? qy[r] : 0.0;
+      q[n] = ox;
+      q[n + nn] = oy;
+      if (mode == MV_PCG) {
+        const double px = sp[0][Y0 + r][X], py = sp[1][Y0 + r][X];
+        p_new[n] = px;
+        p_new[n + nn] = py;
+        dot += px * ox + py * oy;
+      }
     }
   }
   if (mode != MV_PCG) return;
@@ -113,7 +131,7 @@ __global__ void __launch_bounds__(MV_TX* MV_TY)
 void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                    const double* z, const double* p_old, double* p_new, double* q, int mode,
                    PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st) {
-  dim3 grid(div_up(g.nx + 1, MV_TX), div_up(g.ny + 1, MV_TY));
+  dim3 grid(div_up(g.nx + 1, MV_TX), div_up(g.ny + 1, MV_NY));
   k_matvec<<<grid, MV_TX * MV_TY, 0, st>>>(g, ke, E, mask, z, p_old, p_new, q, mode, sc, partials,
                                            alpha_hist);
   MS_CUDA(cudaGetLastError());

@@ -110,6 +110,12 @@ class TwoLevelPreconditioner:
         """R0^T K0^-1 R0 r (CoarseOperator.apply_inverse, coarse.py:156-158)."""
         return self._call(_lib.load().ms_precond_apply_coarse, r)
 
+    def bench_components(self, reps=20):
+        """Each hot-path kernel timed alone (CUDA events), ms per launch."""
+        out = np.zeros(8)
+        _lib.check(_lib.load().ms_precond_bench(self.handle, int(reps), _lib.dptr(out)), self.op._ctx.handle)
+        return {n: float(out[i]) for i, n in enumerate(_lib.BENCH_NAMES)}
+
     def coarse_matrix(self):
         N = self.coarse_dim
         K0 = np.empty((N, N))
