@@ -1,0 +1,135 @@
+"""CPU-only checks: the C-ABI library loads and exports what include/msgpu.h
+declares (no CUDA calls), the host-side API logic, config generators, and the
+oracle's ARPACK eigen path against the dense reference eigenvalues."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+from oracle import mselast_oracle as O
+from paper_2006_13387_b200 import _lib, configs
+import paper_2006_13387_b200 as G
+
+HEADER = ROOT / "include" / "msgpu.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ms_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    decl = declared_functions()
+    assert decl, "no declarations parsed"
+    assert set(decl) == set(_lib.EXPORTS), set(decl) ^ set(_lib.EXPORTS)
+    for name in decl:
+        assert hasattr(lib, name), name
+    m = re.search(r"#define MSGPU_ABI_VERSION (\d+)", HEADER.read_text())
+    assert lib.ms_abi_version() == int(m.group(1))
+
+
+def test_status_codes_map_to_reference_exceptions():
+    for code, exc in ((_lib.MS_E_INVALID, ValueError), (_lib.MS_E_NOT_SPD, ValueError),
+                      (_lib.MS_E_NOMEM, MemoryError), (_lib.MS_E_CUDA, RuntimeError)):
+        with pytest.raises(exc):
+            _lib.check(code)
+    _lib.check(_lib.MS_OK)
+
+
+def test_struct_layouts_match_header():
+    # sizes of the ABI structs as the C compiler lays them out (x86-64)
+    import ctypes as C
+
+    # 5 ints (+4 pad), double, 4 ints, pointer, int64
+    assert C.sizeof(_lib.PrecondOpts) == 5 * 4 + 4 + 8 + 4 * 4 + 8 + 8
+    assert C.sizeof(_lib.Report) == 8 + 4 + 4 + 8 * 3
+
+
+def test_variant_table_and_errors():
+    assert set(G.VARIANTS) == {"EE", "EE;Rand", "HH", "HH+Rot", "EH", "EH+Rot", "EH+Rot;Rand"}
+    assert G.get_variant("EH+Rot").enrich and not G.get_variant("EH").enrich
+    with pytest.raises(ValueError):
+        G.get_variant("XX")
+    assert G.EigOptions().n_max == 6
+
+
+def test_grid_and_coefficient_validation():
+    with pytest.raises(ValueError):
+        G.build_fine_mesh(0, 3)
+    mesh = G.build_fine_mesh(8, 8)
+    with pytest.raises(ValueError):
+        G.build_coarse_partition(mesh, 3, 3)
+    part = G.build_coarse_partition(mesh, 4, 4)
+    assert part.n_neighborhoods == 9 and part.mex == 2
+    with pytest.raises(ValueError):
+        G.CoefficientField(np.full(64, 2.0), 0.3, 0.1, 1.0)
+    assert np.allclose(G.simp_modulus([0.0, 1.0], 3, 1e-3, 1.0), [1e-3, 1.0])
+    with pytest.raises(ValueError):
+        G.simp_modulus([1.5], 3, 1e-3, 1.0)
+    f = G.build_load_vector(mesh, G.LoadSpec([(3, 1, -1.0)]))
+    assert f[3 + mesh.n_nodes] == -1.0 and f.sum() == -1.0
+
+
+def test_config_boundary_conditions():
+    c = configs.config1(seed=0)
+    nn = c.n_nodes
+    # cantilever: whole left-edge nodes clamped, unit downward load at right-edge midpoint
+    left = np.arange(0, nn, c.nx + 1)
+    assert np.array_equal(np.sort(c.constrained_dofs), np.sort(np.concatenate([left, left + nn])))
+    assert c.load_full.sum() == -1.0 and c.load_full[(c.ny // 2) * (c.nx + 1) + c.nx + nn] == -1.0
+    m = configs.config4(seed=0, nx=64, ny=32, H=16)
+    nn = m.n_nodes
+    assert m.heat_dirichlet_nodes.size == 0
+    assert (64 + nn) in m.constrained_dofs and 0 in m.constrained_dofs and nn not in m.constrained_dofs
+    assert m.load_full[32 * 65 + nn] == -1.0
+    assert abs(configs.config3(seed=1, n=64, H=16).meta["volume"] - 0.4) < 1e-6
+
+
+def test_config5_sequence_is_seeded_and_bounded():
+    seq = list(configs.config5_densities(seed=0, n=32, steps=3))
+    assert len(seq) == 3 and all(0.0 <= r.min() and r.max() <= 1.0 for r in seq)
+    assert not np.array_equal(seq[0], seq[1])
+    seq2 = list(configs.config5_densities(seed=0, n=32, steps=3))
+    assert all(np.array_equal(a, b) for a, b in zip(seq, seq2))
+
+
+def test_arpack_eigen_path_matches_dense_reference():
+    g = load_golden("ref_bench100_eta1e+06.npz")
+    mesh = O.mesh_for(100, 100)
+    part = O.Partition(mesh, 10, 10)
+    for k in (0, 40, 80):
+        K, M, _ = O.local_heat_problem(mesh, g["E"], part.omegas[k], g["dirichlet_nodes"])
+        w, v = O.lowest_eigenpairs_arpack(K, M, 7)
+        assert np.allclose(w, g["eigenvalues"][k], rtol=1e-9, atol=1e-12 * abs(g["eigenvalues"][k]).max())
+        assert O.gap_count(w, 6) == g["mode_counts"][k]
+
+
+def test_bench_level1_dof_count_matches_oracle_blocks():
+    import bench
+
+    spec = configs.config1(seed=0)
+    mesh = O.mesh_for(spec.nx, spec.ny)
+    total = 0
+    for rect in O.block_rects(mesh, spec.H, spec.delta):
+        a0, a1, b0, b1 = O.subdomain_node_rect(mesh, rect, True)
+        total += 2 * (a1 - a0 + 1) * (b1 - b0 + 1)
+    assert bench.level1_dofs(spec) == total
+
+
+def test_product_path_has_no_cpu_fallback(tmp_path):
+    with pytest.raises(ImportError):
+        _lib.load(tmp_path / "missing.so")
+    mesh = G.build_fine_mesh(4, 4)
+    part = G.build_coarse_partition(mesh, 2, 2)
+    coeff = G.CoefficientField(np.ones(16), 0.3, 1.0, 1.0)
+    with pytest.raises(TypeError):
+        G.build_preconditioner("EH+Rot", object(), mesh, part, coeff, [])
+    with pytest.raises(NotImplementedError):
+        G.build_preconditioner("EE", object(), mesh, part, coeff, [])
+    with pytest.raises(TypeError):
+        G.pcg_solve(np.eye(3), np.ones(3))
