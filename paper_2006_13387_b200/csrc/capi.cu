@@ -23,6 +23,8 @@
 
 using namespace msgpu;
 
+constexpr int kPcgChunk = 8;  // iterations per host convergence poll / graph replay
+
 namespace {
 
 std::mutex g_err_mu;
@@ -125,37 +127,64 @@ void heat_elements(double h, HeatParam& hp) {
 
 // Optional CUDA-event profiling of every hot-path kernel launch, tagged with
 // the PCG iteration it belongs to (launches after convergence are dropped).
+// Launches of PCG iteration i use the fixed event pair tab[i % chunk][comp],
+// so the same recording works under CUDA-graph capture (event-record nodes):
+// after each replay the captured pairs are re-queued with their iteration.
 struct Prof {
   bool on = false;
   double ms[MS_PROF_N] = {};
   long long cnt[MS_PROF_N] = {};
   std::vector<cudaEvent_t> pool;
+  cudaEvent_t tab[kPcgChunk][MS_PROF_N][2] = {};
+  bool capturing = false;
   struct Rec {
     int comp, it;
     cudaEvent_t a, b;
   };
   std::vector<Rec> pending;
+  std::vector<std::pair<int, int>> captured;  // (comp, iteration within chunk)
+  cudaEvent_t make() {
+    cudaEvent_t e;
+    MS_CUDA(cudaEventCreate(&e));
+    return e;
+  }
   cudaEvent_t get() {
-    if (pool.empty()) {
-      cudaEvent_t e;
-      MS_CUDA(cudaEventCreate(&e));
-      return e;
-    }
+    if (pool.empty()) return make();
     cudaEvent_t e = pool.back();
     pool.pop_back();
     return e;
   }
-  cudaEvent_t begin(cudaStream_t st) {
+  // under capture an event must be recorded as an external node to be timed
+  void record(cudaEvent_t e, cudaStream_t st) {
+    if (capturing)
+      MS_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else
+      MS_CUDA(cudaEventRecord(e, st));
+  }
+  cudaEvent_t slot(int comp, int it, int side) {
+    cudaEvent_t& e = tab[it % kPcgChunk][comp][side];
+    if (!e) e = make();
+    return e;
+  }
+  cudaEvent_t begin(int comp, int it, cudaStream_t st) {
     if (!on) return nullptr;
-    cudaEvent_t a = get();
-    MS_CUDA(cudaEventRecord(a, st));
+    cudaEvent_t a = it >= 0 ? slot(comp, it, 0) : get();
+    record(a, st);
     return a;
   }
   void end(int comp, int it, cudaStream_t st, cudaEvent_t a) {
     if (!on) return;
-    cudaEvent_t b = get();
-    MS_CUDA(cudaEventRecord(b, st));
-    pending.push_back({comp, it, a, b});
+    cudaEvent_t b = it >= 0 ? slot(comp, it, 1) : get();
+    record(b, st);
+    if (capturing)
+      captured.push_back({comp, it % kPcgChunk});
+    else
+      pending.push_back({comp, it, a, b});
+  }
+  // after a replay of the captured chunk starting at iteration it0
+  void replayed(int it0) {
+    for (const auto& c : captured)
+      pending.push_back({c.first, it0 + c.second, tab[c.second][c.first][0], tab[c.second][c.first][1]});
   }
   // call after a stream sync; keep records of iterations < valid_iters
   void flush(int valid_iters) {
@@ -166,8 +195,10 @@ struct Prof {
         ms[r.comp] += t;
         cnt[r.comp] += 1;
       }
-      pool.push_back(r.a);
-      pool.push_back(r.b);
+      if (r.it < 0) {
+        pool.push_back(r.a);
+        pool.push_back(r.b);
+      }
     }
     pending.clear();
   }
@@ -196,6 +227,14 @@ struct ms_problem {
   DBuf<double> partials;
   DBuf<double> hres, halpha, hbeta;
   int hcap = 0;
+  // captured PCG chunk (CUDA graph) of plain CG solves; preconditioned solves
+  // keep theirs in the ms_precond (it captures both objects' buffers)
+  cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;
+  std::vector<std::pair<int, int>> captured;
+  ~ms_problem() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (gexec_prof) cudaGraphExecDestroy(gexec_prof);
+  }
   void ensure_workspace() {
     if (x.p) return;
     const cudaStream_t st = ctx->st;
@@ -227,12 +266,18 @@ struct ms_precond {
   CoarseDev cd{};
   DBuf<int> nsel, hoff;
   DBuf<int64_t> psioff;
-  DBuf<double> psi, chi, K0inv, f0, y0, part, evals, K0keep;
+  DBuf<double> psi, chi, K0inv, f0, y0, part, evals, K0keep, chi4, psi4, rpart;
   std::vector<int> h_nsel;
   std::vector<double> h_evals;
   int N_c = 0;
   int max_pass = 0;
   ms_precond_info info{};
+  cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;  // captured PCG chunks for (prob, this)
+  std::vector<std::pair<int, int>> captured;
+  ~ms_precond() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (gexec_prof) cudaGraphExecDestroy(gexec_prof);
+  }
 };
 
 #define MS_API_BEGIN try {
@@ -309,27 +354,30 @@ static void level1_axis(int n_el, int nblocks, int kind, int delta, std::vector<
 }
 
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
+// `restricted`: the cell restriction partials of r were already produced
+// (fused into the residual update); only their reduction remains.
 static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgScalars* sc,
-                               double* beta_hist, int it = -1) {
+                               double* beta_hist, int it = -1, bool restricted = false) {
   ms_problem* P = pc->prob;
   const cudaStream_t st = P->ctx->st;
   Prof& pf = P->ctx->prof;
   const int* done = sc ? &sc->done : nullptr;
   cudaEvent_t a;
   if (pc->nsys > 0) {
-    a = pf.begin(st);
+    a = pf.begin(MS_PROF_LEVEL1, it, st);
     launch_l1_solve(P->g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
     pf.end(MS_PROF_LEVEL1, it, st, a);
   }
   if (pc->has_coarse) {
-    a = pf.begin(st);
-    launch_restrict(P->g, pc->cd, r, pc->f0.p, done, st);
+    a = pf.begin(MS_PROF_RESTRICT, it, st);
+    if (!restricted) launch_restrict_cells(P->g, pc->cd, r, done, st);
+    launch_restrict_reduce(pc->cd, pc->f0.p, done, st);
     pf.end(MS_PROF_RESTRICT, it, st, a);
-    a = pf.begin(st);
+    a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
     launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st);
     pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
   }
-  a = pf.begin(st);
+  a = pf.begin(MS_PROF_COMBINE, it, st);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
                  pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st);
   pf.end(MS_PROF_COMBINE, it, st, a);
@@ -687,6 +735,14 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     cd.psi = pc->psi.p;
     cd.chi = pc->chi.p;
     launch_pou_table(g, cd, pc->chi.p, st);
+    pc->chi4.alloc((size_t)g.n_nodes * 4);
+    pc->psi4.alloc((size_t)g.n_nodes * 4);
+    pc->rpart.alloc((size_t)o->Nx * o->Ny * 4 * kSlots);
+    pc->rpart.zero(st);
+    launch_node_tables(g, cd, pc->chi4.p, pc->psi4.p, st);
+    cd.chi4 = pc->chi4.p;
+    cd.psi4 = pc->psi4.p;
+    cd.rpart = pc->rpart.p;
     // K0 = R0 A R0^T, symmetrised, inverted
     const int N = pc->N_c;
     DBuf<double> K0;
@@ -765,7 +821,8 @@ int ms_precond_apply_coarse(ms_precond* pc, const double* r, double* z) {
   const cudaStream_t st = P->ctx->st;
   MS_CUDA(cudaSetDevice(P->ctx->device));
   load_free(P, r, P->r.p);
-  launch_restrict(P->g, pc->cd, P->r.p, pc->f0.p, nullptr, st);
+  launch_restrict_cells(P->g, pc->cd, P->r.p, nullptr, st);
+  launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st);
   launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
   launch_combine(P->g, P->mask.p, nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, P->r.p, P->z.p,
                  nullptr, nullptr, nullptr, st);
@@ -816,7 +873,10 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
       launch_l1_solve(g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, nullptr, st);
     });
   if (pc->has_coarse) {
-    ms[MS_BENCH_RESTRICT] = timeit([&] { launch_restrict(g, pc->cd, r, pc->f0.p, nullptr, st); });
+    ms[MS_BENCH_RESTRICT] = timeit([&] {
+      launch_restrict_cells(g, pc->cd, r, nullptr, st);
+      launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st);
+    });
     ms[MS_BENCH_COARSE_SOLVE] = timeit([&] {
       launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
     });
@@ -887,27 +947,59 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
   int it = 0;
   int done = 0;
-  const int chunk = 8;
-  while (!done && it < maxit) {
-    const int upto = std::min(maxit, it + chunk);
-    for (; it < upto; ++it) {
-      double* pold = (it & 1) ? P->p1.p : P->p0.p;
-      double* pnew = (it & 1) ? P->p0.p : P->p1.p;
-      Prof& pf = P->ctx->prof;
-      cudaEvent_t a = pf.begin(st);
-      launch_matvec(P->g, P->ke, P->E.p, P->mask.p, zp, pold, pnew, P->q.p, MV_PCG, P->sc.p,
-                    P->partials.p, P->halpha.p, st);
-      pf.end(MS_PROF_MATVEC, it, st, a);
-      a = pf.begin(st);
+  const int chunk = kPcgChunk;
+  auto launch_iter = [&](int i) {
+    double* pold = (i & 1) ? P->p1.p : P->p0.p;
+    double* pnew = (i & 1) ? P->p0.p : P->p1.p;
+    Prof& pf = P->ctx->prof;
+    cudaEvent_t a = pf.begin(MS_PROF_MATVEC, i, st);
+    launch_matvec(P->g, P->ke, P->E.p, P->mask.p, zp, pold, pnew, P->q.p, MV_PCG, P->sc.p,
+                  P->partials.p, P->halpha.p, st);
+    pf.end(MS_PROF_MATVEC, i, st, a);
+    a = pf.begin(MS_PROF_UPDATE, i, st);
+    const bool fused = pc && pc->has_coarse;
+    if (fused)  // residual update + coarse restriction partials in one pass
+      launch_update_restrict(P->g, n, P->x.p, pnew, P->r.p, P->q.p, pc->cd, P->sc.p, P->partials.p,
+                             P->hres.p, st);
+    else
       launch_pcg_update(n, P->x.p, pnew, P->r.p, P->q.p, P->sc.p, P->partials.p, P->hres.p, st);
-      pf.end(MS_PROF_UPDATE, it, st, a);
-      if (pc) {
-        precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, it);
-      } else {
-        a = pf.begin(st);
-        launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
-        pf.end(MS_PROF_COMBINE, it, st, a);
-      }
+    pf.end(MS_PROF_UPDATE, i, st, a);
+    if (pc) {
+      precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, i, fused);
+    } else {
+      a = pf.begin(MS_PROF_COMBINE, i, st);
+      launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
+      pf.end(MS_PROF_COMBINE, i, st, a);
+    }
+  };
+  // A chunk of iterations (even length, so the p double-buffer parity is the
+  // same at every chunk start) is captured once per (problem, preconditioner)
+  // into a CUDA graph and replayed; the device `done` flag turns iterations
+  // past convergence into no-ops.  Profiling mode launches directly.
+  Prof& prof = P->ctx->prof;
+  const bool use_graph = maxit >= chunk;
+  cudaGraphExec_t& gexec = prof.on ? (pc ? pc->gexec_prof : P->gexec_prof) : (pc ? pc->gexec : P->gexec);
+  if (use_graph && !gexec) {
+    cudaGraph_t graph;
+    prof.capturing = true;
+    prof.captured.clear();
+    MS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < chunk; ++i) launch_iter(i);
+    MS_CUDA(cudaStreamEndCapture(st, &graph));
+    prof.capturing = false;
+    MS_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+    MS_CUDA(cudaGraphDestroy(graph));
+    if (prof.on) (pc ? pc->captured : P->captured) = prof.captured;
+  }
+  if (prof.on && use_graph) prof.captured = pc ? pc->captured : P->captured;
+  while (!done && it < maxit) {
+    if (use_graph && it + chunk <= maxit) {
+      MS_CUDA(cudaGraphLaunch(gexec, st));
+      if (prof.on) prof.replayed(it);
+      it += chunk;
+    } else {
+      const int upto = std::min(maxit, it + chunk);
+      for (; it < upto; ++it) launch_iter(it);
     }
     MS_CUDA(cudaMemcpyAsync(&hs, P->sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     MS_CUDA(cudaStreamSynchronize(st));
@@ -927,7 +1019,10 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   if (alphas && iters > 0) MS_CUDA(cudaMemcpy(alphas, P->halpha.p, iters * sizeof(double), cudaMemcpyDefault));
   if (betas && iters > 1) MS_CUDA(cudaMemcpy(betas, P->hbeta.p, (iters - 1) * sizeof(double), cudaMemcpyDefault));
   if (rep) {
-    rep->kernel_launches = 1 + precond_launches(pc) + (int64_t)iters * (2 + precond_launches(pc));
+    // init: norm + precond (its restriction is not fused: +1); per iteration:
+    // matvec, update(+restriction partials), precond
+    rep->kernel_launches = 1 + precond_launches(pc) + ((pc && pc->has_coarse) ? 1 : 0) +
+                           (int64_t)iters * (2 + precond_launches(pc));
     rep->iterations = iters;
     rep->converged = hs.converged;
     rep->final_residual = hs.res;

@@ -90,7 +90,6 @@ __device__ __forceinline__ int basis_row(const CoarseDev& cd, int k, int bi, int
 // template parameter (dispatched per CTA), so the 2*NM+1 accumulators live in
 // registers and are reduced together: one shuffle tree per value and a
 // single shared-memory pass.  Node rows map onto lanes (coalesced r/psi/chi).
-constexpr int kMaxModes = 6;
 
 template <int NM>
 __device__ __forceinline__ void restrict_center(const Grid& g, const CoarseDev& cd, int k, int I,
@@ -166,6 +165,227 @@ void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double
 // combine: node-centric sum of the overlapping local solutions (in the
 // reference's J-major subdomain order, schwarz.py:79-81), then the coarse
 // prolongation; fused r.z reduction for PCG.
+// ---------------------------------------------------------------------------
+// Node-major coarse tables: for each node, the chi (and chi * psi_0) of the
+// 4 corner centres of its coarse cell, so the per-iteration restriction and
+// prolongation read one contiguous 32-byte record per node instead of 4-8
+// scattered per-centre streams.
+__device__ __forceinline__ void node_cell(const Grid& g, const CoarseDev& cd, int a, int b, int& ci,
+                                          int& cj) {
+  ci = min(a / cd.mex, cd.Nx - 1);
+  cj = min(b / cd.mey, cd.Ny - 1);
+}
+
+__global__ void k_node_tables(Grid g, CoarseDev cd, double* __restrict__ chi4,
+                              double* __restrict__ psi4) {
+  const int NL = cd.NLx * cd.NLy;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(n % g.nnx), b = (int)(n / g.nnx);
+    int ci, cj;
+    node_cell(g, cd, a, b, ci, cj);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int I = ci + (c & 1), J = cj + (c >> 1);
+      double ch = 0.0, ps = 0.0;
+      if (I >= 1 && I <= cd.Nx - 1 && J >= 1 && J <= cd.Ny - 1) {
+        const int k = center_index(cd, I, J), ln = local_node(cd, I, J, a, b);
+        ch = cd.chi[(int64_t)k * NL + ln];
+        ps = __dmul_rn(ch, cd.psi[cd.psioff[k] + ln]);
+      }
+      chi4[n * 4 + c] = ch;
+      psi4[n * 4 + c] = ps;
+    }
+  }
+}
+
+void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double* psi4,
+                        cudaStream_t st) {
+  if (cd.n_centers == 0) return;
+  k_node_tables<<<148 * 8, 256, 0, st>>>(g, cd, chi4, psi4);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Cell-tiled restriction, optionally fused with the PCG residual update.
+// One CTA per coarse cell accumulates, for each of its <= 4 corner centres,
+// the mode-0 x/y rows and the rotation row over the cell's nodes (extra modes
+// in a second pass), and writes them to rpart[cell][corner][slot]; the
+// partials of the 4 cells around a centre are summed in a fixed order by
+// k_restrict_reduce.  With UPD, the same pass performs x += alpha p,
+// r -= alpha q and the ||r||^2 grid reduction / convergence test.
+constexpr int kCellThreads = 256;
+
+template <bool UPD>
+__global__ void __launch_bounds__(kCellThreads)
+    k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, double* __restrict__ x,
+                    const double* __restrict__ p, double* __restrict__ r,
+                    const double* __restrict__ q, PcgScalars* sc, double* partials,
+                    double* res_hist, const int* done) {
+  if (UPD ? sc->done : (done && *(volatile const int*)done)) return;
+  __shared__ double sred[13 * (kCellThreads / 32)];
+  const int64_t nn = g.n_nodes;
+  const int ci = blockIdx.x, cj = blockIdx.y, Nx = gridDim.x, Ny = gridDim.y;
+  const int mx = g.nx / Nx, my = g.ny / Ny;
+  const int a_lo = ci * mx, a_hi = (ci == Nx - 1) ? g.nx : a_lo + mx - 1;
+  const int b_lo = cj * my, b_hi = (cj == Ny - 1) ? g.ny : b_lo + my - 1;
+  const int w = a_hi - a_lo + 1, hgt = b_hi - b_lo + 1;
+  const double alpha = UPD ? sc->alpha : 0.0;
+  bool cok[4];
+  int cns[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int I = ci + (c & 1), J = cj + (c >> 1);
+    cok[c] = has_coarse && I >= 1 && I <= Nx - 1 && J >= 1 && J <= Ny - 1;
+    cns[c] = cok[c] ? __ldg(cd.nsel + (J - 1) * (Nx - 1) + (I - 1)) : 0;
+  }
+  double acc[13];
+#pragma unroll
+  for (int v = 0; v < 13; ++v) acc[v] = 0.0;  // [4 corners][x, y, rot] + ||r||^2
+  for (int t = threadIdx.x; t < w * hgt; t += kCellThreads) {
+    const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
+    const int64_t n = (int64_t)b * g.nnx + a;
+    double rx = r[n], ry = r[n + nn];
+    if (UPD) {
+      x[n] += alpha * p[n];
+      x[n + nn] += alpha * p[n + nn];
+      rx -= alpha * q[n];
+      ry -= alpha * q[n + nn];
+      r[n] = rx;
+      r[n + nn] = ry;
+      acc[12] += rx * rx + ry * ry;
+    }
+    if (has_coarse) {
+      const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n;
+      const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n;
+      const double2 c4a = __ldg(c2), c4b = __ldg(c2 + 1), p4a = __ldg(p2), p4b = __ldg(p2 + 1);
+      const double ch4[4] = {c4a.x, c4a.y, c4b.x, c4b.y};
+      const double ps4[4] = {p4a.x, p4a.y, p4b.x, p4b.y};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int I = ci + (c & 1), J = cj + (c >> 1);
+        double ex, ey;
+        rot_xy(cd, I, J, a, b, ex, ey);
+        acc[3 * c] += ps4[c] * rx;
+        acc[3 * c + 1] += ps4[c] * ry;
+        acc[3 * c + 2] += __dmul_rn(ch4[c], ex) * rx + __dmul_rn(ch4[c], ey) * ry;
+      }
+    }
+  }
+  // one multi-value block reduction (13 values)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < 13; ++v) {
+    const double s = warp_sum(acc[v]);
+    if (lane == 0) sred[v * (kCellThreads / 32) + warp] = s;
+  }
+  __syncthreads();
+  double* rp = cd.rpart + ((int64_t)cj * Nx + ci) * 4 * kSlots;
+  __shared__ double rrblk;
+  if (threadIdx.x < 13) {
+    double s = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < kCellThreads / 32; ++w2) s += sred[threadIdx.x * (kCellThreads / 32) + w2];
+    if (threadIdx.x == 12) {
+      rrblk = s;
+    } else if (has_coarse) {
+      const int c = threadIdx.x / 3, v = threadIdx.x % 3;
+      rp[c * kSlots + (v == 2 ? 2 * kMaxModes : v)] = s;
+    }
+  }
+  // extra modes (rare): second pass over the cell for corners with nsel > 1
+  if (has_coarse && (cns[0] > 1 || cns[1] > 1 || cns[2] > 1 || cns[3] > 1)) {
+    __syncthreads();  // r of this cell is final
+    const int NL = cd.NLx * cd.NLy;
+    for (int c = 0; c < 4; ++c) {
+      const int I = ci + (c & 1), J = cj + (c >> 1);
+      if (cns[c] <= 1) continue;
+      const int k = (J - 1) * (Nx - 1) + (I - 1);
+      const double* psk = cd.psi + __ldg(cd.psioff + k);
+      for (int m = 1; m < cns[c]; ++m) {
+        double sx = 0.0, sy = 0.0;
+        for (int t = threadIdx.x; t < w * hgt; t += kCellThreads) {
+          const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
+          const int64_t n = (int64_t)b * g.nnx + a;
+          const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
+          const double v = cd.chi4[n * 4 + c] * __ldg(psk + (int64_t)m * NL + ln);
+          sx += v * r[n];
+          sy += v * r[n + nn];
+        }
+        const double tx = block_sum(sx, sred), ty = block_sum(sy, sred);
+        if (threadIdx.x == 0) {
+          rp[c * kSlots + 2 * m] = tx;
+          rp[c * kSlots + 2 * m + 1] = ty;
+        }
+      }
+    }
+  }
+  if (!UPD) return;
+  __syncthreads();
+  double tot;
+  if (grid_reduce_last(threadIdx.x == 0 ? rrblk : 0.0, partials, &sc->tickets[1], &tot, sred)) {
+    if (threadIdx.x == 0) {
+      sc->rr = tot;
+      const double res = sqrt(tot) / sc->bnorm;
+      sc->res = res;
+      sc->iter += 1;
+      if (res_hist) res_hist[sc->iter] = res;
+      if (res <= sc->tol) {
+        sc->converged = 1;
+        sc->done = 1;
+      } else if (sc->iter >= sc->maxit) {
+        sc->done = 1;
+      }
+    }
+  }
+}
+
+void launch_update_restrict(const Grid& g, int64_t n_full, double* x, const double* p, double* r,
+                            const double* q, const CoarseDev& cd, PcgScalars* sc,
+                            double* partials, double* res_hist, cudaStream_t st) {
+  (void)n_full;
+  k_cell_restrict<true><<<dim3(cd.Nx, cd.Ny), kCellThreads, 0, st>>>(g, cd, 1, x, p, r, q, sc,
+                                                                     partials, res_hist, nullptr);
+  MS_CUDA(cudaGetLastError());
+}
+
+void launch_restrict_cells(const Grid& g, const CoarseDev& cd, const double* r, const int* done,
+                           cudaStream_t st) {
+  k_cell_restrict<false><<<dim3(cd.Nx, cd.Ny), kCellThreads, 0, st>>>(
+      g, cd, 1, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+  MS_CUDA(cudaGetLastError());
+}
+
+// f0 rows of centre k = sum of the partials of the 4 cells around it, in
+// J-major cell order; centre (I, J) is corner (I-ci) + 2 (J-cj) of cell (ci, cj)
+__global__ void k_restrict_reduce(CoarseDev cd, double* __restrict__ f0, const int* done) {
+  if (done && *(volatile const int*)done) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = t / kSlots, slot = t % kSlots;
+  if (k >= cd.n_centers) return;
+  const int nsel = cd.nsel[k];
+  const bool rot = slot == 2 * kMaxModes;
+  if (!(slot < 2 * nsel || (rot && cd.enrich))) return;
+  const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
+  double s = 0.0;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx) {
+      const int ci = I - 1 + dx, cj = J - 1 + dy;
+      const int c = (I - ci) + 2 * (J - cj);
+      s += cd.rpart[((int64_t)cj * cd.Nx + ci) * 4 * kSlots + c * kSlots + slot];
+    }
+  f0[rot ? cd.roff + k : cd.hoff[k] + slot] = s;
+}
+
+void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cudaStream_t st) {
+  if (cd.n_centers == 0) return;
+  const int total = cd.n_centers * kSlots;
+  k_restrict_reduce<<<div_up(total, 256), 256, 0, st>>>(cd, f0, done);
+  MS_CUDA(cudaGetLastError());
+}
+
 // One CTA per coarse cell [ci*mex, (ci+1)*mex) x [cj*mey, (cj+1)*mey) (the last
 // cell row/column also owns the domain's far boundary nodes).  Every node of
 // the cell sees the same <= 4 coarse centres (ci..ci+1, cj..cj+1), so their
@@ -245,17 +465,22 @@ __global__ void __launch_bounds__(kCombineThreads)
     }
     if (has_coarse) {
       double cxs = 0.0, cys = 0.0;
+      const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n;
+      const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n;
+      const double2 c4a = __ldg(c2), c4b = __ldg(c2 + 1), p4a = __ldg(p2), p4b = __ldg(p2 + 1);
+      const double ch4[4] = {c4a.x, c4a.y, c4b.x, c4b.y};
+      const double ps4[4] = {p4a.x, p4a.y, p4b.x, p4b.y};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (!cok[c]) continue;
         const int I = ci + (c & 1), J = cj + (c >> 1);
-        const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
-        const double ch = __ldg(cd.chi + (int64_t)ck[c] * NL + ln);
-        const double* ps = cd.psi + cpo[c] + ln;
-#pragma unroll
-        for (int m = 0; m < kMaxModes; ++m) {
-          if (m < cns[c]) {
-            const double vv = ch * __ldg(ps + (int64_t)m * NL);
+        cxs += ps4[c] * cy[c][0];
+        cys += ps4[c] * cy[c][1];
+        if (cns[c] > 1) {  // rare: extra modes from the per-centre store
+          const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
+          const double* ps = cd.psi + cpo[c] + ln;
+          for (int m = 1; m < cns[c]; ++m) {
+            const double vv = ch4[c] * __ldg(ps + (int64_t)m * NL);
             cxs += vv * cy[c][2 * m];
             cys += vv * cy[c][2 * m + 1];
           }
@@ -263,8 +488,8 @@ __global__ void __launch_bounds__(kCombineThreads)
         if (cd.enrich) {
           double ex, ey;
           rot_xy(cd, I, J, a, b, ex, ey);
-          cxs += __dmul_rn(ch, ex) * cy[c][2 * kMaxModes];
-          cys += __dmul_rn(ch, ey) * cy[c][2 * kMaxModes];
+          cxs += __dmul_rn(ch4[c], ex) * cy[c][2 * kMaxModes];
+          cys += __dmul_rn(ch4[c], ey) * cy[c][2 * kMaxModes];
         }
       }
       zx += cxs;

@@ -38,7 +38,28 @@ struct CoarseDev {
   const int64_t* psioff;  // per centre: offset into psi (nsel * NL values)
   const double* psi;      // selected eigenvectors on closed omega, lexicographic
   const double* chi;      // per centre: partition of unity on closed omega (NL values)
+  // node-major tables over the coarse cell containing each node: the 4 corner
+  // centres (ci + (c&1), cj + (c>>1)), c = 0..3, J-major; zero where invalid
+  const double* chi4;     // [n_nodes][4] chi of the corner centres
+  const double* psi4;     // [n_nodes][4] chi * psi (mode 0) of the corner centres
+  double* rpart;          // [Nx*Ny cells][4][2*kMaxModes+1] restriction partials
 };
+
+constexpr int kMaxModes = 6;
+constexpr int kSlots = 2 * kMaxModes + 1;  // heat x/y per mode + rotation
+
+// node-major chi4 / psi4 from the per-centre tables
+void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double* psi4,
+                        cudaStream_t st);
+
+// fused x += alpha p, r -= alpha q, ||r||^2 -> convergence, and restriction
+// partial sums per coarse cell; then f0 = sum of the 4 cell partials per centre
+void launch_update_restrict(const Grid& g, int64_t n_full, double* x, const double* p, double* r,
+                            const double* q, const CoarseDev& cd, PcgScalars* sc,
+                            double* partials, double* res_hist, cudaStream_t st);
+void launch_restrict_cells(const Grid& g, const CoarseDev& cd, const double* r, const int* done,
+                           cudaStream_t st);
+void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cudaStream_t st);
 
 // chi table, bit-identical to the reference's PoU (grid.py:172-207)
 void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStream_t st);
