@@ -693,7 +693,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       launch_band_potrf(hsysd.p, nk, mbw, hLc.p, hLr.p, fail.p, st);
       check_fail(fail, st, "neighbourhood heat pencil (K + sigma M)");
       EigBatch eb{o->Nx, cd.mex, cd.mey, k0, nk, hsysd.p, hLc.p, hLr.p, work.p, pc->evals.p,
-                  evecs.p, passes.p, neumann.p, o->n_max, o->gap_threshold, o->fixed_rule};
+                  evecs.p, passes.p, neumann.p, o->n_max, o->gap_threshold, o->fixed_rule,
+                  1e-15 * 24.0 / (g.h * g.h)};
       launch_subspace(g, P->E.p, hdir.p, hp, eb, 300, 1e-12, st);
       launch_select(nc, pc->evals.p, o->n_max, o->gap_threshold, o->fixed_rule, pc->nsel.p, st);
       std::vector<int> bsel(nk);

@@ -461,7 +461,10 @@ __global__ void __launch_bounds__(kEigThreads)
       bool conv = pass >= 3 && sel == (int)misc[3];
       for (int i = 0; i < need; ++i) {
         const double t = (i + off < sel) ? tol : 1e-8;
-        if (fabs(ritz[i] - ritz_old[i]) > t * fabs(ritz[i]) + 1e-15 * scale) conv = false;
+        // absolute floor: Ritz values of tiny (island) modes jitter at the
+        // round-off level eps * lambda_max of the pencil
+        if (fabs(ritz[i] - ritz_old[i]) > t * fabs(ritz[i]) + fmax(1e-15 * scale, eb.lam_floor))
+          conv = false;
       }
       for (int i = 0; i < P; ++i) ritz_old[i] = ritz[i];
       misc[3] = (double)sel;

@@ -28,6 +28,7 @@ struct EigBatch {
   int n_max;           // selection parameters, used by the stopping rule
   double gap;
   int fixed;
+  double lam_floor;  // absolute convergence floor for Ritz values
 };
 
 // B = K_H + sigma M_H in band form (Dirichlet nodes -> identity rows)
