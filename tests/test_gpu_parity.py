@@ -243,3 +243,55 @@ def test_coarse_apply_matches_oracle(rng):
     for _ in range(3):
         r = rng.standard_normal(op.n_free)
         assert rel(pre.apply_coarse(r), Po.coarse.apply(r)) <= 1e-8
+
+
+def test_config5_sequence_rebuild_matches_oracle():
+    """Config-5 shape at 64^2: density sequence, set_modulus + full rebuild per step."""
+    import scipy.sparse.linalg as spla
+
+    n, H, delta = 64, 16, 2
+    base = configs.config5(seed=1, step=0, n=n, H=H, delta=delta)
+    mesh = G.build_fine_mesh(n, n)
+    op = None
+    for k, rho in enumerate(configs.config5_densities(seed=1, n=n, steps=3)):
+        E = configs.simp(rho, E_min=base.E_min)
+        coeff = G.CoefficientField(E, 0.3, base.E_min, 1.0)
+        if op is None:
+            op = G.ElasticityOperator(mesh, coeff, base.free_dofs())
+        else:
+            op.set_modulus(E)
+        part = G.build_coarse_partition(mesh, n // H, n // H)
+        pre = G.build_preconditioner("EH+Rot", op, mesh, part, coeff, base.heat_dirichlet_nodes,
+                                     level1="blocks", delta=delta)
+        x, rep = G.pcg_solve(op, base.rhs(), pre, tol=1e-8, maxit=5000)
+        spec = configs.ProblemSpec(name="c5", nx=n, ny=n, E=E, E_min=base.E_min, E_max=1.0,
+                                   constrained_dofs=base.constrained_dofs,
+                                   heat_dirichlet_nodes=base.heat_dirichlet_nodes,
+                                   load_full=base.load_full, H=H, delta=delta)
+        prob = O.problem_from_spec(spec)
+        P = O.build_two_level(prob, H=H, delta=delta, level1_mode="blocks")
+        xo, repo = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=5000)
+        assert pre.coarse_dim == P.coarse_dim and pre.mode_counts == P.info["mode_counts"], k
+        assert rep.converged and abs(rep.iterations - repo.iterations) <= max(3, int(0.06 * repo.iterations))
+        x_dir = spla.spsolve(prob.op.matrix.tocsc(), prob.b)
+        assert rel(x, x_dir) <= max(1e-8, 2.0 * rel(xo, x_dir)), k
+
+
+def test_profiling_and_graph_paths_agree():
+    """Direct launches, CUDA-graph replay and graph replay with event
+    profiling must give bit-identical solves."""
+    from paper_2006_13387_b200 import _lib
+
+    g, mesh, op, pre = _bench("1e+06")
+    lib = _lib.load()
+    x_small, r_small = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=7)  # < one chunk: direct launches
+    x_graph, r_graph = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=2000)
+    lib.ms_ctx_set_profiling(op._ctx.handle, 1)
+    try:
+        x_prof, r_prof = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=2000)
+        x_prof7, _ = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=7)
+    finally:
+        lib.ms_ctx_set_profiling(op._ctx.handle, 0)
+    assert np.array_equal(x_graph, x_prof) and r_graph.iterations == r_prof.iterations
+    assert np.array_equal(x_small, x_prof7)
+    assert r_graph.residuals[:8] == r_small.residuals[:8]
