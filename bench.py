@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--local-solver", choices=("banded", "dense"), default="banded",
+                    help="level-1 local solves: banded Cholesky sweeps (default) or explicit packed inverses")
     ap.add_argument("--maxit", type=int, default=1000,
                     help="PCG iteration cap per step (config 3 needs O(1e4) iterations to reach 1e-8)")
     return ap.parse_args()
@@ -215,7 +217,7 @@ def run_ours(args):
     else:
         spec = configs.config3(seed=args.seed + rank, n=args.n or 2048)
     t_gen = time.perf_counter() - t0
-    mesh, op, pre = setup_spec(spec)
+    mesh, op, pre = setup_spec(spec, local_solver=args.local_solver)
     n_free = op.n_free
     lib = _lib.load()
     ctx = op._ctx.handle
@@ -302,7 +304,7 @@ def run_ours(args):
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("k_l1_solve")
+            traffic = json.loads(tp.read_text()).get("k_l1_solve" if args.local_solver == "banded" else "k_l1_dense_apply")
         except Exception:
             traffic = None
 
@@ -326,7 +328,8 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_free,
                 "d2h_bytes_per_step": 8 * n_free + 8 * (3 * (e2e_iters // max(args.e2e_steps, 1)) + 1),
                 "iterations": e2e_iters / max(args.e2e_steps, 1)},
-        "roofline": {"bound": "hbm", "kernel": "k_l1_solve (batched banded fwd/bwd sweeps)",
+        "roofline": {"bound": "hbm", "kernel": ("k_l1_solve (batched banded fwd/bwd sweeps)" if args.local_solver == "banded"
+                                                else "k_l1_dense_apply (batched packed explicit-inverse SYMV)"),
                      "achieved": l1_gbs, "peak": hbm, "unit": "GB/s", "frac": l1_gbs / hbm,
                      "traffic": traffic, "bytes_per_launch": l1_bytes, "ms_per_launch": l1_ms,
                      "peak_kind": pk_kind,

@@ -257,7 +257,9 @@ struct ms_precond {
   int NbX = 0, NbY = 0, nsys = 0, max_bw = 0;
   std::vector<BandSys> hsys;
   DBuf<BandSys> sys;
-  DBuf<double> Lc, Lr, ybuf;
+  DBuf<double> Lc, Lr, ybuf, Xinv;
+  bool dense = false;  // MS_LOCAL_DENSE_INV: packed explicit inverses in Xinv
+  int dense_nt = 0;
   DBuf<int> xcov, ycov, xlo_d, xlen_d, ylo_d, ylen_d;
   DBuf<int64_t> yoff_d;
   L1Dev l1{};
@@ -365,7 +367,10 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
   cudaEvent_t a;
   if (pc->nsys > 0) {
     a = pf.begin(MS_PROF_LEVEL1, it, st);
-    launch_l1_solve(P->g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
+    if (pc->dense)
+      launch_l1_dense_apply(P->g, pc->sys.p, pc->nsys, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
+    else
+      launch_l1_solve(P->g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
     pf.end(MS_PROF_LEVEL1, it, st, a);
   }
   if (pc->has_coarse) {
@@ -541,7 +546,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
   if (o->n_max > kNeig - 1) throw Error(MS_E_INVALID, "n_max > 6 is not supported by the GPU eigensolver");
   if (o->level1_kind == MS_LEVEL1_BLOCKS && o->delta < 1)
     throw Error(MS_E_INVALID, "block level-1 needs overlap delta >= 1");
-  if (o->local_solver != MS_LOCAL_BANDED) throw Error(MS_E_INVALID, "local solver not available");
+  if (o->local_solver != MS_LOCAL_BANDED && o->local_solver != MS_LOCAL_DENSE_INV)
+    throw Error(MS_E_INVALID, "unknown local solver");
   std::unique_ptr<ms_precond> pc(new ms_precond());
   pc->prob = P;
   pc->device = P->ctx->device;
@@ -597,13 +603,34 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->xcov.upload(xcov.data(), xcov.size(), st);
     pc->ycov.upload(ycov.data(), ycov.size(), st);
     pc->Lc.alloc(foff);
-    pc->Lr.alloc(foff);
     pc->ybuf.alloc(yoff);
-    pc->Lr.zero(st);
     fail.zero(st);
     launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p, pc->nsys, pc->Lc.p, st);
-    launch_band_potrf(pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
-    check_fail(fail, st, "level-1 subdomain matrix");
+    pc->dense = o->local_solver == MS_LOCAL_DENSE_INV;
+    if (!pc->dense) {
+      pc->Lr.alloc(foff);
+      pc->Lr.zero(st);
+      launch_band_potrf(pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
+      check_fail(fail, st, "level-1 subdomain matrix");
+    } else {
+      // explicit inverses: band -> packed tiles, batched tiled Cholesky inverse
+      int max_n = 0;
+      for (const BandSys& b : pc->hsys) max_n = std::max(max_n, b.n);
+      pc->dense_nt = div_up(max_n, kTile);
+      const int64_t mw = packed_words(pc->dense_nt);
+      pc->Xinv.alloc((size_t)pc->nsys * mw);
+      const int B = std::min(pc->nsys, 256);
+      DBuf<double> Pw, Ww;
+      Pw.alloc((size_t)B * mw);
+      Ww.alloc((size_t)B * mw);
+      for (int s0 = 0; s0 < pc->nsys; s0 += B) {
+        const int nb = std::min(B, pc->nsys - s0);
+        launch_band_to_tiles(pc->sys.p, s0, nb, pc->dense_nt, pc->Lc.p, Pw.p, st);
+        dense_spd_inverse_batched(pc->dense_nt, nb, Pw.p, Ww.p, pc->Xinv.p + (size_t)s0 * mw, fail.p, st);
+      }
+      check_fail(fail, st, "level-1 subdomain matrix");
+      pc->Lc.release();
+    }
     {
       std::vector<int> xl(pc->NbX), yl(pc->NbY);
       for (int I = 0; I < pc->NbX; ++I) xl[I] = xhi[I] - xlo[I] + 1;
@@ -619,7 +646,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->xlo_d.p, pc->xlen_d.p, pc->ylo_d.p, pc->ylen_d.p,
                    pc->yoff_d.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
     pc->info.n_subdomains = pc->nsys;
-    pc->info.local_bytes = (double)foff * 2 * sizeof(double);
+    pc->info.local_bytes = pc->dense ? (double)pc->nsys * packed_words(pc->dense_nt) * sizeof(double)
+                                     : (double)foff * 2 * sizeof(double);
   }
   MS_CUDA(cudaEventRecord(e1, st));
 
@@ -871,7 +899,10 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
   });
   if (pc->nsys > 0)
     ms[MS_BENCH_LEVEL1] = timeit([&] {
-      launch_l1_solve(g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, nullptr, st);
+      if (pc->dense)
+        launch_l1_dense_apply(g, pc->sys.p, pc->nsys, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, nullptr, st);
+      else
+        launch_l1_solve(g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, nullptr, st);
     });
   if (pc->has_coarse) {
     ms[MS_BENCH_RESTRICT] = timeit([&] {

@@ -637,358 +637,4 @@ void launch_symmetrize(int N, double* A, cudaStream_t st) {
   MS_CUDA(cudaGetLastError());
 }
 
-// ---------------------------------------------------------------------------
-// Dense SPD inverse by tiled Cholesky (potrf), triangular inverse (trtri) and
-// L^-T L^-1 (lauum), all on packed 64x64 lower tiles.  Replaces LAPACK
-// ?potrf/?potrs (coarse.py:143,154): applying the explicit packed inverse is
-// one bandwidth-bound SYMV per PCG iteration instead of two latency-bound
-// triangular sweeps.
-constexpr int T = kTile;
-constexpr int kTT = 256;  // threads per tile CTA (16 x 16, 4 x 4 outputs each)
-
-struct TileAcc {
-  double v[4][4];
-};
-
-// acc += sA * sB where sA[r][q], sB[q][c] are 64x64 row-major in smem
-__device__ __forceinline__ void tile_mma(TileAcc& acc, const double* sA, const double* sB) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll 4
-  for (int q = 0; q < T; ++q) {
-    double a[4], b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = sA[(ty + 16 * i) * T + q];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sB[q * T + tx + 16 * j];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc.v[i][j] += a[i] * b[j];
-  }
-}
-
-// load a 64x64 tile (row-major, contiguous) into smem, optionally transposed
-__device__ __forceinline__ void tile_load(double* s, const double* g, bool trans) {
-  for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
-    const int r = t / T, c = t % T;
-    if (trans)
-      s[c * T + r] = g[t];
-    else
-      s[t] = g[t];
-  }
-}
-
-__device__ __forceinline__ void acc_zero(TileAcc& a) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) a.v[i][j] = 0.0;
-}
-
-__device__ __forceinline__ void acc_store(const TileAcc& a, double* g, double scale, bool add) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int idx = (ty + 16 * i) * T + tx + 16 * j;
-      g[idx] = add ? g[idx] + scale * a.v[i][j] : scale * a.v[i][j];
-    }
-}
-
-__global__ void k_pack_tiles(int N, int nt, const double* __restrict__ A, double* __restrict__ P) {
-  const int64_t total = packed_tiles(nt) * T * T;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t tile = t / (T * T);
-    const int within = (int)(t % (T * T));
-    // invert tile index -> (i, j)
-    int i = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
-    while ((int64_t)(i + 1) * (i + 2) / 2 <= tile) ++i;
-    while ((int64_t)i * (i + 1) / 2 > tile) --i;
-    const int j = (int)(tile - (int64_t)i * (i + 1) / 2);
-    const int r = i * T + within / T, c = j * T + within % T;
-    double v;
-    if (r < N && c < N)
-      v = A[(int64_t)r * N + c];
-    else
-      v = (r == c) ? 1.0 : 0.0;
-    P[t] = v;
-  }
-}
-
-// Cholesky of diagonal tile k in place (lower), plus its triangular inverse
-// written to Winv (tile k,k of the trtri array).
-__global__ void __launch_bounds__(kTT) k_potrf_tile(int k, int N, double* __restrict__ P,
-                                                    double* __restrict__ W, int* fail) {
-  extern __shared__ double sm[];
-  double* a = sm;          // 64 x 64
-  double* inv = sm + T * T;
-  double* D = P + tile_index(k, k) * T * T;
-  tile_load(a, D, false);
-  __syncthreads();
-  for (int c = 0; c < T; ++c) {
-    double d = a[c * T + c];
-    if (!(d > 0.0)) {
-      if (threadIdx.x == 0) atomicCAS(fail, 0, k * T + c + 1);
-      d = 1.0;
-    }
-    const double s = sqrt(d);
-    __syncthreads();
-    if (threadIdx.x == 0) a[c * T + c] = s;
-    for (int r = c + 1 + threadIdx.x; r < T; r += blockDim.x) a[r * T + c] /= s;
-    __syncthreads();
-    for (int t = threadIdx.x; t < (T - c - 1) * (T - c - 1); t += blockDim.x) {
-      const int r = c + 1 + t / (T - c - 1), q = c + 1 + t % (T - c - 1);
-      if (q <= r) a[r * T + q] -= a[r * T + c] * a[q * T + c];
-    }
-    __syncthreads();
-  }
-  // zero the strict upper triangle, write L back
-  for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
-    const int r = t / T, c = t % T;
-    if (c > r) a[t] = 0.0;
-    D[t] = a[t];
-  }
-  __syncthreads();
-  // inverse of lower-triangular L: column j solves L x = e_j by forward
-  // substitution; thread j owns column j (64 columns).
-  if (threadIdx.x < T) {
-    const int j = threadIdx.x;
-    for (int r = 0; r < T; ++r) {
-      double s = (r == j) ? 1.0 : 0.0;
-      for (int q = j; q < r; ++q) s -= a[r * T + q] * inv[q * T + j];
-      inv[r * T + j] = (r < j) ? 0.0 : s / a[r * T + r];
-    }
-  }
-  __syncthreads();
-  double* Wk = W + tile_index(k, k) * T * T;
-  for (int t = threadIdx.x; t < T * T; t += blockDim.x) Wk[t] = inv[t];
-}
-
-// panel: L_ik = A_ik L_kk^-T = A_ik (Winv_kk)^T, i > k
-__global__ void __launch_bounds__(kTT) k_trsm_tiles(int k, int nt, double* __restrict__ P,
-                                                    const double* __restrict__ W) {
-  extern __shared__ double sm[];
-  double* sA = sm;
-  double* sB = sm + T * T;
-  const int i = k + 1 + blockIdx.x;
-  double* Aik = P + tile_index(i, k) * T * T;
-  tile_load(sA, Aik, false);
-  tile_load(sB, W + tile_index(k, k) * T * T, true);  // sB[q][c] = Winv[c][q]
-  __syncthreads();
-  TileAcc acc;
-  acc_zero(acc);
-  tile_mma(acc, sA, sB);
-  __syncthreads();
-  acc_store(acc, Aik, 1.0, false);
-}
-
-// trailing update A_ij -= L_ik L_jk^T for k < j <= i
-__global__ void __launch_bounds__(kTT) k_syrk_tiles(int k, int nt, double* __restrict__ P) {
-  extern __shared__ double sm[];
-  double* sA = sm;
-  double* sB = sm + T * T;
-  // blockIdx.x enumerates (i, j) pairs with k < j <= i < nt
-  const int m = nt - k - 1;
-  int64_t t = blockIdx.x;
-  int ii = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(ii + 1) * (ii + 2) / 2 <= t) ++ii;
-  while ((int64_t)ii * (ii + 1) / 2 > t) --ii;
-  const int jj = (int)(t - (int64_t)ii * (ii + 1) / 2);
-  if (ii >= m) return;
-  const int i = k + 1 + ii, j = k + 1 + jj;
-  tile_load(sA, P + tile_index(i, k) * T * T, false);
-  tile_load(sB, P + tile_index(j, k) * T * T, true);
-  __syncthreads();
-  TileAcc acc;
-  acc_zero(acc);
-  tile_mma(acc, sA, sB);
-  acc_store(acc, P + tile_index(i, j) * T * T, -1.0, true);
-}
-
-// W_ij = -W_ii * sum_{l=j}^{i-1} L_il W_lj for i = j + d
-__global__ void __launch_bounds__(kTT) k_trtri_tiles(int d, int nt, const double* __restrict__ P,
-                                                     double* __restrict__ W) {
-  extern __shared__ double sm[];
-  double* sA = sm;
-  double* sB = sm + T * T;
-  const int j = blockIdx.x, i = j + d;
-  TileAcc acc;
-  acc_zero(acc);
-  for (int l = j; l < i; ++l) {
-    __syncthreads();
-    tile_load(sA, P + tile_index(i, l) * T * T, false);
-    tile_load(sB, W + tile_index(l, j) * T * T, false);
-    __syncthreads();
-    tile_mma(acc, sA, sB);
-  }
-  __syncthreads();
-  // sB <- acc, sA <- W_ii ; result = -(W_ii acc)
-  {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) sB[(ty + 16 * a) * T + tx + 16 * b] = acc.v[a][b];
-  }
-  tile_load(sA, W + tile_index(i, i) * T * T, false);
-  __syncthreads();
-  TileAcc out;
-  acc_zero(out);
-  tile_mma(out, sA, sB);
-  acc_store(out, W + tile_index(i, j) * T * T, -1.0, false);
-}
-
-// X_ij = sum_{l >= i} W_li^T W_lj  (i >= j) = (L^-T L^-1)_ij
-__global__ void __launch_bounds__(kTT) k_lauum_tiles(int nt, const double* __restrict__ W,
-                                                     double* __restrict__ X) {
-  extern __shared__ double sm[];
-  double* sA = sm;
-  double* sB = sm + T * T;
-  const int64_t t = blockIdx.x;
-  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
-  while ((int64_t)i * (i + 1) / 2 > t) --i;
-  const int j = (int)(t - (int64_t)i * (i + 1) / 2);
-  TileAcc acc;
-  acc_zero(acc);
-  for (int l = i; l < nt; ++l) {
-    __syncthreads();
-    tile_load(sA, W + tile_index(l, i) * T * T, true);  // sA[r][q] = W_li[q][r]
-    tile_load(sB, W + tile_index(l, j) * T * T, false);
-    __syncthreads();
-    tile_mma(acc, sA, sB);
-  }
-  acc_store(acc, X + tile_index(i, j) * T * T, 1.0, false);
-}
-
-size_t dense_spd_inverse_work_bytes(int N) {
-  const int nt = div_up(N, T);
-  return (size_t)packed_tiles(nt) * T * T * sizeof(double) * 2;
-}
-
-void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work, int* fail,
-                       cudaStream_t st) {
-  if (N == 0) return;
-  const int nt = div_up(N, T);
-  const int64_t ptiles = packed_tiles(nt);
-  double* P = work;                      // Cholesky factor tiles
-  double* W = work + ptiles * T * T;     // L^-1 tiles
-  const size_t smem = 2 * T * T * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    MS_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MS_CUDA(cudaFuncSetAttribute(k_trsm_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MS_CUDA(cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MS_CUDA(cudaFuncSetAttribute(k_trtri_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MS_CUDA(cudaFuncSetAttribute(k_lauum_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, P);
-  MS_CUDA(cudaMemsetAsync(W, 0, ptiles * T * T * sizeof(double), st));
-  for (int k = 0; k < nt; ++k) {
-    k_potrf_tile<<<1, kTT, smem, st>>>(k, N, P, W, fail);
-    const int m = nt - k - 1;
-    if (m > 0) {
-      k_trsm_tiles<<<m, kTT, smem, st>>>(k, nt, P, W);
-      k_syrk_tiles<<<(unsigned)((int64_t)m * (m + 1) / 2), kTT, smem, st>>>(k, nt, P);
-    }
-  }
-  for (int d = 1; d < nt; ++d) k_trtri_tiles<<<nt - d, kTT, smem, st>>>(d, nt, P, W);
-  k_lauum_tiles<<<(unsigned)ptiles, kTT, smem, st>>>(nt, W, packed_inv);
-  MS_CUDA(cudaGetLastError());
-}
-
-// ---------------------------------------------------------------------------
-// packed-tile SYMV: per tile, u = X_IJ f_J (-> y_I) and, off the diagonal,
-// v = X_IJ^T f_I (-> y_J); partials are reduced in a fixed order.
-__global__ void __launch_bounds__(256)
-    k_symv_tiles(int N, int nt, const double* __restrict__ X, const double* __restrict__ f,
-                 double* __restrict__ part, const int* done) {
-  if (done && *(volatile const int*)done) return;
-  __shared__ double sv[16][T + 1];
-  const int64_t t = blockIdx.x;
-  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
-  while ((int64_t)i * (i + 1) / 2 > t) --i;
-  const int j = (int)(t - (int64_t)i * (i + 1) / 2);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const double* Xt = X + t * T * T;
-  double fj[4], fi[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int cj = j * T + tx * 4 + q, ri = i * T + ty * 4 + q;
-    fj[q] = cj < N ? f[cj] : 0.0;
-    fi[q] = ri < N ? f[ri] : 0.0;
-  }
-  double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
-    const double2 x01 = __ldg(row), x23 = __ldg(row + 1);
-    u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
-    v[0] += x01.x * fi[rr];
-    v[1] += x01.y * fi[rr];
-    v[2] += x23.x * fi[rr];
-    v[3] += x23.y * fi[rr];
-  }
-  // u: reduce over tx (16 lanes of a half warp)
-#pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
-  }
-  double* pu = part + t * 2 * T;
-  double* pv = pu + T;
-  if (tx == 0) {
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) pu[ty * 4 + rr] = u[rr];
-  }
-  if (i != j) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sv[ty][tx * 4 + q] = v[q];
-    __syncthreads();
-    if (threadIdx.x < T) {
-      double s = 0.0;
-#pragma unroll
-      for (int g = 0; g < 16; ++g) s += sv[g][threadIdx.x];
-      pv[threadIdx.x] = s;
-    }
-  }
-}
-
-// y_I = sum_J u(I,J) + sum_{I'>I} v(I',I): 8 groups of 64 threads split the
-// tile list, then a fixed-order combine -> deterministic.
-constexpr int kRedGroups = 8;
-__global__ void __launch_bounds__(T* kRedGroups)
-    k_symv_reduce(int N, int nt, const double* __restrict__ part, double* __restrict__ y,
-                  const int* done) {
-  if (done && *(volatile const int*)done) return;
-  __shared__ double s[kRedGroups][T];
-  const int I = blockIdx.x, r = threadIdx.x % T, grp = threadIdx.x / T;
-  double acc = 0.0;
-  for (int t = grp; t < nt; t += kRedGroups) {
-    acc += (t <= I) ? part[tile_index(I, t) * 2 * T + r] : part[tile_index(t, I) * 2 * T + T + r];
-  }
-  s[grp][r] = acc;
-  __syncthreads();
-  const int row = I * T + threadIdx.x;
-  if (threadIdx.x < T && row < N) {
-    double v = 0.0;
-#pragma unroll
-    for (int q = 0; q < kRedGroups; ++q) v += s[q][threadIdx.x];
-    y[row] = v;
-  }
-}
-
-void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
-                        const int* done, cudaStream_t st) {
-  if (N == 0) return;
-  const int nt = div_up(N, T);
-  k_symv_tiles<<<(unsigned)packed_tiles(nt), 256, 0, st>>>(N, nt, X, f, part, done);
-  k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done);
-  MS_CUDA(cudaGetLastError());
-}
-
 }  // namespace msgpu

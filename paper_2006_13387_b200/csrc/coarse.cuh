@@ -2,6 +2,7 @@
 #pragma once
 
 #include "banded.cuh"
+#include "dense.cuh"
 #include "common.cuh"
 #include "operator.cuh"
 
@@ -79,21 +80,5 @@ void launch_k0_assemble(const Grid& g, const KeParam& ke, const double* E, const
                         const CoarseDev& cd, double* K0, double* scratch, int n_cta,
                         cudaStream_t st);
 void launch_symmetrize(int N, double* A, cudaStream_t st);
-
-// ---- dense SPD inverse in packed 64x64 tiles ------------------------------
-constexpr int kTile = 64;
-__host__ __device__ inline int64_t packed_tiles(int nt) { return (int64_t)nt * (nt + 1) / 2; }
-__host__ __device__ inline int64_t tile_index(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
-
-// A (row-major N x N, lower triangle read) -> packed-tile lower inverse.
-// Returns (via *fail) 1 + the failing pivot row on a non-positive pivot.
-void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work, int* fail,
-                       cudaStream_t st);
-size_t dense_spd_inverse_work_bytes(int N);
-
-// y = X f for X symmetric stored as packed lower tiles.  `part` needs
-// packed_tiles(nt) * 2 * kTile doubles.
-void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
-                        const int* done, cudaStream_t st);
 
 }  // namespace msgpu

@@ -1,0 +1,504 @@
+// Batched dense SPD inverses on packed 64x64 lower tiles, and their SYMVs.
+//
+// Used twice:
+//  * the coarse operator K0 (batch 1): replaces LAPACK ?potrf/?potrs
+//    (coarse.py:143,154) -- applying the explicit packed inverse is one
+//    bandwidth-bound SYMV per PCG iteration instead of two latency-bound
+//    triangular sweeps;
+//  * the MS_LOCAL_DENSE_INV level-1 variant (batch = subdomains): the
+//    "overlapping local subdomain inverses as batched dense fp64 GEMV" of the
+//    design brief, replacing SuperLU (schwarz.py:97-109).
+// Tiled right-looking Cholesky (potrf/trsm/syrk), triangular inverse (trtri)
+// and L^-T L^-1 (lauum); every tile kernel takes the batch index from
+// blockIdx.y and works on packed lower tiles.
+#include <algorithm>
+
+#include "dense.cuh"
+
+namespace msgpu {
+
+constexpr int T = kTile;
+constexpr int kTT = 256;  // threads per tile CTA (16 x 16, 4 x 4 outputs each)
+
+struct TileAcc {
+  double v[4][4];
+};
+
+// acc += sA * sB where sA[r][q], sB[q][c] are 64x64 row-major in smem
+__device__ __forceinline__ void tile_mma(TileAcc& acc, const double* sA, const double* sB) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll 4
+  for (int q = 0; q < T; ++q) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = sA[(ty + 16 * i) * T + q];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = sB[q * T + tx + 16 * j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc.v[i][j] += a[i] * b[j];
+  }
+}
+
+// load a 64x64 tile (row-major, contiguous) into smem, optionally transposed
+__device__ __forceinline__ void tile_load(double* s, const double* g, bool trans) {
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
+    const int r = t / T, c = t % T;
+    if (trans)
+      s[c * T + r] = g[t];
+    else
+      s[t] = g[t];
+  }
+}
+
+__device__ __forceinline__ void acc_zero(TileAcc& a) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a.v[i][j] = 0.0;
+}
+
+__device__ __forceinline__ void acc_store(const TileAcc& a, double* g, double scale, bool add) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = (ty + 16 * i) * T + tx + 16 * j;
+      g[idx] = add ? g[idx] + scale * a.v[i][j] : scale * a.v[i][j];
+    }
+}
+
+__device__ __forceinline__ void tile_ij(int64_t t, int& i, int& j) {
+  i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= t) ++i;
+  while ((int64_t)i * (i + 1) / 2 > t) --i;
+  j = (int)(t - (int64_t)i * (i + 1) / 2);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_pack_tiles(int N, int nt, const double* __restrict__ A, double* __restrict__ P) {
+  const int64_t total = packed_words(nt);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int i, j;
+    tile_ij(t / (T * T), i, j);
+    const int within = (int)(t % (T * T));
+    const int r = i * T + within / T, c = j * T + within % T;
+    P[t] = (r < N && c < N) ? A[(int64_t)r * N + c] : (r == c ? 1.0 : 0.0);
+  }
+}
+
+__global__ void k_band_to_tiles(const BandSys* __restrict__ sys, int s0, int nt,
+                                const double* __restrict__ band, double* __restrict__ P) {
+  const int b = blockIdx.y;
+  const BandSys s = sys[s0 + b];
+  const int S = s.bw + 1;
+  const double* A = band + s.foff;
+  double* Pb = P + (int64_t)b * packed_words(nt);
+  const int64_t total = packed_words(nt);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int i, j;
+    tile_ij(t / (T * T), i, j);
+    const int within = (int)(t % (T * T));
+    const int R = i * T + within / T, Cc = j * T + within % T;
+    double v;
+    if (R < s.n && Cc < s.n) {
+      const int lo = min(R, Cc), d = abs(R - Cc);
+      v = d <= s.bw ? A[(int64_t)lo * S + d] : 0.0;
+    } else {
+      v = (R == Cc) ? 1.0 : 0.0;
+    }
+    Pb[t] = v;
+  }
+}
+
+void launch_band_to_tiles(const BandSys* sys, int s0, int B, int nt, const double* band, double* P,
+                          cudaStream_t st) {
+  k_band_to_tiles<<<dim3(256, B), 256, 0, st>>>(sys, s0, nt, band, P);
+  MS_CUDA(cudaGetLastError());
+}
+
+// Cholesky of diagonal tile k in place (lower), plus its triangular inverse
+// written to tile (k,k) of W.
+__global__ void __launch_bounds__(kTT) k_potrf_tile(int k, int nt, double* __restrict__ P,
+                                                    double* __restrict__ W, int* fail) {
+  extern __shared__ double sm[];
+  double* a = sm;
+  double* inv = sm + T * T;
+  const int64_t mw = packed_words(nt);
+  double* D = P + blockIdx.y * mw + tile_index(k, k) * T * T;
+  tile_load(a, D, false);
+  __syncthreads();
+  for (int c = 0; c < T; ++c) {
+    double d = a[c * T + c];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) atomicCAS(fail, 0, (int)(blockIdx.y * nt * T + k * T + c + 1));
+      d = 1.0;
+    }
+    const double s = sqrt(d);
+    __syncthreads();
+    if (threadIdx.x == 0) a[c * T + c] = s;
+    for (int r = c + 1 + threadIdx.x; r < T; r += blockDim.x) a[r * T + c] /= s;
+    __syncthreads();
+    for (int t = threadIdx.x; t < (T - c - 1) * (T - c - 1); t += blockDim.x) {
+      const int r = c + 1 + t / (T - c - 1), q = c + 1 + t % (T - c - 1);
+      if (q <= r) a[r * T + q] -= a[r * T + c] * a[q * T + c];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
+    const int r = t / T, c = t % T;
+    if (c > r) a[t] = 0.0;
+    D[t] = a[t];
+  }
+  __syncthreads();
+  // inverse of the lower-triangular tile, column j by thread j
+  if (threadIdx.x < T) {
+    const int j = threadIdx.x;
+    for (int r = 0; r < T; ++r) {
+      double s = (r == j) ? 1.0 : 0.0;
+      for (int q = j; q < r; ++q) s -= a[r * T + q] * inv[q * T + j];
+      inv[r * T + j] = (r < j) ? 0.0 : s / a[r * T + r];
+    }
+  }
+  __syncthreads();
+  double* Wk = W + blockIdx.y * mw + tile_index(k, k) * T * T;
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) Wk[t] = inv[t];
+}
+
+// panel: L_ik = A_ik L_kk^-T = A_ik (Winv_kk)^T, i > k
+__global__ void __launch_bounds__(kTT) k_trsm_tiles(int k, int nt, double* __restrict__ P,
+                                                    const double* __restrict__ W) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  const int64_t mw = packed_words(nt);
+  P += blockIdx.y * mw;
+  W += blockIdx.y * mw;
+  const int i = k + 1 + blockIdx.x;
+  double* Aik = P + tile_index(i, k) * T * T;
+  tile_load(sA, Aik, false);
+  tile_load(sB, W + tile_index(k, k) * T * T, true);
+  __syncthreads();
+  TileAcc acc;
+  acc_zero(acc);
+  tile_mma(acc, sA, sB);
+  __syncthreads();
+  acc_store(acc, Aik, 1.0, false);
+}
+
+// trailing update A_ij -= L_ik L_jk^T for k < j <= i
+__global__ void __launch_bounds__(kTT) k_syrk_tiles(int k, int nt, double* __restrict__ P) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  P += blockIdx.y * packed_words(nt);
+  const int m = nt - k - 1;
+  int ii, jj;
+  tile_ij(blockIdx.x, ii, jj);
+  if (ii >= m) return;
+  const int i = k + 1 + ii, j = k + 1 + jj;
+  tile_load(sA, P + tile_index(i, k) * T * T, false);
+  tile_load(sB, P + tile_index(j, k) * T * T, true);
+  __syncthreads();
+  TileAcc acc;
+  acc_zero(acc);
+  tile_mma(acc, sA, sB);
+  acc_store(acc, P + tile_index(i, j) * T * T, -1.0, true);
+}
+
+// W_ij = -W_ii * sum_{l=j}^{i-1} L_il W_lj for i = j + d
+__global__ void __launch_bounds__(kTT) k_trtri_tiles(int d, int nt, const double* __restrict__ P,
+                                                     double* __restrict__ W) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  const int64_t mw = packed_words(nt);
+  P += blockIdx.y * mw;
+  W += blockIdx.y * mw;
+  const int j = blockIdx.x, i = j + d;
+  TileAcc acc;
+  acc_zero(acc);
+  for (int l = j; l < i; ++l) {
+    __syncthreads();
+    tile_load(sA, P + tile_index(i, l) * T * T, false);
+    tile_load(sB, W + tile_index(l, j) * T * T, false);
+    __syncthreads();
+    tile_mma(acc, sA, sB);
+  }
+  __syncthreads();
+  {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) sB[(ty + 16 * a) * T + tx + 16 * b] = acc.v[a][b];
+  }
+  tile_load(sA, W + tile_index(i, i) * T * T, false);
+  __syncthreads();
+  TileAcc out;
+  acc_zero(out);
+  tile_mma(out, sA, sB);
+  acc_store(out, W + tile_index(i, j) * T * T, -1.0, false);
+}
+
+// X_ij = sum_{l >= i} W_li^T W_lj  (i >= j) = (L^-T L^-1)_ij
+__global__ void __launch_bounds__(kTT) k_lauum_tiles(int nt, const double* __restrict__ W,
+                                                     double* __restrict__ X) {
+  extern __shared__ double sm[];
+  double* sA = sm;
+  double* sB = sm + T * T;
+  const int64_t mw = packed_words(nt);
+  W += blockIdx.y * mw;
+  X += blockIdx.y * mw;
+  int i, j;
+  tile_ij(blockIdx.x, i, j);
+  TileAcc acc;
+  acc_zero(acc);
+  for (int l = i; l < nt; ++l) {
+    __syncthreads();
+    tile_load(sA, W + tile_index(l, i) * T * T, true);
+    tile_load(sB, W + tile_index(l, j) * T * T, false);
+    __syncthreads();
+    tile_mma(acc, sA, sB);
+  }
+  acc_store(acc, X + tile_index(i, j) * T * T, 1.0, false);
+}
+
+void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, int* fail,
+                               cudaStream_t st) {
+  if (nt == 0 || B == 0) return;
+  const size_t smem = 2 * T * T * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    MS_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_trsm_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_trtri_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS_CUDA(cudaFuncSetAttribute(k_lauum_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  MS_CUDA(cudaMemsetAsync(W, 0, (size_t)B * packed_words(nt) * sizeof(double), st));
+  for (int k = 0; k < nt; ++k) {
+    k_potrf_tile<<<dim3(1, B), kTT, smem, st>>>(k, nt, P, W, fail);
+    const int m = nt - k - 1;
+    if (m > 0) {
+      k_trsm_tiles<<<dim3(m, B), kTT, smem, st>>>(k, nt, P, W);
+      k_syrk_tiles<<<dim3((unsigned)((int64_t)m * (m + 1) / 2), B), kTT, smem, st>>>(k, nt, P);
+    }
+  }
+  for (int d = 1; d < nt; ++d) k_trtri_tiles<<<dim3(nt - d, B), kTT, smem, st>>>(d, nt, P, W);
+  k_lauum_tiles<<<dim3((unsigned)packed_tiles(nt), B), kTT, smem, st>>>(nt, W, X);
+  MS_CUDA(cudaGetLastError());
+}
+
+size_t dense_spd_inverse_work_bytes(int N) {
+  const int nt = div_up(N, T);
+  return (size_t)packed_words(nt) * sizeof(double) * 2;
+}
+
+void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work, int* fail,
+                       cudaStream_t st) {
+  if (N == 0) return;
+  const int nt = div_up(N, T);
+  double* P = work;
+  double* W = work + packed_words(nt);
+  k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, P);
+  MS_CUDA(cudaGetLastError());
+  dense_spd_inverse_batched(nt, 1, P, W, packed_inv, fail, st);
+}
+
+// ---------------------------------------------------------------------------
+// packed-tile SYMV (batch 1): per tile, u = X_IJ f_J (-> y_I) and, off the
+// diagonal, v = X_IJ^T f_I (-> y_J); partials are reduced in a fixed order.
+__global__ void __launch_bounds__(256)
+    k_symv_tiles(int N, int nt, const double* __restrict__ X, const double* __restrict__ f,
+                 double* __restrict__ part, const int* done) {
+  if (done && *(volatile const int*)done) return;
+  __shared__ double sv[16][T + 1];
+  const int64_t t = blockIdx.x;
+  int i, j;
+  tile_ij(t, i, j);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const double* Xt = X + t * T * T;
+  double fj[4], fi[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int cj = j * T + tx * 4 + q, ri = i * T + ty * 4 + q;
+    fj[q] = cj < N ? f[cj] : 0.0;
+    fi[q] = ri < N ? f[ri] : 0.0;
+  }
+  double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
+    const double2 x01 = __ldg(row), x23 = __ldg(row + 1);
+    u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
+    v[0] += x01.x * fi[rr];
+    v[1] += x01.y * fi[rr];
+    v[2] += x23.x * fi[rr];
+    v[3] += x23.y * fi[rr];
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
+  }
+  double* pu = part + t * 2 * T;
+  double* pv = pu + T;
+  if (tx == 0) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) pu[ty * 4 + rr] = u[rr];
+  }
+  if (i != j) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[ty][tx * 4 + q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < T) {
+      double s = 0.0;
+#pragma unroll
+      for (int g = 0; g < 16; ++g) s += sv[g][threadIdx.x];
+      pv[threadIdx.x] = s;
+    }
+  }
+}
+
+// y_I = sum_J u(I,J) + sum_{I'>I} v(I',I): 8 groups of 64 threads split the
+// tile list, then a fixed-order combine -> deterministic.
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(T* kRedGroups)
+    k_symv_reduce(int N, int nt, const double* __restrict__ part, double* __restrict__ y,
+                  const int* done) {
+  if (done && *(volatile const int*)done) return;
+  __shared__ double s[kRedGroups][T];
+  const int I = blockIdx.x, r = threadIdx.x % T, grp = threadIdx.x / T;
+  double acc = 0.0;
+  for (int t = grp; t < nt; t += kRedGroups)
+    acc += (t <= I) ? part[tile_index(I, t) * 2 * T + r] : part[tile_index(t, I) * 2 * T + T + r];
+  s[grp][r] = acc;
+  __syncthreads();
+  const int row = I * T + threadIdx.x;
+  if (threadIdx.x < T && row < N) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRedGroups; ++q) v += s[q][threadIdx.x];
+    y[row] = v;
+  }
+}
+
+void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
+                        const int* done, cudaStream_t st) {
+  if (N == 0) return;
+  const int nt = div_up(N, T);
+  k_symv_tiles<<<(unsigned)packed_tiles(nt), 256, 0, st>>>(N, nt, X, f, part, done);
+  k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Level-1 apply with explicit inverses: CTA per subdomain streams its
+// packed_tiles(nt) tiles (4x4 doubles per thread, next tile prefetched into
+// registers) and accumulates y in shared memory in tile order.
+constexpr int kDenseApplyThreads = 256;
+
+__global__ void __launch_bounds__(kDenseApplyThreads)
+    k_l1_dense_apply(Grid g, const BandSys* __restrict__ sys, int nt, const double* __restrict__ X,
+                     const double* __restrict__ r, double* __restrict__ ybuf, const int* done) {
+  if (done && *(volatile const int*)done) return;
+  extern __shared__ double sm[];
+  const int NP = nt * T;
+  double* f = sm;                 // NP
+  double* y = f + NP;             // NP
+  double* sv = y + NP;            // 16 x (T+1)
+  double* su = sv + 16 * (T + 1); // T
+  const BandSys s = sys[blockIdx.x];
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    double v = 0.0;
+    if (i < s.n) {
+      const int ln = s.ncomp == 2 ? (i >> 1) : i, c = s.ncomp == 2 ? (i & 1) : 0;
+      int a, b;
+      band_node_of(s, ln, a, b);
+      v = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
+    }
+    f[i] = v;
+    y[i] = 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const double* Xs = X + (int64_t)blockIdx.x * packed_words(nt);
+  const int64_t ntiles = packed_tiles(nt);
+  double2 cur[8], nxt[8];
+  auto load = [&](int64_t t, double2(&dst)[8]) {
+    const double* Xt = Xs + t * T * T;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
+      dst[2 * rr] = __ldg(row);
+      dst[2 * rr + 1] = __ldg(row + 1);
+    }
+  };
+  load(0, cur);
+  int i = 0, j = 0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) load(t + 1, nxt);
+    double fj[4], fi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      fj[q] = f[j * T + tx * 4 + q];
+      fi[q] = f[i * T + ty * 4 + q];
+    }
+    double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2 x01 = cur[2 * rr], x23 = cur[2 * rr + 1];
+      u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
+      v[0] += x01.x * fi[rr];
+      v[1] += x01.y * fi[rr];
+      v[2] += x23.x * fi[rr];
+      v[3] += x23.y * fi[rr];
+    }
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
+    if (tx == 0)
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) su[ty * 4 + rr] = u[rr];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sv[ty * (T + 1) + tx * 4 + q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < T) {
+      y[i * T + threadIdx.x] += su[threadIdx.x];
+    } else if (threadIdx.x < 2 * T && i != j) {
+      const int c = threadIdx.x - T;
+      double sacc = 0.0;
+#pragma unroll
+      for (int gq = 0; gq < 16; ++gq) sacc += sv[gq * (T + 1) + c];
+      y[j * T + c] += sacc;
+    }
+    __syncthreads();
+    if (++j > i) {
+      ++i;
+      j = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+  }
+  double* out = ybuf + s.yoff;
+  for (int k = threadIdx.x; k < s.n; k += blockDim.x) out[k] = y[k];
+}
+
+void launch_l1_dense_apply(const Grid& g, const BandSys* sys, int nsys, int nt, const double* X,
+                           const double* r, double* ybuf, const int* done, cudaStream_t st) {
+  if (nsys == 0) return;
+  const size_t smem = sizeof(double) * ((size_t)2 * nt * T + 16 * (T + 1) + T);
+  if (smem > 220 * 1024) throw Error(-1, "subdomain too large for the dense level-1 apply");
+  MS_CUDA(cudaFuncSetAttribute(k_l1_dense_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_l1_dense_apply<<<nsys, kDenseApplyThreads, smem, st>>>(g, sys, nt, X, r, ybuf, done);
+  MS_CUDA(cudaGetLastError());
+}
+
+}  // namespace msgpu

@@ -1,0 +1,44 @@
+// Batched dense SPD inverses in packed 64x64 lower tiles, and packed SYMVs.
+#pragma once
+
+#include "banded.cuh"
+#include "common.cuh"
+
+namespace msgpu {
+
+constexpr int kTile = 64;
+__host__ __device__ inline int64_t packed_tiles(int nt) { return (int64_t)nt * (nt + 1) / 2; }
+__host__ __device__ inline int64_t tile_index(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
+__host__ __device__ inline int64_t packed_words(int nt) { return packed_tiles(nt) * kTile * kTile; }
+
+// B symmetric positive definite matrices, each nt x nt packed lower tiles (a
+// matrix of order N < nt*64 is padded with an identity block) stored at
+// P + b * packed_words(nt).  On exit X + b * packed_words(nt) holds the
+// inverse (full symmetric diagonal tiles, lower off-diagonal tiles); P is
+// overwritten by the Cholesky factor and W (same size as P) is workspace.
+// *fail receives 1 + (b * nt * 64 + row) of the first non-positive pivot.
+void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, int* fail,
+                               cudaStream_t st);
+
+// single matrix from a row-major N x N array (lower triangle read): the
+// coarse operator K0 (coarse.py:136-147)
+void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work, int* fail,
+                       cudaStream_t st);
+size_t dense_spd_inverse_work_bytes(int N);
+
+// y = X f for one packed symmetric matrix; `part` needs packed_tiles(nt)*2*64 doubles
+void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
+                        const int* done, cudaStream_t st);
+
+// level-1 band (unfactored, column-band layout of BandSys) -> packed tiles,
+// for systems [s0, s0 + B) into P (B matrices of nt tiles)
+void launch_band_to_tiles(const BandSys* sys, int s0, int B, int nt, const double* band, double* P,
+                          cudaStream_t st);
+
+// level-1 apply with explicit packed inverses: per subdomain s, gather R_s r,
+// y_s = X_s (R_s r) into ybuf[yoff_s ...]; one CTA per subdomain, y and the
+// gathered residual in shared memory, tiles streamed with register prefetch.
+void launch_l1_dense_apply(const Grid& g, const BandSys* sys, int nsys, int nt, const double* X,
+                           const double* r, double* ybuf, const int* done, cudaStream_t st);
+
+}  // namespace msgpu

@@ -133,7 +133,7 @@ class TwoLevelPreconditioner:
 
 
 def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None, *,
-                         level1="neighborhoods", delta=None, use_coarse=True):
+                         level1="neighborhoods", delta=None, use_coarse=True, local_solver="banded"):
     """Build a two-level preconditioner by variant name (schwarz.py:176-211).
 
     level1='neighborhoods' is the reference's layout (subdomains = omega_j);
@@ -166,7 +166,9 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
     o.gap_threshold = 50.0
     o.enrich = 1 if variant.enrich else 0
     o.fixed_rule = 1 if rule == "fixed" else 0
-    o.local_solver = _lib.MS_LOCAL_BANDED
+    if local_solver not in ("banded", "dense"):
+        raise ValueError(f"unknown local solver {local_solver!r}")
+    o.local_solver = _lib.MS_LOCAL_BANDED if local_solver == "banded" else _lib.MS_LOCAL_DENSE_INV
     o.use_coarse = 1 if use_coarse else 0
     o.heat_dirichlet_nodes = hd.ctypes.data_as(C.POINTER(C.c_int64)) if hd.size else None
     o.n_heat_dirichlet = hd.size
@@ -184,6 +186,6 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "basis_kind": "H+Rot" if variant.enrich else "H", "selection_rule": rule,
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
         "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,
-        "coarse_bytes": inf.coarse_bytes, "level1": level1, "delta": delta,
+        "coarse_bytes": inf.coarse_bytes, "level1": level1, "delta": delta, "local_solver": local_solver,
     }
     return TwoLevelPreconditioner(variant, op, h, info)

@@ -295,3 +295,22 @@ def test_profiling_and_graph_paths_agree():
     assert np.array_equal(x_graph, x_prof) and r_graph.iterations == r_prof.iterations
     assert np.array_equal(x_small, x_prof7)
     assert r_graph.residuals[:8] == r_small.residuals[:8]
+
+
+def test_dense_inverse_local_solver_matches_banded(rng):
+    """MS_LOCAL_DENSE_INV: explicit packed inverses give the same level-1 apply
+    and the same PCG as the banded factors (to the inverse's round-off)."""
+    g = load_golden("ref_config1.npz")
+    spec = spec_from_golden(g)
+    from paper_2006_13387_b200.solve import setup_spec
+
+    _, op, pre_b = setup_spec(spec, local_solver="banded")
+    _, op_d, pre_d = setup_spec(spec, local_solver="dense")
+    assert pre_d.info["local_solver"] == "dense" and pre_d.coarse_dim == pre_b.coarse_dim
+    for _ in range(3):
+        r = rng.standard_normal(op.n_free)
+        assert rel(pre_d.apply(r), pre_b.apply(r)) <= 1e-8
+    assert rel(pre_d.apply(g["apply_r"]), g["apply_z"]) <= 1e-7
+    x, rep = G.pcg_solve(op_d, spec.rhs(), pre_d, tol=1e-8, maxit=5000)
+    ref_it = int(g["iters"])
+    assert rep.converged and abs(rep.iterations - ref_it) <= max(3, int(0.06 * ref_it))
