@@ -9,7 +9,7 @@ LIB := paper_2006_13387_b200/libmsgpu.so
 all: $(LIB)
 
 $(LIB): $(SRC) $(HDR)
-	$(NVCC) $(ARCH) $(NVFLAGS) -shared $(SRC) -o $@ 2> /tmp/ptxas.log || (cat /tmp/ptxas.log; false)
+	$(NVCC) $(ARCH) $(NVFLAGS) -shared $(SRC) -o $@ -ldl 2> /tmp/ptxas.log || (cat /tmp/ptxas.log; false)
 
 clean:
 	rm -f $(LIB)

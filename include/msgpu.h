@@ -121,6 +121,36 @@ int ms_ctx_profile_get(const ms_ctx* ctx, double* ms, long long* counts); /* MS_
 /* the context's cudaStream_t (for event timing by callers) */
 void* ms_ctx_stream(const ms_ctx* ctx);
 
+/* ---- multi-GPU strips ----------------------------------
+ * One process per GPU.  Attach a communicator to the context before creating
+ * the problem; ms_precond_build then shards subdomain rows (coarse block rows)
+ * across ranks, every rank holding full-size vectors but updating only its
+ * strip, with halo exchanges (p/z: 1 node row, r: overlap+1 rows, level-1
+ * boundary subdomain rows, one row of coarse-restriction cell partials),
+ * allreduces of the three PCG dot products and of the coarse residual f0,
+ * and a replicated K0^-1 SYMV.
+ * The reference is single-process; these entry points have no counterpart. */
+typedef struct ms_comm_callbacks {
+  void* user;
+  /* device buffers; called after the context stream is synchronised; must
+   * complete before returning; return 0 on success */
+  int (*allreduce_sum)(void* user, double* dev, int64_t n);
+  int (*broadcast)(void* user, void* dev, int64_t bytes, int root);
+  int (*sendrecv)(void* user, const void* send_dev, int64_t send_bytes, int dst, void* recv_dev,
+                  int64_t recv_bytes, int src); /* dst/src may be -1 */
+} ms_comm_callbacks;
+int ms_nccl_unique_id(void* out128);
+int ms_ctx_attach_nccl(ms_ctx* ctx, int rank, int world, const void* unique_id128);
+int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_callbacks* cb);
+/* synchronous copy between host and/or device buffers (callback helpers) */
+int ms_copy(void* dst, const void* src, size_t bytes);
+/* node-row halo plan of rank `rank` owning rows [lo, hi] of 0..ny, depth k:
+ * out12 = {send_lo, send_n, dst, recv_lo, recv_n, src} for slot 0 (towards the
+ * previous rank) then slot 1 (towards the next); pure arithmetic, no CUDA */
+int ms_halo_plan(int lo, int hi, int ny, int k, int rank, int world, int* out12);
+/* strip partition used for `nrows` block rows: rank owns [*lo, *hi) */
+int ms_strip_rows(int nrows, int world, int rank, int* lo, int* hi);
+
 /* ---- operator: assemble_elasticity (assembly.py:208-220) ---------------
  * E: per-element modulus, n_el = nx*ny, row-major (e = j*nx + i).
  * free_dofs: sorted ascending full-dof ids (component-grouped), n_free of them.

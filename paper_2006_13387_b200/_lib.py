@@ -26,7 +26,18 @@ EXPORTS = (
     "ms_operator_apply", "ms_precond_build", "ms_precond_destroy", "ms_precond_apply",
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
     "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
+    "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_strip_rows", "ms_copy",
+    "ms_halo_plan",
 )
+
+ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+BROADCAST_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int)
+SENDRECV_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int)
+
+
+class CommCallbacks(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE_CB), ("broadcast", BROADCAST_CB),
+                ("sendrecv", SENDRECV_CB)]
 BENCH_NAMES = ("matvec", "level1", "restrict", "coarse_solve", "combine", "combine_l1", "combine_coarse")
 PROF_NAMES = ("matvec", "update", "level1", "restrict", "coarse_solve", "combine")
 MS_PROF_N = 8
@@ -110,6 +121,12 @@ def load(path: str | os.PathLike | None = None):
         "ms_ctx_profile_get": (C.c_int, [vp, dp, C.POINTER(C.c_longlong)]),
         "ms_ctx_stream": (C.c_void_p, [vp]),
         "ms_precond_bench": (C.c_int, [vp, C.c_int, dp]),
+        "ms_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "ms_ctx_attach_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
+        "ms_ctx_attach_callbacks": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(CommCallbacks)]),
+        "ms_strip_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
+        "ms_copy": (C.c_int, [vp, vp, C.c_size_t]),
+        "ms_halo_plan": (C.c_int, [C.c_int] * 6 + [ip]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

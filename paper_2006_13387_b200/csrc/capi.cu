@@ -17,6 +17,7 @@
 #include "../../include/msgpu.h"
 #include "banded.cuh"
 #include "coarse.cuh"
+#include "comm.cuh"
 #include "common.cuh"
 #include "eigen.cuh"
 #include "operator.cuh"
@@ -209,11 +210,17 @@ struct ms_ctx {
   cudaStream_t st = nullptr;
   std::string err;
   Prof prof;
+  std::unique_ptr<Comm> comm;  // multi-GPU strips (world > 1)
+  int world() const { return comm ? comm->world : 1; }
+  int rank() const { return comm ? comm->rank : 0; }
 };
 
 struct ms_problem {
   ms_ctx* ctx = nullptr;
   Grid g{};
+  // owned node rows (strip); whole mesh on one rank, set by ms_precond_build otherwise
+  int b_lo = 0, b_hi = -1;
+  std::vector<int> rank_lo, rank_hi;  // every rank's owned node rows
   double nu = 0.3;
   KeParam ke{};
   DBuf<double> E;
@@ -274,6 +281,9 @@ struct ms_precond {
   int N_c = 0;
   int max_pass = 0;
   ms_precond_info info{};
+  // strip ownership: level-1 subdomain rows [J0, J1) -> subdomains [s0, s1);
+  // coarse cell rows [C0, C1); centres [kc0, kc1).  One rank owns everything.
+  int J0 = 0, J1 = 0, s0 = 0, s1 = 0, C0 = 0, C1 = 0, kc0 = 0, kc1 = 0, halo_rows = 1;
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;  // captured PCG chunks for (prob, this)
   std::vector<std::pair<int, int>> captured;
   ~ms_precond() {
@@ -355,6 +365,111 @@ static void level1_axis(int n_el, int nblocks, int kind, int delta, std::vector<
   }
 }
 
+// ---------------------------------------------------------------------------
+// multi-rank helpers.  Every rank holds full-length vectors; rank r updates
+// node rows [rank_lo[r], rank_hi[r]] ("owned") and receives halo rows.
+
+static int row_hi(const ms_problem* P) { return P->b_hi < 0 ? P->g.ny : P->b_hi; }
+
+// Halo plan for k node rows: rows [lo, hi] owned, neighbours prev/next.
+// slot 0: send my lowest rows to prev, receive next's lowest rows above me;
+// slot 1: send my highest rows to next, receive prev's highest rows below me.
+struct HaloPlan {
+  int send_lo[2], send_n[2], dst[2];
+  int recv_lo[2], recv_n[2], src[2];
+};
+
+static HaloPlan halo_plan(int lo, int hi, int ny, int k, int rank, int world) {
+  HaloPlan h{};
+  const int prev = rank > 0 ? rank - 1 : -1, next = rank < world - 1 ? rank + 1 : -1;
+  const int kd = std::min(k, hi - lo + 1);
+  const int kb = std::min(k, lo), ka = std::min(k, ny - hi);
+  h.dst[0] = prev;
+  h.send_lo[0] = lo;
+  h.send_n[0] = prev >= 0 ? kd : 0;
+  h.src[0] = next;
+  h.recv_lo[0] = hi + 1;
+  h.recv_n[0] = next >= 0 ? ka : 0;
+  h.dst[1] = next;
+  h.send_lo[1] = hi - kd + 1;
+  h.send_n[1] = next >= 0 ? kd : 0;
+  h.src[1] = prev;
+  h.recv_lo[1] = lo - kb;
+  h.recv_n[1] = prev >= 0 ? kb : 0;
+  return h;
+}
+
+// exchange k node rows of both planes with the neighbouring strips
+static void exchange_rows(ms_problem* P, double* v, int k) {
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1 || k <= 0) return;
+  const HaloPlan h = halo_plan(P->b_lo, row_hi(P), P->g.ny, k, c->rank, c->world);
+  const int64_t rowb = (int64_t)P->g.nnx * sizeof(double);
+  for (int plane = 0; plane < 2; ++plane) {
+    char* base = reinterpret_cast<char*>(v + plane * P->g.n_nodes);
+    c->sendrecv2(base + h.send_lo[0] * rowb, h.send_n[0] * rowb, h.dst[0], base + h.recv_lo[0] * rowb,
+                 h.recv_n[0] * rowb, h.src[0], base + h.send_lo[1] * rowb, h.send_n[1] * rowb, h.dst[1],
+                 base + h.recv_lo[1] * rowb, h.recv_n[1] * rowb, h.src[1], P->ctx->st);
+  }
+}
+
+// every rank ends with every rank's owned rows (solution / operator output)
+static void allgather_rows(ms_problem* P, double* v) {
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1) return;
+  const int64_t rowb = (int64_t)P->g.nnx * sizeof(double);
+  for (int r = 0; r < c->world; ++r)
+    for (int plane = 0; plane < 2; ++plane) {
+      char* base = reinterpret_cast<char*>(v + plane * P->g.n_nodes);
+      c->broadcast(base + P->rank_lo[r] * rowb, (P->rank_hi[r] - P->rank_lo[r] + 1) * rowb, r, P->ctx->st);
+    }
+}
+
+// level-1 solutions of the neighbours' boundary subdomain rows (their overlap
+// reaches into my strip)
+static void exchange_ybuf(ms_precond* pc) {
+  ms_problem* P = pc->prob;
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1) return;
+  const int r = c->rank, W = c->world;
+  const int prev = r > 0 ? r - 1 : -1, next = r < W - 1 ? r + 1 : -1;
+  auto seg = [&](int J, int64_t& off, int64_t& bytes) {
+    const BandSys& a = pc->hsys[(size_t)J * pc->NbX];
+    const BandSys& b = pc->hsys[(size_t)J * pc->NbX + pc->NbX - 1];
+    off = a.yoff;
+    bytes = (b.yoff + b.n - a.yoff) * (int64_t)sizeof(double);
+  };
+  int64_t o_first, b_first, o_last, b_last, o_pl, b_pl, o_nf, b_nf;
+  seg(pc->J0, o_first, b_first);
+  seg(pc->J1 - 1, o_last, b_last);
+  if (prev >= 0) seg(pc->J0 - 1, o_pl, b_pl); else o_pl = b_pl = 0;
+  if (next >= 0) seg(pc->J1, o_nf, b_nf); else o_nf = b_nf = 0;
+  double* y = pc->ybuf.p;
+  c->sendrecv2(y + o_first, prev >= 0 ? b_first : 0, prev, y + o_nf, b_nf, next,
+               y + o_last, next >= 0 ? b_last : 0, next, y + o_pl, b_pl, prev, P->ctx->st);
+}
+
+// restriction partials of the cell row below my lowest centre row (prev's last)
+static void exchange_rpart(ms_precond* pc) {
+  ms_problem* P = pc->prob;
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1) return;
+  const int r = c->rank, W = c->world;
+  const int prev = r > 0 ? r - 1 : -1, next = r < W - 1 ? r + 1 : -1;
+  const int64_t rowd = (int64_t)pc->cd.Nx * 4 * kSlots;
+  double* rp = pc->rpart.p;
+  c->sendrecv2(nullptr, 0, -1, nullptr, 0, -1, rp + (pc->C1 - 1) * rowd,
+               next >= 0 ? rowd * sizeof(double) : 0, next, rp + (pc->C0 - 1) * rowd,
+               prev >= 0 ? rowd * sizeof(double) : 0, prev, P->ctx->st);
+}
+
+static void dist_finalize(ms_problem* P, int kind, double* hist) {
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1) return;
+  c->allreduce_sum(&P->sc.p->part[kind], 1, P->ctx->st);
+  launch_finalize(P->sc.p, kind, hist, P->ctx->st);
+}
+
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
 // `restricted`: the cell restriction partials of r were already produced
 // (fused into the residual update); only their reduction remains.
@@ -365,18 +480,26 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
   Prof& pf = P->ctx->prof;
   const int* done = sc ? &sc->done : nullptr;
   cudaEvent_t a;
-  if (pc->nsys > 0) {
+  const bool dist = P->ctx->world() > 1;
+  const int ns = pc->s1 - pc->s0;
+  if (ns > 0) {
     a = pf.begin(MS_PROF_LEVEL1, it, st);
     if (pc->dense)
-      launch_l1_dense_apply(P->g, pc->sys.p, pc->nsys, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
+      launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
     else
-      launch_l1_solve(P->g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
+      launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
     pf.end(MS_PROF_LEVEL1, it, st, a);
+    if (dist) exchange_ybuf(pc);
   }
   if (pc->has_coarse) {
     a = pf.begin(MS_PROF_RESTRICT, it, st);
-    if (!restricted) launch_restrict_cells(P->g, pc->cd, r, done, st);
-    launch_restrict_reduce(pc->cd, pc->f0.p, done, st);
+    if (!restricted) launch_restrict_cells(P->g, pc->C0, pc->C1, pc->cd, r, done, st);
+    if (dist) {
+      exchange_rpart(pc);
+      MS_CUDA(cudaMemsetAsync(pc->f0.p, 0, pc->N_c * sizeof(double), st));
+    }
+    launch_restrict_reduce(pc->cd, pc->f0.p, done, st, pc->kc0, pc->kc1);
+    if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
     pf.end(MS_PROF_RESTRICT, it, st, a);
     a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
     launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st);
@@ -384,8 +507,12 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
   }
   a = pf.begin(MS_PROF_COMBINE, it, st);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
-                 pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st);
+                 pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st, pc->C0, pc->C1);
   pf.end(MS_PROF_COMBINE, it, st, a);
+  if (dist) {
+    if (sc) dist_finalize(P, PART_RZ, beta_hist);
+    exchange_rows(P, z, 1);  // the next matvec refreshes p on one halo row
+  }
 }
 
 static int precond_launches(const ms_precond* pc) {
@@ -448,6 +575,49 @@ int ms_ctx_profile_get(const ms_ctx* ctx, double* ms, long long* counts) {
 }
 
 void* ms_ctx_stream(const ms_ctx* ctx) { return ctx ? (void*)ctx->st : nullptr; }
+
+int ms_nccl_unique_id(void* out128) {
+  MS_API_BEGIN
+  if (!out128) throw Error(MS_E_INVALID, "null argument");
+  nccl_unique_id(out128);
+  MS_API_END(nullptr)
+}
+
+int ms_ctx_attach_nccl(ms_ctx* ctx, int rank, int world, const void* unique_id128) {
+  MS_API_BEGIN
+  if (!ctx || !unique_id128 || world < 1 || rank < 0 || rank >= world) throw Error(MS_E_INVALID, "bad argument");
+  ctx->comm = make_nccl_comm(rank, world, unique_id128, ctx->device);
+  MS_API_END(ctx)
+}
+
+int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_callbacks* cb) {
+  MS_API_BEGIN
+  if (!ctx || world < 1 || rank < 0 || rank >= world) throw Error(MS_E_INVALID, "bad argument");
+  ctx->comm = make_callback_comm(rank, world, cb);
+  MS_API_END(ctx)
+}
+
+int ms_copy(void* dst, const void* src, size_t bytes) {
+  MS_API_BEGIN
+  if (bytes && (!dst || !src)) throw Error(MS_E_INVALID, "null argument");
+  if (bytes) MS_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  MS_API_END(nullptr)
+}
+
+int ms_halo_plan(int lo, int hi, int ny, int k, int rank, int world, int* out12) {
+  if (!out12 || world < 1 || rank < 0 || rank >= world) return MS_E_INVALID;
+  const HaloPlan h = halo_plan(lo, hi, ny, k, rank, world);
+  const int v[12] = {h.send_lo[0], h.send_n[0], h.dst[0], h.recv_lo[0], h.recv_n[0], h.src[0],
+                     h.send_lo[1], h.send_n[1], h.dst[1], h.recv_lo[1], h.recv_n[1], h.src[1]};
+  std::memcpy(out12, v, sizeof(v));
+  return MS_OK;
+}
+
+int ms_strip_rows(int nrows, int world, int rank, int* lo, int* hi) {
+  if (!lo || !hi || world < 1 || rank < 0 || rank >= world || nrows < world) return MS_E_INVALID;
+  strip_rows(nrows, world, rank, *lo, *hi);
+  return MS_OK;
+}
 
 int ms_ctx_destroy(ms_ctx* ctx) {
   if (!ctx) return MS_OK;
@@ -528,7 +698,8 @@ int ms_operator_apply(ms_problem* P, const double* p, double* q) {
   MS_CUDA(cudaSetDevice(P->ctx->device));
   load_free(P, p, P->tmp.p);
   launch_matvec(P->g, P->ke, P->E.p, P->mask.p, nullptr, P->tmp.p, nullptr, P->q.p, MV_PLAIN,
-                nullptr, nullptr, nullptr, P->ctx->st);
+                nullptr, nullptr, nullptr, P->ctx->st, P->b_lo, row_hi(P));
+  allgather_rows(P, P->q.p);
   store_free(P, P->q.p, q);
   MS_API_END(P ? P->ctx : nullptr)
 }
@@ -548,6 +719,9 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     throw Error(MS_E_INVALID, "block level-1 needs overlap delta >= 1");
   if (o->local_solver != MS_LOCAL_BANDED && o->local_solver != MS_LOCAL_DENSE_INV)
     throw Error(MS_E_INVALID, "unknown local solver");
+  const int W = P->ctx->world(), R = P->ctx->rank();
+  if (W > 1 && (o->level1_kind != MS_LEVEL1_BLOCKS || !o->use_coarse || o->Ny < W))
+    throw Error(MS_E_INVALID, "multi-GPU strips need the block level-1 layout, a coarse level and Ny >= ranks");
   std::unique_ptr<ms_precond> pc(new ms_precond());
   pc->prob = P;
   pc->device = P->ctx->device;
@@ -573,15 +747,42 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->NbX = (int)xlo.size();
     pc->NbY = (int)ylo.size();
     pc->nsys = pc->NbX * pc->NbY;
+    // strip of subdomain rows owned by this rank (all of them on one rank)
+    if (W > 1) {
+      strip_rows(o->Ny, W, R, pc->J0, pc->J1);
+    } else {
+      pc->J0 = 0;
+      pc->J1 = pc->NbY;
+    }
+    pc->s0 = pc->J0 * pc->NbX;
+    pc->s1 = pc->J1 * pc->NbX;
+    // coarse cells = coarse blocks (Ny rows whatever the level-1 layout)
+    pc->C0 = W > 1 ? pc->J0 : 0;
+    pc->C1 = W > 1 ? pc->J1 : o->Ny;
+    if (W > 1) {
+      const int mey = g.ny / o->Ny;
+      P->rank_lo.assign(W, 0);
+      P->rank_hi.assign(W, 0);
+      for (int q = 0; q < W; ++q) {
+        int a, b;
+        strip_rows(o->Ny, W, q, a, b);
+        P->rank_lo[q] = a * mey;
+        P->rank_hi[q] = (b == o->Ny) ? g.ny : b * mey - 1;
+      }
+      P->b_lo = P->rank_lo[R];
+      P->b_hi = P->rank_hi[R];
+      pc->halo_rows = std::max(1, o->delta);
+    }
     int64_t foff = 0, yoff = 0;
     for (int J = 0; J < pc->NbY; ++J)
       for (int I = 0; I < pc->NbX; ++I) {
         BandSys s{};
         if (xhi[I] < xlo[I] || yhi[J] < ylo[J]) throw Error(MS_E_INVALID, "empty level-1 subdomain");
         band_setup(s, xlo[I], xhi[I], ylo[J], yhi[J], 2);
-        s.foff = foff;
+        const int sid = J * pc->NbX + I;
+        s.foff = foff;  // factors stored for owned subdomains only
         s.yoff = yoff;
-        foff += (int64_t)s.n * (s.bw + 1);
+        if (sid >= pc->s0 && sid < pc->s1) foff += (int64_t)s.n * (s.bw + 1);
         yoff += s.n;
         pc->max_bw = std::max(pc->max_bw, s.bw);
         pc->hsys.push_back(s);
@@ -605,12 +806,13 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->Lc.alloc(foff);
     pc->ybuf.alloc(yoff);
     fail.zero(st);
-    launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p, pc->nsys, pc->Lc.p, st);
+    const int ns = pc->s1 - pc->s0;
+    launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
     pc->dense = o->local_solver == MS_LOCAL_DENSE_INV;
     if (!pc->dense) {
       pc->Lr.alloc(foff);
       pc->Lr.zero(st);
-      launch_band_potrf(pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
+      launch_band_potrf(pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
       check_fail(fail, st, "level-1 subdomain matrix");
     } else {
       // explicit inverses: band -> packed tiles, batched tiled Cholesky inverse
@@ -618,15 +820,15 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       for (const BandSys& b : pc->hsys) max_n = std::max(max_n, b.n);
       pc->dense_nt = div_up(max_n, kTile);
       const int64_t mw = packed_words(pc->dense_nt);
-      pc->Xinv.alloc((size_t)pc->nsys * mw);
-      const int B = std::min(pc->nsys, 256);
+      pc->Xinv.alloc((size_t)ns * mw);
+      const int B = std::min(ns, 256);
       DBuf<double> Pw, Ww;
       Pw.alloc((size_t)B * mw);
       Ww.alloc((size_t)B * mw);
-      for (int s0 = 0; s0 < pc->nsys; s0 += B) {
-        const int nb = std::min(B, pc->nsys - s0);
-        launch_band_to_tiles(pc->sys.p, s0, nb, pc->dense_nt, pc->Lc.p, Pw.p, st);
-        dense_spd_inverse_batched(pc->dense_nt, nb, Pw.p, Ww.p, pc->Xinv.p + (size_t)s0 * mw, fail.p, st);
+      for (int b0 = 0; b0 < ns; b0 += B) {
+        const int nb = std::min(B, ns - b0);
+        launch_band_to_tiles(pc->sys.p, pc->s0 + b0, nb, pc->dense_nt, pc->Lc.p, Pw.p, st);
+        dense_spd_inverse_batched(pc->dense_nt, nb, Pw.p, Ww.p, pc->Xinv.p + (size_t)b0 * mw, fail.p, st);
       }
       check_fail(fail, st, "level-1 subdomain matrix");
       pc->Lc.release();
@@ -646,7 +848,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->xlo_d.p, pc->xlen_d.p, pc->ylo_d.p, pc->ylen_d.p,
                    pc->yoff_d.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
     pc->info.n_subdomains = pc->nsys;
-    pc->info.local_bytes = pc->dense ? (double)pc->nsys * packed_words(pc->dense_nt) * sizeof(double)
+    pc->info.local_bytes = pc->dense ? (double)ns * packed_words(pc->dense_nt) * sizeof(double)
                                      : (double)foff * 2 * sizeof(double);
   }
   MS_CUDA(cudaEventRecord(e1, st));
@@ -689,12 +891,29 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->psi.alloc((size_t)nc * o->n_max * NL);
     std::vector<int64_t> h_psioff(nc, 0);
     pc->h_nsel.assign(nc, 0);
-    const int batch = std::min(nc, 1024);
+    // owned centre rows: [max(J0,1), min(J1, Ny)) (centre row J sits on block row J)
+    {
+      const int cj0 = std::max(pc->C0, 1), cj1 = std::min(pc->C1, o->Ny);
+      pc->kc0 = (cj0 - 1) * (o->Nx - 1);
+      pc->kc1 = std::max(pc->kc0, (cj1 - 1) * (o->Nx - 1));
+    }
+    const int batch = std::min(std::max(pc->kc1 - pc->kc0, 1), 1024);
     DBuf<BandSys> hsysd;
     DBuf<double> hLc, hLr, work, evecs;
+    // own centres' vectors are compacted with local offsets, then placed at
+    // their global offsets once every rank's mode counts are known
+    DBuf<double> psi_local_buf;
+    double* psi_local = pc->psi.p;
+    if (W > 1) {
+      psi_local_buf.alloc((size_t)std::max(pc->kc1 - pc->kc0, 1) * o->n_max * NL);
+      psi_local = psi_local_buf.p;
+    }
+    DBuf<int64_t> psioff_local;
+    psioff_local.alloc(nc);
+    std::vector<int64_t> h_psioff_local(nc, 0);
     int64_t psi_cursor = 0;
-    for (int k0 = 0; k0 < nc; k0 += batch) {
-      const int nk = std::min(batch, nc - k0);
+    for (int k0 = pc->kc0; k0 < pc->kc1; k0 += batch) {
+      const int nk = std::min(batch, pc->kc1 - k0);
       std::vector<BandSys> hs(nk);
       int64_t foff = 0;
       int mbw = 0;
@@ -729,12 +948,52 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       MS_CUDA(cudaMemcpyAsync(bsel.data(), pc->nsel.p + k0, nk * sizeof(int), cudaMemcpyDeviceToHost, st));
       MS_CUDA(cudaStreamSynchronize(st));
       for (int kb = 0; kb < nk; ++kb) {
-        h_psioff[k0 + kb] = psi_cursor;
+        h_psioff_local[k0 + kb] = psi_cursor;
         psi_cursor += (int64_t)bsel[kb] * NL;
         pc->h_nsel[k0 + kb] = bsel[kb];
       }
-      pc->psioff.upload(h_psioff.data(), nc, st);
-      launch_compact_psi(eb, cd.NLx, pc->nsel.p, pc->psioff.p, pc->psi.p, st);
+      psioff_local.upload(h_psioff_local.data(), nc, st);
+      launch_compact_psi(eb, cd.NLx, pc->nsel.p, psioff_local.p, psi_local, st);
+    }
+    if (W > 1) {
+      // every owner's eigenvalues, mode counts and passes to every rank
+      Comm* cm = P->ctx->comm.get();
+      for (int q = 0; q < W; ++q) {
+        int a, b;
+        strip_rows(o->Ny, W, q, a, b);
+        const int qk0 = (std::max(a, 1) - 1) * (o->Nx - 1);
+        const int qk1 = std::max(qk0, (std::min(b, o->Ny) - 1) * (o->Nx - 1));
+        if (qk1 <= qk0) continue;
+        cm->broadcast(pc->evals.p + (size_t)qk0 * kNeig, (size_t)(qk1 - qk0) * kNeig * sizeof(double), q, st);
+        cm->broadcast(pc->nsel.p + qk0, (size_t)(qk1 - qk0) * sizeof(int), q, st);
+        cm->broadcast(passes.p + qk0, (size_t)(qk1 - qk0) * sizeof(int), q, st);
+      }
+      MS_CUDA(cudaMemcpyAsync(pc->h_nsel.data(), pc->nsel.p, nc * sizeof(int), cudaMemcpyDeviceToHost, st));
+      MS_CUDA(cudaStreamSynchronize(st));
+    }
+    // global psi offsets (prefix over all centres)
+    psi_cursor = 0;
+    for (int k = 0; k < nc; ++k) {
+      h_psioff[k] = psi_cursor;
+      psi_cursor += (int64_t)pc->h_nsel[k] * NL;
+    }
+    pc->psioff.upload(h_psioff.data(), nc, st);
+    if (W > 1) {
+      Comm* cm = P->ctx->comm.get();
+      if (pc->kc1 > pc->kc0) {
+        const int64_t n_own = h_psioff[pc->kc1 - 1] + (int64_t)pc->h_nsel[pc->kc1 - 1] * NL - h_psioff[pc->kc0];
+        MS_CUDA(cudaMemcpyAsync(pc->psi.p + h_psioff[pc->kc0], psi_local, n_own * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+      }
+      for (int q = 0; q < W; ++q) {
+        int a, b;
+        strip_rows(o->Ny, W, q, a, b);
+        const int qk0 = (std::max(a, 1) - 1) * (o->Nx - 1);
+        const int qk1 = std::max(qk0, (std::min(b, o->Ny) - 1) * (o->Nx - 1));
+        if (qk1 <= qk0) continue;
+        const int64_t o0 = h_psioff[qk0], o1 = h_psioff[qk1 - 1] + (int64_t)pc->h_nsel[qk1 - 1] * NL;
+        cm->broadcast(pc->psi.p + o0, (size_t)(o1 - o0) * sizeof(double), q, st);
+      }
     }
     {
       std::vector<int> hp_(nc);
@@ -777,10 +1036,12 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     DBuf<double> K0;
     K0.alloc((size_t)N * N);
     K0.zero(st);
-    const int ncta = std::min(nc, 148 * 4);
+    const int ncta = std::max(1, std::min(pc->kc1 - pc->kc0, 148 * 4));
     DBuf<double> scratch;
     scratch.alloc((size_t)ncta * 4 * NL);
-    launch_k0_assemble(g, P->ke, P->E.p, P->mask.p, cd, K0.p, scratch.p, ncta, st);
+    // columns of the owned centres' basis functions; the sum over ranks is K0
+    launch_k0_assemble(g, P->ke, P->E.p, P->mask.p, cd, K0.p, scratch.p, ncta, st, pc->kc0, pc->kc1);
+    if (W > 1) P->ctx->comm->allreduce_sum(K0.p, (size_t)N * N, st);
     launch_symmetrize(N, K0.p, st);
     const int nt = div_up(N, kTile);
     pc->K0inv.alloc((size_t)packed_tiles(nt) * kTile * kTile);
@@ -838,6 +1099,7 @@ int ms_precond_apply(ms_precond* pc, const double* r, double* z) {
   MS_CUDA(cudaSetDevice(P->ctx->device));
   load_free(P, r, P->r.p);
   precond_apply_full(pc, P->r.p, P->z.p, nullptr, nullptr);
+  allgather_rows(P, P->z.p);
   store_free(P, P->z.p, z);
   MS_API_END(pc ? pc->prob->ctx : nullptr)
 }
@@ -850,11 +1112,18 @@ int ms_precond_apply_coarse(ms_precond* pc, const double* r, double* z) {
   const cudaStream_t st = P->ctx->st;
   MS_CUDA(cudaSetDevice(P->ctx->device));
   load_free(P, r, P->r.p);
-  launch_restrict_cells(P->g, pc->cd, P->r.p, nullptr, st);
-  launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st);
+  const bool dist = P->ctx->world() > 1;
+  launch_restrict_cells(P->g, pc->C0, pc->C1, pc->cd, P->r.p, nullptr, st);
+  if (dist) {
+    exchange_rpart(pc);
+    MS_CUDA(cudaMemsetAsync(pc->f0.p, 0, pc->N_c * sizeof(double), st));
+  }
+  launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st, pc->kc0, pc->kc1);
+  if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
   launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
   launch_combine(P->g, P->mask.p, nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, P->r.p, P->z.p,
-                 nullptr, nullptr, nullptr, st);
+                 nullptr, nullptr, nullptr, st, pc->C0, pc->C1);
+  allgather_rows(P, P->z.p);
   store_free(P, P->z.p, z);
   MS_API_END(pc ? pc->prob->ctx : nullptr)
 }
@@ -900,14 +1169,16 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
   if (pc->nsys > 0)
     ms[MS_BENCH_LEVEL1] = timeit([&] {
       if (pc->dense)
-        launch_l1_dense_apply(g, pc->sys.p, pc->nsys, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, nullptr, st);
+        launch_l1_dense_apply(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p,
+                              nullptr, st);
       else
-        launch_l1_solve(g, pc->sys.p, pc->nsys, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, nullptr, st);
+        launch_l1_solve(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->max_bw, pc->Lc.p, pc->Lr.p, r,
+                        pc->ybuf.p, nullptr, st);
     });
   if (pc->has_coarse) {
     ms[MS_BENCH_RESTRICT] = timeit([&] {
-      launch_restrict_cells(g, pc->cd, r, nullptr, st);
-      launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st);
+      launch_restrict_cells(g, pc->C0, pc->C1, pc->cd, r, nullptr, st);
+      launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st, pc->kc0, pc->kc1);
     });
     ms[MS_BENCH_COARSE_SOLVE] = timeit([&] {
       launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
@@ -960,10 +1231,14 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   P->x.zero(st);
   P->p0.zero(st);
   P->p1.zero(st);
+  const bool dist = P->ctx->world() > 1;
+  if (dist && (!pc || !pc->has_coarse))
+    throw Error(MS_E_INVALID, "multi-GPU solves need the two-level preconditioner");
   PcgScalars hs{};
   hs.tol = tol;
   hs.maxit = maxit;
   hs.first = 1;
+  hs.dist = dist ? 1 : 0;
   hs.done = maxit == 0 ? 1 : 0;
   MS_CUDA(cudaMemcpyAsync(P->sc.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
   cudaEvent_t t0, t1;
@@ -986,16 +1261,21 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     Prof& pf = P->ctx->prof;
     cudaEvent_t a = pf.begin(MS_PROF_MATVEC, i, st);
     launch_matvec(P->g, P->ke, P->E.p, P->mask.p, zp, pold, pnew, P->q.p, MV_PCG, P->sc.p,
-                  P->partials.p, P->halpha.p, st);
+                  P->partials.p, P->halpha.p, st, P->b_lo, row_hi(P));
     pf.end(MS_PROF_MATVEC, i, st, a);
+    if (dist) dist_finalize(P, PART_PQ, P->halpha.p);
     a = pf.begin(MS_PROF_UPDATE, i, st);
     const bool fused = pc && pc->has_coarse;
     if (fused)  // residual update + coarse restriction partials in one pass
-      launch_update_restrict(P->g, n, P->x.p, pnew, P->r.p, P->q.p, pc->cd, P->sc.p, P->partials.p,
-                             P->hres.p, st);
+      launch_update_restrict(P->g, pc->C0, pc->C1, P->x.p, pnew, P->r.p, P->q.p, pc->cd, P->sc.p,
+                             P->partials.p, P->hres.p, st);
     else
       launch_pcg_update(n, P->x.p, pnew, P->r.p, P->q.p, P->sc.p, P->partials.p, P->hres.p, st);
     pf.end(MS_PROF_UPDATE, i, st, a);
+    if (dist) {
+      dist_finalize(P, PART_RR, P->hres.p);
+      exchange_rows(P, P->r.p, pc->halo_rows);  // level-1 subdomains reach delta rows out
+    }
     if (pc) {
       precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, i, fused);
     } else {
@@ -1009,7 +1289,7 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   // into a CUDA graph and replayed; the device `done` flag turns iterations
   // past convergence into no-ops.  Profiling mode launches directly.
   Prof& prof = P->ctx->prof;
-  const bool use_graph = maxit >= chunk;
+  const bool use_graph = maxit >= chunk && (!dist || P->ctx->comm->capturable());
   cudaGraphExec_t& gexec = prof.on ? (pc ? pc->gexec_prof : P->gexec_prof) : (pc ? pc->gexec : P->gexec);
   if (use_graph && !gexec) {
     cudaGraph_t graph;
@@ -1041,6 +1321,7 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   }
   MS_CUDA(cudaEventRecord(t1, st));
   MS_CUDA(cudaMemcpyAsync(&hs, P->sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  allgather_rows(P, P->x.p);
   store_free(P, P->x.p, x);
   float ms = 0.f;
   MS_CUDA(cudaEventElapsedTime(&ms, t0, t1));

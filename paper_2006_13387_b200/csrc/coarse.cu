@@ -218,14 +218,14 @@ constexpr int kCellThreads = 256;
 
 template <bool UPD>
 __global__ void __launch_bounds__(kCellThreads)
-    k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, double* __restrict__ x,
+    k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, int J0, double* __restrict__ x,
                     const double* __restrict__ p, double* __restrict__ r,
                     const double* __restrict__ q, PcgScalars* sc, double* partials,
                     double* res_hist, const int* done) {
   if (UPD ? sc->done : (done && *(volatile const int*)done)) return;
   __shared__ double sred[13 * (kCellThreads / 32)];
   const int64_t nn = g.n_nodes;
-  const int ci = blockIdx.x, cj = blockIdx.y, Nx = gridDim.x, Ny = gridDim.y;
+  const int ci = blockIdx.x, cj = J0 + blockIdx.y, Nx = cd.Nx, Ny = cd.Ny;
   const int mx = g.nx / Nx, my = g.ny / Ny;
   const int a_lo = ci * mx, a_hi = (ci == Nx - 1) ? g.nx : a_lo + mx - 1;
   const int b_lo = cj * my, b_hi = (cj == Ny - 1) ? g.ny : b_lo + my - 1;
@@ -325,44 +325,37 @@ __global__ void __launch_bounds__(kCellThreads)
   double tot;
   if (grid_reduce_last(threadIdx.x == 0 ? rrblk : 0.0, partials, &sc->tickets[1], &tot, sred)) {
     if (threadIdx.x == 0) {
-      sc->rr = tot;
-      const double res = sqrt(tot) / sc->bnorm;
-      sc->res = res;
-      sc->iter += 1;
-      if (res_hist) res_hist[sc->iter] = res;
-      if (res <= sc->tol) {
-        sc->converged = 1;
-        sc->done = 1;
-      } else if (sc->iter >= sc->maxit) {
-        sc->done = 1;
-      }
+      if (sc->dist)
+        sc->part[PART_RR] = tot;
+      else
+        fin_res(sc, tot, res_hist);
     }
   }
 }
 
-void launch_update_restrict(const Grid& g, int64_t n_full, double* x, const double* p, double* r,
+void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const double* p, double* r,
                             const double* q, const CoarseDev& cd, PcgScalars* sc,
                             double* partials, double* res_hist, cudaStream_t st) {
-  (void)n_full;
-  k_cell_restrict<true><<<dim3(cd.Nx, cd.Ny), kCellThreads, 0, st>>>(g, cd, 1, x, p, r, q, sc,
-                                                                     partials, res_hist, nullptr);
+  k_cell_restrict<true><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc,
+                                                                       partials, res_hist, nullptr);
   MS_CUDA(cudaGetLastError());
 }
 
-void launch_restrict_cells(const Grid& g, const CoarseDev& cd, const double* r, const int* done,
-                           cudaStream_t st) {
-  k_cell_restrict<false><<<dim3(cd.Nx, cd.Ny), kCellThreads, 0, st>>>(
-      g, cd, 1, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+void launch_restrict_cells(const Grid& g, int J0, int J1, const CoarseDev& cd, const double* r,
+                           const int* done, cudaStream_t st) {
+  k_cell_restrict<false><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(
+      g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
   MS_CUDA(cudaGetLastError());
 }
 
 // f0 rows of centre k = sum of the partials of the 4 cells around it, in
 // J-major cell order; centre (I, J) is corner (I-ci) + 2 (J-cj) of cell (ci, cj)
-__global__ void k_restrict_reduce(CoarseDev cd, double* __restrict__ f0, const int* done) {
+__global__ void k_restrict_reduce(CoarseDev cd, double* __restrict__ f0, const int* done, int k_begin,
+                                  int k_end) {
   if (done && *(volatile const int*)done) return;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k = t / kSlots, slot = t % kSlots;
-  if (k >= cd.n_centers) return;
+  const int k = k_begin + t / kSlots, slot = t % kSlots;
+  if (k >= k_end) return;
   const int nsel = cd.nsel[k];
   const bool rot = slot == 2 * kMaxModes;
   if (!(slot < 2 * nsel || (rot && cd.enrich))) return;
@@ -379,10 +372,12 @@ __global__ void k_restrict_reduce(CoarseDev cd, double* __restrict__ f0, const i
   f0[rot ? cd.roff + k : cd.hoff[k] + slot] = s;
 }
 
-void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cudaStream_t st) {
-  if (cd.n_centers == 0) return;
-  const int total = cd.n_centers * kSlots;
-  k_restrict_reduce<<<div_up(total, 256), 256, 0, st>>>(cd, f0, done);
+void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cudaStream_t st,
+                            int k_begin, int k_end) {
+  if (k_end < 0) k_end = cd.n_centers;
+  if (k_end <= k_begin) return;
+  const int total = (k_end - k_begin) * kSlots;
+  k_restrict_reduce<<<div_up(total, 256), 256, 0, st>>>(cd, f0, done, k_begin, k_end);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -397,13 +392,13 @@ constexpr int kCombineThreads = 256;
 
 __global__ void __launch_bounds__(kCombineThreads)
     k_combine(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, int has_l1, CoarseDev cd,
-              int has_coarse, int Nx, int Ny, const double* __restrict__ y0,
+              int has_coarse, int Nx, int Ny, int J0, const double* __restrict__ y0,
               const double* __restrict__ r, double* __restrict__ z, PcgScalars* sc,
               double* partials, double* beta_hist) {
   if (sc && sc->done) return;
   __shared__ double sred[kCombineThreads / 32];
   const int64_t nn = g.n_nodes;
-  const int ci = blockIdx.x, cj = blockIdx.y;
+  const int ci = blockIdx.x, cj = J0 + blockIdx.y;
   const int mx = g.nx / Nx, my = g.ny / Ny;
   const int a_lo = ci * mx, a_hi = (ci == Nx - 1) ? g.nx : a_lo + mx - 1;
   const int b_lo = cj * my, b_hi = (cj == Ny - 1) ? g.ny : b_lo + my - 1;
@@ -506,27 +501,24 @@ __global__ void __launch_bounds__(kCombineThreads)
   double tot;
   if (grid_reduce_last(bs, partials, &sc->tickets[2], &tot, sred)) {
     if (threadIdx.x == 0) {
-      if (sc->first) {
-        sc->beta = 0.0;
-        sc->first = 0;
-      } else {
-        sc->beta = tot / sc->rz;
-        if (beta_hist) beta_hist[sc->iter - 1] = sc->beta;
-      }
-      sc->rz = tot;
+      if (sc->dist)
+        sc->part[PART_RZ] = tot;
+      else
+        fin_beta(sc, tot, beta_hist);
     }
   }
 }
 
 void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
                     int Nx, int Ny, const double* y0, const double* r, double* z, PcgScalars* sc,
-                    double* partials, double* beta_hist, cudaStream_t st) {
+                    double* partials, double* beta_hist, cudaStream_t st, int J0, int J1) {
   L1Dev l1v{};
   CoarseDev cdv{};
   if (l1) l1v = *l1;
   if (cd) cdv = *cd;
-  k_combine<<<dim3(Nx, Ny), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0, Nx,
-                                                      Ny, y0, r, z, sc, partials, beta_hist);
+  if (J1 < 0) J1 = Ny;
+  k_combine<<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0,
+                                                           Nx, Ny, J0, y0, r, z, sc, partials, beta_hist);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -538,13 +530,13 @@ void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const C
 __global__ void __launch_bounds__(256)
     k_k0_assemble(Grid g, KeParam ke, const double* __restrict__ E,
                   const uint8_t* __restrict__ mask, CoarseDev cd, double* __restrict__ K0,
-                  double* __restrict__ scratch) {
+                  double* __restrict__ scratch, int k_begin, int k_end) {
   __shared__ double sred[8];
   const int NL = cd.NLx * cd.NLy;
   double* v = scratch + (int64_t)blockIdx.x * 4 * NL;  // [2][NL]
   double* u = v + 2 * NL;                              // [2][NL]
   const int nex = 2 * cd.mex, ney = 2 * cd.mey;
-  for (int k = blockIdx.x; k < cd.n_centers; k += gridDim.x) {
+  for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x) {
     const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
     const int nsel = cd.nsel[k], nb = 2 * nsel + cd.enrich;
     const int ax0 = (I - 1) * cd.mex, by0 = (J - 1) * cd.mey;
@@ -613,9 +605,10 @@ __global__ void __launch_bounds__(256)
 
 void launch_k0_assemble(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                         const CoarseDev& cd, double* K0, double* scratch, int n_cta,
-                        cudaStream_t st) {
+                        cudaStream_t st, int k_begin, int k_end) {
   if (cd.n_centers == 0) return;
-  k_k0_assemble<<<n_cta, 256, 0, st>>>(g, ke, E, mask, cd, K0, scratch);
+  if (k_end < 0) k_end = cd.n_centers;
+  k_k0_assemble<<<n_cta, 256, 0, st>>>(g, ke, E, mask, cd, K0, scratch, k_begin, k_end);
   MS_CUDA(cudaGetLastError());
 }
 

@@ -55,12 +55,14 @@ void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double
 
 // fused x += alpha p, r -= alpha q, ||r||^2 -> convergence, and restriction
 // partial sums per coarse cell; then f0 = sum of the 4 cell partials per centre
-void launch_update_restrict(const Grid& g, int64_t n_full, double* x, const double* p, double* r,
+// cells of coarse block rows [J0, J1) (the caller's strip)
+void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const double* p, double* r,
                             const double* q, const CoarseDev& cd, PcgScalars* sc,
                             double* partials, double* res_hist, cudaStream_t st);
-void launch_restrict_cells(const Grid& g, const CoarseDev& cd, const double* r, const int* done,
-                           cudaStream_t st);
-void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cudaStream_t st);
+void launch_restrict_cells(const Grid& g, int J0, int J1, const CoarseDev& cd, const double* r,
+                           const int* done, cudaStream_t st);
+void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cudaStream_t st,
+                            int k_begin = 0, int k_end = -1);
 
 // chi table, bit-identical to the reference's PoU (grid.py:172-207)
 void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStream_t st);
@@ -73,12 +75,12 @@ void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double
 // optionally r.z -> beta (PCG mode when sc != nullptr).
 void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
                     int Nx, int Ny, const double* y0, const double* r, double* z, PcgScalars* sc,
-                    double* partials, double* beta_hist, cudaStream_t st);
+                    double* partials, double* beta_hist, cudaStream_t st, int J0 = 0, int J1 = -1);
 
 // K0 = R0 A R0^T (dense row-major N_c x N_c), symmetrised (coarse.py:161-168)
 void launch_k0_assemble(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                         const CoarseDev& cd, double* K0, double* scratch, int n_cta,
-                        cudaStream_t st);
+                        cudaStream_t st, int k_begin = 0, int k_end = -1);
 void launch_symmetrize(int N, double* A, cudaStream_t st);
 
 }  // namespace msgpu

@@ -5,6 +5,8 @@
 // component-grouped layout [x-plane | y-plane] of (nx+1)(ny+1) nodes each;
 // constrained dofs are held at exactly zero by a byte mask, which makes the
 // full-layout Krylov recurrence identical to the reference's free-dof one.
+#include <algorithm>
+
 #include "operator.cuh"
 
 namespace msgpu {
@@ -28,13 +30,13 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, 3)
     k_matvec(Grid g, KeParam ke, const double* __restrict__ E, const uint8_t* __restrict__ mask,
              const double* __restrict__ z, const double* __restrict__ p_old,
              double* __restrict__ p_new, double* __restrict__ q, int mode, PcgScalars* sc,
-             double* partials, double* alpha_hist) {
+             double* partials, double* alpha_hist, int b_lo, int b_hi, int tile_y0) {
   if (mode == MV_PCG && sc->done) return;
   __shared__ double sp[2][MV_NY + 2][MV_TX + 2];
   __shared__ double sE[MV_NY + 1][MV_TX + 1];
   __shared__ double sred[MV_TX * MV_TY / 32];
 
-  const int a0 = blockIdx.x * MV_TX, b0 = blockIdx.y * MV_NY;
+  const int a0 = blockIdx.x * MV_TX, b0 = (blockIdx.y + tile_y0) * MV_NY;
   const int tid = threadIdx.x;
   const double beta = (mode == MV_PCG) ? sc->beta : 0.0;
   const int64_t nn = g.n_nodes;
@@ -102,17 +104,20 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, 3)
 #pragma unroll
   for (int r = 0; r < MV_RPT; ++r) {
     const int b = b0 + ty * MV_RPT + r;
-    if (a <= g.nx && b <= g.ny) {
+    if (a <= g.nx && b >= b_lo - 1 && b <= b_hi + 1 && b <= g.ny) {
       const int64_t n = (int64_t)b * g.nnx + a;
+      const bool own = b >= b_lo && b <= b_hi;
       const double ox = mask[n] ? qx[r] : 0.0;
       const double oy = mask[n + nn] ? qy[r] : 0.0;
-      q[n] = ox;
-      q[n + nn] = oy;
+      if (own) {
+        q[n] = ox;
+        q[n + nn] = oy;
+      }
       if (mode == MV_PCG) {
         const double px = sp[0][Y0 + r][X], py = sp[1][Y0 + r][X];
-        p_new[n] = px;
+        p_new[n] = px;  // owned rows and one halo row on each side
         p_new[n + nn] = py;
-        dot += px * ox + py * oy;
+        if (own) dot += px * ox + py * oy;
       }
     }
   }
@@ -121,19 +126,23 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, 3)
   double tot;
   if (grid_reduce_last(bs, partials, &sc->tickets[0], &tot, sred)) {
     if (threadIdx.x == 0) {
-      sc->pq = tot;
-      sc->alpha = sc->rz / tot;
-      if (alpha_hist) alpha_hist[sc->iter] = sc->alpha;
+      if (sc->dist)
+        sc->part[PART_PQ] = tot;
+      else
+        fin_alpha(sc, tot, alpha_hist);
     }
   }
 }
 
 void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                    const double* z, const double* p_old, double* p_new, double* q, int mode,
-                   PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st) {
-  dim3 grid(div_up(g.nx + 1, MV_TX), div_up(g.ny + 1, MV_NY));
+                   PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st,
+                   int b_lo, int b_hi) {
+  if (b_hi < 0) b_hi = g.ny;
+  const int ty0 = std::max(0, b_lo - 1) / MV_NY, ty1 = std::min(g.ny, b_hi + 1) / MV_NY;
+  dim3 grid(div_up(g.nx + 1, MV_TX), ty1 - ty0 + 1);
   k_matvec<<<grid, MV_TX * MV_TY, 0, st>>>(g, ke, E, mask, z, p_old, p_new, q, mode, sc, partials,
-                                           alpha_hist);
+                                           alpha_hist, b_lo, b_hi, ty0);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -171,19 +180,7 @@ __global__ void __launch_bounds__(kReduceThreads)
   const double bs = block_sum(acc, sred);
   double tot;
   if (grid_reduce_last(bs, partials, &sc->tickets[1], &tot, sred)) {
-    if (threadIdx.x == 0) {
-      sc->rr = tot;
-      const double res = sqrt(tot) / sc->bnorm;
-      sc->res = res;
-      sc->iter += 1;
-      if (res_hist) res_hist[sc->iter] = res;
-      if (res <= sc->tol) {
-        sc->converged = 1;
-        sc->done = 1;
-      } else if (sc->iter >= sc->maxit) {
-        sc->done = 1;
-      }
-    }
+    if (threadIdx.x == 0) fin_res(sc, tot, res_hist);
   }
 }
 
@@ -206,16 +203,7 @@ __global__ void __launch_bounds__(kReduceThreads)
   const double bs = block_sum(acc, sred);
   double tot;
   if (grid_reduce_last(bs, partials, &sc->tickets[2], &tot, sred)) {
-    if (threadIdx.x == 0) {
-      if (sc->first) {
-        sc->beta = 0.0;
-        sc->first = 0;
-      } else {
-        sc->beta = tot / sc->rz;
-        if (beta_hist) beta_hist[sc->iter - 1] = sc->beta;
-      }
-      sc->rz = tot;
-    }
+    if (threadIdx.x == 0) fin_beta(sc, tot, beta_hist);
   }
 }
 
@@ -255,6 +243,24 @@ void launch_init_norm(int64_t n, const double* b, PcgScalars* sc, double* partia
 }
 
 // ---------------------------------------------------------------------------
+__global__ void k_finalize(PcgScalars* sc, int kind, double* hist) {
+  // the partial of an iteration already marked done was never produced
+  if (kind != PART_RR && sc->done) return;
+  if (kind == PART_RR && sc->done) return;
+  const double v = sc->part[kind];
+  if (kind == PART_PQ)
+    fin_alpha(sc, v, hist);
+  else if (kind == PART_RR)
+    fin_res(sc, v, hist);
+  else
+    fin_beta(sc, v, hist);
+}
+
+void launch_finalize(PcgScalars* sc, int kind, double* hist, cudaStream_t st) {
+  k_finalize<<<1, 1, 0, st>>>(sc, kind, hist);
+  MS_CUDA(cudaGetLastError());
+}
+
 __global__ void k_scatter_free(int64_t n_free, const int64_t* __restrict__ free_dofs,
                                const double* __restrict__ src, double* __restrict__ dst) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_free;

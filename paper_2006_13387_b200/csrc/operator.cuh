@@ -20,9 +20,46 @@ struct PcgScalars {
   int done;
   int converged;
   int first;       // next z.r reduction starts the recurrence (beta = 0)
-  int pad;
+  int dist;        // multi-rank: reductions leave partials in part[], finalised after allreduce
+  double part[4];  // per-rank partial sums: [PART_PQ], [PART_RR], [PART_RZ]
   unsigned int tickets[8];
 };
+
+enum { PART_PQ = 0, PART_RR = 1, PART_RZ = 2 };
+
+// scalar recurrences, shared by the single-rank last-CTA path and the
+// multi-rank finalize kernel (krylov.py:115-129)
+__device__ __forceinline__ void fin_alpha(PcgScalars* sc, double pq, double* alpha_hist) {
+  sc->pq = pq;
+  sc->alpha = sc->rz / pq;
+  if (alpha_hist) alpha_hist[sc->iter] = sc->alpha;
+}
+__device__ __forceinline__ void fin_res(PcgScalars* sc, double rr, double* res_hist) {
+  sc->rr = rr;
+  const double res = sqrt(rr) / sc->bnorm;
+  sc->res = res;
+  sc->iter += 1;
+  if (res_hist) res_hist[sc->iter] = res;
+  if (res <= sc->tol) {
+    sc->converged = 1;
+    sc->done = 1;
+  } else if (sc->iter >= sc->maxit) {
+    sc->done = 1;
+  }
+}
+__device__ __forceinline__ void fin_beta(PcgScalars* sc, double rz, double* beta_hist) {
+  if (sc->first) {
+    sc->beta = 0.0;
+    sc->first = 0;
+  } else {
+    sc->beta = rz / sc->rz;
+    if (beta_hist) beta_hist[sc->iter - 1] = sc->beta;
+  }
+  sc->rz = rz;
+}
+
+// multi-rank: finalize one allreduced partial (kind = PART_*)
+void launch_finalize(PcgScalars* sc, int kind, double* hist, cudaStream_t st);
 
 // Element stiffness of the unit modulus Q1 plane-stress element, passed by
 // value (kernel parameter space is a broadcast constant bank).
@@ -35,9 +72,11 @@ constexpr int MV_TY = 8;   // nodes per CTA in y (one node per thread)
 
 enum { MV_PLAIN = 0, MV_PCG = 1 };
 
+// b_lo..b_hi: owned node rows (q and p.q there; p refreshed on b_lo-1..b_hi+1)
 void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                    const double* z, const double* p_old, double* p_new, double* q, int mode,
-                   PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st);
+                   PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st,
+                   int b_lo = 0, int b_hi = -1);
 
 void launch_pcg_update(int64_t n, double* x, const double* p, double* r, const double* q,
                        PcgScalars* sc, double* partials, double* res_hist, cudaStream_t st);

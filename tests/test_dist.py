@@ -1,0 +1,142 @@
+"""Multi-rank (strip-sharded) path.
+
+CPU: world_size-2 gloo process groups check that the C++ strip partition and
+halo plans (the exact functions the solver uses, via the ABI, no CUDA) pair
+up across ranks.  GPU: two ranks on the single available B200 talk through
+gloo host callbacks (their kernels never wait on each other) and must
+reproduce the one-rank solve.
+"""
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+# ---------------------------------------------------------------------------
+# CPU: partition and halo pairing
+
+
+def _plan_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    from paper_2006_13387_b200 import dist as D
+
+    _init(rank, world, port)
+    try:
+        out = {}
+        for nrows, H, ny, k in ((4, 16, 64, 2), (7, 32, 224, 3), (64, 32, 2048, 2)):
+            lo, hi = D.strip_rows(nrows, world, rank)
+            b_lo = lo * H
+            b_hi = ny if hi == nrows else hi * H - 1
+            plan = D.halo_plan(b_lo, b_hi, ny, k, rank, world)
+            allp = [None] * world
+            dist.all_gather_object(allp, (lo, hi, b_lo, b_hi, plan))
+            out[(nrows, H, ny, k)] = allp
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strip_partition_and_halo_pairing_gloo(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for key, allp in res[0].items():
+        nrows, H, ny, k = key
+        # every rank saw the same plans
+        assert all(res[r][key] == allp for r in range(world))
+        # strips tile [0, nrows) and node rows tile [0, ny]
+        assert allp[0][0] == 0 and allp[-1][1] == nrows
+        assert all(allp[r][1] == allp[r + 1][0] for r in range(world - 1))
+        assert allp[0][2] == 0 and allp[-1][3] == ny
+        assert all(allp[r][3] + 1 == allp[r + 1][2] for r in range(world - 1))
+        # every send matches the partner's receive (rows and counts)
+        for r in range(world):
+            for slot in (0, 1):
+                s_lo, s_n, dst, _, _, _ = allp[r][4][slot]
+                if dst < 0:
+                    assert s_n == 0
+                    continue
+                _, _, _, r_lo, r_n, src = allp[dst][4][slot]
+                assert src == r and r_lo == s_lo and r_n == s_n and s_n == min(k, allp[r][3] - allp[r][2] + 1)
+
+
+# ---------------------------------------------------------------------------
+# GPU: 2 ranks on one device through gloo host callbacks
+
+
+def _solve_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    _init(rank, world, port)
+    try:
+        from paper_2006_13387_b200 import configs, dist as D, pcg_solve
+        from paper_2006_13387_b200.solve import setup_spec
+
+        D.init_host_callbacks(0)
+        spec = configs.config1(seed=0, n=64, H=16, delta=2)
+        mesh, op, pre = setup_spec(spec)
+        x, rep = pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
+        z = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
+        q.put((rank, x, rep.iterations, rep.converged, pre.coarse_dim, list(pre.mode_counts), z))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_one_gpu_match_single_rank():
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_solve_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((v[0], v[1:]) for v in (q.get(timeout=600) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    sys.path.insert(0, str(ROOT))
+    from paper_2006_13387_b200 import configs, pcg_solve
+    from paper_2006_13387_b200.solve import setup_spec
+
+    spec = configs.config1(seed=0, n=64, H=16, delta=2)
+    mesh, op, pre = setup_spec(spec)
+    x1, rep1 = pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
+    z1 = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
+    for r in (0, 1):
+        x, iters, conv, nc, modes, z = res[r]
+        assert conv and nc == pre.coarse_dim and modes == list(pre.mode_counts)
+        assert np.linalg.norm(z - z1) <= 1e-12 * np.linalg.norm(z1)
+        assert abs(iters - rep1.iterations) <= max(3, int(0.06 * rep1.iterations))
+        assert np.linalg.norm(x - x1) <= 1e-7 * np.linalg.norm(x1)
+    assert np.array_equal(res[0][0], res[1][0])
