@@ -19,7 +19,7 @@ value = n_free * iterations * K / device time of the K solves (CUDA events on
 the solver's stream), inputs resident in HBM.  e2e = the same metric through
 the public API with host numpy buffers (H2D of b, D2H of x and the residual
 history inside the timed region).  The level-1 factors (11.9 GB) exceed L2,
-so no L2 flush is needed between solves.  Under torchrun (N>1) each rank
+so no L2 flush is needed between solves.  Under torchrun (N>1) each
 rank owns a strip of subdomain rows of the SAME problem (NCCL halo exchanges,
 dot-product and coarse-residual allreduces, replicated coarse solve):
 "scaling": "strong".
