@@ -71,6 +71,12 @@ typedef struct ms_precond_opts {
   int use_coarse;        /* 1 (default); 0 drops level 2 (diagnostics)                  */
   const int64_t* heat_dirichlet_nodes; /* whole nodes clamped in the heat eigenproblems */
   int64_t n_heat_dirichlet;
+  /* EH+Rot;Rand (solve_local_eig_randomized, spectral.py:103-158): forcings
+   * [n_centers][n_snapshots][(2H+1)^2] (closed-neighbourhood nodes, row-major,
+   * zero at clamped nodes) drawn by the caller from default_rng([seed, centre]) */
+  int randomized;
+  int n_snapshots;
+  const double* snapshots;
 } ms_precond_opts;
 
 /* Build metadata, the `info` dict of schwarz.py:202-210 plus eigensolver stats. */

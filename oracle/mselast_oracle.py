@@ -275,6 +275,59 @@ def lowest_eigenpairs_arpack(K, M, k):
     return w, v
 
 
+def randomized_eigenpairs(K, M, k, n_snapshots, seed, n_passes=4):
+    """Randomized snapshot eigen-approximation (spectral.py:103-158).
+
+    Deflated shift-invert block iteration on uniform(-1,1) forcings drawn from
+    ``default_rng(seed)``, enrichment with the constant (heat kernel
+    candidate), SVD orthonormalisation with a 1e-10 rank cut, Rayleigh-Ritz.
+    """
+    if n_snapshots < k:
+        raise ValueError("need at least k snapshots")
+    A, B = K.matrix, M.matrix
+    n = A.shape[0]
+    rng = np.random.default_rng(seed)
+    Z = np.ones((n, 1))
+    MZ = B @ Z
+    G = Z.T @ MZ
+    F = rng.uniform(-1.0, 1.0, size=(n, n_snapshots))
+    F = F - MZ @ np.linalg.solve(G, Z.T @ F)
+
+    def deflate(X):
+        return X - Z @ np.linalg.solve(G, MZ.T @ X)
+
+    sigma = 1e-8 * (A.diagonal().sum() / n)
+    lu = spla.splu((A + sigma * B).tocsc())
+    U = deflate(lu.solve(F))
+    for _ in range(n_passes - 1):
+        U, _ = np.linalg.qr(U)
+        U = deflate(lu.solve(B @ U))
+    W = np.hstack([U, Z])
+    nrm = np.linalg.norm(W, axis=0)
+    nrm[nrm == 0.0] = 1.0
+    Q, s, _ = np.linalg.svd(W / nrm, full_matrices=False)
+    Q = Q[:, s > 1e-10 * s[0]]
+    Kr = Q.T @ (A @ Q)
+    Mr = Q.T @ (B @ Q)
+    w, v = sla.eigh(0.5 * (Kr + Kr.T), 0.5 * (Mr + Mr.T))
+    m = min(k, w.size)
+    return w[:m], Q @ v[:, :m]
+
+
+def randomized_solver(n_max=6, n_snapshots=None, seed=0):
+    """eig_solver hook for heat_rot_coarse_space: per-centre seed [seed, centre]
+    (schwarz.py:156-160); n_snapshots defaults to n_max + 5."""
+    counter = {"k": 0}
+
+    def solve(K, M, kk):
+        centre = counter["k"]
+        counter["k"] += 1
+        ns = n_snapshots or (n_max + 5)
+        return randomized_eigenpairs(K, M, kk, min(ns, K.n_free), [seed, centre])
+
+    return solve
+
+
 def gap_count(lam, n_max, threshold=50.0):
     """Gap rule (spectral.py:161-186): largest i<=n_max with l[i]/max(l[i-1],eps)>=thr."""
     if n_max < 1:

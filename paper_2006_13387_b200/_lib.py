@@ -49,6 +49,7 @@ class PrecondOpts(C.Structure):
         ("n_max", C.c_int), ("gap_threshold", C.c_double), ("enrich", C.c_int),
         ("fixed_rule", C.c_int), ("local_solver", C.c_int), ("use_coarse", C.c_int),
         ("heat_dirichlet_nodes", C.POINTER(C.c_int64)), ("n_heat_dirichlet", C.c_int64),
+        ("randomized", C.c_int), ("n_snapshots", C.c_int), ("snapshots", C.c_void_p),
     ]
 
 

@@ -730,6 +730,9 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
   if (o->heat_dirichlet_nodes && o->n_heat_dirichlet > 0)
     pc->heat_dir.assign(o->heat_dirichlet_nodes, o->heat_dirichlet_nodes + o->n_heat_dirichlet);
   pc->opts.heat_dirichlet_nodes = nullptr;
+  pc->opts.snapshots = nullptr;
+  if (o->randomized && (!o->snapshots || o->n_snapshots < 1 || o->n_snapshots + 1 > kEigBlock - 2))
+    throw Error(MS_E_INVALID, "randomized eigensolver needs 1..13 snapshots and the forcings array");
   DBuf<int> fail;
   fail.alloc(1);
 
@@ -899,7 +902,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     }
     const int batch = std::min(std::max(pc->kc1 - pc->kc0, 1), 1024);
     DBuf<BandSys> hsysd;
-    DBuf<double> hLc, hLr, work, evecs;
+    DBuf<double> hLc, hLr, work, evecs, rsig, rF;
     // own centres' vectors are compacted with local offsets, then placed at
     // their global offsets once every rank's mode counts are known
     DBuf<double> psi_local_buf;
@@ -936,13 +939,26 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       hsysd.upload(hs.data(), nk, st);
       MS_CUDA(cudaMemsetAsync(hLr.p, 0, foff * sizeof(double), st));
       fail.zero(st);
-      launch_heat_assemble(g, P->E.p, hdir.p, hp, sigma, hsysd.p, nk, hLc.p, st);
+      if (o->randomized) {
+        // the reference's shift (spectral.py:133) and this batch's forcings
+        if (rsig.n < (size_t)nk) rsig.alloc(nk);
+        launch_rand_sigma(g, P->E.p, hdir.p, hp, hsysd.p, nk, rsig.p, st);
+        const size_t fcount = (size_t)nk * o->n_snapshots * NL;
+        if (rF.n < fcount) rF.alloc(fcount);
+        MS_CUDA(cudaMemcpyAsync(rF.p, o->snapshots + (size_t)k0 * o->n_snapshots * NL, fcount * sizeof(double),
+                                cudaMemcpyDefault, st));
+      }
+      launch_heat_assemble(g, P->E.p, hdir.p, hp, sigma, hsysd.p, nk, hLc.p, st,
+                           o->randomized ? rsig.p : nullptr);
       launch_band_potrf(hsysd.p, nk, mbw, hLc.p, hLr.p, fail.p, st);
       check_fail(fail, st, "neighbourhood heat pencil (K + sigma M)");
       EigBatch eb{o->Nx, cd.mex, cd.mey, k0, nk, hsysd.p, hLc.p, hLr.p, work.p, pc->evals.p,
                   evecs.p, passes.p, neumann.p, o->n_max, o->gap_threshold, o->fixed_rule,
                   1e-15 * 24.0 / (g.h * g.h)};
-      launch_subspace(g, P->E.p, hdir.p, hp, eb, 300, 1e-12, st);
+      if (o->randomized)
+        launch_randomized(g, P->E.p, hdir.p, hp, eb, rF.p, o->n_snapshots, st);
+      else
+        launch_subspace(g, P->E.p, hdir.p, hp, eb, 300, 1e-12, st);
       launch_select(nc, pc->evals.p, o->n_max, o->gap_threshold, o->fixed_rule, pc->nsel.p, st);
       std::vector<int> bsel(nk);
       MS_CUDA(cudaMemcpyAsync(bsel.data(), pc->nsel.p + k0, nk * sizeof(int), cudaMemcpyDeviceToHost, st));

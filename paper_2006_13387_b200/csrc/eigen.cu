@@ -9,6 +9,8 @@
 // (K_H + sigma M_H)^{-1} comes from the batched banded Cholesky.  For a pure
 // Neumann neighbourhood the constant (exact kernel, spectral.py:37-45) is
 // locked and deflated from the block every pass.
+#include <math_constants.h>
+
 #include <algorithm>
 
 #include "eigen.cuh"
@@ -24,8 +26,9 @@ constexpr int kEPD = 4;   // software prefetch depth of the banded sweeps
 __global__ void __launch_bounds__(256)
     k_heat_assemble(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
                     HeatParam hp, double sigma, const BandSys* __restrict__ sys,
-                    double* __restrict__ Lc) {
+                    double* __restrict__ Lc, const double* __restrict__ sigma_per_sys) {
   const BandSys s = sys[blockIdx.x];
+  if (sigma_per_sys) sigma = sigma_per_sys[blockIdx.x];
   const int S = s.bw + 1;
   const int64_t total = (int64_t)s.n * S;
   const int ex_lo = s.a0, ex_hi = s.a0 + s.w - 2, ey_lo = s.b0, ey_hi = s.b0 + s.hgt - 2;
@@ -61,9 +64,9 @@ __global__ void __launch_bounds__(256)
 
 void launch_heat_assemble(const Grid& g, const double* E, const uint8_t* hdir,
                           const HeatParam& hp, double sigma, const BandSys* sys, int nsys,
-                          double* Lc, cudaStream_t st) {
+                          double* Lc, cudaStream_t st, const double* sigma_per_sys) {
   if (nsys == 0) return;
-  k_heat_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sigma, sys, Lc);
+  k_heat_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sigma, sys, Lc, sigma_per_sys);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -523,6 +526,317 @@ void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const 
   if (smem > 220 * 1024) throw Error(-1, "neighbourhood too large for the eigensolver tile");
   MS_CUDA(cudaFuncSetAttribute(k_subspace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_subspace<<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, max_pass, tol);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Randomized snapshot eigensolver, EH+Rot;Rand (spectral.py:103-158), one CTA
+// per centre.  Same algorithm as the reference on the same forcings (host
+// PCG64, seeds [seed, centre]) and the same shift sigma = 1e-8 tr(K)/n:
+// F -= MZ (Z^T F)/G; U = deflate(B^-1 F); 3 x { U = orth(U); U = deflate(B^-1 M U) };
+// Q = orthonormal basis of [U, Z] (1e-10 rank cut); Rayleigh-Ritz on (Q^T K Q,
+// Q^T M Q).  Z = 1 on free nodes, deflate(X) = X - Z (MZ^T X)/G.
+__device__ void cgs2_euclid(double* cols, int ncols, int n, double* red, double* dots,
+                            double* keep_flag) {
+  // in place Euclidean CGS2 of `ncols` columns; zeroes columns that vanish
+  double v[P + 1];
+  for (int c = 0; c < ncols; ++c) {
+    double* w = cols + (int64_t)c * n;
+    double nrm0 = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) nrm0 += w[i] * w[i];
+#pragma unroll
+    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    v[0] = nrm0;
+    block_sum_multi(v, 1, red, dots);
+    nrm0 = dots[0];
+    for (int rep = 0; rep < 2; ++rep) {
+#pragma unroll
+      for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+          if (l < c) v[l] += cols[(int64_t)l * n + i] * w[i];
+      }
+      block_sum_multi(v, P + 1, red, dots);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double x = w[i];
+        for (int l = 0; l < c; ++l) x -= dots[l] * cols[(int64_t)l * n + i];
+        w[i] = x;
+      }
+      __syncthreads();
+    }
+    double nrm = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) nrm += w[i] * w[i];
+#pragma unroll
+    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    v[0] = nrm;
+    block_sum_multi(v, 1, red, dots);
+    const bool ok = dots[0] > 1e-20 * nrm0 && dots[0] > 0.0;
+    const double inv = ok ? 1.0 / sqrt(dots[0]) : 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] *= inv;
+    if (threadIdx.x == 0 && keep_flag) keep_flag[c] = ok ? 1.0 : 0.0;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kEigThreads)
+    k_randomized(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
+                 HeatParam hp, EigBatch eb, const double* __restrict__ F, int ns, int nlx) {
+  extern __shared__ double sm[];
+  const int kb = blockIdx.x, k = eb.k0 + kb;
+  const BandSys s = eb.sys[kb];
+  const int n = s.n, S = s.bw + 1;
+  const int nex = 2 * eb.mex, ney = 2 * eb.mey;
+  constexpr int LD = P + 1;
+  double* sE = sm;
+  double* win = sE + nex * ney;
+  double* red = win + S * P;
+  double* dots = red + (P + 1) * 8;
+  double* Am = dots + (P + 1);
+  double* Vm = Am + P * LD;
+  double* ritz = Vm + P * LD;
+  double* keep = ritz + P;  // P flags
+  double* misc = keep + P;
+  int* order = reinterpret_cast<int*>(misc + 4);
+  uint8_t* dir = reinterpret_cast<uint8_t*>(order + P);
+  __shared__ double hlap[16], hmel[16];
+  __shared__ double Lm[P][P + 1], Cm[P][P + 1];
+  if (threadIdx.x < 16) {
+    hlap[threadIdx.x] = hp.lap[threadIdx.x];
+    hmel[threadIdx.x] = hp.mel[threadIdx.x];
+  }
+  for (int t = threadIdx.x; t < nex * ney; t += blockDim.x)
+    sE[t] = E[(int64_t)(s.b0 + t / nex) * g.nx + s.a0 + t % nex];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int a, b;
+    band_node_of(s, i, a, b);
+    dir[i] = hdir[(int64_t)b * g.nnx + a];
+  }
+  __syncthreads();
+  const EigCtx ctx{s, n, nex, ney, sE, dir, hlap, hmel};
+  double* X = eb.work + (int64_t)kb * 2 * P * n;  // cols 0..P-3: basis; P-2: MZ; P-1: Z
+  double* W = X + (int64_t)P * n;                 // solve workspace
+  double* Zc = X + (int64_t)(P - 1) * n;
+  double* MZ = X + (int64_t)(P - 2) * n;
+  double v[P + 1];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) Zc[i] = dir[i] ? 0.0 : 1.0;
+  __syncthreads();
+  double G;
+  {
+#pragma unroll
+    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double mz = dir[i] ? 0.0 : stencil(ctx, Zc, i, hmel);
+      MZ[i] = mz;
+      v[0] += Zc[i] * mz;
+    }
+    block_sum_multi(v, 1, red, dots);
+    G = dots[0];
+  }
+  // forcings (lexicographic node index in F -> band order)
+  const double* Fk = F + (int64_t)kb * ns * (nlx * (n / nlx));
+  for (int t = threadIdx.x; t < n * P; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    double val = 0.0;
+    if (c < ns && !dir[i]) {
+      int a, b;
+      band_node_of(s, i, a, b);
+      val = Fk[(int64_t)c * n + (a - s.a0) + (int64_t)(b - s.b0) * nlx];
+    }
+    W[t] = val;
+  }
+  __syncthreads();
+  // F -= MZ (Z^T F) / G
+  {
+#pragma unroll
+    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+      for (int c = 0; c < P; ++c)
+        if (c < ns) v[c] += Zc[i] * W[(int64_t)c * n + i];
+    block_sum_multi(v, P + 1, red, dots);
+    for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
+      const int c = t / n, i = t % n;
+      W[t] -= MZ[i] * (dots[c] / G);
+    }
+    __syncthreads();
+  }
+  auto deflate = [&]() {
+#pragma unroll
+    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+      for (int c = 0; c < P; ++c)
+        if (c < ns) v[c] += MZ[i] * W[(int64_t)c * n + i];
+    block_sum_multi(v, P + 1, red, dots);
+    for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
+      const int c = t / n, i = t % n;
+      W[t] -= Zc[i] * (dots[c] / G);
+    }
+    __syncthreads();
+  };
+  band_solve_block(s, eb.Lc, eb.Lr, W, win);
+  deflate();
+  for (int pass = 1; pass < 4; ++pass) {
+    cgs2_euclid(W, ns, n, red, dots, nullptr);
+    for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
+      const int c = t / n, i = t % n;
+      X[t] = dir[i] ? 0.0 : stencil(ctx, W + (int64_t)c * n, i, hmel);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n * ns; t += blockDim.x) W[t] = X[t];
+    __syncthreads();
+    band_solve_block(s, eb.Lc, eb.Lr, W, win);
+    deflate();
+  }
+  // Q = orthonormal basis of [U, Z] (columns normalised first, 1e-10 rank cut)
+  const int m0 = ns + 1;
+  for (int t = threadIdx.x; t < n * m0; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    X[t] = (c < ns) ? W[t] : Zc[i];
+  }
+  __syncthreads();
+  cgs2_euclid(X, m0, n, red, dots, keep);
+  int m = 0;
+  if (threadIdx.x == 0) {
+    // compact kept columns to the front (order preserved)
+    int q = 0;
+    for (int c = 0; c < m0; ++c)
+      if (keep[c] != 0.0) order[q++] = c;
+    misc[0] = (double)q;
+  }
+  __syncthreads();
+  m = (int)misc[0];
+  for (int q = 0; q < m; ++q) {
+    const int c = order[q];
+    if (c != q)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) X[(int64_t)q * n + i] = X[(int64_t)c * n + i];
+    __syncthreads();
+  }
+  // Kr (-> Am) and Mr (-> Cm), column by column
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* coef = pass == 0 ? hlap : hmel;
+    for (int c = 0; c < m; ++c) {
+#pragma unroll
+      for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+      const double* xc = X + (int64_t)c * n;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double ax = dir[i] ? 0.0 : stencil(ctx, xc, i, coef);
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+          if (l <= c) v[l] += ax * X[(int64_t)l * n + i];
+      }
+      block_sum_multi(v, c + 1, red, dots);
+      if (threadIdx.x <= c) {
+        if (pass == 0)
+          Am[threadIdx.x * LD + c] = Am[c * LD + threadIdx.x] = dots[threadIdx.x];
+        else
+          Cm[threadIdx.x][c] = Cm[c][threadIdx.x] = dots[threadIdx.x];
+      }
+      __syncthreads();
+    }
+  }
+  // generalized m x m eigenproblem: Mr = L L^T, C = L^-1 Kr L^-T (thread 0),
+  // Jacobi on C padded to P x P with a huge diagonal
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double a = Cm[i][j];
+        for (int q = 0; q < j; ++q) a -= Lm[i][q] * Lm[j][q];
+        Lm[i][j] = (i == j) ? sqrt(fmax(a, 1e-300)) : a / Lm[j][j];
+      }
+    // T = L^-1 Kr (rows), then C = T L^-T
+    for (int c = 0; c < m; ++c)
+      for (int i = 0; i < m; ++i) {
+        double a = Am[i * LD + c];
+        for (int q = 0; q < i; ++q) a -= Lm[i][q] * Cm[q][c];
+        Cm[i][c] = a / Lm[i][i];
+      }
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        double a = Cm[i][j];
+        for (int q = 0; q < j; ++q) a -= Am[i * LD + q] * Lm[j][q];
+        Am[i * LD + j] = a / Lm[j][j];  // reuse Am as C (row i done before being read)
+      }
+    for (int i = 0; i < P; ++i)
+      for (int j = 0; j < P; ++j)
+        if (i >= m || j >= m) Am[i * LD + j] = (i == j) ? 1e300 : 0.0;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < i; ++j) Am[i * LD + j] = Am[j * LD + i] = 0.5 * (Am[i * LD + j] + Am[j * LD + i]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) jacobi_warp(Am, Vm, ritz, order);
+  __syncthreads();
+  // Ritz vectors: x = Q (L^-T y), y = Vm[:, order[c]]
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < kNeig && c < m; ++c) {
+      const int oc = order[c];
+      for (int i = m - 1; i >= 0; --i) {
+        double a = Vm[i * LD + oc];
+        for (int q = i + 1; q < m; ++q) a -= Lm[q][i] * Cm[q][c];
+        Cm[i][c] = a / Lm[i][i];  // coefficients of Ritz vector c
+      }
+    }
+  }
+  __syncthreads();
+  double* ev = eb.evecs + (int64_t)kb * kNeig * n;
+  const int kk = min(kNeig, m);
+  for (int t = threadIdx.x; t < kNeig * n; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    double a = 0.0;
+    if (c < kk)
+      for (int q = 0; q < m; ++q) a += X[(int64_t)q * n + i] * Cm[q][c];
+    ev[t] = a;
+  }
+  if (threadIdx.x < kNeig)
+    eb.evals[(int64_t)k * kNeig + threadIdx.x] = threadIdx.x < kk ? ritz[threadIdx.x] : CUDART_NAN;
+  if (threadIdx.x == 0) {
+    eb.passes[k] = 4;
+    eb.neumann[k] = 0;
+  }
+}
+
+// sigma_k = 1e-8 * tr(K_free) / n_free on the closed neighbourhood (spectral.py:133)
+__global__ void k_rand_sigma(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
+                             HeatParam hp, const BandSys* __restrict__ sys, double* __restrict__ sigma) {
+  __shared__ double sred[8];
+  const BandSys s = sys[blockIdx.x];
+  double tr = 0.0, nf = 0.0;
+  for (int i = threadIdx.x; i < s.n; i += blockDim.x) {
+    int a, b;
+    band_node_of(s, i, a, b);
+    if (hdir[(int64_t)b * g.nnx + a]) continue;
+    nf += 1.0;
+    // K_ii = sum over the node's elements inside the neighbourhood of E_e * lap[c][c]
+    for (int e = 0; e < 4; ++e) {
+      const int ei = a - 1 + (e == 1 || e == 2), ej = b - 1 + (e >= 2);
+      if (ei < s.a0 || ej < s.b0 || ei > s.a0 + s.w - 2 || ej > s.b0 + s.hgt - 2) continue;
+      const int cn = (e == 0) ? 2 : (e == 1) ? 3 : (e == 2) ? 0 : 1;
+      tr += E[(int64_t)ej * g.nx + ei] * hp.lap[cn * 4 + cn];
+    }
+  }
+  const double t = block_sum(tr, sred), m = block_sum(nf, sred);
+  if (threadIdx.x == 0) sigma[blockIdx.x] = 1e-8 * (t / m);
+}
+
+void launch_rand_sigma(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
+                       const BandSys* sys, int nsys, double* sigma, cudaStream_t st) {
+  if (nsys == 0) return;
+  k_rand_sigma<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sys, sigma);
+  MS_CUDA(cudaGetLastError());
+}
+
+void launch_randomized(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
+                       const EigBatch& b, const double* F, int ns, cudaStream_t st) {
+  if (b.nk == 0) return;
+  if (ns + 1 > P - 2) throw Error(-1, "too many snapshots for the randomized eigensolver (<= 13)");
+  const int NLx = 2 * b.mex + 1, NLy = 2 * b.mey + 1;
+  const int max_bw = std::min(NLx, NLy) + 1;
+  const size_t smem = sizeof(double) * ((size_t)(2 * b.mex) * (2 * b.mey) + (size_t)(max_bw + 1) * P +
+                                        (P + 1) * 8 + (P + 1) + 2 * P * (P + 1) + 2 * P + 4) +
+                      sizeof(int) * P + (size_t)NLx * NLy + 16;
+  MS_CUDA(cudaFuncSetAttribute(k_randomized, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_randomized<<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, NLx);
   MS_CUDA(cudaGetLastError());
 }
 

@@ -34,11 +34,21 @@ struct EigBatch {
 // B = K_H + sigma M_H in band form (Dirichlet nodes -> identity rows)
 void launch_heat_assemble(const Grid& g, const double* E, const uint8_t* hdir,
                           const HeatParam& hp, double sigma, const BandSys* sys, int nsys,
-                          double* Lc, cudaStream_t st);
+                          double* Lc, cudaStream_t st, const double* sigma_per_sys = nullptr);
 
 // shift-invert block subspace iteration with Jacobi Rayleigh-Ritz, one CTA per centre
 void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
                      const EigBatch& b, int max_pass, double tol, cudaStream_t st);
+
+// randomized snapshot eigensolver (EH+Rot;Rand): F = forcings of the batch,
+// [centre][ns][NL] lexicographic closed-neighbourhood nodes (zero rows at
+// Dirichlet nodes); factors of K + sigma_k M with the reference's shift
+void launch_randomized(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
+                       const EigBatch& b, const double* F, int ns, cudaStream_t st);
+
+// per-centre reference shift sigma_k = 1e-8 tr(K_free)/n_free (spectral.py:133)
+void launch_rand_sigma(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
+                       const BandSys* sys, int nsys, double* sigma, cudaStream_t st);
 
 // gap / fixed selection on device (spectral.py:161-186)
 void launch_select(int n_centers, const double* evals, int n_max, double threshold, int fixed,

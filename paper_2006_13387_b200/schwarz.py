@@ -39,7 +39,7 @@ VARIANTS = {
         PreconditionerVariant("EH+Rot;Rand", "elasticity", "heat", True, True),
     ]
 }
-GPU_VARIANTS = ("EH", "EH+Rot")
+GPU_VARIANTS = ("EH", "EH+Rot", "EH+Rot;Rand")
 
 
 def get_variant(tag):
@@ -132,6 +132,25 @@ class TwoLevelPreconditioner:
             self.handle = None
 
 
+def randomized_forcings(mesh, part, dirichlet_nodes, n_snapshots, seed):
+    """Host forcings of solve_local_eig_randomized (spectral.py:119-121):
+    centre k draws default_rng([seed, k]).uniform(-1, 1, (n_free_k, n_snap))
+    over its free closed-neighbourhood nodes (schwarz.py:156-160); returned as
+    [centre][snapshot][node] over all (2H+1)^2 nodes, zero at clamped nodes."""
+    NLx, NLy = 2 * part.mex + 1, 2 * part.mey + 1
+    clamped = np.zeros(mesh.n_nodes, dtype=bool)
+    clamped[np.asarray(dirichlet_nodes, dtype=np.int64)] = True
+    F = np.zeros((part.n_neighborhoods, n_snapshots, NLx * NLy))
+    for k, (I, J) in enumerate(part.coarse_nodes):
+        a0, b0 = (I - 1) * part.mex, (J - 1) * part.mey
+        gids = ((b0 + np.arange(NLy))[:, None] * (mesh.nx + 1) + (a0 + np.arange(NLx))[None, :]).ravel()
+        free = np.nonzero(~clamped[gids])[0]
+        ns = min(n_snapshots, free.size)
+        Fk = np.random.default_rng([seed, k]).uniform(-1.0, 1.0, size=(free.size, ns))
+        F[k, :ns][:, free] = Fk.T
+    return F
+
+
 def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None, *,
                          level1="neighborhoods", delta=None, use_coarse=True, local_solver="banded"):
     """Build a two-level preconditioner by variant name (schwarz.py:176-211).
@@ -172,6 +191,11 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
     o.use_coarse = 1 if use_coarse else 0
     o.heat_dirichlet_nodes = hd.ctypes.data_as(C.POINTER(C.c_int64)) if hd.size else None
     o.n_heat_dirichlet = hd.size
+    F = None
+    if variant.randomized:
+        ns = opts.n_snapshots or (opts.n_max + 5)
+        F = np.ascontiguousarray(randomized_forcings(mesh, part, hd, ns, opts.seed))
+        o.randomized, o.n_snapshots, o.snapshots = 1, ns, F.ctypes.data
     lib = _lib.load()
     h = C.c_void_p()
     _lib.check(lib.ms_precond_build(op.handle, C.byref(o), C.byref(h)), op._ctx.handle)
@@ -184,6 +208,7 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "t_level1": inf.t_level1, "t_coarse": inf.t_coarse, "t_eig": inf.t_eig,
         "coarse_dim": inf.coarse_dim, "mode_counts": [int(c) for c in counts[:nc]],
         "basis_kind": "H+Rot" if variant.enrich else "H", "selection_rule": rule,
+        "eig_solver": "randomized" if variant.randomized else "subspace",
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
         "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,
         "coarse_bytes": inf.coarse_bytes, "level1": level1, "delta": delta, "local_solver": local_solver,

@@ -82,6 +82,32 @@ def bench100(eta):
          apply_r=r, apply_z=pre.apply(r), nu=0.3, **out)
 
 
+def bench100_rand(eta):
+    """EH+Rot;Rand on the reference's benchmark cell (randomized eigensolver)."""
+    cfg = cli.BenchmarkConfig(tol=1e-8)
+    res = cli.run_single(cfg, eta, "EH+Rot;Rand")
+    op, rep = res["operator"], res["report"]
+    mesh = grid.build_fine_mesh(100, 100)
+    part = grid.build_coarse_partition(mesh, 10, 10)
+    coeff = coefficients.generate_coefficient(cfg.layout, mesh, eta, nu=cfg.nu)
+    dirichlet = mesh.boundary_nodes()
+    lams = []
+    for center, patch in enumerate(part.neighborhoods):
+        prob = spectral.build_local_eigproblem(mesh, coeff, patch, "diffusion", dirichlet)
+        k = min(7, prob.dim)
+        sel = spectral.solve_local_eig_randomized(prob, k, n_snapshots=min(11, prob.dim), seed=[0, center])
+        lams.append(sel.eigenvalues)
+    pre = schwarz.build_preconditioner("EH+Rot;Rand", op, mesh, part, coeff, dirichlet)
+    rng = np.random.default_rng(7)
+    r = rng.standard_normal(op.n_free)
+    save(f"ref_bench100_rand_eta{eta:g}.npz", E=coeff.values, dirichlet_nodes=dirichlet,
+         free_dofs=op.free_dofs, b=res["rhs"], iters=rep.iterations, x=res["solution"],
+         residuals=np.array(rep.residuals), coarse_dim=res["coarse_dim"],
+         mode_counts=np.array(pre.info["mode_counts"]), eigenvalues=np.array(lams),
+         apply_r=r, apply_z=pre.apply(r))
+    print("rand", eta, rep.iterations, res["coarse_dim"])
+
+
 class _KeptPatch(Patch):
     """Patch whose kept nodes follow the frozen block rule."""
 
@@ -150,12 +176,15 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000):
 
 
 def main():
-    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s"}
+    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand"}
     if "elements" in which:
         elements()
     if "bench" in which:
         bench100(1.0)
         bench100(1e6)
+    if "rand" in which:
+        bench100_rand(1.0)
+        bench100_rand(1e6)
     if "cfg1" in which:
         adapter_case(configs.config1(seed=0), "ref_config1.npz")
     if "mbb" in which:

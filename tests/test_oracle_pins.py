@@ -91,3 +91,23 @@ def test_configs_are_deterministic():
     c = configs.config3(seed=0, n=64, H=16)
     assert abs(c.meta["volume"] - 0.4) < 1e-6
     assert c.E.min() >= 1e-6 - 1e-18 and c.E.max() <= 1.0
+
+
+@pytest.mark.parametrize("eta", ["1", "1e+06"])
+def test_randomized_variant_matches_reference(eta):
+    """EH+Rot;Rand: the oracle's restatement of solve_local_eig_randomized
+    (spectral.py:103-158, seeds [0, centre]) reproduces the reference."""
+    g = load_golden(f"ref_bench100_rand_eta{eta}.npz")
+    mesh = O.mesh_for(100, 100)
+    op = O.elasticity_operator(mesh, g["E"], 0.3, O.whole_node_dofs(mesh, g["dirichlet_nodes"]))
+    prob = O.OracleProblem(mesh, op, g["E"], 0.3, g["b"], g["dirichlet_nodes"])
+    P = O.build_two_level(prob, H=10, level1_mode="neighborhoods", eig_solver=O.randomized_solver())
+    lam = np.array(P.coarse_space.eigenvalues)
+    assert np.allclose(lam, g["eigenvalues"], rtol=1e-10, atol=1e-12 * np.abs(g["eigenvalues"]).max())
+    assert P.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(P.info["mode_counts"]), g["mode_counts"])
+    z = P.apply(g["apply_r"])
+    assert np.linalg.norm(z - g["apply_z"]) <= 1e-12 * np.linalg.norm(g["apply_z"])
+    x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=2000)
+    assert rep.iterations == int(g["iters"])
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
