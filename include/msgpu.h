@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MSGPU_ABI_VERSION 1
+#define MSGPU_ABI_VERSION 2
 
 enum {
   MS_OK = 0,
@@ -50,6 +50,12 @@ typedef struct ms_precond ms_precond;
 enum {
   MS_LEVEL1_NEIGHBORHOODS = 0, /* reference: subdomains = omega_j, strictly interior nodes (schwarz.py:97-109) */
   MS_LEVEL1_BLOCKS = 1         /* BASELINE configs: delta-extended HxH blocks               */
+};
+
+/* level-1 operator (PreconditionerVariant.level1, schwarz.py:24-41) */
+enum {
+  MS_L1_ELASTICITY = 0, /* EH, EH+Rot: restrictions of K (schwarz.py:97-109)                     */
+  MS_L1_HEAT = 1        /* HH, HH+Rot: one scalar diffusion factor for both blocks (:112-140)    */
 };
 
 /* level-1 local solver */
@@ -77,6 +83,8 @@ typedef struct ms_precond_opts {
   int randomized;
   int n_snapshots;
   const double* snapshots;
+  int level1_operator;   /* MS_L1_* (needs whole-node constraints for MS_L1_HEAT)       */
+  int reserved;          /* 0                                                           */
 } ms_precond_opts;
 
 /* Build metadata, the `info` dict of schwarz.py:202-210 plus eigensolver stats. */

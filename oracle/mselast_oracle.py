@@ -508,6 +508,40 @@ def level1_solvers(op, mesh, rects, keep_domain_boundary):
     return out
 
 
+def heat_level1_solvers(op, mesh, E, rects, keep_domain_boundary):
+    """HH / HH+Rot level 1 (schwarz.py:112-140): one scalar factor of the
+    E-weighted diffusion matrix restricted to the subdomain's free nodes,
+    applied to the x block and to the y block.  Needs whole-node constraints
+    (the reference's layout assumption, schwarz.py:113-117)."""
+    nn = mesh.n_nodes
+    cons = np.setdiff1d(np.arange(mesh.n_dofs), op.free_dofs)
+    cnodes = cons[cons < nn]
+    if not np.array_equal(cnodes + nn, cons[cons >= nn]):
+        raise ValueError("heat level-1 needs whole-node constraints")
+    E = np.asarray(E, dtype=float).ravel()
+    D = _assemble_free(mesh.quad_nodes(), E[:, None, None] * laplace_element()[None], nn,
+                       free_complement(nn, cnodes))
+    sindex = D.free_index()
+    out = []
+    for rect in rects:
+        nodes = rect_nodes(mesh, *subdomain_node_rect(mesh, rect, keep_domain_boundary))
+        sidx = sindex[nodes]
+        sidx = sidx[sidx >= 0]
+        if sidx.size == 0:
+            continue
+        lu = spla.splu(D.matrix[sidx][:, sidx].tocsc())
+        m = sidx.size
+
+        def solve(r, lu=lu, m=m):
+            out_ = np.empty_like(r)
+            out_[:m] = lu.solve(r[:m])
+            out_[m:] = lu.solve(r[m:])
+            return out_
+
+        out.append((np.concatenate([sidx, sidx + D.n_free]), solve))
+    return out
+
+
 class TwoLevel:
     """Additive level-1 + coarse correction (schwarz.py:66-84)."""
 
@@ -631,8 +665,8 @@ def problem_from_spec(spec):
 
 
 def build_two_level(prob, H, delta=None, n_max=6, threshold=50.0, enrich=True, rule="gap",
-                    level1_mode="blocks", eig_solver=None):
-    """EH(+Rot) preconditioner.
+                    level1_mode="blocks", eig_solver=None, level1_op="elasticity"):
+    """EH(+Rot) preconditioner; level1_op='heat' gives HH(+Rot).
 
     level1_mode='neighborhoods': reference semantics (subdomains = omega_j,
     strictly interior nodes; schwarz.py:176-211).  'blocks': ADAPTER with
@@ -642,9 +676,13 @@ def build_two_level(prob, H, delta=None, n_max=6, threshold=50.0, enrich=True, r
     part = Partition(mesh, mesh.nx // H, mesh.ny // H)
     t0 = time.perf_counter()
     if level1_mode == "neighborhoods":
-        l1 = level1_solvers(prob.op, mesh, part.omegas, keep_domain_boundary=False)
+        rects, keep = part.omegas, False
     else:
-        l1 = level1_solvers(prob.op, mesh, block_rects(mesh, H, delta), keep_domain_boundary=True)
+        rects, keep = block_rects(mesh, H, delta), True
+    if level1_op == "heat":
+        l1 = heat_level1_solvers(prob.op, mesh, prob.E, rects, keep)
+    else:
+        l1 = level1_solvers(prob.op, mesh, rects, keep)
     t_l1 = time.perf_counter() - t0
     t0 = time.perf_counter()
     cs = heat_rot_coarse_space(prob.op, mesh, part, prob.E, prob.heat_dirichlet_nodes, n_max,

@@ -19,6 +19,7 @@ void band_setup(BandSys& s, int a0, int a1, int b0, int b1, int ncomp) {
   s.hgt = b1 - b0 + 1;
   s.fastx = s.w <= s.hgt ? 1 : 0;
   s.ncomp = ncomp;
+  s.nrhs = 1;
   s.n = ncomp * s.w * s.hgt;
   const int fast = s.fastx ? s.w : s.hgt;
   int bw = ncomp == 2 ? 2 * fast + 3 : fast + 1;
@@ -72,6 +73,62 @@ void launch_l1_assemble(const Grid& g, const KeParam& ke, const double* E, const
                         const BandSys* sys, int nsys, double* Lc, cudaStream_t st) {
   if (nsys == 0) return;
   k_l1_assemble<<<nsys, 256, 0, st>>>(g, ke, E, mask, sys, Lc);
+  MS_CUDA(cudaGetLastError());
+}
+
+// Heat level-1 band: entry (k + j, k) of D[sidx][:, sidx] (schwarz.py:124-128),
+// D the E-weighted Q1 Laplacian (assembly.py:223-233); same element order as
+// the reference's duplicate summation.
+__global__ void __launch_bounds__(256)
+    k_l1_heat_assemble(Grid g, LapParam lp, const double* __restrict__ E,
+                       const uint8_t* __restrict__ mask, const BandSys* __restrict__ sys,
+                       double* __restrict__ Lc) {
+  const BandSys s = sys[blockIdx.x];
+  const int S = s.bw + 1;
+  const int64_t total = (int64_t)s.n * S;
+  for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
+    const int k = (int)(t / S), j = (int)(t % S);
+    const int row = k + j;
+    double v = 0.0;
+    if (row < s.n) {
+      int ak, bk, ar, br;
+      band_node_of(s, k, ak, bk);
+      band_node_of(s, row, ar, br);
+      const int64_t gk = (int64_t)bk * g.nnx + ak, gr = (int64_t)br * g.nnx + ar;
+      if (!mask[gk] || !mask[gr]) {
+        v = (row == k) ? 1.0 : 0.0;
+      } else if (abs(ar - ak) <= 1 && abs(br - bk) <= 1) {
+        const int ilo = max(max(ak, ar) - 1, 0), ihi = min(min(ak, ar), g.nx - 1);
+        const int jlo = max(max(bk, br) - 1, 0), jhi = min(min(bk, br), g.ny - 1);
+        for (int ej = jlo; ej <= jhi; ++ej)
+          for (int ei = ilo; ei <= ihi; ++ei) {
+            const int dk = ak - ei, ek = bk - ej, dr = ar - ei, er = br - ej;
+            const int ck = dk + 3 * ek - 2 * dk * ek, cr = dr + 3 * er - 2 * dr * er;
+            v += E[(int64_t)ej * g.nx + ei] * lp.lap[cr * 4 + ck];
+          }
+      }
+    }
+    Lc[s.foff + t] = v;
+  }
+}
+
+void launch_l1_heat_assemble(const Grid& g, const double* lap, const double* E, const uint8_t* mask,
+                             const BandSys* sys, int nsys, double* Lc, cudaStream_t st) {
+  if (nsys == 0) return;
+  LapParam lp;
+  for (int i = 0; i < 16; ++i) lp.lap[i] = lap[i];
+  k_l1_heat_assemble<<<nsys, 256, 0, st>>>(g, lp, E, mask, sys, Lc);
+  MS_CUDA(cudaGetLastError());
+}
+
+__global__ void k_whole_node_check(int64_t n_nodes, const uint8_t* __restrict__ mask, int* fail) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (mask[i] != mask[i + n_nodes]) *fail = 1;
+}
+
+void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cudaStream_t st) {
+  k_whole_node_check<<<4 * 148, 256, 0, st>>>(g.n_nodes, mask, fail);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -154,7 +211,7 @@ void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, dou
 constexpr int kSolveWarps = 4;
 constexpr int kPD = 4;
 
-template <int T, bool REV>
+template <int T, int NR, bool REV>
 __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, int bw,
                                            double* __restrict__ y, int lane) {
   constexpr int R = T + 1;  // register slots (blocks of 32 rows) per lane
@@ -162,16 +219,19 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
   auto lcol = [&](int k) -> const double* {
     return REV ? L + (int64_t)(n - 1 - k) * S : L + (int64_t)k * S;
   };
-  auto yat = [&](int r) -> double* { return REV ? y + (n - 1 - r) : y + r; };
+  auto yat = [&](int r, int c) -> double* { return y + (int64_t)(REV ? (n - 1 - r) : r) * NR + c; };
 
-  double acc[R];
+  double acc[NR][R], rnext[NR];
 #pragma unroll
-  for (int s = 0; s < R - 1; ++s) {
-    const int r = 32 * s + lane;
-    acc[s] = r < n ? *yat(r) : 0.0;
+  for (int c = 0; c < NR; ++c) {
+#pragma unroll
+    for (int s = 0; s < R - 1; ++s) {
+      const int r = 32 * s + lane;
+      acc[c][s] = r < n ? *yat(r, c) : 0.0;
+    }
+    acc[c][R - 1] = 0.0;
+    rnext[c] = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane, c) : 0.0;
   }
-  acc[R - 1] = 0.0;
-  double rnext = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane) : 0.0;
 
   // prefetch ring: band values of the next PD steps
   double lv[kPD][T], dv[kPD];
@@ -191,12 +251,15 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
 
   for (int k0 = 0; k0 < n; k0 += 32) {
     // rows of block (k0/32 + R-1) enter the window
-    acc[R - 1] = rnext;
-    {
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      acc[c][R - 1] = rnext[c];
       const int r = k0 + 32 * R + lane;
-      rnext = r < n ? *yat(r) : 0.0;
+      rnext[c] = r < n ? *yat(r, c) : 0.0;
     }
-    double wout = 0.0;
+    double wout[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) wout[c] = 0.0;
 #pragma unroll 1
     for (int u0 = 0; u0 < 32; u0 += kPD) {
 #pragma unroll
@@ -204,34 +267,38 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
       const int u = u0 + q;
       const int k = k0 + u;
       if (k < n) {
-        const double wloc = acc[0] * dv[q];
-        const double wk = __shfl_sync(0xffffffffu, wloc, u);
-        if (lane == u) wout = wk;
-        const int base = ((lane - u - 1) & 31) + 1;
         const bool hi = lane <= u;  // row k+base lies in the next block
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-          const double upd = lv[q][t] * wk;  // zero when k+j is outside the band
-          if (hi) {
-            if (t + 1 < R) acc[t + 1] -= upd;
-          } else {
-            acc[t] -= upd;
+        for (int c = 0; c < NR; ++c) {
+          const double wloc = acc[c][0] * dv[q];
+          const double wk = __shfl_sync(0xffffffffu, wloc, u);
+          if (lane == u) wout[c] = wk;
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const double upd = lv[q][t] * wk;  // zero when k+j is outside the band
+            if (hi) {
+              if (t + 1 < R) acc[c][t + 1] -= upd;
+            } else {
+              acc[c][t] -= upd;
+            }
           }
-          (void)base;
         }
         load(k + kPD, (u + kPD) & 31, lv[q], dv[q]);
       }
      }
     }
-    if (k0 + lane < n) *yat(k0 + lane) = wout;
-    // rotate the register window by one block
 #pragma unroll
-    for (int s = 0; s < R - 1; ++s) acc[s] = acc[s + 1];
-    acc[R - 1] = 0.0;
+    for (int c = 0; c < NR; ++c) {
+      if (k0 + lane < n) *yat(k0 + lane, c) = wout[c];
+      // rotate the register window by one block
+#pragma unroll
+      for (int s = 0; s < R - 1; ++s) acc[c][s] = acc[c][s + 1];
+      acc[c][R - 1] = 0.0;
+    }
   }
 }
 
-template <int T>
+template <int T, int NR>
 __global__ void __launch_bounds__(kSolveWarps * 32)
     k_l1_solve(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                const double* __restrict__ Lr, const double* __restrict__ r,
@@ -242,41 +309,53 @@ __global__ void __launch_bounds__(kSolveWarps * 32)
   if (sid >= nsys) return;
   const BandSys s = sys[sid];
   double* y = ybuf + s.yoff;
-  // gather R_s r (node-interleaved local order)
-  for (int i = lane; i < s.n; i += 32) {
-    const int ln = s.ncomp == 2 ? (i >> 1) : i, c = s.ncomp == 2 ? (i & 1) : 0;
+  // gather R_s r (node-interleaved local order; NR = 2: scalar rows, 2 rhs)
+  for (int i = lane; i < s.n * NR; i += 32) {
+    const int ln = i >> 1, c = i & 1;
     int a, b;
     band_node_of(s, ln, a, b);
     y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
   }
   __syncwarp();
-  band_sweep<T, false>(Lc + s.foff, s.n, s.bw, y, lane);
+  band_sweep<T, NR, false>(Lc + s.foff, s.n, s.bw, y, lane);
   __syncwarp();
-  band_sweep<T, true>(Lr + s.foff, s.n, s.bw, y, lane);
+  band_sweep<T, NR, true>(Lr + s.foff, s.n, s.bw, y, lane);
 }
 
-template <int T>
+template <int T, int NR>
 static void solve_t(const Grid& g, const BandSys* sys, int nsys, const double* Lc, const double* Lr,
                     const double* r, double* ybuf, const int* done, cudaStream_t st) {
-  k_l1_solve<T><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, 0, st>>>(g, sys, nsys, Lc, Lr, r,
-                                                                        ybuf, done);
+  k_l1_solve<T, NR><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, 0, st>>>(g, sys, nsys, Lc, Lr, r,
+                                                                            ybuf, done);
 }
 
-void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
-                     const double* Lr, const double* r, double* ybuf, const int* done,
-                     cudaStream_t st) {
+void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
+                     const double* Lc, const double* Lr, const double* r, double* ybuf,
+                     const int* done, cudaStream_t st) {
   if (nsys == 0) return;
   const int T = std::max(1, div_up(max_bw, 32));
-  switch (T) {
-    case 1: solve_t<1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 2: solve_t<2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 3: solve_t<3>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 4: solve_t<4>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 5: solve_t<5>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 6: solve_t<6>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 7: solve_t<7>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    case 8: solve_t<8>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-    default: throw Error(-1, "level-1 band wider than 256 unsupported");
+  if (nrhs == 1) {
+    switch (T) {
+      case 1: solve_t<1, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 2: solve_t<2, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 3: solve_t<3, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 4: solve_t<4, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 5: solve_t<5, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 6: solve_t<6, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 7: solve_t<7, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 8: solve_t<8, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      default: throw Error(-1, "level-1 band wider than 256 unsupported");
+    }
+  } else if (nrhs == 2) {
+    switch (T) {
+      case 1: solve_t<1, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 2: solve_t<2, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 3: solve_t<3, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 4: solve_t<4, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      default: throw Error(-1, "heat level-1 band wider than 128 unsupported");
+    }
+  } else {
+    throw Error(-1, "nrhs must be 1 or 2");
   }
   MS_CUDA(cudaGetLastError());
 }

@@ -17,6 +17,7 @@ struct BandSys {
   int w, hgt;      // kept nodes along x / y
   int fastx;       // 1: x is the fast (short) axis
   int ncomp;       // 2 elasticity, 1 heat
+  int nrhs;        // right-hand sides per solve: 1, or 2 for the heat level-1 (x and y blocks)
   int n;           // unknowns
   int bw;          // lower bandwidth
   int64_t foff;    // offset into Lc / Lr
@@ -46,6 +47,15 @@ void band_setup(BandSys& s, int a0, int a1, int b0, int b1, int ncomp);
 void launch_l1_assemble(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                         const BandSys* sys, int nsys, double* Lc, cudaStream_t st);
 
+// Heat level-1 band (HH variants, schwarz.py:112-140): the E-weighted
+// diffusion matrix restricted to the subdomain's kept nodes, constrained nodes
+// (x-dof mask 0) as identity rows.  Elements of the whole mesh contribute.
+void launch_l1_heat_assemble(const Grid& g, const double* lap, const double* E, const uint8_t* mask,
+                             const BandSys* sys, int nsys, double* Lc, cudaStream_t st);
+
+// fail = 1 unless every node is either fully constrained or fully free
+void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cudaStream_t st);
+
 // In-place banded Cholesky of every system: Lc holds A's lower band on
 // entry, L on exit (diag slot = 1/L_kk); Lr receives the row band.
 // *fail gets (system index + 1) of a non-positive pivot, else stays 0.
@@ -53,9 +63,11 @@ void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, dou
                        int* fail, cudaStream_t st);
 
 // y_s = K_s^{-1} (R_s r) for every system, warp per system.  r is a full
-// layout vector; the local solutions land in ybuf[yoff ...].
-void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
-                     const double* Lr, const double* r, double* ybuf, const int* done,
-                     cudaStream_t st);
+// layout vector; the local solutions land in ybuf[yoff ...], node-interleaved
+// (2 ln + c).  nrhs = 2: scalar systems applied to the x and y components in
+// one sweep (the factor is read once for both).
+void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
+                     const double* Lc, const double* Lr, const double* r, double* ybuf,
+                     const int* done, cudaStream_t st);
 
 }  // namespace msgpu

@@ -266,6 +266,7 @@ struct ms_precond {
   DBuf<BandSys> sys;
   DBuf<double> Lc, Lr, ybuf, Xinv;
   bool dense = false;  // MS_LOCAL_DENSE_INV: packed explicit inverses in Xinv
+  int nrhs = 1;        // 2: heat level-1 (scalar factor applied to both blocks)
   int dense_nt = 0;
   DBuf<int> xcov, ycov, xlo_d, xlen_d, ylo_d, ylen_d;
   DBuf<int64_t> yoff_d;
@@ -437,7 +438,7 @@ static void exchange_ybuf(ms_precond* pc) {
     const BandSys& a = pc->hsys[(size_t)J * pc->NbX];
     const BandSys& b = pc->hsys[(size_t)J * pc->NbX + pc->NbX - 1];
     off = a.yoff;
-    bytes = (b.yoff + b.n - a.yoff) * (int64_t)sizeof(double);
+    bytes = (b.yoff + (int64_t)b.n * b.nrhs - a.yoff) * (int64_t)sizeof(double);
   };
   int64_t o_first, b_first, o_last, b_last, o_pl, b_pl, o_nf, b_nf;
   seg(pc->J0, o_first, b_first);
@@ -487,7 +488,7 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
     if (pc->dense)
       launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
     else
-      launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
+      launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
     pf.end(MS_PROF_LEVEL1, it, st, a);
     if (dist) exchange_ybuf(pc);
   }
@@ -719,6 +720,11 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     throw Error(MS_E_INVALID, "block level-1 needs overlap delta >= 1");
   if (o->local_solver != MS_LOCAL_BANDED && o->local_solver != MS_LOCAL_DENSE_INV)
     throw Error(MS_E_INVALID, "unknown local solver");
+  if (o->level1_operator != MS_L1_ELASTICITY && o->level1_operator != MS_L1_HEAT)
+    throw Error(MS_E_INVALID, "unknown level-1 operator");
+  const bool heat_l1 = o->level1_operator == MS_L1_HEAT;
+  if (heat_l1 && o->local_solver != MS_LOCAL_BANDED)
+    throw Error(MS_E_INVALID, "the heat level-1 uses the banded local solver");
   const int W = P->ctx->world(), R = P->ctx->rank();
   if (W > 1 && (o->level1_kind != MS_LEVEL1_BLOCKS || !o->use_coarse || o->Ny < W))
     throw Error(MS_E_INVALID, "multi-GPU strips need the block level-1 layout, a coarse level and Ny >= ranks");
@@ -781,12 +787,13 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       for (int I = 0; I < pc->NbX; ++I) {
         BandSys s{};
         if (xhi[I] < xlo[I] || yhi[J] < ylo[J]) throw Error(MS_E_INVALID, "empty level-1 subdomain");
-        band_setup(s, xlo[I], xhi[I], ylo[J], yhi[J], 2);
+        band_setup(s, xlo[I], xhi[I], ylo[J], yhi[J], heat_l1 ? 1 : 2);
+        if (heat_l1) s.nrhs = 2;
         const int sid = J * pc->NbX + I;
         s.foff = foff;  // factors stored for owned subdomains only
         s.yoff = yoff;
         if (sid >= pc->s0 && sid < pc->s1) foff += (int64_t)s.n * (s.bw + 1);
-        yoff += s.n;
+        yoff += (int64_t)s.n * s.nrhs;
         pc->max_bw = std::max(pc->max_bw, s.bw);
         pc->hsys.push_back(s);
       }
@@ -810,8 +817,20 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->ybuf.alloc(yoff);
     fail.zero(st);
     const int ns = pc->s1 - pc->s0;
-    launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
+    if (heat_l1) {
+      launch_whole_node_check(g, P->mask.p, fail.p, st);
+      int bad = 0;
+      MS_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      MS_CUDA(cudaStreamSynchronize(st));
+      if (bad) throw Error(MS_E_INVALID, "heat level-1 (HH variants) needs whole-node constraints");
+      HeatParam hp{};
+      heat_elements(g.h, hp);
+      launch_l1_heat_assemble(g, hp.lap, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
+    } else {
+      launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
+    }
     pc->dense = o->local_solver == MS_LOCAL_DENSE_INV;
+    pc->nrhs = heat_l1 ? 2 : 1;
     if (!pc->dense) {
       pc->Lr.alloc(foff);
       pc->Lr.zero(st);
@@ -1188,7 +1207,7 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
         launch_l1_dense_apply(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p,
                               nullptr, st);
       else
-        launch_l1_solve(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->max_bw, pc->Lc.p, pc->Lr.p, r,
+        launch_l1_solve(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r,
                         pc->ybuf.p, nullptr, st);
     });
   if (pc->has_coarse) {

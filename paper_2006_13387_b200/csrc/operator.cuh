@@ -66,6 +66,9 @@ void launch_finalize(PcgScalars* sc, int kind, double* hist, cudaStream_t st);
 struct KeParam {
   double k[64];
 };
+struct LapParam {
+  double lap[16];  // unit Q1 Laplacian element (assembly.py:133-140)
+};
 
 constexpr int MV_TX = 32;  // nodes per CTA in x
 constexpr int MV_TY = 8;   // nodes per CTA in y (one node per thread)

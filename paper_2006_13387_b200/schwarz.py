@@ -39,7 +39,7 @@ VARIANTS = {
         PreconditionerVariant("EH+Rot;Rand", "elasticity", "heat", True, True),
     ]
 }
-GPU_VARIANTS = ("EH", "EH+Rot", "EH+Rot;Rand")
+GPU_VARIANTS = ("EH", "EH+Rot", "EH+Rot;Rand", "HH", "HH+Rot")
 
 
 def get_variant(tag):
@@ -189,6 +189,7 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         raise ValueError(f"unknown local solver {local_solver!r}")
     o.local_solver = _lib.MS_LOCAL_BANDED if local_solver == "banded" else _lib.MS_LOCAL_DENSE_INV
     o.use_coarse = 1 if use_coarse else 0
+    o.level1_operator = _lib.MS_L1_HEAT if variant.level1 == "heat" else _lib.MS_L1_ELASTICITY
     o.heat_dirichlet_nodes = hd.ctypes.data_as(C.POINTER(C.c_int64)) if hd.size else None
     o.n_heat_dirichlet = hd.size
     F = None
@@ -211,6 +212,6 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "eig_solver": "randomized" if variant.randomized else "subspace",
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
         "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,
-        "coarse_bytes": inf.coarse_bytes, "level1": level1, "delta": delta, "local_solver": local_solver,
+        "coarse_bytes": inf.coarse_bytes, "level1": level1, "level1_operator": variant.level1, "delta": delta, "local_solver": local_solver,
     }
     return TwoLevelPreconditioner(variant, op, h, info)

@@ -108,6 +108,30 @@ def bench100_rand(eta):
     print("rand", eta, rep.iterations, res["coarse_dim"])
 
 
+def bench100_hh(eta, tag):
+    """HH / HH+Rot on the reference's benchmark cell (heat level 1)."""
+    cfg = cli.BenchmarkConfig(tol=1e-8)
+    res = cli.run_single(cfg, eta, tag)
+    op, rep = res["operator"], res["report"]
+    mesh = grid.build_fine_mesh(100, 100)
+    part = grid.build_coarse_partition(mesh, 10, 10)
+    coeff = coefficients.generate_coefficient(cfg.layout, mesh, eta, nu=cfg.nu)
+    dirichlet = mesh.boundary_nodes()
+    pre = schwarz.build_preconditioner(tag, op, mesh, part, coeff, dirichlet)
+    rng = np.random.default_rng(7)
+    r = rng.standard_normal(op.n_free)
+    level1 = schwarz._subdomain_heat_solvers(op, mesh, part, coeff, dirichlet)
+    z1 = np.zeros_like(r)
+    for idx, solve in level1:
+        z1[idx] += solve(r[idx])
+    save(f"ref_bench100_{tag.replace('+', '').lower()}_eta{eta:g}.npz", E=coeff.values,
+         dirichlet_nodes=dirichlet, free_dofs=op.free_dofs, b=res["rhs"], iters=rep.iterations,
+         x=res["solution"], residuals=np.array(rep.residuals), coarse_dim=res["coarse_dim"],
+         mode_counts=np.array(pre.info["mode_counts"]), apply_r=r, apply_z=pre.apply(r),
+         level1_z=z1, cond=rep.cond_estimate)
+    print(tag, eta, rep.iterations, res["coarse_dim"])
+
+
 class _KeptPatch(Patch):
     """Patch whose kept nodes follow the frozen block rule."""
 
@@ -136,7 +160,7 @@ class _Blocks:
         ]
 
 
-def adapter_case(spec, fname, tol=1e-8, maxit=5000):
+def adapter_case(spec, fname, tol=1e-8, maxit=5000, tag="EH+Rot"):
     """BASELINE config through reference functions."""
     mesh = grid.build_fine_mesh(spec.nx, spec.ny)
     coeff = assembly.CoefficientField(spec.E, spec.nu, spec.E_min, spec.E_max)
@@ -145,12 +169,16 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000):
     op = assembly._assemble(mesh.element_dofs(), coeff.values[:, None, None] * Ke[None], mesh.n_dofs, free)
     part = grid.build_coarse_partition(mesh, spec.nx // spec.H, spec.ny // spec.H)
     pou = grid.build_partition_of_unity(part)
-    variant = schwarz.get_variant("EH+Rot")
+    variant = schwarz.get_variant(tag)
     basis, modes, _ = schwarz.build_coarse_space(variant, op, mesh, part, coeff,
                                                  spec.heat_dirichlet_nodes, schwarz.EigOptions(), pou)
     from mselast import coarse
     cop = coarse.assemble_coarse_operator(op, basis)
-    level1 = schwarz._subdomain_elasticity_solvers(op, mesh, _Blocks(mesh, spec.H, spec.delta))
+    if variant.level1 == "heat":
+        level1 = schwarz._subdomain_heat_solvers(op, mesh, _Blocks(mesh, spec.H, spec.delta), coeff,
+                                                 spec.heat_dirichlet_nodes)
+    else:
+        level1 = schwarz._subdomain_elasticity_solvers(op, mesh, _Blocks(mesh, spec.H, spec.delta))
     pre = schwarz.TwoLevelPreconditioner(variant, level1, cop, op.n_free, {})
     b = spec.load_full[free]
     x, rep = krylov.pcg_solve(op.matrix, b, pre, tol=tol, maxit=maxit)
@@ -176,7 +204,7 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000):
 
 
 def main():
-    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand"}
+    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand", "hh"}
     if "elements" in which:
         elements()
     if "bench" in which:
@@ -185,6 +213,11 @@ def main():
     if "rand" in which:
         bench100_rand(1.0)
         bench100_rand(1e6)
+    if "hh" in which:
+        bench100_hh(1.0, "HH+Rot")
+        bench100_hh(1e6, "HH+Rot")
+        bench100_hh(1e6, "HH")
+        adapter_case(configs.config1(seed=0), "ref_config1_hhrot.npz", tag="HH+Rot")
     if "cfg1" in which:
         adapter_case(configs.config1(seed=0), "ref_config1.npz")
     if "mbb" in which:

@@ -176,14 +176,15 @@ def test_deterministic_solves():
     assert np.array_equal(x1, x2) and r1.iterations == r2.iterations
 
 
-@pytest.mark.parametrize("name", ["ref_config1.npz", "ref_mbb_64x32.npz", "ref_config2_n128.npz",
-                                  "ref_config3_n128.npz"])
-def test_baseline_config_against_reference(name):
+@pytest.mark.parametrize("name,tag", [("ref_config1.npz", "EH+Rot"), ("ref_mbb_64x32.npz", "EH+Rot"),
+                                      ("ref_config2_n128.npz", "EH+Rot"), ("ref_config3_n128.npz", "EH+Rot"),
+                                      ("ref_config1_hhrot.npz", "HH+Rot")])
+def test_baseline_config_against_reference(name, tag):
     g = load_golden(name)
     spec = spec_from_golden(g)
     from paper_2006_13387_b200.solve import setup_spec
 
-    mesh, op, pre = setup_spec(spec)
+    mesh, op, pre = setup_spec(spec, tag)
     assert pre.coarse_dim == int(g["coarse_dim"])
     assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
     z = pre.apply(g["apply_r"])
@@ -213,6 +214,40 @@ def test_baseline_config_against_reference(name):
     e_gpu = rel(x, x_dir)
     assert e_gpu <= max(1e-8, 2.0 * e_ref), (e_gpu, e_ref)
     assert rel(x, g["x"]) <= max(1e-8, 3.0 * e_ref, 10 * float(g["jitter_x"].max()))
+
+
+@pytest.mark.parametrize("name,tag", [("ref_bench100_hhrot_eta1.npz", "HH+Rot"),
+                                      ("ref_bench100_hhrot_eta1e+06.npz", "HH+Rot"),
+                                      ("ref_bench100_hh_eta1e+06.npz", "HH")])
+def test_heat_level1_variants_match_reference(name, tag):
+    """HH / HH+Rot (schwarz.py:112-140): one scalar banded factor per
+    subdomain, both displacement blocks solved in one sweep."""
+    g = load_golden(name)
+    mesh = G.build_fine_mesh(100, 100)
+    coeff = G.CoefficientField(g["E"], 0.3, float(g["E"].min()), 1.0)
+    op = G.ElasticityOperator(mesh, coeff, g["free_dofs"])
+    part = G.build_coarse_partition(mesh, 10, 10)
+    l1 = G.build_preconditioner(tag, op, mesh, part, coeff, g["dirichlet_nodes"], use_coarse=False)
+    # banded Cholesky vs SuperLU round-off; the eta 1e6 local problems have
+    # kappa ~ 1e9 (measured 6e-11 there, 1e-13 at eta 1)
+    assert rel(l1.apply(g["apply_r"]), g["level1_z"]) <= 1e-9
+    pre = G.build_preconditioner(tag, op, mesh, part, coeff, g["dirichlet_nodes"])
+    assert pre.info["level1_operator"] == "heat"
+    assert pre.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
+    assert rel(pre.apply(g["apply_r"]), g["apply_z"]) <= 1e-9
+    x, rep = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=2000)
+    assert rep.converged and abs(rep.iterations - int(g["iters"])) <= 1
+    assert rel(x, g["x"]) <= 1e-8
+    assert rep.cond_estimate == pytest.approx(float(g["cond"]), rel=1e-3)
+
+
+def test_heat_level1_rejects_componentwise_constraints():
+    spec = configs.config4(seed=0, nx=64, ny=32, H=16, delta=2, eta=1e4)
+    from paper_2006_13387_b200.solve import setup_spec
+
+    with pytest.raises(ValueError, match="whole-node"):
+        setup_spec(spec, "HH+Rot")
 
 
 def test_level1_only_matches_oracle(rng):

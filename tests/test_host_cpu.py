@@ -45,8 +45,8 @@ def test_struct_layouts_match_header():
     # sizes of the ABI structs as the C compiler lays them out (x86-64)
     import ctypes as C
 
-    # 5 ints (+4 pad), double, 4 ints, pointer, int64, 2 ints, pointer
-    assert C.sizeof(_lib.PrecondOpts) == 5 * 4 + 4 + 8 + 4 * 4 + 8 + 8 + 2 * 4 + 8
+    # 5 ints (+4 pad), double, 4 ints, pointer, int64, 2 ints, pointer, 2 ints
+    assert C.sizeof(_lib.PrecondOpts) == 5 * 4 + 4 + 8 + 4 * 4 + 8 + 8 + 2 * 4 + 8 + 2 * 4
     assert C.sizeof(_lib.Report) == 8 + 4 + 4 + 8 * 3
 
 

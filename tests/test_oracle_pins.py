@@ -47,7 +47,7 @@ def test_reference_benchmark_cell(eta):
         assert rep.cond_estimate == pytest.approx(float(g[f"cond_{tol}"]), rel=1e-8)
 
 
-def _adapter_check(name, apply_only=False):
+def _adapter_check(name, apply_only=False, level1_op="elasticity"):
     g = load_golden(name)
     spec = configs.ProblemSpec(
         name=name, nx=int(g["nx"]), ny=int(g["ny"]), E=g["E"], E_min=float(g["E"].min()),
@@ -55,7 +55,7 @@ def _adapter_check(name, apply_only=False):
         heat_dirichlet_nodes=g["heat_dirichlet_nodes"], load_full=g["load_full"],
         H=int(g["H"]), delta=int(g["delta"]), nu=float(g["nu"]))
     prob = O.problem_from_spec(spec)
-    P = O.build_two_level(prob, H=spec.H, delta=spec.delta, level1_mode="blocks")
+    P = O.build_two_level(prob, H=spec.H, delta=spec.delta, level1_mode="blocks", level1_op=level1_op)
     assert P.coarse_dim == int(g["coarse_dim"])
     assert np.array_equal(np.array(P.info["mode_counts"]), g["mode_counts"])
     assert np.allclose(P.coarse.K0, g["K0"], rtol=0, atol=1e-13 * np.abs(g["K0"]).max())
@@ -111,3 +111,27 @@ def test_randomized_variant_matches_reference(eta):
     x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=2000)
     assert rep.iterations == int(g["iters"])
     assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+
+
+@pytest.mark.parametrize("name,enrich", [("ref_bench100_hhrot_eta1.npz", True),
+                                         ("ref_bench100_hhrot_eta1e+06.npz", True),
+                                         ("ref_bench100_hh_eta1e+06.npz", False)])
+def test_heat_level1_variants_match_reference(name, enrich):
+    """HH / HH+Rot (schwarz.py:112-140): scalar level-1 factor on both blocks."""
+    g = load_golden(name)
+    mesh = O.mesh_for(100, 100)
+    op = O.elasticity_operator(mesh, g["E"], 0.3, O.whole_node_dofs(mesh, g["dirichlet_nodes"]))
+    prob = O.OracleProblem(mesh, op, g["E"], 0.3, g["b"], g["dirichlet_nodes"])
+    P = O.build_two_level(prob, H=10, level1_mode="neighborhoods", enrich=enrich, level1_op="heat")
+    assert P.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(P.info["mode_counts"]), g["mode_counts"])
+    r = g["apply_r"]
+    assert np.linalg.norm(P.level1_apply(r) - g["level1_z"]) <= 1e-13 * np.linalg.norm(g["level1_z"])
+    assert np.linalg.norm(P.apply(r) - g["apply_z"]) <= 1e-12 * np.linalg.norm(g["apply_z"])
+    x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=2000)
+    assert rep.iterations == int(g["iters"])
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])
+
+
+def test_config1_heat_level1_adapter_matches_reference_composition():
+    _adapter_check("ref_config1_hhrot.npz", level1_op="heat")
