@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="EH+Rot", choices=("EH+Rot", "EH", "EH+Rot;Rand", "HH+Rot", "HH"),
+                    help="preconditioner variant (Table 1 tags); the headline is EH+Rot")
     ap.add_argument("--local-solver", choices=("banded", "dense"), default="banded",
                     help="level-1 local solves: banded Cholesky sweeps (default) or explicit packed inverses")
     ap.add_argument("--maxit", type=int, default=1000,
@@ -221,7 +223,7 @@ def run_ours(args):
     else:
         spec = configs.config3(seed=args.seed, n=args.n or 2048)
     t_gen = time.perf_counter() - t0
-    mesh, op, pre = setup_spec(spec, local_solver=args.local_solver)
+    mesh, op, pre = setup_spec(spec, args.variant, local_solver=args.local_solver)
     n_free = op.n_free
     lib = _lib.load()
     ctx = op._ctx.handle
@@ -306,7 +308,7 @@ def run_ours(args):
     iter_gbs = B_iter * sum(iters) / (ms_total * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
+    if tp.exists() and args.variant.startswith("EH"):  # traffic.json holds the elasticity-band kernels
         try:
             traffic = json.loads(tp.read_text()).get("k_l1_solve" if args.local_solver == "banded" else "k_l1_dense_apply")
         except Exception:
@@ -317,10 +319,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": (f"config3: {spec.nx}^2 Q1 plane stress, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
-                                f"filtered-noise tanh density 40%, SIMP p=3, eta=1e6, cantilever, EH+Rot, rtol 1e-8")
+                                f"filtered-noise tanh density 40%, SIMP p=3, eta=1e6, cantilever, {args.variant}, rtol 1e-8")
                    if args.config == 3 else
                    (f"config4: {spec.nx}x{spec.ny} Q1 MBB beam, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
-                    f"filtered-noise tanh density 50%, SIMP p=3, eta=1e9, EH+Rot, rtol 1e-8"),
+                    f"filtered-noise tanh density 50%, SIMP p=3, eta=1e9, {args.variant}, rtol 1e-8"),
                    "n_free": n_free, "iterations_per_step": it_step, "maxit": args.maxit, "converged": bool(conv), "coarse_dim": info["coarse_dim"],
                    "n_subdomains": info["n_subdomains"], "mode_counts_hist": np.bincount(info["mode_counts"], minlength=7).tolist(),
                    "l2": "inputs larger than L2 (level-1 factors %.1f GB)" % (F2 / 1e9),

@@ -13,7 +13,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libmsgpu.so"
+# MSGPU_LIB: load an alternative build of the same library (kernel-variant sweeps)
+LIB_PATH = Path(os.environ.get("MSGPU_LIB") or Path(__file__).resolve().parent / "libmsgpu.so")
 
 MS_OK, MS_E_INVALID, MS_E_NOT_SPD, MS_E_CUDA, MS_E_NOMEM, MS_E_STATE = 0, -1, -2, -3, -4, -5
 MS_LEVEL1_NEIGHBORHOODS, MS_LEVEL1_BLOCKS = 0, 1

@@ -7,6 +7,8 @@
 // 35x35-node subdomains); its Cholesky factor is 1.4 MB instead of the 24 MB
 // of a packed dense inverse, so one apply streams ~8x fewer bytes.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "banded.cuh"
 
@@ -210,8 +212,12 @@ void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, dou
 // reversed numbering (row' = n-1-row).
 constexpr int kSolveWarps = 4;
 constexpr int kPD = 4;
+#ifndef MS_PD_HEAT
+#define MS_PD_HEAT 8
+#endif
+constexpr int kPDHeat = MS_PD_HEAT;
 
-template <int T, int NR, bool REV>
+template <int T, int NR, int PD, bool REV>
 __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, int bw,
                                            double* __restrict__ y, int lane) {
   constexpr int R = T + 1;  // register slots (blocks of 32 rows) per lane
@@ -234,7 +240,7 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
   }
 
   // prefetch ring: band values of the next PD steps
-  double lv[kPD][T], dv[kPD];
+  double lv[PD][T], dv[PD];
   auto load = [&](int k, int u, double(&l)[T], double& d) {
     const int base = ((lane - u - 1) & 31) + 1;
     const bool ok = k < n;
@@ -247,7 +253,7 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
     d = ok ? __ldg(col) : 0.0;
   };
 #pragma unroll
-  for (int u = 0; u < kPD; ++u) load(u, u, lv[u], dv[u]);
+  for (int u = 0; u < PD; ++u) load(u, u, lv[u], dv[u]);
 
   for (int k0 = 0; k0 < n; k0 += 32) {
     // rows of block (k0/32 + R-1) enter the window
@@ -261,9 +267,9 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
 #pragma unroll
     for (int c = 0; c < NR; ++c) wout[c] = 0.0;
 #pragma unroll 1
-    for (int u0 = 0; u0 < 32; u0 += kPD) {
+    for (int u0 = 0; u0 < 32; u0 += PD) {
 #pragma unroll
-     for (int q = 0; q < kPD; ++q) {
+     for (int q = 0; q < PD; ++q) {
       const int u = u0 + q;
       const int k = k0 + u;
       if (k < n) {
@@ -283,7 +289,7 @@ __device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, 
             }
           }
         }
-        load(k + kPD, (u + kPD) & 31, lv[q], dv[q]);
+        load(k + PD, (u + PD) & 31, lv[q], dv[q]);
       }
      }
     }
@@ -317,14 +323,214 @@ __global__ void __launch_bounds__(kSolveWarps * 32)
     y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
   }
   __syncwarp();
-  band_sweep<T, NR, false>(Lc + s.foff, s.n, s.bw, y, lane);
+  // narrow scalar bands: deeper prefetch keeps enough bytes in flight per warp
+  constexpr int PD = NR == 2 ? kPDHeat : kPD;
+  band_sweep<T, NR, PD, false>(Lc + s.foff, s.n, s.bw, y, lane);
   __syncwarp();
-  band_sweep<T, NR, true>(Lr + s.foff, s.n, s.bw, y, lane);
+  band_sweep<T, NR, PD, true>(Lr + s.foff, s.n, s.bw, y, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Same sweeps with the band streamed through shared memory by the bulk-copy
+// (TMA) engine: each warp owns a ring of kNst stages of kCh band columns; lane
+// 0 re-arms a stage's mbarrier and issues one cp.async.bulk per chunk as soon
+// as the chunk kNst back has been consumed.  The bytes in flight no longer
+// cost registers (the prefetch ring of band_sweep does), so narrow bands (the
+// heat level-1, 37 words per column) keep HBM busy too.
+#ifndef MS_TMA_CH
+#define MS_TMA_CH 8
+#endif
+#ifndef MS_TMA_NST
+#define MS_TMA_NST 3
+#endif
+#ifndef MS_TMA_WARPS
+#define MS_TMA_WARPS 4
+#endif
+constexpr int kCh = MS_TMA_CH;  // band columns per stage (divides 32)
+constexpr int kNst = MS_TMA_NST;  // stages per warp
+constexpr int kTmaWarps = MS_TMA_WARPS;
+static_assert(32 % kCh == 0, "stage width must divide 32");
+
+struct Ring {
+  double* buf;     // kNst stages of `stage` words
+  uint64_t* bar;   // kNst mbarriers
+  int stage;       // words per stage (even)
+  uint32_t phase;  // parity bit per stage
+};
+
+// first physical column and count of chunk c (steps [c kCh, c kCh + cnt))
+__device__ __forceinline__ void chunk_cols(bool rev, int n, int c, int& start, int& cnt) {
+  const int k0 = c * kCh;
+  cnt = min(kCh, n - k0);
+  start = rev ? n - k0 - cnt : k0;
+}
+
+template <bool REV>
+__device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int S, int c) {
+  int start, cnt;
+  chunk_cols(REV, n, c, start, cnt);
+  const int64_t w0 = (int64_t)start * S;
+  const int64_t a = w0 & ~(int64_t)1;  // 16-byte aligned source (L itself is)
+  const uint32_t words = (uint32_t)((cnt * S + (int)(w0 - a) + 1) & ~1);
+  const int st = c % kNst;
+  mbar_expect_tx(rg.bar + st, words * 8u);
+  bulk_g2s(rg.buf + (size_t)st * rg.stage, L + a, words * 8u, rg.bar + st);
+}
+
+template <int T, int NR, bool REV>
+__device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw,
+                                                double* __restrict__ y, int lane, Ring& rg) {
+  constexpr int R = T + 1;
+  const int S = bw + 1;
+  const int nch = (n + kCh - 1) / kCh;
+  if (lane == 0)
+    for (int c = 0; c < min(kNst, nch); ++c) ring_issue<REV>(rg, L, n, S, c);
+  auto yat = [&](int r, int c) -> double* { return y + (int64_t)(REV ? (n - 1 - r) : r) * NR + c; };
+
+  double acc[NR][R], rnext[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+#pragma unroll
+    for (int s = 0; s < R - 1; ++s) {
+      const int r = 32 * s + lane;
+      acc[c][s] = r < n ? *yat(r, c) : 0.0;
+    }
+    acc[c][R - 1] = 0.0;
+    rnext[c] = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane, c) : 0.0;
+  }
+
+  for (int k0 = 0; k0 < n; k0 += 32) {
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      acc[c][R - 1] = rnext[c];
+      const int r = k0 + 32 * R + lane;
+      rnext[c] = r < n ? *yat(r, c) : 0.0;
+    }
+    double dsave = 0.0;  // 1/L_kk of this lane's row of the block
+#pragma unroll 1
+    for (int h = 0; h < 32 && k0 + h < n; h += kCh) {
+      const int ch = (k0 + h) / kCh;
+      const int st = ch % kNst;
+      mbar_wait(rg.bar + st, (rg.phase >> st) & 1u);
+      rg.phase ^= 1u << st;
+      int start, cnt;
+      chunk_cols(REV, n, ch, start, cnt);
+      const double* sb = rg.buf + (size_t)st * rg.stage + (int)(((int64_t)start * S) & 1);
+      // Step u of the block: lane owns row k0 + 32 s + lane in slot s, i.e.
+      // band offset j = 32 s + lane - u from the pivot row; rows outside
+      // 1..bw get a zero coefficient (no selects on the update path).
+      auto step = [&](int q) {
+        const int u = h + q;
+        const double* col = sb + (REV ? (cnt - 1 - q) : q) * S;
+        const int jl = lane - u;
+        double m[R];
+        m[0] = (jl >= 1 && jl <= bw) ? col[jl] : 0.0;
+#pragma unroll
+        for (int s = 1; s < R; ++s) m[s] = (jl + 32 * s <= bw) ? col[jl + 32 * s] : 0.0;
+        const double d = col[0];
+        if (lane == u) dsave = d;
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double wk = __shfl_sync(0xffffffffu, acc[c][0] * d, u);
+#pragma unroll
+          for (int s = 0; s < R; ++s) acc[c][s] = fma(-m[s], wk, acc[c][s]);
+        }
+      };
+      if (cnt == kCh) {
+#pragma unroll
+        for (int q = 0; q < kCh; ++q) step(q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kCh; ++q)
+          if (q < cnt) step(q);
+      }
+      __syncwarp();  // every lane is done with this stage before it is refilled
+      if (lane == 0 && ch + kNst < nch) ring_issue<REV>(rg, L, n, S, ch + kNst);
+    }
+    // slot 0 of lane L stopped changing at step L: it holds row k0+L's final
+    // accumulator, and w = acc * (1/L_kk) exactly as the pivot step formed it
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      if (k0 + lane < n) *yat(k0 + lane, c) = acc[c][0] * dsave;
+#pragma unroll
+      for (int s = 0; s < R - 1; ++s) acc[c][s] = acc[c][s + 1];
+      acc[c][R - 1] = 0.0;
+    }
+  }
+}
+
+static int ring_stage_words(int max_bw) { return (kCh * (max_bw + 1) + 3) & ~1; }
+static size_t ring_smem_bytes(int max_bw) {
+  const int nb = (kTmaWarps * kNst + 1) & ~1;
+  return ((size_t)nb + (size_t)kTmaWarps * kNst * ring_stage_words(max_bw)) * sizeof(double);
 }
 
 template <int T, int NR>
-static void solve_t(const Grid& g, const BandSys* sys, int nsys, const double* Lc, const double* Lr,
-                    const double* r, double* ybuf, const int* done, cudaStream_t st) {
+__global__ void __launch_bounds__(kTmaWarps * 32)
+    k_l1_solve_ring(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
+                    const double* __restrict__ Lr, const double* __restrict__ r,
+                    double* __restrict__ ybuf, const int* done, int stage_words) {
+  if (done && *(volatile const int*)done) return;
+  extern __shared__ __align__(16) double smem_ring[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sid = blockIdx.x * kTmaWarps + warp;
+  if (sid >= nsys) return;
+  Ring rg;
+  rg.bar = reinterpret_cast<uint64_t*>(smem_ring) + warp * kNst;
+  rg.buf = smem_ring + ((kTmaWarps * kNst + 1) & ~1) + (size_t)warp * kNst * stage_words;
+  rg.stage = stage_words;
+  rg.phase = 0;
+  if (lane == 0) {
+    for (int st = 0; st < kNst; ++st) mbar_init(rg.bar + st, 1);
+    mbar_fence_init();
+  }
+  const BandSys s = sys[sid];
+  double* y = ybuf + s.yoff;
+  for (int i = lane; i < s.n * NR; i += 32) {
+    const int ln = i >> 1, c = i & 1;
+    int a, b;
+    band_node_of(s, ln, a, b);
+    y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
+  }
+  __syncwarp();
+  band_sweep_ring<T, NR, false>(Lc + s.foff, s.n, s.bw, y, lane, rg);
+  __syncwarp();
+  band_sweep_ring<T, NR, true>(Lr + s.foff, s.n, s.bw, y, lane, rg);
+}
+
+template <int T, int NR>
+static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
+                         const double* Lr, const double* r, double* ybuf, const int* done,
+                         cudaStream_t st) {
+  const size_t smem = ring_smem_bytes(max_bw);
+  static size_t configured[64] = {};  // per instantiation and device
+  int dev = 0;
+  MS_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64 || smem > configured[dev]) {
+    MS_CUDA(cudaFuncSetAttribute(k_l1_solve_ring<T, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    if (dev < 64) configured[dev] = smem;
+  }
+  k_l1_solve_ring<T, NR><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, r, ybuf, done, ring_stage_words(max_bw));
+}
+
+static bool use_ring_sweeps() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_L1_SWEEP");
+    v = (e && std::string(e) == "reg") ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int T, int NR>
+static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
+                    const double* Lr, const double* r, double* ybuf, const int* done, cudaStream_t st) {
+  if (use_ring_sweeps()) {
+    solve_ring_t<T, NR>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st);
+    return;
+  }
   k_l1_solve<T, NR><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, 0, st>>>(g, sys, nsys, Lc, Lr, r,
                                                                             ybuf, done);
 }
@@ -336,22 +542,22 @@ void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, in
   const int T = std::max(1, div_up(max_bw, 32));
   if (nrhs == 1) {
     switch (T) {
-      case 1: solve_t<1, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 2: solve_t<2, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 3: solve_t<3, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 4: solve_t<4, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 5: solve_t<5, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 6: solve_t<6, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 7: solve_t<7, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 8: solve_t<8, 1>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
       default: throw Error(-1, "level-1 band wider than 256 unsupported");
     }
   } else if (nrhs == 2) {
     switch (T) {
-      case 1: solve_t<1, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 2: solve_t<2, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 3: solve_t<3, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
-      case 4: solve_t<4, 2>(g, sys, nsys, Lc, Lr, r, ybuf, done, st); break;
+      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
       default: throw Error(-1, "heat level-1 band wider than 128 unsupported");
     }
   } else {

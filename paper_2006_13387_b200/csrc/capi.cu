@@ -792,7 +792,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
         const int sid = J * pc->NbX + I;
         s.foff = foff;  // factors stored for owned subdomains only
         s.yoff = yoff;
-        if (sid >= pc->s0 && sid < pc->s1) foff += (int64_t)s.n * (s.bw + 1);
+        // even offsets: the ring sweeps bulk-copy 16-byte aligned chunks
+        if (sid >= pc->s0 && sid < pc->s1) foff += ((int64_t)s.n * (s.bw + 1) + 1) & ~(int64_t)1;
         yoff += (int64_t)s.n * s.nrhs;
         pc->max_bw = std::max(pc->max_bw, s.bw);
         pc->hsys.push_back(s);
@@ -813,7 +814,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->sys.upload(pc->hsys.data(), pc->hsys.size(), st);
     pc->xcov.upload(xcov.data(), xcov.size(), st);
     pc->ycov.upload(ycov.data(), ycov.size(), st);
-    pc->Lc.alloc(foff);
+    pc->Lc.alloc(foff + 2);  // + slack: an aligned chunk may read one word past the last column
     pc->ybuf.alloc(yoff);
     fail.zero(st);
     const int ns = pc->s1 - pc->s0;
@@ -832,7 +833,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->dense = o->local_solver == MS_LOCAL_DENSE_INV;
     pc->nrhs = heat_l1 ? 2 : 1;
     if (!pc->dense) {
-      pc->Lr.alloc(foff);
+      pc->Lr.alloc(foff + 2);
       pc->Lr.zero(st);
       launch_band_potrf(pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
       check_fail(fail, st, "level-1 subdomain matrix");
