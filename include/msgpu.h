@@ -212,6 +212,46 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms);
 int ms_pcg_solve(ms_problem* prob, ms_precond* pc, const double* b, double tol, int maxit,
                  double* x, ms_report* rep, double* residuals, double* alphas, double* betas);
 
+/* ---- Topology-optimisation caller --------------------
+ * The per-design-step coefficient pipeline of the SIMP loop (topopt.py:123-216)
+ * on the device.  Vectors may be host or device pointers (device ones stay on
+ * the device; host ones are staged).  Element vectors have nx*ny entries in
+ * element order e = j*nx + i; full-dof vectors are [x-plane | y-plane]. */
+typedef struct ms_filter ms_filter;
+
+/* DensityFilter(mesh, radius) (assembly.py:290-325): cone weights
+ * max(0, radius - h |d|), rows normalised by their (edge-clipped) sums. */
+int ms_filter_create(ms_ctx* ctx, int nx, int ny, double h, double radius, ms_filter** out);
+int ms_filter_destroy(ms_filter* f);
+/* DensityFilter.apply (assembly.py:327-328): out = W rho, bit-identical */
+int ms_filter_apply(ms_filter* f, const double* rho, double* out);
+/* DensityFilter.adjoint (assembly.py:330-331): out = W^T v, bit-identical */
+int ms_filter_adjoint(ms_filter* f, const double* v, double* out);
+
+/* simp_modulus (assembly.py:280-287) written straight into the operator's
+ * modulus (replaces re-assembly, topopt.py:161-164).  MS_E_INVALID when
+ * rho_f leaves [-1e-12, 1 + 1e-12] or p < 1. */
+int ms_problem_set_density(ms_problem* prob, const double* rho_f, double p, double E_min,
+                           double E_max);
+
+/* compliance_and_sensitivity (topopt.py:59-70): *g0 = f.u,
+ * sens_e = -p clip(rho_f,0,1)^(p-1) (E_max - E_min) u_e^T k0 u_e. */
+int ms_compliance_sensitivity(ms_ctx* ctx, int nx, int ny, double nu, const double* u_full,
+                              const double* f_full, const double* rho_f, double p, double E_min,
+                              double E_max, double* g0, double* sens);
+
+/* oc_update (topopt.py:73-107): multiplier bracket (64 tries) + bisection
+ * (200 steps, |vol - v*| <= 1e-8 v*) on the device; the volume measure is
+ * volumes . W rho_new (filt != NULL) or volumes . rho_new.  MS_E_STATE when
+ * the bracket search fails (the reference's RuntimeError).  *evaluations
+ * (may be NULL) receives the number of candidate-volume evaluations. */
+int ms_oc_update(ms_ctx* ctx, int64_t n, const ms_filter* filt, const double* rho, const double* dg,
+                 const double* volumes, double v_star, double move, double damping, double* rho_new,
+                 int* evaluations);
+
+/* deterministic device dot product of n doubles (volume / compliance logs) */
+int ms_dot(ms_ctx* ctx, int64_t n, const double* a, const double* b, double* out);
+
 #ifdef __cplusplus
 }
 #endif

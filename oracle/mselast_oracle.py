@@ -695,3 +695,165 @@ def build_two_level(prob, H, delta=None, n_max=6, threshold=50.0, enrich=True, r
     P.coarse_space = cs
     P.partition = part
     return P
+
+
+# ---------------------------------------------------------------------------
+# topology-optimisation caller: body-force load
+# (assembly.py:63-77), SIMP + density filter (assembly.py:280-336),
+# sensitivity, OC update and the reuse loop (topopt.py:20-216)
+
+
+def body_force_load(mesh, fx, fy):
+    """Consistent nodal load of a uniform body force (assembly.py:69-76):
+    element mass-row sums scattered to the corners in element order."""
+    corner = mass_element(mesh.h).sum(axis=1)
+    nodal = np.zeros(mesh.n_nodes)
+    np.add.at(nodal, mesh.quad_nodes().ravel(), np.tile(corner, mesh.nx * mesh.ny))
+    f = np.zeros(mesh.n_dofs)
+    f[: mesh.n_nodes] += fx * nodal
+    f[mesh.n_nodes:] += fy * nodal
+    return f
+
+
+def simp(rho_f, p, E_min, E_max):
+    """simp_modulus (assembly.py:280-287)."""
+    rho_f = np.asarray(rho_f, dtype=float)
+    if rho_f.min() < -1e-12 or rho_f.max() > 1 + 1e-12:
+        raise ValueError("density out of [0, 1]")
+    return E_min + np.clip(rho_f, 0.0, 1.0) ** p * (E_max - E_min)
+
+
+class ConeFilter:
+    """DensityFilter (assembly.py:290-336): W = diag(1/rowsum) C with
+    C_ek = max(0, r - h |c_e - c_k|) over the offsets with positive weight.
+    Built with the same scipy calls (COO -> CSR, row sums, diagonal scaling),
+    which fixes the stored order (descending columns) and the rounding."""
+
+    def __init__(self, mesh, radius):
+        nx, ny, h = mesh.nx, mesh.ny, mesh.h
+        reach = max(int(np.ceil(radius / h)) - 1, 0) if radius > 0 else 0
+        stencil = []
+        for di in range(-reach, reach + 1):
+            for dj in range(-reach, reach + 1):
+                d = h * np.hypot(di, dj)
+                if radius - d > 0:
+                    stencil.append((di, dj, max(radius - d, 0.0) if radius > 0 else 1.0))
+        if not stencil:
+            stencil = [(0, 0, max(radius, 0.0) if radius > 0 else 1.0)]
+        e = np.arange(nx * ny)
+        ii, jj = e % nx, e // nx
+        r_, c_, v_ = [], [], []
+        for di, dj, w in stencil:
+            ik, jk = ii + di, jj + dj
+            ok = (ik >= 0) & (ik < nx) & (jk >= 0) & (jk < ny)
+            r_.append(e[ok])
+            c_.append((jk * nx + ik)[ok])
+            v_.append(np.full(int(ok.sum()), w))
+        Cm = sp.coo_matrix((np.concatenate(v_), (np.concatenate(r_), np.concatenate(c_))),
+                           shape=(nx * ny, nx * ny)).tocsr()
+        self.W = (sp.diags(1.0 / np.asarray(Cm.sum(axis=1)).ravel()) @ Cm).tocsr()
+
+    def apply(self, rho):
+        return self.W @ np.asarray(rho, dtype=float).ravel()
+
+    def adjoint(self, v):
+        return self.W.T @ np.asarray(v, dtype=float).ravel()
+
+
+def compliance_and_sensitivity(mesh, u_full, f_full, rho_f, p, E_min, E_max, nu):
+    """topopt.py:59-70: g0 = f.u and -p rho^(p-1) (E_max-E_min) u_e^T k0 u_e."""
+    g0 = float(f_full @ u_full)
+    ue = u_full[mesh.quad_dofs()]
+    energy = np.einsum("ni,ij,nj->n", ue, elasticity_element(nu), ue)
+    return g0, -p * np.clip(rho_f, 0.0, 1.0) ** (p - 1) * (E_max - E_min) * energy
+
+
+def oc_update(rho, dg, volumes, v_star, move=0.2, damping=0.5, filt=None):
+    """topopt.py:73-107: bracket the multiplier (64 tries), then bisect
+    (<= 200 steps) until the (filtered) volume is within 1e-8 of v_star."""
+    rho = np.asarray(rho, dtype=float)
+    gain = np.maximum(-np.asarray(dg, dtype=float), 0.0)
+
+    def cand(lam):
+        step = rho * (gain / (lam * volumes)) ** damping
+        return np.clip(np.clip(step, rho - move, rho + move), 0.0, 1.0)
+
+    def vol(lam):
+        x = cand(lam)
+        return volumes @ (filt.apply(x) if filt is not None else x)
+
+    lo, hi = 1e-9, 1e9
+    for _ in range(64):
+        if vol(lo) >= v_star >= vol(hi):
+            break
+        lo, hi = 0.5 * lo, 2.0 * hi
+    else:
+        raise RuntimeError("OC bisection failed to bracket the volume constraint")
+    for _ in range(200):
+        mid = np.sqrt(lo * hi)
+        v = vol(mid)
+        if v > v_star:
+            lo = mid
+        else:
+            hi = mid
+        if abs(v - v_star) <= 1e-8 * v_star:
+            break
+    return cand(np.sqrt(lo * hi))
+
+
+def optimize(nx=60, ny=60, Nx=3, Ny=3, volfrac=0.3, penal=3.0, radius_factor=2.5, E_max=1.0,
+             E_min=None, nu=0.3, n_iterations=100, variant="EH+Rot;Rand", tol=1e-6, maxit=2000,
+             move=0.2, damping=0.5, period=1, max_inner=None, seed=0):
+    """The SIMP loop with preconditioner reuse (topopt.py:123-216), reference
+    semantics: neighbourhood level-1, fully clamped boundary, body force
+    (0, -1), rebuild when due or when the solve fails (once)."""
+    mesh = mesh_for(nx, ny)
+    E_min = 1e-6 * E_max if E_min is None else E_min
+    filt = ConeFilter(mesh, radius_factor * mesh.h)
+    bnodes = np.nonzero(_boundary_mask(mesh))[0]
+    cons = whole_node_dofs(mesh, bnodes)
+    f_full = body_force_load(mesh, 0.0, -1.0)
+    volumes = np.full(nx * ny, mesh.h * mesh.h)
+    v_star = volfrac * volumes.sum()
+    rho = np.full(nx * ny, volfrac)
+    enrich = "+Rot" in variant
+    eig = randomized_solver(seed=seed) if variant.endswith(";Rand") else None
+    P, age, last, rebuilds, log = None, 0, 0, 0, []
+    for it in range(n_iterations):
+        rho_f = filt.apply(rho)
+        E = simp(rho_f, penal, E_min, E_max)
+        op = elasticity_operator(mesh, E, nu, cons)
+        prob = OracleProblem(mesh, op, E, nu, f_full[op.free_dofs], bnodes)
+
+        def build():
+            return build_two_level(prob, H=nx // Nx, level1_mode="neighborhoods", enrich=enrich,
+                                   eig_solver=randomized_solver(seed=seed) if eig else None,
+                                   level1_op="heat" if variant.startswith("HH") else "elasticity")
+
+        due = P is None or age >= period or (max_inner is not None and last > max_inner)
+        if due:
+            P, age = build(), 0
+            rebuilds += 1
+        rebuilt = due
+        u, rep = pcg(op.matrix, prob.b, P, tol=tol, maxit=maxit)
+        if not rep.converged:
+            P, age = build(), 0
+            rebuilds += 1
+            rebuilt = True
+            u, rep = pcg(op.matrix, prob.b, P, tol=tol, maxit=maxit)
+            if not rep.converged:
+                raise RuntimeError(f"state solve failed at iteration {it}")
+        age += 1
+        last = rep.iterations
+        u_full = np.zeros(mesh.n_dofs)
+        u_full[op.free_dofs] = u
+        g0, sens = compliance_and_sensitivity(mesh, u_full, f_full, rho_f, penal, E_min, E_max, nu)
+        rho = oc_update(rho, filt.adjoint(sens), volumes, v_star, move, damping, filt)
+        log.append({"iteration": it, "g0": g0, "volume": float(volumes @ filt.apply(rho)),
+                    "inner_iterations": rep.iterations, "rebuilt": rebuilt})
+    return rho, filt.apply(rho), log, rebuilds
+
+
+def _boundary_mask(mesh):
+    jj, ii = np.divmod(np.arange(mesh.n_nodes), mesh.nx + 1)
+    return (ii == 0) | (ii == mesh.nx) | (jj == 0) | (jj == mesh.ny)

@@ -1,8 +1,9 @@
 """B200-native two-level spectral Schwarz PCG for high-contrast elasticity.
 
-Drop-in for the solve path of the reference package ``mselast`` (EH / EH+Rot
-variants): the public names below mirror ``mselast.grid``,
-``mselast.assembly``, ``mselast.schwarz`` and ``mselast.krylov``; every
+Drop-in for the solve path of the reference package ``mselast`` (EH, EH+Rot,
+EH+Rot;Rand, HH, HH+Rot variants) and its SIMP caller: the public names below
+mirror ``mselast.grid``, ``mselast.assembly``, ``mselast.schwarz``,
+``mselast.krylov`` and ``mselast.topopt``; every
 solver call runs in hand-written sm_100a kernels behind the C ABI
 ``include/msgpu.h`` (``libmsgpu.so``).  There is no CPU fallback.
 """
@@ -14,5 +15,8 @@ from .schwarz import (VARIANTS, GPU_VARIANTS, EigOptions, IdentityPreconditioner
                       TwoLevelPreconditioner, build_preconditioner, get_variant)
 from .krylov import SolveReport, estimate_condition, pcg_solve
 from .solve import solve_spec
+from . import topopt
+from .topopt import (DensityFilter, OptimizeConfig, OptimizationResult, ReusePolicy,
+                     compliance_and_sensitivity, oc_update, optimize)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -29,7 +29,8 @@ EXPORTS = (
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
     "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
     "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_strip_rows", "ms_copy",
-    "ms_halo_plan",
+    "ms_halo_plan", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
+    "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot",
 )
 
 ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
@@ -131,6 +132,15 @@ def load(path: str | os.PathLike | None = None):
         "ms_strip_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
         "ms_copy": (C.c_int, [vp, vp, C.c_size_t]),
         "ms_halo_plan": (C.c_int, [C.c_int] * 6 + [ip]),
+        "ms_filter_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(vp)]),
+        "ms_filter_destroy": (C.c_int, [vp]),
+        "ms_filter_apply": (C.c_int, [vp, vp, vp]),
+        "ms_filter_adjoint": (C.c_int, [vp, vp, vp]),
+        "ms_problem_set_density": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_double]),
+        "ms_compliance_sensitivity": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, vp, vp, vp, C.c_double,
+                                                C.c_double, C.c_double, dp, vp]),
+        "ms_oc_update": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_double, C.c_double, vp, ip]),
+        "ms_dot": (C.c_int, [vp, C.c_int64, vp, vp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

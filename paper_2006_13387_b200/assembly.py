@@ -41,16 +41,30 @@ class CoefficientField:
 
 @dataclass
 class LoadSpec:
-    point_loads: list = field(default_factory=list)  # (node, component, magnitude)
+    """Point loads (node, component, magnitude) plus an optional uniform body force (assembly.py:55-60)."""
+
+    point_loads: list = field(default_factory=list)
+    body_force: tuple | None = None  # (fx, fy) per unit area
 
 
 def build_load_vector(mesh, load):
-    """Full-layout load vector from point loads (assembly.py:63-77, point-load part)."""
+    """Full-layout load vector (assembly.py:63-77): point loads, then the
+    consistent body force (each element adds the row sums of its Q1 mass
+    element to its corners, in element order)."""
     f = np.zeros(mesh.n_dofs)
     for node, comp, mag in load.point_loads:
         if not (0 <= node < mesh.n_nodes) or comp not in (0, 1):
             raise ValueError(f"invalid point load ({node}, {comp})")
         f[node + comp * mesh.n_nodes] += mag
+    if load.body_force is not None:
+        fx, fy = load.body_force
+        h2 = mesh.h * mesh.h / 36.0
+        corner = (h2 * np.array([[4.0, 2.0, 1.0, 2.0], [2.0, 4.0, 2.0, 1.0], [1.0, 2.0, 4.0, 2.0],
+                                 [2.0, 1.0, 2.0, 4.0]])).sum(axis=1)
+        nodal = np.zeros(mesh.n_nodes)
+        np.add.at(nodal, mesh.element_nodes().ravel(), np.tile(corner, mesh.n_elements))
+        f[: mesh.n_nodes] += fx * nodal
+        f[mesh.n_nodes:] += fy * nodal
     return f
 
 
@@ -136,6 +150,16 @@ class ElasticityOperator:
     def set_modulus(self, E):
         E = np.ascontiguousarray(E, dtype=np.float64)
         _lib.check(_lib.load().ms_problem_set_modulus(self.handle, C.c_void_p(E.ctypes.data)),
+                   self._ctx.handle)
+
+    def set_density(self, rho_f, p, E_min, E_max):
+        """E = simp_modulus(rho_f, p, E_min, E_max) computed on the device into the
+        operator's modulus (assembly.py:280-287 + the re-assembly of topopt.py:161-164).
+        rho_f: numpy array or float64 CUDA tensor of element densities."""
+        pp, keep, _ = _lib.vec_ptr(rho_f)
+        if keep.shape[0] != self.mesh.n_elements:
+            raise ValueError("density field does not match mesh")
+        _lib.check(_lib.load().ms_problem_set_density(self.handle, pp, float(p), float(E_min), float(E_max)),
                    self._ctx.handle)
 
     def __del__(self):

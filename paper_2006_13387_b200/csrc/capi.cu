@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "eigen.cuh"
 #include "operator.cuh"
+#include "topopt.cuh"
 
 using namespace msgpu;
 
@@ -211,6 +212,17 @@ struct ms_ctx {
   std::string err;
   Prof prof;
   std::unique_ptr<Comm> comm;  // multi-GPU strips (world > 1)
+  // scratch of the caller-pipeline entry points (dot / OC reductions)
+  DBuf<double> red;
+  DBuf<unsigned int> ticket;
+  DBuf<double> dval;
+  void ensure_scratch() {
+    if (red.p) return;
+    red.alloc(2 * kDotBlocks);
+    ticket.alloc(1);
+    ticket.zero(st);
+    dval.alloc(8);
+  }
   int world() const { return comm ? comm->world : 1; }
   int rank() const { return comm ? comm->rank : 0; }
 };
@@ -1379,6 +1391,267 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     rep->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   }
   MS_API_END(P ? P->ctx : nullptr)
+}
+
+// ---------------------------------------------------------------------------
+// Topology-optimisation caller
+
+struct ms_filter {
+  ms_ctx* ctx = nullptr;
+  int nx = 0, ny = 0;
+  DBuf<int2> off;
+  DBuf<double> w, inv;
+  FilterDev dev{};
+};
+
+// numpy's pairwise float64 summation (the reduction behind scipy's
+// W.sum(axis=1) through np.add.reduceat): n < 8 sequential, n <= 128 eight
+// accumulators, larger blocks split in two
+static double np_pairwise(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+// an ABI vector of n doubles on the device (host inputs are staged)
+struct DevIn {
+  const double* d = nullptr;
+  DBuf<double> buf;
+  DevIn(const double* p, int64_t n, cudaStream_t st) {
+    if (is_device_ptr(p)) {
+      d = p;
+    } else {
+      buf.upload(p, n, st);
+      d = buf.p;
+    }
+  }
+};
+struct DevOut {
+  double* user;
+  double* d = nullptr;
+  int64_t n;
+  DBuf<double> buf;
+  DevOut(double* p, int64_t n_, cudaStream_t) : user(p), n(n_) {
+    if (is_device_ptr(p)) {
+      d = p;
+    } else {
+      buf.alloc(n);
+      d = buf.p;
+    }
+  }
+  void finish(cudaStream_t st) {
+    if (d != user) MS_CUDA(cudaMemcpyAsync(user, d, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    MS_CUDA(cudaStreamSynchronize(st));
+  }
+};
+
+int ms_filter_create(ms_ctx* ctx, int nx, int ny, double h, double radius, ms_filter** out) {
+  MS_API_BEGIN
+  if (!ctx || !out) throw Error(MS_E_INVALID, "null argument");
+  if (nx < 1 || ny < 1 || !(h > 0)) throw Error(MS_E_INVALID, "bad mesh");
+  if (radius < 0) throw Error(MS_E_INVALID, "filter radius must be nonnegative");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const cudaStream_t st = ctx->st;
+  // stencil (assembly.py:303-314): offsets with radius - h |d| > 0, weight max(0, .)
+  int reach = radius > 0 ? (int)std::ceil(radius / h) - 1 : 0;
+  reach = std::max(reach, 0);
+  std::vector<int2> offs;
+  std::vector<double> wts;
+  for (int di = -reach; di <= reach; ++di)
+    for (int dj = -reach; dj <= reach; ++dj) {
+      const double dist = h * std::hypot((double)di, (double)dj);
+      if (radius - dist > 0) {
+        offs.push_back(make_int2(di, dj));
+        wts.push_back(radius > 0 ? std::max(radius - dist, 0.0) : 1.0);
+      }
+    }
+  if (offs.empty()) {
+    offs.push_back(make_int2(0, 0));
+    wts.push_back(radius > 0 ? std::max(radius - h * std::hypot(0.0, 0.0), 0.0) : 1.0);
+  }
+  // descending column order (dj, di): the stored order of the reference's rows
+  std::vector<int> ord(offs.size());
+  for (size_t o = 0; o < ord.size(); ++o) ord[o] = (int)o;
+  std::sort(ord.begin(), ord.end(), [&](int a, int b) {
+    return offs[a].y != offs[b].y ? offs[a].y > offs[b].y : offs[a].x > offs[b].x;
+  });
+  std::vector<int2> soff(ord.size());
+  std::vector<double> sw(ord.size());
+  for (size_t o = 0; o < ord.size(); ++o) {
+    soff[o] = offs[ord[o]];
+    sw[o] = wts[ord[o]];
+  }
+  // row sums a[0] + pairwise(a[1:]) over ascending columns; rows only differ
+  // by how the stencil is clipped at the edges, so memoise per clip class
+  const int64_t n = (int64_t)nx * ny;
+  std::vector<double> inv(n);
+  std::vector<double> cache;
+  const int R1 = reach + 1;
+  cache.assign((size_t)R1 * R1 * R1 * R1, 0.0);
+  std::vector<char> have(cache.size(), 0);
+  std::vector<double> row;
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      const int li = std::min(i, reach), ri = std::min(nx - 1 - i, reach);
+      const int lj = std::min(j, reach), rj = std::min(ny - 1 - j, reach);
+      const size_t key = (((size_t)li * R1 + ri) * R1 + lj) * R1 + rj;
+      if (!have[key]) {
+        row.clear();
+        for (int o = (int)soff.size() - 1; o >= 0; --o) {  // ascending columns
+          const int ik = i + soff[o].x, jk = j + soff[o].y;
+          if (ik >= 0 && ik < nx && jk >= 0 && jk < ny) row.push_back(sw[o]);
+        }
+        cache[key] = row[0] + np_pairwise(row.data() + 1, (int64_t)row.size() - 1);
+        have[key] = 1;
+      }
+      inv[(int64_t)j * nx + i] = 1.0 / cache[key];
+    }
+  std::unique_ptr<ms_filter> f(new ms_filter());
+  f->ctx = ctx;
+  f->nx = nx;
+  f->ny = ny;
+  f->off.upload(soff.data(), soff.size(), st);
+  f->w.upload(sw.data(), sw.size(), st);
+  f->inv.upload(inv.data(), inv.size(), st);
+  MS_CUDA(cudaStreamSynchronize(st));
+  f->dev = FilterDev{nx, ny, (int)soff.size(), f->off.p, f->w.p, f->inv.p};
+  *out = f.release();
+  MS_API_END(ctx)
+}
+
+int ms_filter_destroy(ms_filter* f) {
+  MS_API_BEGIN
+  if (f) {
+    cudaSetDevice(f->ctx->device);
+    delete f;
+  }
+  MS_API_END(nullptr)
+}
+
+static int filter_run(ms_filter* f, const double* x, double* y, bool adjoint) {
+  MS_API_BEGIN
+  if (!f || !x || !y) throw Error(MS_E_INVALID, "null argument");
+  MS_CUDA(cudaSetDevice(f->ctx->device));
+  const cudaStream_t st = f->ctx->st;
+  const int64_t n = (int64_t)f->nx * f->ny;
+  DevIn in(x, n, st);
+  DevOut o(y, n, st);
+  if (in.d == o.d) throw Error(MS_E_INVALID, "filter output must not alias its input");
+  if (adjoint)
+    launch_filter_adjoint(f->dev, in.d, o.d, st);
+  else
+    launch_filter_apply(f->dev, in.d, o.d, st);
+  o.finish(st);
+  MS_API_END(f ? f->ctx : nullptr)
+}
+
+int ms_filter_apply(ms_filter* f, const double* rho, double* out) { return filter_run(f, rho, out, false); }
+int ms_filter_adjoint(ms_filter* f, const double* v, double* out) { return filter_run(f, v, out, true); }
+
+int ms_problem_set_density(ms_problem* P, const double* rho_f, double p, double E_min, double E_max) {
+  MS_API_BEGIN
+  if (!P || !rho_f) throw Error(MS_E_INVALID, "null argument");
+  if (p < 1) throw Error(MS_E_INVALID, "penalization exponent must be >= 1");
+  MS_CUDA(cudaSetDevice(P->ctx->device));
+  const cudaStream_t st = P->ctx->st;
+  const int64_t n = (int64_t)P->g.nx * P->g.ny;
+  DevIn in(rho_f, n, st);
+  DBuf<int> bad;
+  bad.alloc(1);
+  bad.zero(st);
+  launch_simp(n, in.d, p, E_min, E_max, P->E.p, bad.p, st);
+  int hb = 0;
+  MS_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  if (hb) throw Error(MS_E_INVALID, "density out of [0, 1]");
+  MS_API_END(P ? P->ctx : nullptr)
+}
+
+int ms_compliance_sensitivity(ms_ctx* ctx, int nx, int ny, double nu, const double* u_full,
+                              const double* f_full, const double* rho_f, double p, double E_min,
+                              double E_max, double* g0, double* sens) {
+  MS_API_BEGIN
+  if (!ctx || !u_full || !f_full || !rho_f || !g0 || !sens) throw Error(MS_E_INVALID, "null argument");
+  if (nx < 1 || ny < 1) throw Error(MS_E_INVALID, "bad mesh");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const cudaStream_t st = ctx->st;
+  ctx->ensure_scratch();
+  Grid g{nx, ny, nx + 1, (int64_t)(nx + 1) * (ny + 1), 1.0 / nx};
+  const int64_t n_el = (int64_t)nx * ny, n_dofs = 2 * g.n_nodes;
+  DevIn u(u_full, n_dofs, st), f(f_full, n_dofs, st), r(rho_f, n_el, st);
+  DevOut o(sens, n_el, st);
+  KeParam ke{};
+  unit_elasticity(nu, ke.k);
+  launch_dot(n_dofs, f.d, u.d, ctx->dval.p, ctx->red.p, ctx->ticket.p, st);
+  launch_compliance_sens(g, ke, u.d, r.d, p, E_min, E_max, o.d, st);
+  MS_CUDA(cudaMemcpyAsync(g0, ctx->dval.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  o.finish(st);
+  MS_API_END(ctx)
+}
+
+int ms_dot(ms_ctx* ctx, int64_t n, const double* a, const double* b, double* out) {
+  MS_API_BEGIN
+  if (!ctx || !a || !b || !out || n < 0) throw Error(MS_E_INVALID, "bad argument");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const cudaStream_t st = ctx->st;
+  ctx->ensure_scratch();
+  DevIn da(a, n, st), db(b, n, st);
+  launch_dot(n, da.d, db.d, ctx->dval.p, ctx->red.p, ctx->ticket.p, st);
+  MS_CUDA(cudaMemcpyAsync(out, ctx->dval.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  MS_API_END(ctx)
+}
+
+int ms_oc_update(ms_ctx* ctx, int64_t n, const ms_filter* filt, const double* rho, const double* dg,
+                 const double* volumes, double v_star, double move, double damping, double* rho_new,
+                 int* evaluations) {
+  MS_API_BEGIN
+  if (!ctx || !rho || !dg || !volumes || !rho_new || n < 1) throw Error(MS_E_INVALID, "bad argument");
+  if (filt && (int64_t)filt->nx * filt->ny != n) throw Error(MS_E_INVALID, "filter does not match the design");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const cudaStream_t st = ctx->st;
+  ctx->ensure_scratch();
+  DevIn r(rho, n, st), d(dg, n, st), v(volumes, n, st);
+  DevOut o(rho_new, n, st);
+  // measure(lam) = volumes . W candidate(lam) = (W^T volumes) . candidate(lam)
+  DBuf<double> wv;
+  const double* wvp = v.d;
+  if (filt) {
+    wv.alloc(n);
+    launch_filter_adjoint(filt->dev, v.d, wv.p, st);
+    wvp = wv.p;
+  }
+  DBuf<OcState> state;
+  state.alloc(1);
+  launch_oc_init(state.p, v_star, move, damping, st);
+  OcState hs{};
+  for (int launched = 0; launched < 64 + 200;) {
+    for (int b = 0; b < 8 && launched < 64 + 200; ++b, ++launched)
+      launch_oc_eval(n, r.d, d.d, v.d, wvp, state.p, ctx->red.p, ctx->ticket.p, st);
+    MS_CUDA(cudaMemcpyAsync(&hs, state.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    MS_CUDA(cudaStreamSynchronize(st));
+    if (hs.phase >= 2) break;
+  }
+  if (evaluations) *evaluations = hs.evals;
+  if (hs.phase == 3) throw Error(MS_E_STATE, "OC bisection failed to bracket the volume constraint");
+  launch_oc_final(n, r.d, d.d, v.d, state.p, o.d, st);
+  o.finish(st);
+  MS_API_END(ctx)
 }
 
 }  // extern "C"

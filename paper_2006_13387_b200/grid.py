@@ -37,6 +37,12 @@ class FineMesh:
         X, Y = np.meshgrid(np.arange(self.nx + 1) * self.h, np.arange(self.ny + 1) * self.h)
         return np.column_stack([X.ravel(), Y.ravel()])
 
+    def element_nodes(self):
+        """(n_elements, 4) corner node ids, counter-clockwise from lower-left (grid.py:40-48)."""
+        jj, ii = np.divmod(np.arange(self.n_elements), self.nx)
+        n0 = jj * (self.nx + 1) + ii
+        return np.stack([n0, n0 + 1, n0 + self.nx + 2, n0 + self.nx + 1], axis=1)
+
     def boundary_nodes(self):
         jj, ii = np.divmod(np.arange(self.n_nodes), self.nx + 1)
         on = (ii == 0) | (ii == self.nx) | (jj == 0) | (jj == self.ny)

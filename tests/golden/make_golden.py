@@ -132,6 +132,68 @@ def bench100_hh(eta, tag):
     print(tag, eta, rep.iterations, res["coarse_dim"])
 
 
+def topopt_cases():
+    """SIMP caller (topopt.py, assembly.py:280-336): filter, sensitivity, OC
+    update and short optimize runs of the unmodified reference."""
+    from mselast import topopt
+
+    out = {}
+    rng = np.random.default_rng(3)
+    for tag, (nx, ny, fac) in {"a": (30, 20, 2.5), "b": (33, 17, 4.0), "c": (24, 24, 9.0)}.items():
+        mesh = grid.build_fine_mesh(nx, ny)
+        filt = assembly.DensityFilter(mesh, fac * mesh.h)
+        x = rng.uniform(0.0, 1.0, mesh.n_elements)
+        v = rng.standard_normal(mesh.n_elements)
+        out.update({f"filt_{tag}_shape": np.array([nx, ny]), f"filt_{tag}_radius": fac * mesh.h,
+                    f"filt_{tag}_x": x, f"filt_{tag}_Wx": filt.apply(x), f"filt_{tag}_v": v,
+                    f"filt_{tag}_WTv": filt.adjoint(v)})
+    # sensitivity on a solved state (reference test setup, test_topopt.py:35-41)
+    mesh = grid.build_fine_mesh(16, 16)
+    f = assembly.build_load_vector(mesh, assembly.LoadSpec(body_force=(0.0, -1.0)))
+    rho = np.random.default_rng(42).uniform(0.2, 0.9, mesh.n_elements)
+    E = assembly.simp_modulus(rho, 3.0, 1e-6, 1.0)
+    op = assembly.assemble_elasticity(mesh, assembly.CoefficientField(E, 0.3, E.min(), 1.0),
+                                      mesh.boundary_nodes())
+    import scipy.sparse.linalg as spla
+
+    u = op.expand(spla.spsolve(op.matrix.tocsc(), op.restrict(f)))
+    g0, sens = topopt.compliance_and_sensitivity(mesh, u, f, rho, 3.0, 1e-6, 1.0, 0.3)
+    out.update(sens_u=u, sens_f=f, sens_rho=rho, sens_E=E, sens_g0=g0, sens_sens=sens)
+    # OC update, unfiltered and filtered
+    n = 200
+    r0 = rng.uniform(0.1, 0.9, n)
+    dg = -rng.uniform(0.1, 10.0, n)
+    vol = rng.uniform(0.5, 1.5, n)
+    out.update(oc_rho=r0, oc_dg=dg, oc_vol=vol, oc_vstar=0.45 * vol.sum(),
+               oc_new=topopt.oc_update(r0, dg, vol, 0.45 * vol.sum(), move=0.15))
+    mesh = grid.build_fine_mesh(30, 20)
+    filt = assembly.DensityFilter(mesh, 2.5 * mesh.h)
+    r1 = rng.uniform(0.1, 0.9, mesh.n_elements)
+    dg1 = -rng.uniform(0.1, 10.0, mesh.n_elements)
+    vol1 = np.full(mesh.n_elements, mesh.h ** 2)
+    out.update(ocf_rho=r1, ocf_dg=dg1, ocf_vol=vol1, ocf_vstar=0.45 * vol1.sum(),
+               ocf_new=topopt.oc_update(r1, dg1, vol1, 0.45 * vol1.sum(), filt=filt))
+    save("ref_topopt_units.npz", **out)
+
+    runs = {
+        "ehrot": dict(variant="EH+Rot", tol=1e-8),
+        "rand_reuse3": dict(variant="EH+Rot;Rand", tol=1e-8, reuse=topopt.ReusePolicy(period=3)),
+        "hhrot_thresh": dict(variant="HH+Rot", tol=1e-8,
+                             reuse=topopt.ReusePolicy(period=100, max_inner_iterations=40)),
+    }
+    for name, kw in runs.items():
+        cfg = topopt.OptimizeConfig(nx=40, ny=40, Nx=4, Ny=4, n_iterations=6, volfrac=0.3, **kw)
+        res = topopt.optimize(cfg)
+        log = res.log
+        save(f"ref_topopt_{name}.npz", rho=res.rho, rho_f=res.rho_f,
+             g0=np.array([r["g0"] for r in log]), volume=np.array([r["volume"] for r in log]),
+             inner=np.array([r["inner_iterations"] for r in log]),
+             rebuilt=np.array([r["rebuilt"] for r in log]), cond=np.array([r["cond_estimate"] for r in log]),
+             rebuilds=res.rebuilds, period=kw.get("reuse", topopt.ReusePolicy()).period,
+             max_inner=kw.get("reuse", topopt.ReusePolicy()).max_inner_iterations or 0)
+        print(name, [r["inner_iterations"] for r in log], [r["rebuilt"] for r in log])
+
+
 class _KeptPatch(Patch):
     """Patch whose kept nodes follow the frozen block rule."""
 
@@ -204,7 +266,7 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000, tag="EH+Rot"):
 
 
 def main():
-    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand", "hh"}
+    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand", "hh", "topopt"}
     if "elements" in which:
         elements()
     if "bench" in which:
@@ -218,6 +280,8 @@ def main():
         bench100_hh(1e6, "HH+Rot")
         bench100_hh(1e6, "HH")
         adapter_case(configs.config1(seed=0), "ref_config1_hhrot.npz", tag="HH+Rot")
+    if "topopt" in which:
+        topopt_cases()
     if "cfg1" in which:
         adapter_case(configs.config1(seed=0), "ref_config1.npz")
     if "mbb" in which:

@@ -133,3 +133,23 @@ def test_product_path_has_no_cpu_fallback(tmp_path):
         G.build_preconditioner("EE", object(), mesh, part, coeff, [])
     with pytest.raises(TypeError):
         G.pcg_solve(np.eye(3), np.ones(3))
+
+
+def test_topopt_host_pieces():
+    """ReusePolicy validation and config defaults (topopt.py:20-56); the
+    body-force load vector is bit-identical to the reference's."""
+    from paper_2006_13387_b200 import topopt as T
+
+    with pytest.raises(ValueError):
+        T.ReusePolicy(period=0)
+    with pytest.raises(ValueError):
+        T.ReusePolicy(period=1, max_inner_iterations=0)
+    c = T.OptimizeConfig()
+    assert (c.nx, c.ny, c.Nx, c.Ny, c.volfrac, c.penal, c.filter_radius_factor, c.variant, c.tol, c.maxit,
+            c.move_limit, c.damping, c.solver) == (60, 60, 3, 3, 0.3, 3.0, 2.5, "EH+Rot;Rand", 1e-6, 2000,
+                                                   0.2, 0.5, "pcg")
+    g = load_golden("ref_topopt_units.npz")
+    mesh = G.build_fine_mesh(16, 16)
+    assert np.array_equal(G.build_load_vector(mesh, G.LoadSpec(body_force=(0.0, -1.0))), g["sens_f"])
+    with pytest.raises(ValueError):
+        T.optimize(T.OptimizeConfig(solver="direct"))

@@ -135,3 +135,47 @@ def test_heat_level1_variants_match_reference(name, enrich):
 
 def test_config1_heat_level1_adapter_matches_reference_composition():
     _adapter_check("ref_config1_hhrot.npz", level1_op="heat")
+
+
+# ---------------------------------------------------------------------------
+# SIMP caller (row f2)
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_cone_filter_bitwise(tag):
+    g = load_golden("ref_topopt_units.npz")
+    nx, ny = g[f"filt_{tag}_shape"]
+    filt = O.ConeFilter(O.mesh_for(int(nx), int(ny)), float(g[f"filt_{tag}_radius"]))
+    assert np.array_equal(filt.apply(g[f"filt_{tag}_x"]), g[f"filt_{tag}_Wx"])
+    assert np.array_equal(filt.adjoint(g[f"filt_{tag}_v"]), g[f"filt_{tag}_WTv"])
+
+
+def test_sensitivity_and_oc_units():
+    g = load_golden("ref_topopt_units.npz")
+    mesh = O.mesh_for(16, 16)
+    assert np.array_equal(O.body_force_load(mesh, 0.0, -1.0), g["sens_f"])
+    assert np.array_equal(O.simp(g["sens_rho"], 3.0, 1e-6, 1.0), g["sens_E"])
+    g0, sens = O.compliance_and_sensitivity(mesh, g["sens_u"], g["sens_f"], g["sens_rho"], 3.0, 1e-6, 1.0, 0.3)
+    assert g0 == pytest.approx(float(g["sens_g0"]), rel=1e-14)
+    assert np.allclose(sens, g["sens_sens"], rtol=1e-13, atol=0)
+    new = O.oc_update(g["oc_rho"], g["oc_dg"], g["oc_vol"], float(g["oc_vstar"]), move=0.15)
+    assert np.array_equal(new, g["oc_new"])
+    filt = O.ConeFilter(O.mesh_for(30, 20), 2.5 / 30)
+    new = O.oc_update(g["ocf_rho"], g["ocf_dg"], g["ocf_vol"], float(g["ocf_vstar"]), filt=filt)
+    assert np.array_equal(new, g["ocf_new"])
+    with pytest.raises(RuntimeError):
+        O.oc_update(np.full(20, 0.9), np.full(20, -1.0), np.ones(20), 2.0, move=0.01)
+
+
+@pytest.mark.parametrize("name,variant", [("ehrot", "EH+Rot"), ("rand_reuse3", "EH+Rot;Rand"),
+                                          ("hhrot_thresh", "HH+Rot")])
+def test_optimize_loop_matches_reference(name, variant):
+    g = load_golden(f"ref_topopt_{name}.npz")
+    mi = int(g["max_inner"])
+    rho, rho_f, log, rebuilds = O.optimize(nx=40, ny=40, Nx=4, Ny=4, n_iterations=6, volfrac=0.3,
+                                           variant=variant, tol=1e-8, period=int(g["period"]),
+                                           max_inner=mi or None)
+    assert [r["rebuilt"] for r in log] == list(g["rebuilt"]) and rebuilds == int(g["rebuilds"])
+    assert [r["inner_iterations"] for r in log] == list(g["inner"])
+    assert np.allclose([r["g0"] for r in log], g["g0"], rtol=1e-10, atol=0)
+    assert np.allclose(rho, g["rho"], rtol=0, atol=1e-9)
