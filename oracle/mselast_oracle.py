@@ -249,7 +249,7 @@ def local_heat_problem(mesh, E, rect, dirichlet_nodes):
     return K, M, pmesh
 
 
-def lowest_eigenpairs(K, M, k):
+def lowest_eigenpairs(K, M, k, Z=None):
     """Dense generalized eigensolve, LAPACK ?sygvx (spectral.py:93-100)."""
     if k > K.matrix.shape[0]:
         raise ValueError("more modes requested than dofs")
@@ -275,19 +275,20 @@ def lowest_eigenpairs_arpack(K, M, k):
     return w, v
 
 
-def randomized_eigenpairs(K, M, k, n_snapshots, seed, n_passes=4):
+def randomized_eigenpairs(K, M, k, n_snapshots, seed, n_passes=4, Z=None):
     """Randomized snapshot eigen-approximation (spectral.py:103-158).
 
     Deflated shift-invert block iteration on uniform(-1,1) forcings drawn from
-    ``default_rng(seed)``, enrichment with the constant (heat kernel
-    candidate), SVD orthonormalisation with a 1e-10 rank cut, Rayleigh-Ritz.
+    ``default_rng(seed)``, enrichment with the near-null candidates Z (the
+    constant for heat, the rigid-body modes for elasticity), SVD
+    orthonormalisation with a 1e-10 rank cut, Rayleigh-Ritz.
     """
     if n_snapshots < k:
         raise ValueError("need at least k snapshots")
     A, B = K.matrix, M.matrix
     n = A.shape[0]
     rng = np.random.default_rng(seed)
-    Z = np.ones((n, 1))
+    Z = np.ones((n, 1)) if Z is None else Z
     MZ = B @ Z
     G = Z.T @ MZ
     F = rng.uniform(-1.0, 1.0, size=(n, n_snapshots))
@@ -319,11 +320,11 @@ def randomized_solver(n_max=6, n_snapshots=None, seed=0):
     (schwarz.py:156-160); n_snapshots defaults to n_max + 5."""
     counter = {"k": 0}
 
-    def solve(K, M, kk):
+    def solve(K, M, kk, Z=None):
         centre = counter["k"]
         counter["k"] += 1
         ns = n_snapshots or (n_max + 5)
-        return randomized_eigenpairs(K, M, kk, min(ns, K.n_free), [seed, centre])
+        return randomized_eigenpairs(K, M, kk, min(ns, K.n_free), [seed, centre], Z=Z)
 
     return solve
 
@@ -432,6 +433,73 @@ def heat_rot_coarse_space(op, mesh, part, E, dirichlet_nodes, n_max=6, threshold
     if enrich:
         R0 = sp.vstack([R0, rot.csr()]).tocsr()
     return CoarseSpace(R0, modes, lams, vecs, t_eig)
+
+
+def local_elasticity_problem(mesh, E, nu, rect, dirichlet_nodes):
+    """Neumann elasticity pencil on omega (spectral.py:63-90, kind 'elasticity'):
+    K restricted to the patch elements with whole-node Dirichlet where the
+    patch meets clamped nodes, M the E-weighted block-diagonal Q1 mass
+    (assembly.py:236-259), both on the free patch dofs."""
+    ex0, ex1, ey0, ey1 = rect
+    pmesh = Mesh(ex1 - ex0, ey1 - ey0, mesh.h)
+    Eloc = np.asarray(E).reshape(mesh.ny, mesh.nx)[ey0:ey1, ex0:ex1].ravel()
+    gids = rect_nodes(mesh, ex0, ex1, ey0, ey1)
+    local_dir = np.nonzero(np.isin(gids, np.asarray(dirichlet_nodes, dtype=np.int64)))[0]
+    K = elasticity_operator(pmesh, Eloc, nu, whole_node_dofs(pmesh, local_dir))
+    me = mass_element(mesh.h)
+    blk = np.zeros((8, 8))
+    blk[:4, :4] = me
+    blk[4:, 4:] = me
+    M = _assemble_free(pmesh.quad_dofs(), Eloc[:, None, None] * blk[None], pmesh.n_dofs, K.free_dofs)
+    return K, M, pmesh
+
+
+def rigid_body_modes(pmesh, free_dofs):
+    """x/y translations and the rotation about the patch centroid
+    (assembly.py:262-273 with LocalEigProblem.kernel_basis, spectral.py:37-44)."""
+    xy = pmesh.xy()
+    c = xy.mean(axis=0)
+    n = pmesh.n_nodes
+    Z = np.zeros((2 * n, 3))
+    Z[:n, 0] = 1.0
+    Z[n:, 1] = 1.0
+    Z[:n, 2] = -(xy[:, 1] - c[1])
+    Z[n:, 2] = xy[:, 0] - c[0]
+    return Z[free_dofs]
+
+
+def elasticity_coarse_space(op, mesh, part, E, nu, dirichlet_nodes, n_max=6, eig_solver=None):
+    """EE / EE;Rand coarse space: per centre the min(n_max, k) lowest
+    elasticity eigenvectors (rule 'fixed', schwarz.py:148-173), each giving one
+    vector-valued basis row chi * psi (coarse.py:76-91)."""
+    eig_solver = eig_solver or lowest_eigenpairs
+    fidx = op.free_index()
+    pou_ids, pou_vals = pou_values(part)
+    chi_full = np.zeros(mesh.n_nodes)
+    rows = _Rows(op.n_free)
+    modes, lams, vecs = [], [], []
+    t_eig = 0.0
+    for k, rect in enumerate(part.omegas):
+        t0 = time.perf_counter()
+        K, M, pmesh = local_elasticity_problem(mesh, E, nu, rect, dirichlet_nodes)
+        kk = min(n_max + 1, K.n_free)
+        lam, V = eig_solver(K, M, kk, Z=rigid_body_modes(pmesh, K.free_dofs))
+        n = min(n_max, lam.size)
+        t_eig += time.perf_counter() - t0
+        modes.append(n)
+        lams.append(lam)
+        vecs.append(V[:, :n])
+        gn = rect_nodes(mesh, *rect)
+        chi_full[:] = 0.0
+        chi_full[pou_ids[k]] = pou_vals[k]
+        chi = chi_full[gn]
+        fx, fy = fidx[gn], fidx[gn + mesh.n_nodes]
+        npn = pmesh.n_nodes
+        for m in range(n):
+            psi = np.zeros(2 * npn)
+            psi[K.free_dofs] = V[:, m]
+            rows.push(fx, fy, chi * psi[:npn], chi * psi[npn:])
+    return CoarseSpace(rows.csr(), modes, lams, vecs, t_eig)
 
 
 class CoarseSolver:
@@ -665,7 +733,7 @@ def problem_from_spec(spec):
 
 
 def build_two_level(prob, H, delta=None, n_max=6, threshold=50.0, enrich=True, rule="gap",
-                    level1_mode="blocks", eig_solver=None, level1_op="elasticity"):
+                    level1_mode="blocks", eig_solver=None, level1_op="elasticity", eig_kind="heat"):
     """EH(+Rot) preconditioner; level1_op='heat' gives HH(+Rot).
 
     level1_mode='neighborhoods': reference semantics (subdomains = omega_j,
@@ -685,12 +753,17 @@ def build_two_level(prob, H, delta=None, n_max=6, threshold=50.0, enrich=True, r
         l1 = level1_solvers(prob.op, mesh, rects, keep)
     t_l1 = time.perf_counter() - t0
     t0 = time.perf_counter()
-    cs = heat_rot_coarse_space(prob.op, mesh, part, prob.E, prob.heat_dirichlet_nodes, n_max,
-                               threshold, enrich, rule, eig_solver)
+    if eig_kind == "elasticity":
+        cs = elasticity_coarse_space(prob.op, mesh, part, prob.E, prob.nu, prob.heat_dirichlet_nodes, n_max,
+                                     eig_solver)
+    else:
+        cs = heat_rot_coarse_space(prob.op, mesh, part, prob.E, prob.heat_dirichlet_nodes, n_max,
+                                   threshold, enrich, rule, eig_solver)
     coarse = CoarseSolver(prob.op, cs.R0)
     t_c = time.perf_counter() - t0
     info = {"t_level1": t_l1, "t_coarse": t_c, "t_eig": cs.t_eig, "coarse_dim": cs.N_c,
-            "mode_counts": cs.modes, "basis_kind": "H+Rot" if enrich else "H", "selection_rule": rule}
+            "mode_counts": cs.modes, "basis_kind": "E" if eig_kind == "elasticity" else ("H+Rot" if enrich else "H"),
+            "selection_rule": "fixed" if eig_kind == "elasticity" else rule}
     P = TwoLevel(l1, coarse, prob.op.n_free, info)
     P.coarse_space = cs
     P.partition = part

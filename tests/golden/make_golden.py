@@ -132,6 +132,35 @@ def bench100_hh(eta, tag):
     print(tag, eta, rep.iterations, res["coarse_dim"])
 
 
+def bench100_ee(eta, tag):
+    """EE / EE;Rand on the reference's benchmark cell (elasticity eigenproblems, rule 'fixed')."""
+    cfg = cli.BenchmarkConfig(tol=1e-8)
+    res = cli.run_single(cfg, eta, tag)
+    op, rep = res["operator"], res["report"]
+    mesh = grid.build_fine_mesh(100, 100)
+    part = grid.build_coarse_partition(mesh, 10, 10)
+    coeff = coefficients.generate_coefficient(cfg.layout, mesh, eta, nu=cfg.nu)
+    dirichlet = mesh.boundary_nodes()
+    lams = []
+    for center, patch in enumerate(part.neighborhoods):
+        prob = spectral.build_local_eigproblem(mesh, coeff, patch, "elasticity", dirichlet)
+        k = min(7, prob.dim)
+        if tag.endswith(";Rand"):
+            sel = spectral.solve_local_eig_randomized(prob, k, n_snapshots=min(11, prob.dim), seed=[0, center])
+        else:
+            sel = spectral.solve_local_eig_dense(prob, k)
+        lams.append(sel.eigenvalues)
+    pre = schwarz.build_preconditioner(tag, op, mesh, part, coeff, dirichlet)
+    rng = np.random.default_rng(7)
+    r = rng.standard_normal(op.n_free)
+    save(f"ref_bench100_{tag.replace(';', '_').lower()}_eta{eta:g}.npz", E=coeff.values,
+         dirichlet_nodes=dirichlet, free_dofs=op.free_dofs, b=res["rhs"], iters=rep.iterations,
+         x=res["solution"], residuals=np.array(rep.residuals), coarse_dim=res["coarse_dim"],
+         mode_counts=np.array(pre.info["mode_counts"]), eigenvalues=np.array(lams),
+         apply_r=r, apply_z=pre.apply(r), cond=rep.cond_estimate)
+    print(tag, eta, rep.iterations, res["coarse_dim"])
+
+
 def topopt_cases():
     """SIMP caller (topopt.py, assembly.py:280-336): filter, sensitivity, OC
     update and short optimize runs of the unmodified reference."""
@@ -266,7 +295,7 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000, tag="EH+Rot"):
 
 
 def main():
-    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand", "hh", "topopt"}
+    which = set(sys.argv[1:]) or {"elements", "bench", "cfg1", "mbb", "cfg3s", "cfg2s", "rand", "hh", "topopt", "ee"}
     if "elements" in which:
         elements()
     if "bench" in which:
@@ -280,6 +309,10 @@ def main():
         bench100_hh(1e6, "HH+Rot")
         bench100_hh(1e6, "HH")
         adapter_case(configs.config1(seed=0), "ref_config1_hhrot.npz", tag="HH+Rot")
+    if "ee" in which:
+        for tag in ("EE", "EE;Rand"):
+            bench100_ee(1.0, tag)
+            bench100_ee(1e6, tag)
     if "topopt" in which:
         topopt_cases()
     if "cfg1" in which:

@@ -179,3 +179,24 @@ def test_optimize_loop_matches_reference(name, variant):
     assert [r["inner_iterations"] for r in log] == list(g["inner"])
     assert np.allclose([r["g0"] for r in log], g["g0"], rtol=1e-10, atol=0)
     assert np.allclose(rho, g["rho"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["ee_eta1", "ee_eta1e+06", "ee_rand_eta1", "ee_rand_eta1e+06"])
+def test_elasticity_eigen_variants_match_reference(name):
+    """EE / EE;Rand (row f4): elasticity eigenproblems, rule 'fixed'."""
+    g = load_golden(f"ref_bench100_{name}.npz")
+    mesh = O.mesh_for(100, 100)
+    op = O.elasticity_operator(mesh, g["E"], 0.3, O.whole_node_dofs(mesh, g["dirichlet_nodes"]))
+    prob = O.OracleProblem(mesh, op, g["E"], 0.3, g["b"], g["dirichlet_nodes"])
+    eig = O.randomized_solver() if "rand" in name else None
+    P = O.build_two_level(prob, H=10, level1_mode="neighborhoods", eig_kind="elasticity", eig_solver=eig)
+    assert P.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(P.info["mode_counts"]), g["mode_counts"])
+    lam = np.array(P.coarse_space.eigenvalues)
+    scale = np.abs(g["eigenvalues"]).max()
+    assert np.allclose(lam, g["eigenvalues"], rtol=1e-9, atol=1e-12 * scale)
+    z = P.apply(g["apply_r"])
+    assert np.linalg.norm(z - g["apply_z"]) <= 1e-11 * np.linalg.norm(g["apply_z"])
+    x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=2000)
+    assert rep.iterations == int(g["iters"])
+    assert np.linalg.norm(x - g["x"]) <= 1e-9 * np.linalg.norm(g["x"])
