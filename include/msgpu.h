@@ -58,6 +58,12 @@ enum {
   MS_L1_HEAT = 1        /* HH, HH+Rot: one scalar diffusion factor for both blocks (:112-140)    */
 };
 
+/* coarse-space eigenproblem kind (PreconditionerVariant.eig_kind, schwarz.py:24-41) */
+enum {
+  MS_EIG_HEAT = 0,       /* EH*, HH*: scalar diffusion pencil, gap rule, 2 rows per mode (+ rotation) */
+  MS_EIG_ELASTICITY = 1  /* EE, EE;Rand: elasticity pencil, rule 'fixed', 1 vector row per mode      */
+};
+
 /* level-1 local solver */
 enum {
   MS_LOCAL_BANDED = 0,  /* banded Cholesky factor, forward/backward sweeps per apply */
@@ -77,14 +83,15 @@ typedef struct ms_precond_opts {
   int use_coarse;        /* 1 (default); 0 drops level 2 (diagnostics)                  */
   const int64_t* heat_dirichlet_nodes; /* whole nodes clamped in the heat eigenproblems */
   int64_t n_heat_dirichlet;
-  /* EH+Rot;Rand (solve_local_eig_randomized, spectral.py:103-158): forcings
-   * [n_centers][n_snapshots][(2H+1)^2] (closed-neighbourhood nodes, row-major,
-   * zero at clamped nodes) drawn by the caller from default_rng([seed, centre]) */
+  /* EH+Rot;Rand / EE;Rand (solve_local_eig_randomized, spectral.py:103-158):
+   * forcings [n_centers][n_snapshots][d (2H+1)^2] (closed-neighbourhood nodes,
+   * row-major; d = 2 for MS_EIG_ELASTICITY: x-plane then y-plane; zero at
+   * clamped nodes) drawn by the caller from default_rng([seed, centre]) */
   int randomized;
   int n_snapshots;
   const double* snapshots;
   int level1_operator;   /* MS_L1_* (needs whole-node constraints for MS_L1_HEAT)       */
-  int reserved;          /* 0                                                           */
+  int eig_kind;          /* MS_EIG_*: neighbourhood eigenproblem kind                   */
 } ms_precond_opts;
 
 /* Build metadata, the `info` dict of schwarz.py:202-210 plus eigensolver stats. */

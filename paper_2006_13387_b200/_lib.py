@@ -20,6 +20,7 @@ MS_OK, MS_E_INVALID, MS_E_NOT_SPD, MS_E_CUDA, MS_E_NOMEM, MS_E_STATE = 0, -1, -2
 MS_LEVEL1_NEIGHBORHOODS, MS_LEVEL1_BLOCKS = 0, 1
 MS_LOCAL_BANDED, MS_LOCAL_DENSE_INV = 0, 1
 MS_L1_ELASTICITY, MS_L1_HEAT = 0, 1
+MS_EIG_HEAT, MS_EIG_ELASTICITY = 0, 1
 
 # every symbol include/msgpu.h declares
 EXPORTS = (
@@ -53,7 +54,7 @@ class PrecondOpts(C.Structure):
         ("fixed_rule", C.c_int), ("local_solver", C.c_int), ("use_coarse", C.c_int),
         ("heat_dirichlet_nodes", C.POINTER(C.c_int64)), ("n_heat_dirichlet", C.c_int64),
         ("randomized", C.c_int), ("n_snapshots", C.c_int), ("snapshots", C.c_void_p),
-        ("level1_operator", C.c_int), ("reserved", C.c_int),
+        ("level1_operator", C.c_int), ("eig_kind", C.c_int),
     ]
 
 

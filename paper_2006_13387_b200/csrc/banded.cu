@@ -138,9 +138,13 @@ void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cuda
 // Banded Cholesky, one CTA per system.  A sliding window of the next bw+1
 // columns lives in shared memory (column c in slot c % S); each step k folds
 // column k into the window with a rank-1 update a_j1 a_j2 / d and retires it.
+// ldl = 1: square-root-free L D L^T (pivots may be negative, e.g. round-off
+// level pivots of shifted singular pencils); stored so that the same sweeps
+// apply it: Lc holds the Schur column a_{k+j,k} with 1/d_k on the diagonal
+// (forward sweep -> D^-1 L^-1 b), Lr the unit factor l_{k+j,k} with 1.
 __global__ void __launch_bounds__(256)
     k_band_potrf(const BandSys* __restrict__ sys, double* __restrict__ Lc,
-                 double* __restrict__ Lr, int* fail) {
+                 double* __restrict__ Lr, int* fail, int ldl) {
   extern __shared__ double smem[];
   const BandSys s = sys[blockIdx.x];
   const int bw = s.bw, S = bw + 1, n = s.n;
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(256)
   for (int k = 0; k < n; ++k) {
     const int sk = k % S;
     double d = W[sk * S];
-    if (!(d > 0.0)) {
+    if (ldl ? !(d != 0.0 && isfinite(d)) : !(d > 0.0)) {
       bad = true;
       d = 1.0;
     }
@@ -174,11 +178,17 @@ __global__ void __launch_bounds__(256)
       W[((k + j2) % S) * S + (j1 - j2)] -= W[sk * S + j1] * W[sk * S + j2] * invd;
     }
     __syncthreads();
-    const double lkk = sqrt(d), inv = 1.0 / lkk;
+    const double lkk = ldl ? 1.0 : sqrt(d), inv = 1.0 / lkk;
     for (int j = threadIdx.x; j < S; j += blockDim.x) {
-      const double v = (j == 0) ? inv : W[sk * S + j] * inv;
-      colc[(int64_t)k * S + j] = v;
-      if (k + j < n) colr[(int64_t)(k + j) * S + j] = v;
+      double vc, vr;
+      if (ldl) {
+        vc = (j == 0) ? invd : W[sk * S + j];
+        vr = (j == 0) ? 1.0 : W[sk * S + j] * invd;
+      } else {
+        vc = vr = (j == 0) ? inv : W[sk * S + j] * inv;
+      }
+      colc[(int64_t)k * S + j] = vc;
+      if (k + j < n) colr[(int64_t)(k + j) * S + j] = vr;
       const int cn = k + S;  // next column into the freed slot
       W[sk * S + j] = (cn < n) ? colc[(int64_t)cn * S + j] : 0.0;
     }
@@ -188,13 +198,13 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, double* Lr, int* fail,
-                       cudaStream_t st) {
+                       cudaStream_t st, int ldl) {
   if (nsys == 0) return;
   const int S = max_bw + 1;
   const size_t smem = (size_t)S * S * sizeof(double) + (size_t)(max_bw * (max_bw + 1) / 2 + 1) * 4;
   if (smem > 220 * 1024) throw Error(-1, "band too wide for the shared-memory Cholesky window");
   MS_CUDA(cudaFuncSetAttribute(k_band_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_band_potrf<<<nsys, 256, smem, st>>>(sys, Lc, Lr, fail);
+  k_band_potrf<<<nsys, 256, smem, st>>>(sys, Lc, Lr, fail, ldl);
   MS_CUDA(cudaGetLastError());
 }
 

@@ -60,7 +60,7 @@ void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cuda
 // entry, L on exit (diag slot = 1/L_kk); Lr receives the row band.
 // *fail gets (system index + 1) of a non-positive pivot, else stays 0.
 void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, double* Lr,
-                       int* fail, cudaStream_t st);
+                       int* fail, cudaStream_t st, int ldl = 0);
 
 // y_s = K_s^{-1} (R_s r) for every system, warp per system.  r is a full
 // layout vector; the local solutions land in ybuf[yoff ...], node-interleaved

@@ -107,6 +107,29 @@ void unit_elasticity(double nu, double K[64]) {
     for (int j = 0; j < 8; ++j) K[i * 8 + j] = 0.5 * (A[i][j] + A[j][i]);
 }
 
+// largest eigenvalue of a symmetric PSD 8x8 matrix (power iteration)
+double max_eig_sym8(const double* A) {
+  double x[8], y[8], lam = 0.0;
+  for (int i = 0; i < 8; ++i) x[i] = 1.0 + 0.1 * i;
+  for (int it = 0; it < 500; ++it) {
+    double nrm = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      y[i] = 0.0;
+      for (int j = 0; j < 8; ++j) y[i] += A[i * 8 + j] * x[j];
+      nrm += y[i] * y[i];
+    }
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) return 0.0;
+    lam = 0.0;
+    for (int i = 0; i < 8; ++i) lam += x[i] * y[i];
+    double xn = 0.0;
+    for (int i = 0; i < 8; ++i) xn += x[i] * x[i];
+    lam /= xn;
+    for (int i = 0; i < 8; ++i) x[i] = y[i] / nrm;
+  }
+  return lam;
+}
+
 void heat_elements(double h, HeatParam& hp) {
   const double g[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
   double A[4][4] = {};
@@ -735,6 +758,12 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
   if (o->level1_operator != MS_L1_ELASTICITY && o->level1_operator != MS_L1_HEAT)
     throw Error(MS_E_INVALID, "unknown level-1 operator");
   const bool heat_l1 = o->level1_operator == MS_L1_HEAT;
+  if (o->eig_kind != MS_EIG_HEAT && o->eig_kind != MS_EIG_ELASTICITY)
+    throw Error(MS_E_INVALID, "unknown eigenproblem kind");
+  const bool el = o->eig_kind == MS_EIG_ELASTICITY;
+  if (el && o->enrich)
+    throw Error(MS_E_INVALID, "rotation enrichment applies to heat bases, not the elasticity basis 'E'");
+  const int nd = el ? 2 : 1;  // unknowns per node of the neighbourhood eigenproblems
   if (heat_l1 && o->local_solver != MS_LOCAL_BANDED)
     throw Error(MS_E_INVALID, "the heat level-1 uses the banded local solver");
   const int W = P->ctx->world(), R = P->ctx->rank();
@@ -900,6 +929,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     cd.NLy = 2 * cd.mey + 1;
     cd.n_centers = (o->Nx - 1) * (o->Ny - 1);
     cd.enrich = o->enrich ? 1 : 0;
+    cd.vec = el ? 1 : 0;
     cd.h = g.h;
     const int nc = cd.n_centers;
     const int NL = cd.NLx * cd.NLy;
@@ -915,15 +945,21 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     hdir.upload(hd.data(), hd.size(), st);
     HeatParam hp{};
     heat_elements(g.h, hp);
-    // shift: relative 1e-12 of the pencil's spectral bound 24/h^2
-    const double sigma = 1e-12 * 24.0 / (g.h * g.h);
+    ElastParam ep{};
+    for (int i = 0; i < 64; ++i) ep.ke[i] = P->ke.k[i];
+    for (int i = 0; i < 16; ++i) ep.mel[i] = hp.mel[i];
+    // shift: relative 1e-12 of the pencil's spectral bound:
+    // heat 24/h^2; elasticity lambda_max(k0) / lambda_min(m_e) = lambda_max(k0) 36/h^2
+    const double bound = el ? max_eig_sym8(P->ke.k) * 36.0 / (g.h * g.h) : 24.0 / (g.h * g.h);
+    const double sigma = 1e-12 * bound;
+    const int NLd = nd * NL;  // values per eigenvector
     pc->evals.alloc((size_t)nc * kNeig);
     DBuf<int> passes, neumann;
     passes.alloc(nc);
     neumann.alloc(nc);
     pc->nsel.alloc(nc);
     pc->psioff.alloc(nc);
-    pc->psi.alloc((size_t)nc * o->n_max * NL);
+    pc->psi.alloc((size_t)nc * o->n_max * NLd);
     std::vector<int64_t> h_psioff(nc, 0);
     pc->h_nsel.assign(nc, 0);
     // owned centre rows: [max(J0,1), min(J1, Ny)) (centre row J sits on block row J)
@@ -940,7 +976,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     DBuf<double> psi_local_buf;
     double* psi_local = pc->psi.p;
     if (W > 1) {
-      psi_local_buf.alloc((size_t)std::max(pc->kc1 - pc->kc0, 1) * o->n_max * NL);
+      psi_local_buf.alloc((size_t)std::max(pc->kc1 - pc->kc0, 1) * o->n_max * NLd);
       psi_local = psi_local_buf.p;
     }
     DBuf<int64_t> psioff_local;
@@ -956,7 +992,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
         const int k = k0 + kb;
         const int I = k % (o->Nx - 1) + 1, J = k / (o->Nx - 1) + 1;
         BandSys s{};
-        band_setup(s, (I - 1) * cd.mex, (I + 1) * cd.mex, (J - 1) * cd.mey, (J + 1) * cd.mey, 1);
+        band_setup(s, (I - 1) * cd.mex, (I + 1) * cd.mex, (J - 1) * cd.mey, (J + 1) * cd.mey, nd);
         s.foff = foff;
         foff += (int64_t)s.n * (s.bw + 1);
         mbw = std::max(mbw, s.bw);
@@ -965,8 +1001,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       if (!hLc.p || hLc.n < (size_t)foff) {
         hLc.alloc(foff);
         hLr.alloc(foff);
-        work.alloc((size_t)nk * 2 * kEigBlock * NL);
-        evecs.alloc((size_t)nk * kNeig * NL);
+        work.alloc((size_t)nk * (2 * kEigBlock + (el ? 6 : 0)) * NLd);
+        evecs.alloc((size_t)nk * kNeig * NLd);
       }
       hsysd.upload(hs.data(), nk, st);
       MS_CUDA(cudaMemsetAsync(hLr.p, 0, foff * sizeof(double), st));
@@ -974,34 +1010,48 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       if (o->randomized) {
         // the reference's shift (spectral.py:133) and this batch's forcings
         if (rsig.n < (size_t)nk) rsig.alloc(nk);
-        launch_rand_sigma(g, P->E.p, hdir.p, hp, hsysd.p, nk, rsig.p, st);
-        const size_t fcount = (size_t)nk * o->n_snapshots * NL;
+        if (el)
+          launch_rand_sigma_el(g, P->E.p, hdir.p, ep, hsysd.p, nk, rsig.p, st);
+        else
+          launch_rand_sigma(g, P->E.p, hdir.p, hp, hsysd.p, nk, rsig.p, st);
+        const size_t fcount = (size_t)nk * o->n_snapshots * NLd;
         if (rF.n < fcount) rF.alloc(fcount);
-        MS_CUDA(cudaMemcpyAsync(rF.p, o->snapshots + (size_t)k0 * o->n_snapshots * NL, fcount * sizeof(double),
+        MS_CUDA(cudaMemcpyAsync(rF.p, o->snapshots + (size_t)k0 * o->n_snapshots * NLd, fcount * sizeof(double),
                                 cudaMemcpyDefault, st));
       }
-      launch_heat_assemble(g, P->E.p, hdir.p, hp, sigma, hsysd.p, nk, hLc.p, st,
-                           o->randomized ? rsig.p : nullptr);
-      launch_band_potrf(hsysd.p, nk, mbw, hLc.p, hLr.p, fail.p, st);
-      check_fail(fail, st, "neighbourhood heat pencil (K + sigma M)");
+      if (el)
+        launch_el_assemble(g, P->E.p, hdir.p, ep, sigma, hsysd.p, nk, hLc.p, st, o->randomized ? rsig.p : nullptr);
+      else
+        launch_heat_assemble(g, P->E.p, hdir.p, hp, sigma, hsysd.p, nk, hLc.p, st,
+                             o->randomized ? rsig.p : nullptr);
+      // elasticity pencils: LDL^T (the shifted rigid-body kernel leaves round-off level pivots)
+      launch_band_potrf(hsysd.p, nk, mbw, hLc.p, hLr.p, fail.p, st, el ? 1 : 0);
+      check_fail(fail, st, el ? "neighbourhood elasticity pencil (K + sigma M)" : "neighbourhood heat pencil (K + sigma M)");
+      const int fixed = el ? 1 : o->fixed_rule;
       EigBatch eb{o->Nx, cd.mex, cd.mey, k0, nk, hsysd.p, hLc.p, hLr.p, work.p, pc->evals.p,
-                  evecs.p, passes.p, neumann.p, o->n_max, o->gap_threshold, o->fixed_rule,
-                  1e-15 * 24.0 / (g.h * g.h)};
-      if (o->randomized)
+                  evecs.p, passes.p, neumann.p, o->n_max, o->gap_threshold, fixed, 1e-15 * bound};
+      if (el && o->randomized)
+        launch_randomized_el(g, P->E.p, hdir.p, ep, eb, mbw, rF.p, o->n_snapshots, st);
+      else if (el)
+        launch_subspace_el(g, P->E.p, hdir.p, ep, eb, mbw, 300, 1e-12, st);
+      else if (o->randomized)
         launch_randomized(g, P->E.p, hdir.p, hp, eb, rF.p, o->n_snapshots, st);
       else
         launch_subspace(g, P->E.p, hdir.p, hp, eb, 300, 1e-12, st);
-      launch_select(nc, pc->evals.p, o->n_max, o->gap_threshold, o->fixed_rule, pc->nsel.p, st);
+      launch_select(nc, pc->evals.p, o->n_max, o->gap_threshold, fixed, pc->nsel.p, st);
       std::vector<int> bsel(nk);
       MS_CUDA(cudaMemcpyAsync(bsel.data(), pc->nsel.p + k0, nk * sizeof(int), cudaMemcpyDeviceToHost, st));
       MS_CUDA(cudaStreamSynchronize(st));
       for (int kb = 0; kb < nk; ++kb) {
         h_psioff_local[k0 + kb] = psi_cursor;
-        psi_cursor += (int64_t)bsel[kb] * NL;
+        psi_cursor += (int64_t)bsel[kb] * NLd;
         pc->h_nsel[k0 + kb] = bsel[kb];
       }
       psioff_local.upload(h_psioff_local.data(), nc, st);
-      launch_compact_psi(eb, cd.NLx, pc->nsel.p, psioff_local.p, psi_local, st);
+      if (el)
+        launch_compact_psi_el(eb, cd.NLx, pc->nsel.p, psioff_local.p, psi_local, st);
+      else
+        launch_compact_psi(eb, cd.NLx, pc->nsel.p, psioff_local.p, psi_local, st);
     }
     if (W > 1) {
       // every owner's eigenvalues, mode counts and passes to every rank
@@ -1023,13 +1073,13 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     psi_cursor = 0;
     for (int k = 0; k < nc; ++k) {
       h_psioff[k] = psi_cursor;
-      psi_cursor += (int64_t)pc->h_nsel[k] * NL;
+      psi_cursor += (int64_t)pc->h_nsel[k] * NLd;
     }
     pc->psioff.upload(h_psioff.data(), nc, st);
     if (W > 1) {
       Comm* cm = P->ctx->comm.get();
       if (pc->kc1 > pc->kc0) {
-        const int64_t n_own = h_psioff[pc->kc1 - 1] + (int64_t)pc->h_nsel[pc->kc1 - 1] * NL - h_psioff[pc->kc0];
+        const int64_t n_own = h_psioff[pc->kc1 - 1] + (int64_t)pc->h_nsel[pc->kc1 - 1] * NLd - h_psioff[pc->kc0];
         MS_CUDA(cudaMemcpyAsync(pc->psi.p + h_psioff[pc->kc0], psi_local, n_own * sizeof(double),
                                 cudaMemcpyDeviceToDevice, st));
       }
@@ -1039,7 +1089,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
         const int qk0 = (std::max(a, 1) - 1) * (o->Nx - 1);
         const int qk1 = std::max(qk0, (std::min(b, o->Ny) - 1) * (o->Nx - 1));
         if (qk1 <= qk0) continue;
-        const int64_t o0 = h_psioff[qk0], o1 = h_psioff[qk1 - 1] + (int64_t)pc->h_nsel[qk1 - 1] * NL;
+        const int64_t o0 = h_psioff[qk0], o1 = h_psioff[qk1 - 1] + (int64_t)pc->h_nsel[qk1 - 1] * NLd;
         cm->broadcast(pc->psi.p + o0, (size_t)(o1 - o0) * sizeof(double), q, st);
       }
     }
@@ -1058,7 +1108,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     int acc = 0;
     for (int k = 0; k < nc; ++k) {
       h_hoff[k] = acc;
-      acc += 2 * pc->h_nsel[k];
+      acc += (el ? 1 : 2) * pc->h_nsel[k];
     }
     cd.roff = acc;
     pc->N_c = acc + (cd.enrich ? nc : 0);

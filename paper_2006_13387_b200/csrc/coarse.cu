@@ -66,12 +66,14 @@ void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStrea
 }
 
 // value of basis row `bi` of centre k at global node (a, b), component c.
-// bi < 2*nsel: heat mode bi/2 in slot bi%2; bi == 2*nsel: rotation.
+// heat: bi < 2*nsel: mode bi/2 in slot bi%2; bi == 2*nsel: rotation.
+// vec (EE): mode bi, component c of chi * psi (coarse.py:76-91).
 __device__ __forceinline__ double basis_value(const CoarseDev& cd, int k, int I, int J, int bi,
                                               int nsel, int a, int b, int c) {
   const int NL = cd.NLx * cd.NLy;
   const int ln = local_node(cd, I, J, a, b);
   const double chi = cd.chi[(int64_t)k * NL + ln];
+  if (cd.vec) return __dmul_rn(chi, cd.psi[cd.psioff[k] + ((int64_t)bi * 2 + c) * NL + ln]);
   if (bi < 2 * nsel) {
     if ((bi & 1) != c) return 0.0;
     return __dmul_rn(chi, cd.psi[cd.psioff[k] + (int64_t)(bi >> 1) * NL + ln]);
@@ -82,7 +84,11 @@ __device__ __forceinline__ double basis_value(const CoarseDev& cd, int k, int I,
 }
 
 __device__ __forceinline__ int basis_row(const CoarseDev& cd, int k, int bi, int nsel) {
-  return bi < 2 * nsel ? cd.hoff[k] + bi : cd.roff + k;
+  return (cd.vec || bi < 2 * nsel) ? cd.hoff[k] + bi : cd.roff + k;
+}
+
+__device__ __forceinline__ int basis_count(const CoarseDev& cd, int nsel) {
+  return cd.vec ? nsel : 2 * nsel + cd.enrich;
 }
 
 // ---------------------------------------------------------------------------
@@ -216,7 +222,7 @@ void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double
 // r -= alpha q and the ||r||^2 grid reduction / convergence test.
 constexpr int kCellThreads = 256;
 
-template <bool UPD>
+template <bool UPD, bool VEC>
 __global__ void __launch_bounds__(kCellThreads)
     k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, int J0, double* __restrict__ x,
                     const double* __restrict__ p, double* __restrict__ r,
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kCellThreads)
       r[n + nn] = ry;
       acc[12] += rx * rx + ry * ry;
     }
-    if (has_coarse) {
+    if (!VEC && has_coarse) {
       const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n;
       const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n;
       const double2 c4a = __ldg(c2), c4b = __ldg(c2 + 1), p4a = __ldg(p2), p4b = __ldg(p2 + 1);
@@ -288,13 +294,53 @@ __global__ void __launch_bounds__(kCellThreads)
     for (int w2 = 0; w2 < kCellThreads / 32; ++w2) s += sred[threadIdx.x * (kCellThreads / 32) + w2];
     if (threadIdx.x == 12) {
       rrblk = s;
-    } else if (has_coarse) {
+    } else if (!VEC && has_coarse) {
       const int c = threadIdx.x / 3, v = threadIdx.x % 3;
       rp[c * kSlots + (v == 2 ? 2 * kMaxModes : v)] = s;
     }
   }
+  // vec basis: all modes in one pass, <= 4 corners x kMaxModes rows
+  if constexpr (VEC) {
+    __syncthreads();  // r of this cell is final
+    const int NL = cd.NLx * cd.NLy;
+    double va[4 * kMaxModes];
+#pragma unroll
+    for (int v = 0; v < 4 * kMaxModes; ++v) va[v] = 0.0;
+    const double* psk[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int I = ci + (c & 1), J = cj + (c >> 1);
+      psk[c] = cok[c] ? cd.psi + __ldg(cd.psioff + (J - 1) * (Nx - 1) + (I - 1)) : cd.psi;
+    }
+    for (int t = threadIdx.x; t < w * hgt; t += kCellThreads) {
+      const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
+      const int64_t n = (int64_t)b * g.nnx + a;
+      const double rx = r[n], ry = r[n + nn];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!cok[c]) continue;
+        const int I = ci + (c & 1), J = cj + (c >> 1);
+        const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
+        const double ch = cd.chi4[n * 4 + c];
+#pragma unroll
+        for (int m = 0; m < kMaxModes; ++m)
+          if (m < cns[c]) {
+            const double* pm = psk[c] + (int64_t)m * 2 * NL + ln;
+            va[c * kMaxModes + m] += __dmul_rn(ch, __ldg(pm)) * rx + __dmul_rn(ch, __ldg(pm + NL)) * ry;
+          }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 4 * kMaxModes; ++v) {
+      const int c = v / kMaxModes, m = v % kMaxModes;
+      if (m < cns[c]) {  // CTA-uniform
+        const double tv = block_sum(va[v], sred);
+        if (threadIdx.x == 0) rp[c * kSlots + m] = tv;
+      }
+    }
+  }
   // extra modes (rare): second pass over the cell for corners with nsel > 1
-  if (has_coarse && (cns[0] > 1 || cns[1] > 1 || cns[2] > 1 || cns[3] > 1)) {
+  if (!VEC && has_coarse && (cns[0] > 1 || cns[1] > 1 || cns[2] > 1 || cns[3] > 1)) {
     __syncthreads();  // r of this cell is final
     const int NL = cd.NLx * cd.NLy;
     for (int c = 0; c < 4; ++c) {
@@ -336,15 +382,23 @@ __global__ void __launch_bounds__(kCellThreads)
 void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const double* p, double* r,
                             const double* q, const CoarseDev& cd, PcgScalars* sc,
                             double* partials, double* res_hist, cudaStream_t st) {
-  k_cell_restrict<true><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc,
-                                                                       partials, res_hist, nullptr);
+  if (cd.vec)
+    k_cell_restrict<true, true><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc,
+                                                                             partials, res_hist, nullptr);
+  else
+    k_cell_restrict<true, false><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc,
+                                                                              partials, res_hist, nullptr);
   MS_CUDA(cudaGetLastError());
 }
 
 void launch_restrict_cells(const Grid& g, int J0, int J1, const CoarseDev& cd, const double* r,
                            const int* done, cudaStream_t st) {
-  k_cell_restrict<false><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(
-      g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+  if (cd.vec)
+    k_cell_restrict<false, true><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(
+        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+  else
+    k_cell_restrict<false, false><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(
+        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -357,8 +411,8 @@ __global__ void k_restrict_reduce(CoarseDev cd, double* __restrict__ f0, const i
   const int k = k_begin + t / kSlots, slot = t % kSlots;
   if (k >= k_end) return;
   const int nsel = cd.nsel[k];
-  const bool rot = slot == 2 * kMaxModes;
-  if (!(slot < 2 * nsel || (rot && cd.enrich))) return;
+  const bool rot = !cd.vec && slot == 2 * kMaxModes;
+  if (!(slot < (cd.vec ? nsel : 2 * nsel) || (rot && cd.enrich))) return;
   const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
   double s = 0.0;
 #pragma unroll
@@ -390,6 +444,7 @@ void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cu
 // coarse part in J-major centre order, then their sum.
 constexpr int kCombineThreads = 256;
 
+template <bool VEC>
 __global__ void __launch_bounds__(kCombineThreads)
     k_combine(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, int has_l1, CoarseDev cd,
               int has_coarse, int Nx, int Ny, int J0, const double* __restrict__ y0,
@@ -421,7 +476,7 @@ __global__ void __launch_bounds__(kCombineThreads)
     const int c = threadIdx.x / (2 * kMaxModes + 1), m = threadIdx.x % (2 * kMaxModes + 1);
     double v = 0.0;
     if (cok[c]) {
-      if (m < 2 * cns[c])
+      if (m < (cd.vec ? cns[c] : 2 * cns[c]))
         v = y0[__ldg(cd.hoff + ck[c]) + m];
       else if (m == 2 * kMaxModes && cd.enrich)
         v = y0[cd.roff + ck[c]];
@@ -458,7 +513,23 @@ __global__ void __launch_bounds__(kCombineThreads)
           zy += v[tj][ti].y;
         }
     }
-    if (has_coarse) {
+    if (VEC && has_coarse) {
+      double cxs = 0.0, cys = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!cok[c]) continue;
+        const int I = ci + (c & 1), J = cj + (c >> 1);
+        const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
+        const double ch = cd.chi4[n * 4 + c];
+        const double* ps = cd.psi + cpo[c] + ln;
+        for (int m = 0; m < cns[c]; ++m) {
+          cxs += __dmul_rn(ch, __ldg(ps + (int64_t)m * 2 * NL)) * cy[c][m];
+          cys += __dmul_rn(ch, __ldg(ps + (int64_t)m * 2 * NL + NL)) * cy[c][m];
+        }
+      }
+      zx += cxs;
+      zy += cys;
+    } else if (!VEC && has_coarse) {
       double cxs = 0.0, cys = 0.0;
       const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n;
       const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n;
@@ -517,8 +588,12 @@ void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const C
   if (l1) l1v = *l1;
   if (cd) cdv = *cd;
   if (J1 < 0) J1 = Ny;
-  k_combine<<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0,
-                                                           Nx, Ny, J0, y0, r, z, sc, partials, beta_hist);
+  if (cd && cd->vec)
+    k_combine<true><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, 1, Nx, Ny, J0,
+                                                                   y0, r, z, sc, partials, beta_hist);
+  else
+    k_combine<false><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0,
+                                                                    Nx, Ny, J0, y0, r, z, sc, partials, beta_hist);
   MS_CUDA(cudaGetLastError());
 }
 
@@ -538,7 +613,7 @@ __global__ void __launch_bounds__(256)
   const int nex = 2 * cd.mex, ney = 2 * cd.mey;
   for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x) {
     const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
-    const int nsel = cd.nsel[k], nb = 2 * nsel + cd.enrich;
+    const int nsel = cd.nsel[k], nb = basis_count(cd, nsel);
     const int ax0 = (I - 1) * cd.mex, by0 = (J - 1) * cd.mey;
     for (int ai = 0; ai < nb; ++ai) {
       for (int ln = threadIdx.x; ln < NL; ln += blockDim.x) {
@@ -581,7 +656,7 @@ __global__ void __launch_bounds__(256)
       for (int J2 = max(1, J - 1); J2 <= min(cd.Ny - 1, J + 1); ++J2)
         for (int I2 = max(1, I - 1); I2 <= min(cd.Nx - 1, I + 1); ++I2) {
           const int k2 = center_index(cd, I2, J2);
-          const int nsel2 = cd.nsel[k2], nb2 = 2 * nsel2 + cd.enrich;
+          const int nsel2 = cd.nsel[k2], nb2 = basis_count(cd, nsel2);
           // overlap of the closed neighbourhoods, in omega_k local coordinates
           const int xa = max(ax0, (I2 - 1) * cd.mex), xb = min(ax0 + nex, (I2 + 1) * cd.mex);
           const int ya = max(by0, (J2 - 1) * cd.mey), yb = min(by0 + ney, (J2 + 1) * cd.mey);

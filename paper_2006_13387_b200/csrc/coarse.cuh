@@ -31,13 +31,15 @@ struct CoarseDev {
   int NLx, NLy;           // closed-omega nodes per axis: 2*mex+1, 2*mey+1
   int n_centers;
   int enrich;
+  int vec;                // 1: elasticity basis (EE): one row per mode, psi has x and y parts
   int N_c;
   int roff;               // first rotation row = 2 * sum(nsel)
   double h;
   const int* nsel;        // per centre
-  const int* hoff;        // per centre: first heat row (2 * prefix sum of nsel)
-  const int64_t* psioff;  // per centre: offset into psi (nsel * NL values)
+  const int* hoff;        // per centre: first row (prefix sum of 2*nsel, or nsel if vec)
+  const int64_t* psioff;  // per centre: offset into psi (nsel * NL values, 2 * nsel * NL if vec)
   const double* psi;      // selected eigenvectors on closed omega, lexicographic
+                          // (vec: per mode the x-part then the y-part)
   const double* chi;      // per centre: partition of unity on closed omega (NL values)
   // node-major tables over the coarse cell containing each node: the 4 corner
   // centres (ci + (c&1), cj + (c>>1)), c = 0..3, J-major; zero where invalid

@@ -151,22 +151,24 @@ __device__ __forceinline__ void block_sum_multi(double (&v)[P + 1], int nv, doub
   __syncthreads();
 }
 
-// multi-RHS banded sweeps in place on W (P columns, column-major, length n)
+// multi-RHS banded sweeps in place on W (P columns, column-major, length n);
+// KJ band offsets per 16-thread group: bw <= 16 KJ
+template <int KJ = kJmax>
 __device__ void band_solve_block(const BandSys& s, const double* __restrict__ Lc,
                                  const double* __restrict__ Lr, double* W, double* win) {
   const int n = s.n, bw = s.bw, S = bw + 1;
   const int c = threadIdx.x & (P - 1), grp = threadIdx.x / P;  // 16 groups
   double* Wc = W + (int64_t)c * n;
-  double lv[kEPD][kJmax], dv[kEPD], rv[kEPD];
+  double lv[kEPD][KJ], dv[kEPD], rv[kEPD];
   // ---------------- forward ----------------
   {
     const double* L = Lc + s.foff;
     for (int t = threadIdx.x; t < min(bw, n) * P; t += blockDim.x)
       win[(t / P) * P + (t % P)] = W[(int64_t)(t % P) * n + t / P];
     __syncthreads();
-    auto load = [&](int k, double(&l)[kJmax], double& d, double& rr) {
+    auto load = [&](int k, double(&l)[KJ], double& d, double& rr) {
 #pragma unroll
-      for (int q = 0; q < kJmax; ++q) {
+      for (int q = 0; q < KJ; ++q) {
         const int j = grp + 1 + 16 * q;
         l[q] = (k < n && j <= bw) ? __ldg(L + (int64_t)k * S + j) : 0.0;
       }
@@ -183,7 +185,7 @@ __device__ void band_solve_block(const BandSys& s, const double* __restrict__ Lc
           const int sk = k % S;
           const double wk = win[sk * P + c] * dv[u];
 #pragma unroll
-          for (int q = 0; q < kJmax; ++q) {
+          for (int q = 0; q < KJ; ++q) {
             const int j = grp + 1 + 16 * q;
             if (j <= bw) {
               const int sl = (sk + j) >= S ? sk + j - S : sk + j;
@@ -207,9 +209,9 @@ __device__ void band_solve_block(const BandSys& s, const double* __restrict__ Lc
       win[(row % S) * P + cc] = W[(int64_t)cc * n + row];
     }
     __syncthreads();
-    auto load = [&](int k, double(&l)[kJmax], double& d, double& rr) {
+    auto load = [&](int k, double(&l)[KJ], double& d, double& rr) {
 #pragma unroll
-      for (int q = 0; q < kJmax; ++q) {
+      for (int q = 0; q < KJ; ++q) {
         const int j = grp + 1 + 16 * q;
         l[q] = (k >= 0 && j <= bw) ? __ldg(L + (int64_t)k * S + j) : 0.0;
       }
@@ -226,7 +228,7 @@ __device__ void band_solve_block(const BandSys& s, const double* __restrict__ Lc
           const int sk = k % S;
           const double yk = win[sk * P + c] * dv[u];
 #pragma unroll
-          for (int q = 0; q < kJmax; ++q) {
+          for (int q = 0; q < KJ; ++q) {
             const int j = grp + 1 + 16 * q;
             if (j <= bw && k - j >= 0) {
               const int sl = (sk - j) < 0 ? sk - j + S : sk - j;
@@ -927,6 +929,743 @@ void launch_compact_psi(const EigBatch& b, int NLx, const int* nsel, const int64
   if (b.nk == 0) return;
   k_compact_psi<<<b.nk, 256, 0, st>>>(b, NLx, nsel, psioff, psi);
   MS_CUDA(cudaGetLastError());
+}
+
+// ===========================================================================
+// Elasticity eigenproblems (EE, EE;Rand).  Same machinery as the heat kind on
+// the two-component pencil: K_E = sum E_e k0 over the neighbourhood's elements
+// (Neumann outside, whole-node Dirichlet at clamped nodes), M_E = sum E_e
+// blockdiag(m_e, m_e) (assembly.py:236-259), unknowns node-interleaved.  On
+// a pure Neumann neighbourhood the three rigid-body modes -- the exact kernel
+// (spectral.py:37-45, assembly.py:262-273) -- are M-orthonormalised, locked
+// and deflated, so the iteration only resolves the remaining kNeig - 3 pairs.
+
+template <int NV>
+__device__ __forceinline__ void block_sum_nv(double (&v)[NV], int nv, double* red, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    if (t < nv) {
+      double x = warp_sum(v[t]);
+      if (lane == 0) red[t * 8 + wid] = x;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kEigThreads / 32; ++w) s += red[threadIdx.x * 8 + w];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+struct EigCtxE {
+  BandSys s;
+  int n, nex, ney;
+  const double* sE;
+  const uint8_t* dirn;  // per band-order node
+  const double* ke;
+  const double* mel;
+};
+
+// (K v)_i (mass = false) or (M v)_i on the closed neighbourhood, i = 2 ln + c
+__device__ __forceinline__ double el_stencil(const EigCtxE& c, const double* __restrict__ v, int i,
+                                             bool mass) {
+  const int ln = i >> 1, comp = i & 1;
+  int a, b;
+  band_node_of(c.s, ln, a, b);
+  const int la = a - c.s.a0, lb = b - c.s.b0;
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int ex = la - 1 + (e == 1 || e == 2), ey = lb - 1 + (e >= 2);
+    if (ex < 0 || ey < 0 || ex >= c.nex || ey >= c.ney) continue;
+    const int cn = (e == 0) ? 2 : (e == 1) ? 3 : (e == 2) ? 0 : 1;
+    const int gx = c.s.a0 + ex, gy = c.s.b0 + ey;
+    const int l[4] = {band_local_node(c.s, gx, gy), band_local_node(c.s, gx + 1, gy),
+                      band_local_node(c.s, gx + 1, gy + 1), band_local_node(c.s, gx, gy + 1)};
+    double sacc = 0.0;
+    if (mass) {
+      const double* mr = c.mel + cn * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sacc += mr[q] * v[2 * l[q] + comp];
+    } else {
+      const double* kr = c.ke + (comp * 4 + cn) * 8;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sacc += kr[q] * v[2 * l[q]] + kr[4 + q] * v[2 * l[q] + 1];
+    }
+    acc += c.sE[ey * c.nex + ex] * sacc;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256)
+    k_el_assemble(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
+                  ElastParam ep, double sigma, const BandSys* __restrict__ sys,
+                  double* __restrict__ Lc, const double* __restrict__ sigma_per_sys) {
+  const BandSys s = sys[blockIdx.x];
+  if (sigma_per_sys) sigma = sigma_per_sys[blockIdx.x];
+  const int S = s.bw + 1;
+  const int64_t total = (int64_t)s.n * S;
+  const int ex_lo = s.a0, ex_hi = s.a0 + s.w - 2, ey_lo = s.b0, ey_hi = s.b0 + s.hgt - 2;
+  for (int64_t t = threadIdx.x; t < total; t += blockDim.x) {
+    const int k = (int)(t / S), j = (int)(t % S);
+    const int row = k + j;
+    double v = 0.0;
+    if (row < s.n) {
+      int ak, bk, ar, br;
+      band_node_of(s, k >> 1, ak, bk);
+      band_node_of(s, row >> 1, ar, br);
+      const int ck = k & 1, cr = row & 1;
+      const int64_t nk = (int64_t)bk * g.nnx + ak, nr = (int64_t)br * g.nnx + ar;
+      if (hdir[nk] || hdir[nr]) {
+        v = (row == k) ? 1.0 : 0.0;
+      } else if (abs(ar - ak) <= 1 && abs(br - bk) <= 1) {
+        const int ilo = max(max(ak, ar) - 1, ex_lo), ihi = min(min(ak, ar), ex_hi);
+        const int jlo = max(max(bk, br) - 1, ey_lo), jhi = min(min(bk, br), ey_hi);
+        double kv = 0.0, mv = 0.0;
+        for (int ej = jlo; ej <= jhi; ++ej)
+          for (int ei = ilo; ei <= ihi; ++ei) {
+            const int dk = ak - ei, ek = bk - ej, dr = ar - ei, er = br - ej;
+            const int qk = dk + 3 * ek - 2 * dk * ek, qr = dr + 3 * er - 2 * dr * er;
+            const double Ee = E[(int64_t)ej * g.nx + ei];
+            kv += Ee * ep.ke[(cr * 4 + qr) * 8 + ck * 4 + qk];
+            if (cr == ck) mv += Ee * ep.mel[qr * 4 + qk];
+          }
+        v = kv + sigma * mv;
+      }
+    }
+    Lc[s.foff + t] = v;
+  }
+}
+
+void launch_el_assemble(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                        double sigma, const BandSys* sys, int nsys, double* Lc, cudaStream_t st,
+                        const double* sigma_per_sys) {
+  if (nsys == 0) return;
+  k_el_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, ep, sigma, sys, Lc, sigma_per_sys);
+  MS_CUDA(cudaGetLastError());
+}
+
+// shared-memory carve-up common to the two elasticity kernels
+struct ElSmem {
+  double *sE, *win, *red, *dots, *Am, *Vm, *ritz, *ritz_old, *misc;
+  int* order;
+  uint8_t* dirn;
+};
+constexpr int kElNV = P + 3;  // reduction width: P block columns + 3 kernel modes
+
+__device__ __forceinline__ ElSmem el_smem(double* sm, int nex, int ney, int S, int NL) {
+  ElSmem m;
+  m.sE = sm;
+  m.win = m.sE + nex * ney;
+  m.red = m.win + S * P;
+  m.dots = m.red + kElNV * 8;
+  m.Am = m.dots + kElNV;
+  m.Vm = m.Am + P * (P + 1);
+  m.ritz = m.Vm + P * (P + 1);
+  m.ritz_old = m.ritz + P;
+  m.misc = m.ritz_old + P;
+  m.order = reinterpret_cast<int*>(m.misc + 4);
+  m.dirn = reinterpret_cast<uint8_t*>(m.order + P);
+  (void)NL;
+  return m;
+}
+
+static size_t el_smem_bytes(int mex, int mey, int max_bw) {
+  const int NL = (2 * mex + 1) * (2 * mey + 1);
+  return sizeof(double) * ((size_t)(2 * mex) * (2 * mey) + (size_t)(max_bw + 1) * P + kElNV * 8 + kElNV +
+                           2 * P * (P + 1) + 2 * P + 4) +
+         sizeof(int) * P + (size_t)NL + 16;
+}
+
+// M-orthonormal rigid-body modes Zo (3 columns) and MZo = M Zo, CGS2 in the M
+// inner product; translations and the rotation about the neighbourhood centre
+__device__ void el_rigid_modes(const EigCtxE& c, double h, int mex, int mey, double* Zo, double* MZo,
+                               double* red, double* dots) {
+  const int n = c.n;
+  double v[kElNV];
+  for (int j = 0; j < 3; ++j) {
+    double* w = Zo + (int64_t)j * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int ln = i >> 1, comp = i & 1;
+      int a, b;
+      band_node_of(c.s, ln, a, b);
+      const double x = (double)(a - c.s.a0 - mex) * h, y = (double)(b - c.s.b0 - mey) * h;
+      w[i] = (j == 0) ? (comp == 0 ? 1.0 : 0.0) : (j == 1) ? (comp == 1 ? 1.0 : 0.0) : (comp == 0 ? -y : x);
+    }
+    __syncthreads();
+    for (int rep = 0; rep < 2; ++rep) {
+#pragma unroll
+      for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int l = 0; l < j; ++l) v[l] += MZo[(int64_t)l * n + i] * w[i];
+      block_sum_nv(v, 3, red, dots);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double x = w[i];
+        for (int l = 0; l < j; ++l) x -= dots[l] * Zo[(int64_t)l * n + i];
+        w[i] = x;
+      }
+      __syncthreads();
+    }
+    double nrm = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double mw = el_stencil(c, w, i, true);
+      MZo[(int64_t)j * n + i] = mw;
+      nrm += mw * w[i];
+    }
+#pragma unroll
+    for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+    v[0] = nrm;
+    block_sum_nv(v, 1, red, dots);
+    const double inv = 1.0 / sqrt(dots[0]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      w[i] *= inv;
+      MZo[(int64_t)j * n + i] *= inv;
+    }
+    __syncthreads();
+  }
+}
+
+template <int KJ>
+__global__ void __launch_bounds__(kEigThreads)
+    k_subspace_el(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
+                  ElastParam ep, EigBatch eb, int max_pass, double tol) {
+  extern __shared__ double sm[];
+  const int kb = blockIdx.x, k = eb.k0 + kb;
+  const BandSys s = eb.sys[kb];
+  const int n = s.n, S = s.bw + 1, NLn = n / 2;
+  const int nex = 2 * eb.mex, ney = 2 * eb.mey;
+  constexpr int LD = P + 1;
+  const ElSmem m = el_smem(sm, nex, ney, S, NLn);
+  __shared__ double ske[64], smel[16];
+  if (threadIdx.x < 64) ske[threadIdx.x] = ep.ke[threadIdx.x];
+  if (threadIdx.x < 16) smel[threadIdx.x] = ep.mel[threadIdx.x];
+  for (int t = threadIdx.x; t < nex * ney; t += blockDim.x)
+    m.sE[t] = E[(int64_t)(s.b0 + t / nex) * g.nx + s.a0 + t % nex];
+  int ndir = 0;
+  for (int ln = threadIdx.x; ln < NLn; ln += blockDim.x) {
+    int a, b;
+    band_node_of(s, ln, a, b);
+    m.dirn[ln] = hdir[(int64_t)b * g.nnx + a];
+    ndir += m.dirn[ln];
+  }
+  __syncthreads();
+  const EigCtxE ctx{s, n, nex, ney, m.sE, m.dirn, ske, smel};
+  double* X = eb.work + (int64_t)kb * (2 * P + 6) * n;
+  double* W = X + (int64_t)P * n;
+  double* Zo = W + (int64_t)P * n;
+  double* MZo = Zo + 3 * (int64_t)n;
+  double v[kElNV];
+#pragma unroll
+  for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+  v[0] = (double)ndir;
+  block_sum_nv(v, 1, m.red, m.dots);
+  const bool neumann = m.dots[0] == 0.0;
+  const int nz = neumann ? 3 : 0;
+  if (neumann) el_rigid_modes(ctx, g.h, eb.mex, eb.mey, Zo, MZo, m.red, m.dots);
+  for (int t = threadIdx.x; t < n * P; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    X[t] = m.dirn[i >> 1] ? 0.0 : hash_unif(((uint64_t)k << 32) ^ ((uint64_t)c << 24) ^ (uint64_t)i);
+  }
+  if (threadIdx.x < P) m.ritz_old[threadIdx.x] = 0.0;
+  __syncthreads();
+  const int need = kNeig - nz;
+  int pass = 0;
+  for (pass = 1; pass <= max_pass; ++pass) {
+    // (1) W = M X (zero rows at Dirichlet nodes)
+    for (int t = threadIdx.x; t < n * P; t += blockDim.x) {
+      const int c = t / n, i = t % n;
+      W[t] = m.dirn[i >> 1] ? 0.0 : el_stencil(ctx, X + (int64_t)c * n, i, true);
+    }
+    __syncthreads();
+    // (2) W <- (K + sigma M)^{-1} W
+    band_solve_block<KJ>(s, eb.Lc, eb.Lr, W, m.win);
+    // (3) M-orthonormalise W into X against the locked modes and earlier columns
+    for (int c = 0; c < P; ++c) {
+      double* w = W + (int64_t)c * n;
+      for (int rep = 0; rep < 2; ++rep) {
+#pragma unroll
+        for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          const double mw = el_stencil(ctx, w, i, true);
+#pragma unroll
+          for (int l = 0; l < P; ++l)
+            if (l < c) v[l] += mw * X[(int64_t)l * n + i];
+          for (int j = 0; j < nz; ++j) v[P + j] += MZo[(int64_t)j * n + i] * w[i];
+        }
+        block_sum_nv(v, kElNV, m.red, m.dots);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          double x = w[i];
+          for (int l = 0; l < c; ++l) x -= m.dots[l] * X[(int64_t)l * n + i];
+          for (int j = 0; j < nz; ++j) x -= m.dots[P + j] * Zo[(int64_t)j * n + i];
+          w[i] = m.dirn[i >> 1] ? 0.0 : x;
+        }
+        __syncthreads();
+      }
+      double nrm = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) nrm += w[i] * el_stencil(ctx, w, i, true);
+#pragma unroll
+      for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+      v[0] = nrm;
+      block_sum_nv(v, 1, m.red, m.dots);
+      const double inv = m.dots[0] > 0.0 ? 1.0 / sqrt(m.dots[0]) : 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) X[(int64_t)c * n + i] = w[i] * inv;
+      __syncthreads();
+    }
+    // (4) Kr = X^T K X
+    for (int c = 0; c < P; ++c) {
+#pragma unroll
+      for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+      const double* xc = X + (int64_t)c * n;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double kx = m.dirn[i >> 1] ? 0.0 : el_stencil(ctx, xc, i, false);
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+          if (l <= c) v[l] += kx * X[(int64_t)l * n + i];
+      }
+      block_sum_nv(v, c + 1, m.red, m.dots);
+      if (threadIdx.x <= c) {
+        m.Am[threadIdx.x * LD + c] = m.dots[threadIdx.x];
+        m.Am[c * LD + threadIdx.x] = m.dots[threadIdx.x];
+      }
+      __syncthreads();
+    }
+    // (5) Jacobi, (6) X <- X V
+    if (threadIdx.x < 32) jacobi_warp(m.Am, m.Vm, m.ritz, m.order);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double xr[P];
+#pragma unroll
+      for (int l = 0; l < P; ++l) xr[l] = X[(int64_t)l * n + i];
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        const int oc = m.order[c];
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < P; ++l) acc += xr[l] * m.Vm[l * LD + oc];
+        W[(int64_t)c * n + i] = acc;
+      }
+    }
+    __syncthreads();
+    {
+      double* t = X;
+      X = W;
+      W = t;
+    }
+    // (7) stopping rule ('fixed' selection: the first n_max pairs to tol, the rest to 1e-8)
+    if (threadIdx.x == 0) {
+      const double scale = fabs(m.ritz[P - 1]);
+      const int sel = eb.n_max;
+      bool conv = pass >= 3;
+      for (int i = 0; i < need; ++i) {
+        const double t = (i + nz < sel) ? tol : 1e-8;
+        if (fabs(m.ritz[i] - m.ritz_old[i]) > t * fabs(m.ritz[i]) + fmax(1e-15 * scale, eb.lam_floor))
+          conv = false;
+      }
+      for (int i = 0; i < P; ++i) m.ritz_old[i] = m.ritz[i];
+      m.misc[2] = conv ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (m.misc[2] != 0.0) break;
+  }
+  // outputs: kNeig lowest pairs, ascending; locked modes first (lambda = z^T K z)
+  double* ev = eb.evecs + (int64_t)kb * kNeig * n;
+  for (int j = 0; j < nz; ++j) {
+    const double* z = Zo + (int64_t)j * n;
+    double kk = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      kk += z[i] * el_stencil(ctx, z, i, false);
+      ev[(int64_t)j * n + i] = z[i];
+    }
+#pragma unroll
+    for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+    v[0] = kk;
+    block_sum_nv(v, 1, m.red, m.dots);
+    if (threadIdx.x == 0) eb.evals[(int64_t)k * kNeig + j] = m.dots[0];
+  }
+  for (int t = threadIdx.x; t < (kNeig - nz) * n; t += blockDim.x) {
+    const int q = t / n, i = t % n;
+    ev[(int64_t)(q + nz) * n + i] = X[(int64_t)q * n + i];
+  }
+  if (threadIdx.x < kNeig - nz) eb.evals[(int64_t)k * kNeig + nz + threadIdx.x] = m.ritz[threadIdx.x];
+  if (threadIdx.x == 0) {
+    eb.passes[k] = min(pass, max_pass);
+    eb.neumann[k] = neumann ? 1 : 0;
+  }
+}
+
+template <template <int> class Launch, typename... A>
+static void el_dispatch(int max_bw, A... args) {
+  const int kj = div_up(max_bw, 16);
+  if (kj <= 4)
+    Launch<4>::run(args...);
+  else if (kj <= 8)
+    Launch<8>::run(args...);
+  else if (kj <= 12)
+    Launch<12>::run(args...);
+  else
+    throw Error(-1, "elasticity neighbourhood band too wide for the eigensolver (coarse blocks <= 46 elements)");
+}
+
+template <int KJ>
+struct SubspaceElLaunch {
+  static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
+                  int max_pass, double tol, size_t smem, cudaStream_t st) {
+    MS_CUDA(cudaFuncSetAttribute(k_subspace_el<KJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_subspace_el<KJ><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, max_pass, tol);
+    MS_CUDA(cudaGetLastError());
+  }
+};
+
+void launch_subspace_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                        const EigBatch& b, int max_bw, int max_pass, double tol, cudaStream_t st) {
+  if (b.nk == 0) return;
+  const size_t smem = el_smem_bytes(b.mex, b.mey, max_bw);
+  if (smem > 220 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
+  el_dispatch<SubspaceElLaunch>(max_bw, g, E, hdir, ep, b, max_pass, tol, smem, st);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_compact_psi_el(EigBatch eb, int NLx, const int* __restrict__ nsel, const int64_t* __restrict__ psioff,
+                     double* __restrict__ psi) {
+  __shared__ double sval[8];
+  __shared__ int sidx[8];
+  const int kb = blockIdx.x, k = eb.k0 + kb;
+  const BandSys s = eb.sys[kb];
+  const int n = s.n, NL = n / 2;
+  const double* ev = eb.evecs + (int64_t)kb * kNeig * n;
+  for (int mo = 0; mo < nsel[k]; ++mo) {
+    const double* vm = ev + (int64_t)mo * n;
+    // argmax |v| over (component, lexicographic node) order, ties: smallest index
+    double best = -1.0;
+    int bidx = 0x7fffffff;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int c = t / NL, ln = t % NL;
+      const double x = fabs(vm[2 * band_local_node(s, s.a0 + ln % NLx, s.b0 + ln / NLx) + c]);
+      if (x > best || (x == best && t < bidx)) {
+        best = x;
+        bidx = t;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ob > best || (ob == best && oi < bidx)) {
+        best = ob;
+        bidx = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sval[threadIdx.x >> 5] = best;
+      sidx[threadIdx.x >> 5] = bidx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 1; w < 8; ++w)
+        if (sval[w] > sval[0] || (sval[w] == sval[0] && sidx[w] < sidx[0])) {
+          sval[0] = sval[w];
+          sidx[0] = sidx[w];
+        }
+    __syncthreads();
+    const int ib = sidx[0], cb = ib / NL, lb = ib % NL;
+    const double sign = vm[2 * band_local_node(s, s.a0 + lb % NLx, s.b0 + lb / NLx) + cb] < 0.0 ? -1.0 : 1.0;
+    double* out = psi + psioff[k] + (int64_t)mo * n;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int c = t / NL, ln = t % NL;
+      out[t] = sign * vm[2 * band_local_node(s, s.a0 + ln % NLx, s.b0 + ln / NLx) + c];
+    }
+    __syncthreads();
+  }
+}
+
+void launch_compact_psi_el(const EigBatch& b, int NLx, const int* nsel, const int64_t* psioff,
+                           double* psi, cudaStream_t st) {
+  if (b.nk == 0) return;
+  k_compact_psi_el<<<b.nk, 256, 0, st>>>(b, NLx, nsel, psioff, psi);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// EE;Rand: the randomized snapshot solver (spectral.py:103-158) on the
+// elasticity pencil, kernel candidates Z = the three rigid-body modes on the
+// free dofs (kernel_basis, spectral.py:37-44): G = Z^T M Z,
+// F -= MZ G^-1 Z^T F, deflate(X) = X - Z G^-1 MZ^T X, 4 shift-invert passes,
+// orthonormal basis of [U, Z] (CGS2, rank cut), Rayleigh-Ritz.
+
+__global__ void k_rand_sigma_el(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
+                                ElastParam ep, const BandSys* __restrict__ sys, double* __restrict__ sigma) {
+  __shared__ double sred[8];
+  const BandSys s = sys[blockIdx.x];
+  const int NLn = s.n / 2;
+  double tr = 0.0, nf = 0.0;
+  for (int ln = threadIdx.x; ln < NLn; ln += blockDim.x) {
+    int a, b;
+    band_node_of(s, ln, a, b);
+    if (hdir[(int64_t)b * g.nnx + a]) continue;
+    nf += 2.0;
+    for (int e = 0; e < 4; ++e) {
+      const int ei = a - 1 + (e == 1 || e == 2), ej = b - 1 + (e >= 2);
+      if (ei < s.a0 || ej < s.b0 || ei > s.a0 + s.w - 2 || ej > s.b0 + s.hgt - 2) continue;
+      const int cn = (e == 0) ? 2 : (e == 1) ? 3 : (e == 2) ? 0 : 1;
+      const double Ee = E[(int64_t)ej * g.nx + ei];
+      tr += Ee * ep.ke[cn * 8 + cn] + Ee * ep.ke[(4 + cn) * 8 + 4 + cn];
+    }
+  }
+  const double t = block_sum(tr, sred), m = block_sum(nf, sred);
+  if (threadIdx.x == 0) sigma[blockIdx.x] = 1e-8 * (t / m);
+}
+
+void launch_rand_sigma_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                          const BandSys* sys, int nsys, double* sigma, cudaStream_t st) {
+  if (nsys == 0) return;
+  k_rand_sigma_el<<<nsys, 256, 0, st>>>(g, E, hdir, ep, sys, sigma);
+  MS_CUDA(cudaGetLastError());
+}
+
+template <int KJ>
+__global__ void __launch_bounds__(kEigThreads)
+    k_randomized_el(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir, ElastParam ep,
+                    EigBatch eb, const double* __restrict__ F, int ns, int nlx) {
+  extern __shared__ double sm[];
+  const int kb = blockIdx.x, k = eb.k0 + kb;
+  const BandSys s = eb.sys[kb];
+  const int n = s.n, S = s.bw + 1, NLn = n / 2;
+  const int nex = 2 * eb.mex, ney = 2 * eb.mey;
+  constexpr int LD = P + 1;
+  const ElSmem m = el_smem(sm, nex, ney, S, NLn);
+  __shared__ double ske[64], smel[16], Gi[9], keep[P];
+  __shared__ double Lm[P][P + 1], Cm[P][P + 1];
+  if (threadIdx.x < 64) ske[threadIdx.x] = ep.ke[threadIdx.x];
+  if (threadIdx.x < 16) smel[threadIdx.x] = ep.mel[threadIdx.x];
+  for (int t = threadIdx.x; t < nex * ney; t += blockDim.x)
+    m.sE[t] = E[(int64_t)(s.b0 + t / nex) * g.nx + s.a0 + t % nex];
+  for (int ln = threadIdx.x; ln < NLn; ln += blockDim.x) {
+    int a, b;
+    band_node_of(s, ln, a, b);
+    m.dirn[ln] = hdir[(int64_t)b * g.nnx + a];
+  }
+  __syncthreads();
+  const EigCtxE ctx{s, n, nex, ney, m.sE, m.dirn, ske, smel};
+  double* X = eb.work + (int64_t)kb * (2 * P + 6) * n;
+  double* W = X + (int64_t)P * n;
+  double* Z = W + (int64_t)P * n;
+  double* MZ = Z + 3 * (int64_t)n;
+  double v[kElNV];
+  auto zero_v = [&]() {
+#pragma unroll
+    for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+  };
+  // Z on the free dofs (rotation about the neighbourhood centre), MZ, G^-1
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int ln = i >> 1, comp = i & 1;
+    int a, b;
+    band_node_of(s, ln, a, b);
+    const bool d = m.dirn[ln];
+    const double x = (double)(a - s.a0 - eb.mex) * g.h, y = (double)(b - s.b0 - eb.mey) * g.h;
+    Z[i] = d ? 0.0 : (comp == 0 ? 1.0 : 0.0);
+    Z[n + i] = d ? 0.0 : (comp == 1 ? 1.0 : 0.0);
+    Z[2 * n + i] = d ? 0.0 : (comp == 0 ? -y : x);
+  }
+  __syncthreads();
+  zero_v();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const bool d = m.dirn[i >> 1];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double mz = d ? 0.0 : el_stencil(ctx, Z + (int64_t)j * n, i, true);
+      MZ[(int64_t)j * n + i] = mz;
+#pragma unroll
+      for (int l = 0; l <= j; ++l) v[j * 3 + l] += Z[(int64_t)l * n + i] * mz;
+    }
+  }
+  block_sum_nv(v, 9, m.red, m.dots);
+  if (threadIdx.x == 0) {
+    double G[3][3];
+    for (int j = 0; j < 3; ++j)
+      for (int l = 0; l <= j; ++l) G[j][l] = G[l][j] = m.dots[j * 3 + l];
+    const double det = G[0][0] * (G[1][1] * G[2][2] - G[1][2] * G[2][1]) -
+                       G[0][1] * (G[1][0] * G[2][2] - G[1][2] * G[2][0]) +
+                       G[0][2] * (G[1][0] * G[2][1] - G[1][1] * G[2][0]);
+    const double id = 1.0 / det;
+    Gi[0] = (G[1][1] * G[2][2] - G[1][2] * G[2][1]) * id;
+    Gi[1] = (G[0][2] * G[2][1] - G[0][1] * G[2][2]) * id;
+    Gi[2] = (G[0][1] * G[1][2] - G[0][2] * G[1][1]) * id;
+    Gi[3] = (G[1][2] * G[2][0] - G[1][0] * G[2][2]) * id;
+    Gi[4] = (G[0][0] * G[2][2] - G[0][2] * G[2][0]) * id;
+    Gi[5] = (G[0][2] * G[1][0] - G[0][0] * G[1][2]) * id;
+    Gi[6] = (G[1][0] * G[2][1] - G[1][1] * G[2][0]) * id;
+    Gi[7] = (G[0][1] * G[2][0] - G[0][0] * G[2][1]) * id;
+    Gi[8] = (G[0][0] * G[1][1] - G[0][1] * G[1][0]) * id;
+  }
+  __syncthreads();
+  // X - A G^-1 (B^T X) for the first ns columns of W (A, B in {Z, MZ})
+  auto project = [&](const double* A, const double* B) {
+    for (int c = 0; c < ns; ++c) {
+      double* w = W + (int64_t)c * n;
+      zero_v();
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) v[j] += B[(int64_t)j * n + i] * w[i];
+      block_sum_nv(v, 3, m.red, m.dots);
+      double u[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) u[j] = Gi[j * 3] * m.dots[0] + Gi[j * 3 + 1] * m.dots[1] + Gi[j * 3 + 2] * m.dots[2];
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        w[i] -= A[i] * u[0] + A[n + i] * u[1] + A[2 * (int64_t)n + i] * u[2];
+      __syncthreads();
+    }
+  };
+  // forcings: [ns][2 NL] x-plane then y-plane (lexicographic) -> band order
+  const int NLd = 2 * NLn;
+  const double* Fk = F + (int64_t)kb * ns * NLd;
+  for (int t = threadIdx.x; t < n * P; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    double val = 0.0;
+    if (c < ns && !m.dirn[i >> 1]) {
+      int a, b;
+      band_node_of(s, i >> 1, a, b);
+      val = Fk[(int64_t)c * NLd + (int64_t)(i & 1) * NLn + (a - s.a0) + (int64_t)(b - s.b0) * nlx];
+    }
+    W[t] = val;
+  }
+  __syncthreads();
+  project(MZ, Z);  // F -= MZ G^-1 Z^T F
+  band_solve_block<KJ>(s, eb.Lc, eb.Lr, W, m.win);
+  project(Z, MZ);  // deflate
+  for (int pass = 1; pass < 4; ++pass) {
+    cgs2_euclid(W, ns, n, m.red, m.dots, nullptr);
+    for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
+      const int c = t / n, i = t % n;
+      X[t] = m.dirn[i >> 1] ? 0.0 : el_stencil(ctx, W + (int64_t)c * n, i, true);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n * ns; t += blockDim.x) W[t] = X[t];
+    __syncthreads();
+    band_solve_block<KJ>(s, eb.Lc, eb.Lr, W, m.win);
+    project(Z, MZ);
+  }
+  // Q = orthonormal basis of [U, Z]
+  const int m0 = ns + 3;
+  for (int t = threadIdx.x; t < n * m0; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    X[t] = (c < ns) ? W[t] : Z[(int64_t)(c - ns) * n + i];
+  }
+  __syncthreads();
+  cgs2_euclid(X, m0, n, m.red, m.dots, keep);
+  if (threadIdx.x == 0) {
+    int q = 0;
+    for (int c = 0; c < m0; ++c)
+      if (keep[c] != 0.0) m.order[q++] = c;
+    m.misc[0] = (double)q;
+  }
+  __syncthreads();
+  const int mq = (int)m.misc[0];
+  for (int q = 0; q < mq; ++q) {
+    const int c = m.order[q];
+    if (c != q)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) X[(int64_t)q * n + i] = X[(int64_t)c * n + i];
+    __syncthreads();
+  }
+  // Kr (-> Am) and Mr (-> Cm)
+  for (int ps = 0; ps < 2; ++ps) {
+    for (int c = 0; c < mq; ++c) {
+      zero_v();
+      const double* xc = X + (int64_t)c * n;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double ax = m.dirn[i >> 1] ? 0.0 : el_stencil(ctx, xc, i, ps == 1);
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+          if (l <= c) v[l] += ax * X[(int64_t)l * n + i];
+      }
+      block_sum_nv(v, c + 1, m.red, m.dots);
+      if (threadIdx.x <= c) {
+        if (ps == 0)
+          m.Am[threadIdx.x * LD + c] = m.Am[c * LD + threadIdx.x] = m.dots[threadIdx.x];
+        else
+          Cm[threadIdx.x][c] = Cm[c][threadIdx.x] = m.dots[threadIdx.x];
+      }
+      __syncthreads();
+    }
+  }
+  // generalized mq x mq problem: Mr = L L^T, C = L^-1 Kr L^-T, Jacobi
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < mq; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double a = Cm[i][j];
+        for (int q = 0; q < j; ++q) a -= Lm[i][q] * Lm[j][q];
+        Lm[i][j] = (i == j) ? sqrt(fmax(a, 1e-300)) : a / Lm[j][j];
+      }
+    for (int c = 0; c < mq; ++c)
+      for (int i = 0; i < mq; ++i) {
+        double a = m.Am[i * LD + c];
+        for (int q = 0; q < i; ++q) a -= Lm[i][q] * Cm[q][c];
+        Cm[i][c] = a / Lm[i][i];
+      }
+    for (int i = 0; i < mq; ++i)
+      for (int j = 0; j < mq; ++j) {
+        double a = Cm[i][j];
+        for (int q = 0; q < j; ++q) a -= m.Am[i * LD + q] * Lm[j][q];
+        m.Am[i * LD + j] = a / Lm[j][j];
+      }
+    for (int i = 0; i < P; ++i)
+      for (int j = 0; j < P; ++j)
+        if (i >= mq || j >= mq) m.Am[i * LD + j] = (i == j) ? 1e300 : 0.0;
+    for (int i = 0; i < mq; ++i)
+      for (int j = 0; j < i; ++j)
+        m.Am[i * LD + j] = m.Am[j * LD + i] = 0.5 * (m.Am[i * LD + j] + m.Am[j * LD + i]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) jacobi_warp(m.Am, m.Vm, m.ritz, m.order);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < kNeig && c < mq; ++c) {
+      const int oc = m.order[c];
+      for (int i = mq - 1; i >= 0; --i) {
+        double a = m.Vm[i * LD + oc];
+        for (int q = i + 1; q < mq; ++q) a -= Lm[q][i] * Cm[q][c];
+        Cm[i][c] = a / Lm[i][i];
+      }
+    }
+  }
+  __syncthreads();
+  double* ev = eb.evecs + (int64_t)kb * kNeig * n;
+  const int kk = min(kNeig, mq);
+  for (int t = threadIdx.x; t < kNeig * n; t += blockDim.x) {
+    const int c = t / n, i = t % n;
+    double a = 0.0;
+    if (c < kk)
+      for (int q = 0; q < mq; ++q) a += X[(int64_t)q * n + i] * Cm[q][c];
+    ev[t] = a;
+  }
+  if (threadIdx.x < kNeig)
+    eb.evals[(int64_t)k * kNeig + threadIdx.x] = threadIdx.x < kk ? m.ritz[threadIdx.x] : CUDART_NAN;
+  if (threadIdx.x == 0) {
+    eb.passes[k] = 4;
+    eb.neumann[k] = 0;
+  }
+}
+
+template <int KJ>
+struct RandElLaunch {
+  static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
+                  const double* F, int ns, int nlx, size_t smem, cudaStream_t st) {
+    MS_CUDA(cudaFuncSetAttribute(k_randomized_el<KJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_randomized_el<KJ><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, F, ns, nlx);
+    MS_CUDA(cudaGetLastError());
+  }
+};
+
+void launch_randomized_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                          const EigBatch& b, int max_bw, const double* F, int ns, cudaStream_t st) {
+  if (b.nk == 0) return;
+  if (ns + 3 > P) throw Error(-1, "too many snapshots for the randomized elasticity eigensolver (<= 13)");
+  const size_t smem = el_smem_bytes(b.mex, b.mey, max_bw);
+  if (smem > 200 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
+  el_dispatch<RandElLaunch>(max_bw, g, E, hdir, ep, b, F, ns, 2 * b.mex + 1, smem, st);
 }
 
 }  // namespace msgpu

@@ -50,6 +50,38 @@ void launch_randomized(const Grid& g, const double* E, const uint8_t* hdir, cons
 void launch_rand_sigma(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
                        const BandSys* sys, int nsys, double* sigma, cudaStream_t st);
 
+// ---- elasticity eigenproblems (EE, EE;Rand; spectral.py:63-100 kind 'elasticity') ----
+// Unknowns node-interleaved (2 ln + c) in the band order of the closed
+// neighbourhood; evecs/work of an EigBatch then hold 2*NL values per vector.
+struct ElastParam {
+  double ke[64];   // unit-modulus Q1 plane-stress element, [comp*4 + corner] ordering
+  double mel[16];  // Q1 mass element for side h (block-diagonal per component)
+};
+
+// B = K_E + sigma M_E in band form (whole-node Dirichlet -> identity rows)
+void launch_el_assemble(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                        double sigma, const BandSys* sys, int nsys, double* Lc, cudaStream_t st,
+                        const double* sigma_per_sys = nullptr);
+
+// shift-invert block subspace iteration (rigid-body modes locked on Neumann
+// neighbourhoods); work holds (2p + 6) * n doubles per centre
+void launch_subspace_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                        const EigBatch& b, int max_bw, int max_pass, double tol, cudaStream_t st);
+
+// randomized snapshot solver with the rigid-body modes as kernel candidates;
+// F = [centre][ns][2 NL] (x-plane then y-plane, lexicographic, zero at Dirichlet)
+void launch_randomized_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                          const EigBatch& b, int max_bw, const double* F, int ns, cudaStream_t st);
+
+// sigma_k = 1e-8 tr(K_free) / n_free (spectral.py:133), elasticity pencil
+void launch_rand_sigma_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
+                          const BandSys* sys, int nsys, double* sigma, cudaStream_t st);
+
+// selected vectors -> psi store: per mode the x-part then the y-part over the
+// closed neighbourhood (lexicographic), sign-normalised
+void launch_compact_psi_el(const EigBatch& b, int NLx, const int* nsel, const int64_t* psioff,
+                           double* psi, cudaStream_t st);
+
 // gap / fixed selection on device (spectral.py:161-186)
 void launch_select(int n_centers, const double* evals, int n_max, double threshold, int fixed,
                    int* nsel, cudaStream_t st);

@@ -39,7 +39,7 @@ VARIANTS = {
         PreconditionerVariant("EH+Rot;Rand", "elasticity", "heat", True, True),
     ]
 }
-GPU_VARIANTS = ("EH", "EH+Rot", "EH+Rot;Rand", "HH", "HH+Rot")
+GPU_VARIANTS = ("EH", "EH+Rot", "EH+Rot;Rand", "HH", "HH+Rot", "EE", "EE;Rand")
 
 
 def get_variant(tag):
@@ -132,19 +132,26 @@ class TwoLevelPreconditioner:
             self.handle = None
 
 
-def randomized_forcings(mesh, part, dirichlet_nodes, n_snapshots, seed):
+def randomized_forcings(mesh, part, dirichlet_nodes, n_snapshots, seed, kind="diffusion"):
     """Host forcings of solve_local_eig_randomized (spectral.py:119-121):
     centre k draws default_rng([seed, k]).uniform(-1, 1, (n_free_k, n_snap))
-    over its free closed-neighbourhood nodes (schwarz.py:156-160); returned as
-    [centre][snapshot][node] over all (2H+1)^2 nodes, zero at clamped nodes."""
+    over its free closed-neighbourhood dofs (schwarz.py:156-160); returned as
+    [centre][snapshot][d * node] over all (2H+1)^2 nodes, zero at clamped
+    nodes.  kind='elasticity' (d = 2): the free dofs are the x-dofs of the free
+    nodes then their y-dofs (the reference's component-grouped order), stored
+    as an x-plane followed by a y-plane."""
     NLx, NLy = 2 * part.mex + 1, 2 * part.mey + 1
+    NL = NLx * NLy
+    d = 2 if kind == "elasticity" else 1
     clamped = np.zeros(mesh.n_nodes, dtype=bool)
     clamped[np.asarray(dirichlet_nodes, dtype=np.int64)] = True
-    F = np.zeros((part.n_neighborhoods, n_snapshots, NLx * NLy))
+    F = np.zeros((part.n_neighborhoods, n_snapshots, d * NL))
     for k, (I, J) in enumerate(part.coarse_nodes):
         a0, b0 = (I - 1) * part.mex, (J - 1) * part.mey
         gids = ((b0 + np.arange(NLy))[:, None] * (mesh.nx + 1) + (a0 + np.arange(NLx))[None, :]).ravel()
         free = np.nonzero(~clamped[gids])[0]
+        if d == 2:
+            free = np.concatenate([free, NL + free])
         ns = min(n_snapshots, free.size)
         Fk = np.random.default_rng([seed, k]).uniform(-1.0, 1.0, size=(free.size, ns))
         F[k, :ns][:, free] = Fk.T
@@ -167,9 +174,12 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
     if not isinstance(op, ElasticityOperator):
         raise TypeError("build_preconditioner needs the GPU ElasticityOperator from assemble_elasticity")
     opts = opts or EigOptions()
-    rule = opts.rule or "gap"
+    elastic = variant.eig_kind == "elasticity"
+    rule = opts.rule or ("fixed" if elastic else "gap")
     if rule not in ("gap", "fixed"):
         raise ValueError(f"unknown selection rule {rule!r}")
+    if elastic and rule == "gap":  # spectral.py:176-177
+        raise ValueError("gap rule is not reliable for elasticity eigenproblems")
     hd = np.ascontiguousarray(np.asarray(dirichlet_nodes, dtype=np.int64).ravel())
     o = _lib.PrecondOpts()
     o.Nx, o.Ny = part.Nx, part.Ny
@@ -190,12 +200,14 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
     o.local_solver = _lib.MS_LOCAL_BANDED if local_solver == "banded" else _lib.MS_LOCAL_DENSE_INV
     o.use_coarse = 1 if use_coarse else 0
     o.level1_operator = _lib.MS_L1_HEAT if variant.level1 == "heat" else _lib.MS_L1_ELASTICITY
+    o.eig_kind = _lib.MS_EIG_ELASTICITY if elastic else _lib.MS_EIG_HEAT
     o.heat_dirichlet_nodes = hd.ctypes.data_as(C.POINTER(C.c_int64)) if hd.size else None
     o.n_heat_dirichlet = hd.size
     F = None
     if variant.randomized:
         ns = opts.n_snapshots or (opts.n_max + 5)
-        F = np.ascontiguousarray(randomized_forcings(mesh, part, hd, ns, opts.seed))
+        F = np.ascontiguousarray(randomized_forcings(mesh, part, hd, ns, opts.seed,
+                                                     "elasticity" if elastic else "diffusion"))
         o.randomized, o.n_snapshots, o.snapshots = 1, ns, F.ctypes.data
     lib = _lib.load()
     h = C.c_void_p()
@@ -208,7 +220,7 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
     info = {
         "t_level1": inf.t_level1, "t_coarse": inf.t_coarse, "t_eig": inf.t_eig,
         "coarse_dim": inf.coarse_dim, "mode_counts": [int(c) for c in counts[:nc]],
-        "basis_kind": "H+Rot" if variant.enrich else "H", "selection_rule": rule,
+        "basis_kind": "E" if elastic else ("H+Rot" if variant.enrich else "H"), "selection_rule": rule,
         "eig_solver": "randomized" if variant.randomized else "subspace",
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
         "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,

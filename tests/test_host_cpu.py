@@ -129,8 +129,11 @@ def test_product_path_has_no_cpu_fallback(tmp_path):
     coeff = G.CoefficientField(np.ones(16), 0.3, 1.0, 1.0)
     with pytest.raises(TypeError):
         G.build_preconditioner("EH+Rot", object(), mesh, part, coeff, [])
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(TypeError):
         G.build_preconditioner("EE", object(), mesh, part, coeff, [])
+    with pytest.raises(ValueError):
+        G.build_preconditioner("XX", object(), mesh, part, coeff, [])
+    assert set(G.GPU_VARIANTS) == set(G.VARIANTS)
     with pytest.raises(TypeError):
         G.pcg_solve(np.eye(3), np.ones(3))
 
@@ -153,3 +156,28 @@ def test_topopt_host_pieces():
     assert np.array_equal(G.build_load_vector(mesh, G.LoadSpec(body_force=(0.0, -1.0))), g["sens_f"])
     with pytest.raises(ValueError):
         T.optimize(T.OptimizeConfig(solver="direct"))
+
+
+@pytest.mark.parametrize("kind", ["diffusion", "elasticity"])
+def test_randomized_forcings_follow_reference_dof_order(kind):
+    """Forcing k is default_rng([seed, k]).uniform over the local problem's
+    free dofs in the reference's order (spectral.py:119-121): nodes ascending,
+    x-dofs then y-dofs for elasticity."""
+    from paper_2006_13387_b200.schwarz import randomized_forcings
+
+    mesh_o = O.mesh_for(20, 20)
+    part_o = O.Partition(mesh_o, 4, 4)
+    mesh = G.build_fine_mesh(20, 20)
+    part = G.build_coarse_partition(mesh, 4, 4)
+    clamped = np.nonzero((np.arange(mesh.n_nodes) % 21 == 0))[0]  # left edge
+    F = randomized_forcings(mesh, part, clamped, 11, 5, kind)
+    E = np.ones(400)
+    for k in (0, 3, 8):
+        if kind == "elasticity":
+            K, M, pm = O.local_elasticity_problem(mesh_o, E, 0.3, part_o.omegas[k], clamped)
+        else:
+            K, M, pm = O.local_heat_problem(mesh_o, E, part_o.omegas[k], clamped)
+        ref = np.random.default_rng([5, k]).uniform(-1.0, 1.0, size=(K.n_free, 11))
+        full = np.zeros((F.shape[2], 11))
+        full[K.free_dofs] = ref
+        assert np.array_equal(F[k].T, full)
