@@ -93,7 +93,7 @@ def test_strip_partition_and_halo_pairing_gloo(world):
 # GPU: 2 ranks on one device through gloo host callbacks
 
 
-def _solve_worker(rank, world, port, q):
+def _solve_worker(rank, world, port, q, tag="EH+Rot"):
     sys.path.insert(0, str(ROOT))
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     _init(rank, world, port)
@@ -103,7 +103,7 @@ def _solve_worker(rank, world, port, q):
 
         D.init_host_callbacks(0)
         spec = configs.config1(seed=0, n=64, H=16, delta=2)
-        mesh, op, pre = setup_spec(spec)
+        mesh, op, pre = setup_spec(spec, tag)
         x, rep = pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
         z = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
         q.put((rank, x, rep.iterations, rep.converged, pre.coarse_dim, list(pre.mode_counts), z))
@@ -112,13 +112,14 @@ def _solve_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_two_ranks_on_one_gpu_match_single_rank():
+@pytest.mark.parametrize("tag", ["EH+Rot", "HH+Rot", "EE", "EH+Rot;Rand"])
+def test_two_ranks_on_one_gpu_match_single_rank(tag):
     if not torch.cuda.is_available():  # pragma: no cover
         pytest.skip("no CUDA device")
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_solve_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_solve_worker, args=(r, 2, port, q, tag)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict((v[0], v[1:]) for v in (q.get(timeout=600) for _ in range(2)))
@@ -130,7 +131,7 @@ def test_two_ranks_on_one_gpu_match_single_rank():
     from paper_2006_13387_b200.solve import setup_spec
 
     spec = configs.config1(seed=0, n=64, H=16, delta=2)
-    mesh, op, pre = setup_spec(spec)
+    mesh, op, pre = setup_spec(spec, tag)
     x1, rep1 = pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
     z1 = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
     for r in (0, 1):
