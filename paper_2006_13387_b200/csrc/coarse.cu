@@ -222,8 +222,14 @@ void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double
 // r -= alpha q and the ||r||^2 grid reduction / convergence test.
 constexpr int kCellThreads = 256;
 
+#ifndef MS_CR_MINB
+#define MS_CR_MINB 5
+#endif
+#ifndef MS_CB_MINB
+#define MS_CB_MINB 6
+#endif
 template <bool UPD, bool VEC>
-__global__ void __launch_bounds__(kCellThreads)
+__global__ void __launch_bounds__(kCellThreads, MS_CR_MINB)
     k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, int J0, double* __restrict__ x,
                     const double* __restrict__ p, double* __restrict__ r,
                     const double* __restrict__ q, PcgScalars* sc, double* partials,
@@ -445,7 +451,7 @@ void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cu
 constexpr int kCombineThreads = 256;
 
 template <bool VEC>
-__global__ void __launch_bounds__(kCombineThreads)
+__global__ void __launch_bounds__(kCombineThreads, MS_CB_MINB)
     k_combine(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, int has_l1, CoarseDev cd,
               int has_coarse, int Nx, int Ny, int J0, const double* __restrict__ y0,
               const double* __restrict__ r, double* __restrict__ z, PcgScalars* sc,

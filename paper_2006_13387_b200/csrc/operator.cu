@@ -23,10 +23,16 @@ int reduce_blocks() { return 148 * 8; }
 // gather loops over the 4 corner roles c of a node inside its elements: the
 // two Ke0 rows of corner c are read once per thread and reused for the
 // thread's 4 nodes.
-constexpr int MV_NY = 32;  // nodes per CTA in y
+#ifndef MS_MV_NY
+#define MS_MV_NY 16
+#endif
+constexpr int MV_NY = MS_MV_NY;  // nodes per CTA in y
 constexpr int MV_RPT = MV_NY / MV_TY;  // nodes per thread
 
-__global__ void __launch_bounds__(MV_TX* MV_TY, 3)
+#ifndef MS_MV_MINB
+#define MS_MV_MINB 5
+#endif
+__global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
     k_matvec(Grid g, KeParam ke, const double* __restrict__ E, const uint8_t* __restrict__ mask,
              const double* __restrict__ z, const double* __restrict__ p_old,
              double* __restrict__ p_new, double* __restrict__ q, int mode, PcgScalars* sc,
@@ -41,27 +47,55 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, 3)
   const double beta = (mode == MV_PCG) ? sc->beta : 0.0;
   const int64_t nn = g.n_nodes;
 
-  for (int t = tid; t < (MV_NY + 2) * (MV_TX + 2); t += blockDim.x) {
-    const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
-    const int a = a0 + lx - 1, b = b0 + ly - 1;
-    double px = 0.0, py = 0.0;
-    if (a >= 0 && a <= g.nx && b >= 0 && b <= g.ny) {
-      const int64_t n = (int64_t)b * g.nnx + a;
-      if (mode == MV_PCG) {
-        px = z[n] + beta * p_old[n];
-        py = z[n + nn] + beta * p_old[n + nn];
-      } else {
-        px = p_old[n];
-        py = p_old[n + nn];
+  // Tile loads: every global load of the thread is issued before the first
+  // shared-memory store (compile-time trip counts, predicated), so each
+  // thread keeps ~25 loads in flight instead of one dependent chain.
+  constexpr int kPT = (MV_NY + 2) * (MV_TX + 2);
+  constexpr int kPIt = (kPT + MV_TX * MV_TY - 1) / (MV_TX * MV_TY);
+  constexpr int kET = (MV_NY + 1) * (MV_TX + 1);
+  constexpr int kEIt = (kET + MV_TX * MV_TY - 1) / (MV_TX * MV_TY);
+  {
+    double zx[kPIt], zy[kPIt], ox[kPIt], oy[kPIt], ev[kEIt];
+#pragma unroll
+    for (int it = 0; it < kPIt; ++it) {
+      const int t = tid + it * MV_TX * MV_TY;
+      const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
+      const int a = a0 + lx - 1, b = b0 + ly - 1;
+      zx[it] = zy[it] = ox[it] = oy[it] = 0.0;
+      if (t < kPT && a >= 0 && a <= g.nx && b >= 0 && b <= g.ny) {
+        const int64_t n = (int64_t)b * g.nnx + a;
+        ox[it] = __ldg(p_old + n);
+        oy[it] = __ldg(p_old + n + nn);
+        if (mode == MV_PCG) {
+          zx[it] = __ldg(z + n);
+          zy[it] = __ldg(z + n + nn);
+        }
       }
     }
-    sp[0][ly][lx] = px;
-    sp[1][ly][lx] = py;
-  }
-  for (int t = tid; t < (MV_NY + 1) * (MV_TX + 1); t += blockDim.x) {
-    const int ly = t / (MV_TX + 1), lx = t - ly * (MV_TX + 1);
-    const int i = a0 + lx - 1, j = b0 + ly - 1;
-    sE[ly][lx] = (i >= 0 && i < g.nx && j >= 0 && j < g.ny) ? E[(int64_t)j * g.nx + i] : 0.0;
+#pragma unroll
+    for (int it = 0; it < kEIt; ++it) {
+      const int t = tid + it * MV_TX * MV_TY;
+      const int ly = t / (MV_TX + 1), lx = t - ly * (MV_TX + 1);
+      const int i = a0 + lx - 1, j = b0 + ly - 1;
+      ev[it] = (t < kET && i >= 0 && i < g.nx && j >= 0 && j < g.ny) ? __ldg(E + (int64_t)j * g.nx + i) : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < kPIt; ++it) {
+      const int t = tid + it * MV_TX * MV_TY;
+      if (t < kPT) {
+        const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
+        sp[0][ly][lx] = (mode == MV_PCG) ? zx[it] + beta * ox[it] : ox[it];
+        sp[1][ly][lx] = (mode == MV_PCG) ? zy[it] + beta * oy[it] : oy[it];
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kEIt; ++it) {
+      const int t = tid + it * MV_TX * MV_TY;
+      if (t < kET) {
+        const int ly = t / (MV_TX + 1), lx = t - ly * (MV_TX + 1);
+        sE[ly][lx] = ev[it];
+      }
+    }
   }
   __syncthreads();
 

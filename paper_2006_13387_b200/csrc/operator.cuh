@@ -70,8 +70,11 @@ struct LapParam {
   double lap[16];  // unit Q1 Laplacian element (assembly.py:133-140)
 };
 
-constexpr int MV_TX = 32;  // nodes per CTA in x
-constexpr int MV_TY = 8;   // nodes per CTA in y (one node per thread)
+#ifndef MS_MV_TY
+#define MS_MV_TY 8
+#endif
+constexpr int MV_TX = 32;        // nodes per CTA in x
+constexpr int MV_TY = MS_MV_TY;  // threads per CTA in y
 
 enum { MV_PLAIN = 0, MV_PCG = 1 };
 
