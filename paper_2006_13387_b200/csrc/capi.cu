@@ -320,6 +320,8 @@ struct ms_precond {
   // strip ownership: level-1 subdomain rows [J0, J1) -> subdomains [s0, s1);
   // coarse cell rows [C0, C1); centres [kc0, kc1).  One rank owns everything.
   int J0 = 0, J1 = 0, s0 = 0, s1 = 0, C0 = 0, C1 = 0, kc0 = 0, kc1 = 0, halo_rows = 1;
+  // packed K0^-1 tiles [sym_t0, sym_t1) of the sharded coarse solve (all on one rank)
+  int64_t sym_t0 = 0, sym_t1 = -1;
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;  // captured PCG chunks for (prob, this)
   std::vector<std::pair<int, int>> captured;
   ~ms_precond() {
@@ -506,6 +508,14 @@ static void dist_finalize(ms_problem* P, int kind, double* hist) {
   launch_finalize(P->sc.p, kind, hist, P->ctx->st);
 }
 
+// y0 = K0^-1 f0: each rank streams its share of the packed inverse's tiles,
+// the partial y0 are summed over ranks (N_c doubles)
+static void coarse_solve(ms_precond* pc, const int* done, cudaStream_t st) {
+  launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st, pc->sym_t0, pc->sym_t1);
+  Comm* c = pc->prob->ctx->comm.get();
+  if (c && c->world > 1) c->allreduce_sum(pc->y0.p, pc->N_c, st);
+}
+
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
 // `restricted`: the cell restriction partials of r were already produced
 // (fused into the residual update); only their reduction remains.
@@ -538,7 +548,7 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
     if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
     pf.end(MS_PROF_RESTRICT, it, st, a);
     a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
-    launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st);
+    coarse_solve(pc, done, st);
     pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
   }
   a = pf.begin(MS_PROF_COMBINE, it, st);
@@ -1142,6 +1152,11 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     if (W > 1) P->ctx->comm->allreduce_sum(K0.p, (size_t)N * N, st);
     launch_symmetrize(N, K0.p, st);
     const int nt = div_up(N, kTile);
+    if (W > 1) {  // balanced contiguous share of the packed tiles
+      const int64_t ntl = packed_tiles(nt);
+      pc->sym_t0 = ntl * R / W;
+      pc->sym_t1 = ntl * (R + 1) / W;
+    }
     pc->K0inv.alloc((size_t)packed_tiles(nt) * kTile * kTile);
     DBuf<double> inv_work;
     inv_work.alloc(dense_spd_inverse_work_bytes(N) / sizeof(double));
@@ -1218,7 +1233,7 @@ int ms_precond_apply_coarse(ms_precond* pc, const double* r, double* z) {
   }
   launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st, pc->kc0, pc->kc1);
   if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
-  launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
+  coarse_solve(pc, nullptr, st);
   launch_combine(P->g, P->mask.p, nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, P->r.p, P->z.p,
                  nullptr, nullptr, nullptr, st, pc->C0, pc->C1);
   allgather_rows(P, P->z.p);

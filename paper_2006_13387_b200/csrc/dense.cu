@@ -316,10 +316,10 @@ void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work,
 // diagonal, v = X_IJ^T f_I (-> y_J); partials are reduced in a fixed order.
 __global__ void __launch_bounds__(256)
     k_symv_tiles(int N, int nt, const double* __restrict__ X, const double* __restrict__ f,
-                 double* __restrict__ part, const int* done) {
+                 double* __restrict__ part, const int* done, int64_t t_begin) {
   if (done && *(volatile const int*)done) return;
   __shared__ double sv[16][T + 1];
-  const int64_t t = blockIdx.x;
+  const int64_t t = t_begin + blockIdx.x;
   int i, j;
   tile_ij(t, i, j);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -371,13 +371,16 @@ __global__ void __launch_bounds__(256)
 constexpr int kRedGroups = 8;
 __global__ void __launch_bounds__(T* kRedGroups)
     k_symv_reduce(int N, int nt, const double* __restrict__ part, double* __restrict__ y,
-                  const int* done) {
+                  const int* done, int64_t t_begin, int64_t t_end) {
   if (done && *(volatile const int*)done) return;
   __shared__ double s[kRedGroups][T];
   const int I = blockIdx.x, r = threadIdx.x % T, grp = threadIdx.x / T;
   double acc = 0.0;
-  for (int t = grp; t < nt; t += kRedGroups)
-    acc += (t <= I) ? part[tile_index(I, t) * 2 * T + r] : part[tile_index(t, I) * 2 * T + T + r];
+  for (int t = grp; t < nt; t += kRedGroups) {
+    const int64_t ti = (t <= I) ? tile_index(I, t) : tile_index(t, I);
+    if (ti < t_begin || ti >= t_end) continue;  // another rank's tiles (sharded coarse solve)
+    acc += (t <= I) ? part[ti * 2 * T + r] : part[ti * 2 * T + T + r];
+  }
   s[grp][r] = acc;
   __syncthreads();
   const int row = I * T + threadIdx.x;
@@ -390,11 +393,13 @@ __global__ void __launch_bounds__(T* kRedGroups)
 }
 
 void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
-                        const int* done, cudaStream_t st) {
+                        const int* done, cudaStream_t st, int64_t t_begin, int64_t t_end) {
   if (N == 0) return;
   const int nt = div_up(N, T);
-  k_symv_tiles<<<(unsigned)packed_tiles(nt), 256, 0, st>>>(N, nt, X, f, part, done);
-  k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done);
+  if (t_end < 0) t_end = packed_tiles(nt);
+  if (t_end > t_begin)
+    k_symv_tiles<<<(unsigned)(t_end - t_begin), 256, 0, st>>>(N, nt, X, f, part, done, t_begin);
+  k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done, t_begin, t_end);
   MS_CUDA(cudaGetLastError());
 }
 

@@ -26,9 +26,11 @@ void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work,
                        cudaStream_t st);
 size_t dense_spd_inverse_work_bytes(int N);
 
-// y = X f for one packed symmetric matrix; `part` needs packed_tiles(nt)*2*64 doubles
+// y = X f for one packed symmetric matrix; `part` needs packed_tiles(nt)*2*64 doubles.
+// [t_begin, t_end): only these packed tiles contribute (a rank's share of a
+// sharded coarse solve; the caller sums y over ranks); default all.
 void launch_symv_packed(int N, const double* X, const double* f, double* y, double* part,
-                        const int* done, cudaStream_t st);
+                        const int* done, cudaStream_t st, int64_t t_begin = 0, int64_t t_end = -1);
 
 // level-1 band (unfactored, column-band layout of BandSys) -> packed tiles,
 // for systems [s0, s0 + B) into P (B matrices of nt tiles)
