@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--config", type=int, default=3, choices=(3, 4, 5),
                     help="BASELINE config: 3 (headline, 2048^2), 4 (4096x2048 MBB, eta 1e9), "
                          "5 (1024^2 50-step sequence with rebuild every step)")
-    ap.add_argument("--n", type=int, default=None, help="override the mesh size (nx; ny = nx/2 for config 4)")
+    ap.add_argument("--n", "--mesh-n", dest="n", type=int, default=None, help="override the mesh size (nx; ny = nx/2 for config 4)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-n", type=int, default=256)
@@ -64,6 +64,9 @@ def parse():
                     help="preconditioner variant (Table 1 tags); the headline is EH+Rot")
     ap.add_argument("--local-solver", choices=("banded", "dense"), default="banded",
                     help="level-1 local solves: banded Cholesky sweeps (default) or explicit packed inverses")
+    ap.add_argument("--comm", choices=("nccl", "callbacks"), default="nccl",
+                    help="multi-rank communicator: NCCL (one GPU per rank), or torch.distributed gloo host "
+                         "callbacks (tests the sharded path with ranks sharing one GPU)")
     ap.add_argument("--maxit", type=int, default=None,
                     help="PCG iteration cap per step (default 1000 for configs 3/4, whose solves need O(1e4) "
                          "iterations to reach 1e-8; 20000 for config 5, which solves every step to convergence)")
@@ -209,12 +212,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.comm == "callbacks":  # test mode: ranks may share a GPU, gloo host staging
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2006_13387_b200 import dist as D
 
-        D.init_nccl(local)  # strip-shard the ONE problem across the ranks (NCCL halos/allreduces)
+        if args.comm == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            D.init_nccl(local)  # strip-shard the ONE problem across the ranks (NCCL halos/allreduces)
+        else:
+            dist.init_process_group("gloo")
+            D.init_host_callbacks(local)
 
     def barrier():
         if world > 1:
@@ -263,7 +272,7 @@ def run_ours(args):
                            prof_cnt.ctypes.data_as(C.POINTER(C.c_longlong)))
     lib.ms_ctx_set_profiling(ctx, 0)
     if world > 1:
-        t = torch.tensor([ms_total], device="cuda")
+        t = torch.tensor([ms_total], device="cuda" if args.comm == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
 
@@ -279,7 +288,7 @@ def run_ours(args):
         e2e_ms += e0.elapsed_time(e1)
         e2e_iters += rep_e.iterations
     true_res = None
-    if rank == 0 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:  # every rank: the sharded operator apply is collective
         r = b_host - op.matrix @ x
         true_res = float(np.linalg.norm(r) / np.linalg.norm(b_host))
 
@@ -330,7 +339,8 @@ def run_ours(args):
                    "n_free": n_free, "iterations_per_step": it_step, "maxit": args.maxit, "converged": bool(conv), "coarse_dim": info["coarse_dim"],
                    "n_subdomains": info["n_subdomains"], "mode_counts_hist": np.bincount(info["mode_counts"], minlength=7).tolist(),
                    "l2": "inputs larger than L2 (level-1 factors %.1f GB)" % (F2 / 1e9),
-                   "parallelism": f"strips of subdomain rows x{world} (NCCL halos + allreduces)" if world > 1 else "1 GPU",
+                   "parallelism": (f"strips of subdomain rows x{world} ({'NCCL' if args.comm == 'nccl' else 'gloo host-callback'} halos + allreduces)"
+                                   if world > 1 else "1 GPU"),
                    "build_s": {"t_level1": info["t_level1"], "t_eig": info["t_eig"], "t_coarse": info["t_coarse"],
                                "wall": info.get("t_build_wall"), "max_eig_passes": info["max_eig_passes"],
                                "mean_eig_passes": info["mean_eig_passes"]},

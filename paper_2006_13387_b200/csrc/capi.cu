@@ -269,9 +269,11 @@ struct ms_problem {
   DBuf<double> partials;
   DBuf<double> hres, halpha, hbeta;
   int hcap = 0;
+  int hist_gen = 0;  // bumped when the history buffers move (captured graphs hold their addresses)
   // captured PCG chunk (CUDA graph) of plain CG solves; preconditioned solves
   // keep theirs in the ms_precond (it captures both objects' buffers)
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;
+  int graph_gen = 0;
   std::vector<std::pair<int, int>> captured;
   ~ms_problem() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -323,6 +325,7 @@ struct ms_precond {
   // packed K0^-1 tiles [sym_t0, sym_t1) of the sharded coarse solve (all on one rank)
   int64_t sym_t0 = 0, sym_t1 = -1;
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;  // captured PCG chunks for (prob, this)
+  int graph_gen = 0;  // prob->hist_gen the graphs were captured with
   std::vector<std::pair<int, int>> captured;
   ~ms_precond() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -646,7 +649,12 @@ int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_call
 int ms_copy(void* dst, const void* src, size_t bytes) {
   MS_API_BEGIN
   if (bytes && (!dst || !src)) throw Error(MS_E_INVALID, "null argument");
-  if (bytes) MS_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  if (bytes) {
+    MS_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+    // a pageable host->device cudaMemcpy may return before the DMA lands, and
+    // the solver's streams do not order against the legacy stream: complete it
+    MS_CUDA(cudaDeviceSynchronize());
+  }
   MS_API_END(nullptr)
 }
 
@@ -1339,6 +1347,22 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     P->halpha.alloc(std::max(maxit, 1));
     P->hbeta.alloc(std::max(maxit, 1));
     P->hcap = maxit + 1;
+    ++P->hist_gen;
+  }
+  // graphs captured against the previous history buffers must not be replayed
+  auto drop = [](cudaGraphExec_t& g) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  };
+  if (P->graph_gen != P->hist_gen) {
+    drop(P->gexec);
+    drop(P->gexec_prof);
+    P->graph_gen = P->hist_gen;
+  }
+  if (pc && pc->graph_gen != P->hist_gen) {
+    drop(pc->gexec);
+    drop(pc->gexec_prof);
+    pc->graph_gen = P->hist_gen;
   }
   load_free(P, b, P->r.p);  // r = b
   P->x.zero(st);

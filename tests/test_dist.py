@@ -141,3 +141,28 @@ def test_two_ranks_on_one_gpu_match_single_rank(tag):
         assert abs(iters - rep1.iterations) <= max(3, int(0.06 * rep1.iterations))
         assert np.linalg.norm(x - x1) <= 1e-7 * np.linalg.norm(x1)
     assert np.array_equal(res[0][0], res[1][0])
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_path_runs():
+    """bench.py under torchrun (2 ranks): strip sharding, sharded coarse solve,
+    max-over-ranks timing and the JSON line; ranks share the one GPU through
+    the host-callback communicator (--comm callbacks)."""
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    import json
+    import subprocess
+
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", "2",
+           "--steps", "1", "--warmup", "3", "--comm", "callbacks", "--mesh-n", "256", "--maxit", "16",
+           "--e2e-steps", "1"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["iterations_per_step"] == 16
+    # 16 iterations of a hard solve: the residual norm is not monotone, only finite
+    assert d["e2e"]["value"] > 0 and np.isfinite(d["config"]["true_rel_residual"])

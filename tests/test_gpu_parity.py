@@ -436,3 +436,20 @@ def test_elasticity_randomized_variant_matches_reference(eta):
     x, rep = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=2000)
     assert rep.converged and abs(rep.iterations - int(g["iters"])) <= 1
     assert rel(x, g["x"]) <= 1e-6
+
+
+def test_growing_maxit_reuses_preconditioner_safely():
+    """Solves with increasing maxit on one preconditioner grow the history
+    buffers; graphs captured against the old buffers must be recaptured
+    (regression: replaying them wrote to freed memory)."""
+    spec = configs.config1(seed=0, n=64, H=16, delta=2)
+    from paper_2006_13387_b200.solve import setup_spec
+
+    mesh, op, pre = setup_spec(spec)
+    b = spec.rhs()
+    for m in (5, 20, 100):
+        x, rep = G.pcg_solve(op, b, pre, tol=1e-14, maxit=m)
+        assert rep.iterations == m and np.all(np.isfinite(rep.alphas)) and np.all(np.isfinite(rep.betas))
+    mesh2, op2, pre2 = setup_spec(spec)
+    x2, rep2 = G.pcg_solve(op2, b, pre2, tol=1e-14, maxit=100)
+    assert np.array_equal(x, x2) and np.array_equal(rep.alphas, rep2.alphas)
