@@ -60,7 +60,8 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--variant", default="EH+Rot", choices=("EH+Rot", "EH", "EH+Rot;Rand", "HH+Rot", "HH"),
+    ap.add_argument("--variant", default="EH+Rot", choices=("EH+Rot", "EH", "EH+Rot;Rand", "HH+Rot", "HH", "EE",
+                                                            "EE;Rand"),
                     help="preconditioner variant (Table 1 tags); the headline is EH+Rot")
     ap.add_argument("--local-solver", choices=("banded", "dense"), default="banded",
                     help="level-1 local solves: banded Cholesky sweeps (default) or explicit packed inverses")
