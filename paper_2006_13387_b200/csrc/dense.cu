@@ -18,22 +18,23 @@
 namespace msgpu {
 
 constexpr int T = kTile;
-constexpr int kTT = 256;  // threads per tile CTA (16 x 16, 4 x 4 outputs each)
+constexpr int TP = T + 1;  // shared-memory tile pitch (padding: transposed stores are conflict-free)
+constexpr int kTT = 256;   // threads per tile CTA (16 x 16, 4 x 4 outputs each)
 
 struct TileAcc {
   double v[4][4];
 };
 
-// acc += sA * sB where sA[r][q], sB[q][c] are 64x64 row-major in smem
+// acc += sA * sB where sA[r][q], sB[q][c] are 64x64 row-major in smem (pitch TP)
 __device__ __forceinline__ void tile_mma(TileAcc& acc, const double* sA, const double* sB) {
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll 4
   for (int q = 0; q < T; ++q) {
     double a[4], b[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = sA[(ty + 16 * i) * T + q];
+    for (int i = 0; i < 4; ++i) a[i] = sA[(ty + 16 * i) * TP + q];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sB[q * T + tx + 16 * j];
+    for (int j = 0; j < 4; ++j) b[j] = sB[q * TP + tx + 16 * j];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -41,14 +42,14 @@ __device__ __forceinline__ void tile_mma(TileAcc& acc, const double* sA, const d
   }
 }
 
-// load a 64x64 tile (row-major, contiguous) into smem, optionally transposed
+// load a 64x64 tile (row-major, contiguous) into smem (pitch TP), optionally transposed
 __device__ __forceinline__ void tile_load(double* s, const double* g, bool trans) {
   for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
     const int r = t / T, c = t % T;
     if (trans)
-      s[c * T + r] = g[t];
+      s[c * TP + r] = g[t];
     else
-      s[t] = g[t];
+      s[r * TP + c] = g[t];
   }
 }
 
@@ -127,32 +128,32 @@ __global__ void __launch_bounds__(kTT) k_potrf_tile(int k, int nt, double* __res
                                                     double* __restrict__ W, int* fail) {
   extern __shared__ double sm[];
   double* a = sm;
-  double* inv = sm + T * T;
+  double* inv = sm + T * TP;  // pitch T
   const int64_t mw = packed_words(nt);
   double* D = P + blockIdx.y * mw + tile_index(k, k) * T * T;
   tile_load(a, D, false);
   __syncthreads();
   for (int c = 0; c < T; ++c) {
-    double d = a[c * T + c];
+    double d = a[c * TP + c];
     if (!(d > 0.0)) {
       if (threadIdx.x == 0) atomicCAS(fail, 0, (int)(blockIdx.y * nt * T + k * T + c + 1));
       d = 1.0;
     }
     const double s = sqrt(d);
     __syncthreads();
-    if (threadIdx.x == 0) a[c * T + c] = s;
-    for (int r = c + 1 + threadIdx.x; r < T; r += blockDim.x) a[r * T + c] /= s;
+    if (threadIdx.x == 0) a[c * TP + c] = s;
+    for (int r = c + 1 + threadIdx.x; r < T; r += blockDim.x) a[r * TP + c] /= s;
     __syncthreads();
     for (int t = threadIdx.x; t < (T - c - 1) * (T - c - 1); t += blockDim.x) {
       const int r = c + 1 + t / (T - c - 1), q = c + 1 + t % (T - c - 1);
-      if (q <= r) a[r * T + q] -= a[r * T + c] * a[q * T + c];
+      if (q <= r) a[r * TP + q] -= a[r * TP + c] * a[q * TP + c];
     }
     __syncthreads();
   }
   for (int t = threadIdx.x; t < T * T; t += blockDim.x) {
     const int r = t / T, c = t % T;
-    if (c > r) a[t] = 0.0;
-    D[t] = a[t];
+    if (c > r) a[r * TP + c] = 0.0;
+    D[t] = a[r * TP + c];
   }
   __syncthreads();
   // inverse of the lower-triangular tile, column j by thread j
@@ -160,8 +161,8 @@ __global__ void __launch_bounds__(kTT) k_potrf_tile(int k, int nt, double* __res
     const int j = threadIdx.x;
     for (int r = 0; r < T; ++r) {
       double s = (r == j) ? 1.0 : 0.0;
-      for (int q = j; q < r; ++q) s -= a[r * T + q] * inv[q * T + j];
-      inv[r * T + j] = (r < j) ? 0.0 : s / a[r * T + r];
+      for (int q = j; q < r; ++q) s -= a[r * TP + q] * inv[q * T + j];
+      inv[r * T + j] = (r < j) ? 0.0 : s / a[r * TP + r];
     }
   }
   __syncthreads();
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kTT) k_trsm_tiles(int k, int nt, double* __res
                                                     const double* __restrict__ W) {
   extern __shared__ double sm[];
   double* sA = sm;
-  double* sB = sm + T * T;
+  double* sB = sm + T * TP;
   const int64_t mw = packed_words(nt);
   P += blockIdx.y * mw;
   W += blockIdx.y * mw;
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kTT) k_trsm_tiles(int k, int nt, double* __res
 __global__ void __launch_bounds__(kTT) k_syrk_tiles(int k, int nt, double* __restrict__ P) {
   extern __shared__ double sm[];
   double* sA = sm;
-  double* sB = sm + T * T;
+  double* sB = sm + T * TP;
   P += blockIdx.y * packed_words(nt);
   const int m = nt - k - 1;
   int ii, jj;
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kTT) k_trtri_tiles(int d, int nt, const double
                                                      double* __restrict__ W) {
   extern __shared__ double sm[];
   double* sA = sm;
-  double* sB = sm + T * T;
+  double* sB = sm + T * TP;
   const int64_t mw = packed_words(nt);
   P += blockIdx.y * mw;
   W += blockIdx.y * mw;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(kTT) k_trtri_tiles(int d, int nt, const double
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) sB[(ty + 16 * a) * T + tx + 16 * b] = acc.v[a][b];
+      for (int b = 0; b < 4; ++b) sB[(ty + 16 * a) * TP + tx + 16 * b] = acc.v[a][b];
   }
   tile_load(sA, W + tile_index(i, i) * T * T, false);
   __syncthreads();
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kTT) k_lauum_tiles(int nt, const double* __res
                                                      double* __restrict__ X) {
   extern __shared__ double sm[];
   double* sA = sm;
-  double* sB = sm + T * T;
+  double* sB = sm + T * TP;
   const int64_t mw = packed_words(nt);
   W += blockIdx.y * mw;
   X += blockIdx.y * mw;
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kTT) k_lauum_tiles(int nt, const double* __res
 void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, int* fail,
                                cudaStream_t st) {
   if (nt == 0 || B == 0) return;
-  const size_t smem = 2 * T * T * sizeof(double);
+  const size_t smem = 2 * T * TP * sizeof(double);
   static bool attr = false;
   if (!attr) {
     MS_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
