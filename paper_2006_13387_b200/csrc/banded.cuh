@@ -70,4 +70,107 @@ void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, in
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
                      const int* done, cudaStream_t st);
 
+// ---------------------------------------------------------------------------
+// One warp's banded sweep over a factor read from global memory (L2/L1),
+// window in registers.  Column-oriented (axpy) substitution: after w_k is
+// known, rows k+1..k+bw receive acc[k+j] -= L[k+j][k] * w_k.  Row r's
+// accumulator lives in lane r % 32, register slot (r/32 - current block) --
+// slots rotate every 32 steps, so all register indices are compile-time
+// constants inside the unrolled 32-step block.  Per step the only cross-lane
+// traffic is one shuffle broadcasting w_k from its owner lane; there is no
+// shared memory and no warp barrier, so the band columns, prefetched PD steps
+// ahead, stay in flight.  The backward sweep is the same recurrence on the
+// row band Lr in reversed numbering (row' = n-1-row).  NR right-hand sides
+// share each band read (y interleaved: y[row * NR + c]).
+constexpr int kPD = 4;
+
+template <int T, int NR, int PD, bool REV>
+__device__ __forceinline__ void band_sweep(const double* __restrict__ L, int n, int bw,
+                                           double* __restrict__ y, int lane) {
+  constexpr int R = T + 1;  // register slots (blocks of 32 rows) per lane
+  const int S = bw + 1;
+  auto lcol = [&](int k) -> const double* {
+    return REV ? L + (int64_t)(n - 1 - k) * S : L + (int64_t)k * S;
+  };
+  auto yat = [&](int r, int c) -> double* { return y + (int64_t)(REV ? (n - 1 - r) : r) * NR + c; };
+
+  double acc[NR][R], rnext[NR];
+#pragma unroll
+  for (int c = 0; c < NR; ++c) {
+#pragma unroll
+    for (int s = 0; s < R - 1; ++s) {
+      const int r = 32 * s + lane;
+      acc[c][s] = r < n ? *yat(r, c) : 0.0;
+    }
+    acc[c][R - 1] = 0.0;
+    rnext[c] = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane, c) : 0.0;
+  }
+
+  // prefetch ring: band values of the next PD steps
+  double lv[PD][T], dv[PD];
+  auto load = [&](int k, int u, double(&l)[T], double& d) {
+    const int base = ((lane - u - 1) & 31) + 1;
+    const bool ok = k < n;
+    const double* col = lcol(ok ? k : 0);
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int j = base + 32 * t;
+      l[t] = (ok && j <= bw) ? __ldg(col + j) : 0.0;
+    }
+    d = ok ? __ldg(col) : 0.0;
+  };
+#pragma unroll
+  for (int u = 0; u < PD; ++u) load(u, u, lv[u], dv[u]);
+
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    // rows of block (k0/32 + R-1) enter the window
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      acc[c][R - 1] = rnext[c];
+      const int r = k0 + 32 * R + lane;
+      rnext[c] = r < n ? *yat(r, c) : 0.0;
+    }
+    double wout[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) wout[c] = 0.0;
+#pragma unroll 1
+    for (int u0 = 0; u0 < 32; u0 += PD) {
+#pragma unroll
+     for (int q = 0; q < PD; ++q) {
+      const int u = u0 + q;
+      const int k = k0 + u;
+      if (k < n) {
+        const bool hi = lane <= u;  // row k+base lies in the next block
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double wloc = acc[c][0] * dv[q];
+          const double wk = __shfl_sync(0xffffffffu, wloc, u);
+          if (lane == u) wout[c] = wk;
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const double upd = lv[q][t] * wk;  // zero when k+j is outside the band
+            if (hi) {
+              if (t + 1 < R) acc[c][t + 1] -= upd;
+            } else {
+              acc[c][t] -= upd;
+            }
+          }
+        }
+        load(k + PD, (u + PD) & 31, lv[q], dv[q]);
+      }
+     }
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      if (k0 + lane < n) *yat(k0 + lane, c) = wout[c];
+      // rotate the register window by one block
+#pragma unroll
+      for (int s = 0; s < R - 1; ++s) acc[c][s] = acc[c][s + 1];
+      acc[c][R - 1] = 0.0;
+    }
+  }
+}
+
+
+
 }  // namespace msgpu

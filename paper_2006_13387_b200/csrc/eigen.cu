@@ -246,6 +246,26 @@ __device__ void band_solve_block(const BandSys& s, const double* __restrict__ Lc
   __syncthreads();
 }
 
+// The P columns of W (column-major, length n) solved in place, one warp per
+// column: forward sweep on Lc, backward on Lr, each warp with its own
+// register window and no block barrier between steps (band_sweep,
+// banded.cuh).  The warps move through the same factor in near lockstep, so
+// its columns are served from L1/L2.  T register slots: bw <= 32 T.
+template <int T>
+__device__ void band_solve_cols(const BandSys& s, const double* __restrict__ Lc,
+                                const double* __restrict__ Lr, double* W, int ncols) {
+  __syncthreads();  // W complete
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < ncols; c += nw) {
+    double* y = W + (int64_t)c * s.n;
+    band_sweep<T, 1, kPD, false>(Lc + s.foff, s.n, s.bw, y, lane);
+    __syncwarp();
+    band_sweep<T, 1, kPD, true>(Lr + s.foff, s.n, s.bw, y, lane);
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // cyclic Jacobi on the P x P symmetric matrix A (row stride P+1), one warp;
 // relative-threshold rotations keep small eigenvalues of graded matrices
 // accurate.  On exit: ritz ascending, V columns in the same order.
@@ -304,6 +324,7 @@ __device__ void jacobi_warp(double* A, double* V, double* ritz, int* order) {
   __syncwarp();
 }
 
+template <int T>
 __global__ void __launch_bounds__(kEigThreads)
     k_subspace(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
                HeatParam hp, EigBatch eb, int max_pass, double tol) {
@@ -370,7 +391,7 @@ __global__ void __launch_bounds__(kEigThreads)
     }
     __syncthreads();
     // (2) W <- (K + sigma M)^{-1} W
-    band_solve_block(s, eb.Lc, eb.Lr, W, win);
+    band_solve_cols<T>(s, eb.Lc, eb.Lr, W, P);
     // (3) M-orthonormalise W into X (CGS2 against the constant and earlier columns)
     for (int c = 0; c < P; ++c) {
       double* w = W + (int64_t)c * n;
@@ -513,6 +534,30 @@ __global__ void __launch_bounds__(kEigThreads)
   }
 }
 
+// register slots T of the eigensolver's band sweeps: bw <= 32 T
+template <template <int> class Launch, typename... A>
+static void band_dispatch(int max_bw, A... args) {
+  switch (std::max(1, div_up(max_bw, 32))) {
+    case 1: Launch<1>::run(args...); break;
+    case 2: Launch<2>::run(args...); break;
+    case 3: Launch<3>::run(args...); break;
+    case 4: Launch<4>::run(args...); break;
+    case 5: Launch<5>::run(args...); break;
+    case 6: Launch<6>::run(args...); break;
+    default: throw Error(-1, "neighbourhood band too wide for the eigensolver (coarse blocks <= 46 elements)");
+  }
+}
+
+template <int T>
+struct SubspaceLaunch {
+  static void run(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
+                  int max_pass, double tol, size_t smem, cudaStream_t st) {
+    MS_CUDA(cudaFuncSetAttribute(k_subspace<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_subspace<T><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, max_pass, tol);
+    MS_CUDA(cudaGetLastError());
+  }
+};
+
 void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
                      const EigBatch& b, int max_pass, double tol, cudaStream_t st) {
   if (b.nk == 0) return;
@@ -526,9 +571,7 @@ void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const 
                                         (P + 1) * 8 + (P + 1) + 2 * P * (P + 1) + 2 * P + 4) +
                       sizeof(int) * P + (size_t)max_n + 16;
   if (smem > 220 * 1024) throw Error(-1, "neighbourhood too large for the eigensolver tile");
-  MS_CUDA(cudaFuncSetAttribute(k_subspace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_subspace<<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, max_pass, tol);
-  MS_CUDA(cudaGetLastError());
+  band_dispatch<SubspaceLaunch>(max_bw, g, E, hdir, hp, b, max_pass, tol, smem, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -581,6 +624,7 @@ __device__ void cgs2_euclid(double* cols, int ncols, int n, double* red, double*
   }
 }
 
+template <int T>
 __global__ void __launch_bounds__(kEigThreads)
     k_randomized(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
                  HeatParam hp, EigBatch eb, const double* __restrict__ F, int ns, int nlx) {
@@ -677,7 +721,7 @@ __global__ void __launch_bounds__(kEigThreads)
     }
     __syncthreads();
   };
-  band_solve_block(s, eb.Lc, eb.Lr, W, win);
+  band_solve_cols<T>(s, eb.Lc, eb.Lr, W, ns);
   deflate();
   for (int pass = 1; pass < 4; ++pass) {
     cgs2_euclid(W, ns, n, red, dots, nullptr);
@@ -688,7 +732,7 @@ __global__ void __launch_bounds__(kEigThreads)
     __syncthreads();
     for (int t = threadIdx.x; t < n * ns; t += blockDim.x) W[t] = X[t];
     __syncthreads();
-    band_solve_block(s, eb.Lc, eb.Lr, W, win);
+    band_solve_cols<T>(s, eb.Lc, eb.Lr, W, ns);
     deflate();
   }
   // Q = orthonormal basis of [U, Z] (columns normalised first, 1e-10 rank cut)
@@ -828,6 +872,16 @@ void launch_rand_sigma(const Grid& g, const double* E, const uint8_t* hdir, cons
   MS_CUDA(cudaGetLastError());
 }
 
+template <int T>
+struct RandomizedLaunch {
+  static void run(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
+                  const double* F, int ns, int nlx, size_t smem, cudaStream_t st) {
+    MS_CUDA(cudaFuncSetAttribute(k_randomized<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_randomized<T><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, nlx);
+    MS_CUDA(cudaGetLastError());
+  }
+};
+
 void launch_randomized(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
                        const EigBatch& b, const double* F, int ns, cudaStream_t st) {
   if (b.nk == 0) return;
@@ -837,9 +891,7 @@ void launch_randomized(const Grid& g, const double* E, const uint8_t* hdir, cons
   const size_t smem = sizeof(double) * ((size_t)(2 * b.mex) * (2 * b.mey) + (size_t)(max_bw + 1) * P +
                                         (P + 1) * 8 + (P + 1) + 2 * P * (P + 1) + 2 * P + 4) +
                       sizeof(int) * P + (size_t)NLx * NLy + 16;
-  MS_CUDA(cudaFuncSetAttribute(k_randomized, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_randomized<<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, NLx);
-  MS_CUDA(cudaGetLastError());
+  band_dispatch<RandomizedLaunch>(max_bw, g, E, hdir, hp, b, F, ns, NLx, smem, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1181,7 +1233,7 @@ __global__ void __launch_bounds__(kEigThreads)
     }
     __syncthreads();
     // (2) W <- (K + sigma M)^{-1} W
-    band_solve_block<KJ>(s, eb.Lc, eb.Lr, W, m.win);
+    band_solve_cols<KJ>(s, eb.Lc, eb.Lr, W, P);
     // (3) M-orthonormalise W into X against the locked modes and earlier columns
     for (int c = 0; c < P; ++c) {
       double* w = W + (int64_t)c * n;
@@ -1296,19 +1348,6 @@ __global__ void __launch_bounds__(kEigThreads)
   }
 }
 
-template <template <int> class Launch, typename... A>
-static void el_dispatch(int max_bw, A... args) {
-  const int kj = div_up(max_bw, 16);
-  if (kj <= 4)
-    Launch<4>::run(args...);
-  else if (kj <= 8)
-    Launch<8>::run(args...);
-  else if (kj <= 12)
-    Launch<12>::run(args...);
-  else
-    throw Error(-1, "elasticity neighbourhood band too wide for the eigensolver (coarse blocks <= 46 elements)");
-}
-
 template <int KJ>
 struct SubspaceElLaunch {
   static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
@@ -1324,7 +1363,7 @@ void launch_subspace_el(const Grid& g, const double* E, const uint8_t* hdir, con
   if (b.nk == 0) return;
   const size_t smem = el_smem_bytes(b.mex, b.mey, max_bw);
   if (smem > 220 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
-  el_dispatch<SubspaceElLaunch>(max_bw, g, E, hdir, ep, b, max_pass, tol, smem, st);
+  band_dispatch<SubspaceElLaunch>(max_bw, g, E, hdir, ep, b, max_pass, tol, smem, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1534,7 +1573,7 @@ __global__ void __launch_bounds__(kEigThreads)
   }
   __syncthreads();
   project(MZ, Z);  // F -= MZ G^-1 Z^T F
-  band_solve_block<KJ>(s, eb.Lc, eb.Lr, W, m.win);
+  band_solve_cols<KJ>(s, eb.Lc, eb.Lr, W, ns);
   project(Z, MZ);  // deflate
   for (int pass = 1; pass < 4; ++pass) {
     cgs2_euclid(W, ns, n, m.red, m.dots, nullptr);
@@ -1545,7 +1584,7 @@ __global__ void __launch_bounds__(kEigThreads)
     __syncthreads();
     for (int t = threadIdx.x; t < n * ns; t += blockDim.x) W[t] = X[t];
     __syncthreads();
-    band_solve_block<KJ>(s, eb.Lc, eb.Lr, W, m.win);
+    band_solve_cols<KJ>(s, eb.Lc, eb.Lr, W, ns);
     project(Z, MZ);
   }
   // Q = orthonormal basis of [U, Z]
@@ -1665,7 +1704,7 @@ void launch_randomized_el(const Grid& g, const double* E, const uint8_t* hdir, c
   if (ns + 3 > P) throw Error(-1, "too many snapshots for the randomized elasticity eigensolver (<= 13)");
   const size_t smem = el_smem_bytes(b.mex, b.mey, max_bw);
   if (smem > 200 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
-  el_dispatch<RandElLaunch>(max_bw, g, E, hdir, ep, b, F, ns, 2 * b.mex + 1, smem, st);
+  band_dispatch<RandElLaunch>(max_bw, g, E, hdir, ep, b, F, ns, 2 * b.mex + 1, smem, st);
 }
 
 }  // namespace msgpu

