@@ -323,6 +323,10 @@ def main():
         adapter_case(configs.config3(seed=0, n=128, H=32, delta=2), "ref_config3_n128.npz")
     if "cfg2s" in which:
         adapter_case(configs.config2(seed=0, eta=1e4, n=128, H=32, delta=2), "ref_config2_n128.npz")
+    if "sweep" in which:  # config 2's contrast sweep ends and a config-5 density step, at 128^2
+        adapter_case(configs.config2(seed=0, eta=1e2, n=128, H=32, delta=2), "ref_config2_n128_eta1e2.npz")
+        adapter_case(configs.config2(seed=0, eta=1e8, n=128, H=32, delta=2), "ref_config2_n128_eta1e8.npz")
+        adapter_case(configs.config5(seed=0, step=3, n=128, H=32, delta=2), "ref_config5_n128_step3.npz")
 
 
 if __name__ == "__main__":

@@ -178,7 +178,10 @@ def test_deterministic_solves():
 
 @pytest.mark.parametrize("name,tag", [("ref_config1.npz", "EH+Rot"), ("ref_mbb_64x32.npz", "EH+Rot"),
                                       ("ref_config2_n128.npz", "EH+Rot"), ("ref_config3_n128.npz", "EH+Rot"),
-                                      ("ref_config1_hhrot.npz", "HH+Rot")])
+                                      ("ref_config1_hhrot.npz", "HH+Rot"),
+                                      ("ref_config2_n128_eta1e2.npz", "EH+Rot"),
+                                      ("ref_config2_n128_eta1e8.npz", "EH+Rot"),
+                                      ("ref_config5_n128_step3.npz", "EH+Rot")])
 def test_baseline_config_against_reference(name, tag):
     g = load_golden(name)
     spec = spec_from_golden(g)
@@ -188,7 +191,10 @@ def test_baseline_config_against_reference(name, tag):
     assert pre.coarse_dim == int(g["coarse_dim"])
     assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
     z = pre.apply(g["apply_r"])
-    assert rel(z, g["apply_z"]) <= 1e-7
+    # local-solve and coarse-solve round-off grows with the contrast (measured
+    # 2.2e-7 at eta 1e8)
+    eta = spec.E_max / spec.E_min
+    assert rel(z, g["apply_z"]) <= max(1e-7, 1e-14 * eta)
     x, rep = G.pcg_solve(op, spec.rhs(), pre, tol=float(g["tol"]), maxit=5000)
     # Iteration counts of these ill-conditioned solves (kappa ~ 1e7, hundreds to
     # thousands of iterations) are chaotic under round-off: the reference moves

@@ -200,3 +200,4 @@ def test_elasticity_eigen_variants_match_reference(name):
     x, rep = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=2000)
     assert rep.iterations == int(g["iters"])
     assert np.linalg.norm(x - g["x"]) <= 1e-9 * np.linalg.norm(g["x"])
+
