@@ -19,8 +19,6 @@ namespace msgpu {
 
 constexpr int P = kEigBlock;
 constexpr int kEigThreads = 256;
-constexpr int kJmax = 8;  // band offsets per thread group: bw <= 128
-constexpr int kEPD = 4;   // software prefetch depth of the banded sweeps
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
@@ -147,101 +145,6 @@ __device__ __forceinline__ void block_sum_multi(double (&v)[P + 1], int nv, doub
 #pragma unroll
     for (int w = 0; w < kEigThreads / 32; ++w) s += red[threadIdx.x * 8 + w];
     out[threadIdx.x] = s;
-  }
-  __syncthreads();
-}
-
-// multi-RHS banded sweeps in place on W (P columns, column-major, length n);
-// KJ band offsets per 16-thread group: bw <= 16 KJ
-template <int KJ = kJmax>
-__device__ void band_solve_block(const BandSys& s, const double* __restrict__ Lc,
-                                 const double* __restrict__ Lr, double* W, double* win) {
-  const int n = s.n, bw = s.bw, S = bw + 1;
-  const int c = threadIdx.x & (P - 1), grp = threadIdx.x / P;  // 16 groups
-  double* Wc = W + (int64_t)c * n;
-  double lv[kEPD][KJ], dv[kEPD], rv[kEPD];
-  // ---------------- forward ----------------
-  {
-    const double* L = Lc + s.foff;
-    for (int t = threadIdx.x; t < min(bw, n) * P; t += blockDim.x)
-      win[(t / P) * P + (t % P)] = W[(int64_t)(t % P) * n + t / P];
-    __syncthreads();
-    auto load = [&](int k, double(&l)[KJ], double& d, double& rr) {
-#pragma unroll
-      for (int q = 0; q < KJ; ++q) {
-        const int j = grp + 1 + 16 * q;
-        l[q] = (k < n && j <= bw) ? __ldg(L + (int64_t)k * S + j) : 0.0;
-      }
-      d = (k < n) ? __ldg(L + (int64_t)k * S) : 0.0;
-      rr = (k + bw < n && k < n) ? Wc[k + bw] : 0.0;
-    };
-#pragma unroll
-    for (int u = 0; u < kEPD; ++u) load(u, lv[u], dv[u], rv[u]);
-    for (int k0 = 0; k0 < n; k0 += kEPD) {
-#pragma unroll
-      for (int u = 0; u < kEPD; ++u) {
-        const int k = k0 + u;
-        if (k < n) {
-          const int sk = k % S;
-          const double wk = win[sk * P + c] * dv[u];
-#pragma unroll
-          for (int q = 0; q < KJ; ++q) {
-            const int j = grp + 1 + 16 * q;
-            if (j <= bw) {
-              const int sl = (sk + j) >= S ? sk + j - S : sk + j;
-              if (j == bw) win[sl * P + c] = rv[u];
-              win[sl * P + c] -= lv[u][q] * wk;
-            }
-          }
-          if (grp == 0) Wc[k] = wk;
-          __syncthreads();
-          load(k + kEPD, lv[u], dv[u], rv[u]);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // ---------------- backward ----------------
-  {
-    const double* L = Lr + s.foff;
-    for (int t = threadIdx.x; t < min(bw, n) * P; t += blockDim.x) {
-      const int row = n - 1 - t / P, cc = t % P;
-      win[(row % S) * P + cc] = W[(int64_t)cc * n + row];
-    }
-    __syncthreads();
-    auto load = [&](int k, double(&l)[KJ], double& d, double& rr) {
-#pragma unroll
-      for (int q = 0; q < KJ; ++q) {
-        const int j = grp + 1 + 16 * q;
-        l[q] = (k >= 0 && j <= bw) ? __ldg(L + (int64_t)k * S + j) : 0.0;
-      }
-      d = (k >= 0) ? __ldg(L + (int64_t)k * S) : 0.0;
-      rr = (k >= 0 && k - bw >= 0) ? Wc[k - bw] : 0.0;
-    };
-#pragma unroll
-    for (int u = 0; u < kEPD; ++u) load(n - 1 - u, lv[u], dv[u], rv[u]);
-    for (int k0 = 0; k0 < n; k0 += kEPD) {
-#pragma unroll
-      for (int u = 0; u < kEPD; ++u) {
-        const int k = n - 1 - (k0 + u);
-        if (k >= 0) {
-          const int sk = k % S;
-          const double yk = win[sk * P + c] * dv[u];
-#pragma unroll
-          for (int q = 0; q < KJ; ++q) {
-            const int j = grp + 1 + 16 * q;
-            if (j <= bw && k - j >= 0) {
-              const int sl = (sk - j) < 0 ? sk - j + S : sk - j;
-              if (j == bw) win[sl * P + c] = rv[u];
-              win[sl * P + c] -= lv[u][q] * yk;
-            }
-          }
-          if (grp == 0) Wc[k] = yk;
-          __syncthreads();
-          load(k - kEPD, lv[u], dv[u], rv[u]);
-        }
-      }
-    }
   }
   __syncthreads();
 }
@@ -566,7 +469,6 @@ void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const 
   const int NLx = 2 * b.mex + 1, NLy = 2 * b.mey + 1;
   max_bw = std::min(NLx, NLy) + 1;
   max_n = NLx * NLy;
-  if (max_bw > 16 * kJmax) throw Error(-1, "heat band too wide for the eigensolver sweep");
   const size_t smem = sizeof(double) * ((size_t)(2 * b.mex) * (2 * b.mey) + (size_t)(max_bw + 1) * P +
                                         (P + 1) * 8 + (P + 1) + 2 * P * (P + 1) + 2 * P + 4) +
                       sizeof(int) * P + (size_t)max_n + 16;
