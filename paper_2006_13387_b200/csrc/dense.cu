@@ -273,8 +273,11 @@ void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, i
                                cudaStream_t st) {
   if (nt == 0 || B == 0) return;
   const size_t smem = 2 * T * TP * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr_done[64] = {};  // function attributes are per device
+  int dev = 0;
+  MS_CUDA(cudaGetDevice(&dev));
+  bool& attr = attr_done[dev < 64 ? dev : 63];
+  if (!attr || dev >= 64) {
     MS_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MS_CUDA(cudaFuncSetAttribute(k_trsm_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MS_CUDA(cudaFuncSetAttribute(k_syrk_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
