@@ -138,6 +138,8 @@ enum {
   MS_PROF_N = 8
 };
 int ms_ctx_set_profiling(ms_ctx* ctx, int on); /* also resets the counters */
+/* record only the components in `mask` (bit 1 << MS_PROF_*); 0 = off */
+int ms_ctx_set_profiling_mask(ms_ctx* ctx, unsigned mask);
 int ms_ctx_profile_get(const ms_ctx* ctx, double* ms, long long* counts); /* MS_PROF_N each */
 /* the context's cudaStream_t (for event timing by callers) */
 void* ms_ctx_stream(const ms_ctx* ctx);

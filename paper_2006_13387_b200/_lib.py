@@ -30,7 +30,7 @@ EXPORTS = (
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
     "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
     "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_strip_rows", "ms_copy",
-    "ms_halo_plan", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
+    "ms_halo_plan", "ms_ctx_set_profiling_mask", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
     "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot",
 )
 
@@ -124,6 +124,7 @@ def load(path: str | os.PathLike | None = None):
         "ms_precond_coarse_matrix": (C.c_int, [vp, dp]),
         "ms_pcg_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, vp, C.POINTER(Report), dp, dp, dp]),
         "ms_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
+        "ms_ctx_set_profiling_mask": (C.c_int, [vp, C.c_uint]),
         "ms_ctx_profile_get": (C.c_int, [vp, dp, C.POINTER(C.c_longlong)]),
         "ms_ctx_stream": (C.c_void_p, [vp]),
         "ms_precond_bench": (C.c_int, [vp, C.c_int, dp]),

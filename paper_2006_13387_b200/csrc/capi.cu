@@ -157,6 +157,7 @@ void heat_elements(double h, HeatParam& hp) {
 // after each replay the captured pairs are re-queued with their iteration.
 struct Prof {
   bool on = false;
+  unsigned mask = ~0u;  // components (1 << MS_PROF_*) that record events
   double ms[MS_PROF_N] = {};
   long long cnt[MS_PROF_N] = {};
   std::vector<cudaEvent_t> pool;
@@ -192,13 +193,13 @@ struct Prof {
     return e;
   }
   cudaEvent_t begin(int comp, int it, cudaStream_t st) {
-    if (!on) return nullptr;
+    if (!on || !((mask >> comp) & 1u)) return nullptr;
     cudaEvent_t a = it >= 0 ? slot(comp, it, 0) : get();
     record(a, st);
     return a;
   }
   void end(int comp, int it, cudaStream_t st, cudaEvent_t a) {
-    if (!on) return;
+    if (!on || !((mask >> comp) & 1u)) return;
     cudaEvent_t b = it >= 0 ? slot(comp, it, 1) : get();
     record(b, st);
     if (capturing)
@@ -274,6 +275,7 @@ struct ms_problem {
   // keep theirs in the ms_precond (it captures both objects' buffers)
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;
   int graph_gen = 0;
+  unsigned prof_mask = 0;  // Prof::mask the profiling graph was captured with
   std::vector<std::pair<int, int>> captured;
   ~ms_problem() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -326,6 +328,7 @@ struct ms_precond {
   int64_t sym_t0 = 0, sym_t1 = -1;
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;  // captured PCG chunks for (prob, this)
   int graph_gen = 0;  // prob->hist_gen the graphs were captured with
+  unsigned prof_mask = 0;  // Prof::mask the profiling graph was captured with
   std::vector<std::pair<int, int>> captured;
   ~ms_precond() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -603,10 +606,13 @@ int ms_ctx_create(int device, ms_ctx** out) {
   MS_API_END(c)
 }
 
-int ms_ctx_set_profiling(ms_ctx* ctx, int on) {
+int ms_ctx_set_profiling(ms_ctx* ctx, int on) { return ms_ctx_set_profiling_mask(ctx, on ? ~0u : 0u); }
+
+int ms_ctx_set_profiling_mask(ms_ctx* ctx, unsigned mask) {
   MS_API_BEGIN
   if (!ctx) throw Error(MS_E_INVALID, "null context");
-  ctx->prof.on = on != 0;
+  ctx->prof.on = mask != 0u;
+  ctx->prof.mask = mask;
   for (int i = 0; i < MS_PROF_N; ++i) {
     ctx->prof.ms[i] = 0.0;
     ctx->prof.cnt[i] = 0;
@@ -1363,6 +1369,12 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     drop(pc->gexec);
     drop(pc->gexec_prof);
     pc->graph_gen = P->hist_gen;
+  }
+  // a profiling graph records the events of the mask it was captured with
+  unsigned& pmask = pc ? pc->prof_mask : P->prof_mask;
+  if (P->ctx->prof.on && pmask != P->ctx->prof.mask) {
+    drop(pc ? pc->gexec_prof : P->gexec_prof);
+    pmask = P->ctx->prof.mask;
   }
   load_free(P, b, P->r.p);  // r = b
   P->x.zero(st);
