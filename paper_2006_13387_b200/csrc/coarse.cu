@@ -91,86 +91,7 @@ __device__ __forceinline__ int basis_count(const CoarseDev& cd, int nsel) {
   return cd.vec ? nsel : 2 * nsel + cd.enrich;
 }
 
-// ---------------------------------------------------------------------------
-// f0 = R0 r, one CTA per centre.  The centre's NM selected modes are a
-// template parameter (dispatched per CTA), so the 2*NM+1 accumulators live in
-// registers and are reduced together: one shuffle tree per value and a
-// single shared-memory pass.  Node rows map onto lanes (coalesced r/psi/chi).
 
-template <int NM>
-__device__ __forceinline__ void restrict_center(const Grid& g, const CoarseDev& cd, int k, int I,
-                                                int J, const double* __restrict__ r,
-                                                double* __restrict__ f0, double* sred) {
-  constexpr int NB = 2 * NM + 1;
-  const int NL = cd.NLx * cd.NLy;
-  const double* chi = cd.chi + (int64_t)k * NL;
-  const double* psi = cd.psi + cd.psioff[k];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double acc[NB];
-#pragma unroll
-  for (int t = 0; t < NB; ++t) acc[t] = 0.0;
-  const int ax0 = (I - 1) * cd.mex, by0 = (J - 1) * cd.mey;
-  for (int lb = warp; lb < cd.NLy; lb += nw) {
-    const int b = by0 + lb;
-    const double* rrow = r + (int64_t)b * g.nnx + ax0;
-    for (int la = lane; la < cd.NLx; la += 32) {
-      const int ln = lb * cd.NLx + la;
-      const double ch = chi[ln];
-      const double rx = rrow[la], ry = rrow[la + g.n_nodes];
-#pragma unroll
-      for (int m = 0; m < NM; ++m) {
-        const double v = ch * psi[(int64_t)m * NL + ln];
-        acc[2 * m] += v * rx;
-        acc[2 * m + 1] += v * ry;
-      }
-      double ex, ey;
-      rot_xy(cd, I, J, ax0 + la, b, ex, ey);
-      acc[NB - 1] += __dmul_rn(ch, ex) * rx + __dmul_rn(ch, ey) * ry;
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < NB; ++t) {
-    const double v = warp_sum(acc[t]);
-    if (lane == 0) sred[t * 8 + warp] = v;
-  }
-  __syncthreads();
-  const int nb = 2 * NM + cd.enrich;
-  if (threadIdx.x < nb) {
-    const int t = threadIdx.x < 2 * NM ? threadIdx.x : NB - 1;
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += sred[t * 8 + w];
-    f0[basis_row(cd, k, threadIdx.x, NM)] = s;
-  }
-}
-
-__global__ void __launch_bounds__(256)
-    k_restrict(Grid g, CoarseDev cd, const double* __restrict__ r, double* __restrict__ f0,
-               const int* done) {
-  if (done && *(volatile const int*)done) return;
-  __shared__ double sred[(2 * kMaxModes + 1) * 8];
-  const int k = blockIdx.x;
-  const int I = k % (cd.Nx - 1) + 1, J = k / (cd.Nx - 1) + 1;
-  switch (cd.nsel[k]) {
-    case 1: restrict_center<1>(g, cd, k, I, J, r, f0, sred); break;
-    case 2: restrict_center<2>(g, cd, k, I, J, r, f0, sred); break;
-    case 3: restrict_center<3>(g, cd, k, I, J, r, f0, sred); break;
-    case 4: restrict_center<4>(g, cd, k, I, J, r, f0, sred); break;
-    case 5: restrict_center<5>(g, cd, k, I, J, r, f0, sred); break;
-    default: restrict_center<6>(g, cd, k, I, J, r, f0, sred); break;
-  }
-}
-
-void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double* f0,
-                     const int* done, cudaStream_t st) {
-  if (cd.n_centers == 0) return;
-  k_restrict<<<cd.n_centers, 256, 0, st>>>(g, cd, r, f0, done);
-  MS_CUDA(cudaGetLastError());
-}
-
-// ---------------------------------------------------------------------------
-// combine: node-centric sum of the overlapping local solutions (in the
-// reference's J-major subdomain order, schwarz.py:79-81), then the coarse
-// prolongation; fused r.z reduction for PCG.
 // ---------------------------------------------------------------------------
 // Node-major coarse tables: for each node, the chi (and chi * psi_0) of the
 // 4 corner centres of its coarse cell, so the per-iteration restriction and

@@ -69,9 +69,6 @@ void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cu
 // chi table, bit-identical to the reference's PoU (grid.py:172-207)
 void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStream_t st);
 
-// f0 = R0 r (coarse.py:156-158, restriction half)
-void launch_restrict(const Grid& g, const CoarseDev& cd, const double* r, double* f0,
-                     const int* done, cudaStream_t st);
 
 // z = sum_s R_s^T y_s (level-1, J-major order) + R0^T y0 (if cd) ; masked;
 // optionally r.z -> beta (PCG mode when sc != nullptr).
