@@ -165,6 +165,10 @@ typedef struct ms_comm_callbacks {
 int ms_nccl_unique_id(void* out128);
 int ms_ctx_attach_nccl(ms_ctx* ctx, int rank, int world, const void* unique_id128);
 int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_callbacks* cb);
+/* exercises the attached communicator: out4 = {allreduce of rank+1, allreduce
+ * of 2 (twice through a captured graph when the communicator is capturable),
+ * broadcast of 10*rank+7 from rank 0, the left neighbour's rank via send/recv} */
+int ms_comm_selftest(ms_ctx* ctx, double* out4);
 /* synchronous copy between host and/or device buffers (callback helpers) */
 int ms_copy(void* dst, const void* src, size_t bytes);
 /* node-row halo plan of rank `rank` owning rows [lo, hi] of 0..ny, depth k:

@@ -29,7 +29,7 @@ EXPORTS = (
     "ms_operator_apply", "ms_precond_build", "ms_precond_destroy", "ms_precond_apply",
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
     "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
-    "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_strip_rows", "ms_copy",
+    "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_comm_selftest", "ms_strip_rows", "ms_copy",
     "ms_halo_plan", "ms_ctx_set_profiling_mask", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
     "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot",
 )
@@ -131,6 +131,7 @@ def load(path: str | os.PathLike | None = None):
         "ms_nccl_unique_id": (C.c_int, [C.c_char_p]),
         "ms_ctx_attach_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
         "ms_ctx_attach_callbacks": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(CommCallbacks)]),
+        "ms_comm_selftest": (C.c_int, [vp, dp]),
         "ms_strip_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
         "ms_copy": (C.c_int, [vp, vp, C.c_size_t]),
         "ms_halo_plan": (C.c_int, [C.c_int] * 6 + [ip]),

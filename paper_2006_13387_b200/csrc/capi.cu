@@ -645,6 +645,40 @@ int ms_ctx_attach_nccl(ms_ctx* ctx, int rank, int world, const void* unique_id12
   MS_API_END(ctx)
 }
 
+int ms_comm_selftest(ms_ctx* ctx, double* out4) {
+  MS_API_BEGIN
+  if (!ctx || !out4) throw Error(MS_E_INVALID, "null argument");
+  Comm* c = ctx->comm.get();
+  if (!c) throw Error(MS_E_STATE, "no communicator attached");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const cudaStream_t st = ctx->st;
+  const int R = c->rank, W = c->world;
+  DBuf<double> buf;
+  buf.alloc(5);
+  const double h[5] = {(double)(R + 1), 2.0, (double)(10 * R + 7), (double)R, -1.0};
+  buf.upload(h, 5, st);
+  c->allreduce_sum(buf.p, 2, st);                        // -> W(W+1)/2, 2W
+  c->broadcast(buf.p + 2, sizeof(double), 0, st);        // -> 7 (root 0)
+  c->sendrecv2(buf.p + 3, sizeof(double), (R + 1) % W, buf.p + 4, sizeof(double), (R + W - 1) % W,
+               nullptr, 0, -1, nullptr, 0, -1, st);      // ring: receive the left neighbour's rank
+  if (c->capturable()) {                                 // the PCG chunks capture collectives in graphs
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    MS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    c->allreduce_sum(buf.p + 1, 1, st);
+    MS_CUDA(cudaStreamEndCapture(st, &graph));
+    MS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    MS_CUDA(cudaGraphLaunch(exec, st));                  // -> 2W * W
+    MS_CUDA(cudaGraphExecDestroy(exec));
+    MS_CUDA(cudaGraphDestroy(graph));
+  }
+  double r[5];
+  MS_CUDA(cudaMemcpyAsync(r, buf.p, sizeof(r), cudaMemcpyDeviceToHost, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < 4; ++i) out4[i] = r[i == 3 ? 4 : i];
+  MS_API_END(ctx)
+}
+
 int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_callbacks* cb) {
   MS_API_BEGIN
   if (!ctx || world < 1 || rank < 0 || rank >= world) throw Error(MS_E_INVALID, "bad argument");

@@ -166,3 +166,61 @@ def test_bench_multi_rank_path_runs():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["iterations_per_step"] == 16
     # 16 iterations of a hard solve: the residual norm is not monotone, only finite
     assert d["e2e"]["value"] > 0 and np.isfinite(d["config"]["true_rel_residual"])
+
+
+@pytest.mark.gpu
+def test_nccl_communicator_single_rank_selftest():
+    """The NCCL communicator (dlopen, unique id, ncclCommInitRank, allreduce,
+    broadcast, grouped send/recv, collectives captured in a CUDA graph) on a
+    one-rank communicator: the only NCCL configuration one GPU allows."""
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    import ctypes as C
+
+    sys.path.insert(0, str(ROOT))
+    from paper_2006_13387_b200 import _lib
+
+    lib = _lib.load()
+    ctx = C.c_void_p()
+    _lib.check(lib.ms_ctx_create(0, C.byref(ctx)))
+    try:
+        uid = C.create_string_buffer(128)
+        _lib.check(lib.ms_nccl_unique_id(uid))
+        _lib.check(lib.ms_ctx_attach_nccl(ctx, 0, 1, uid.raw), ctx)
+        out = np.zeros(4)
+        _lib.check(lib.ms_comm_selftest(ctx, _lib.dptr(out)), ctx)
+        assert out.tolist() == [1.0, 2.0, 7.0, 0.0]
+    finally:
+        lib.ms_ctx_destroy(ctx)
+
+
+def _selftest_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    _init(rank, world, port)
+    try:
+        from paper_2006_13387_b200 import _lib, dist as D
+
+        ctx = D.init_host_callbacks(0)
+        out = np.zeros(4)
+        _lib.check(_lib.load().ms_comm_selftest(ctx.handle, _lib.dptr(out)), ctx.handle)
+        q.put((rank, out.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_callback_communicator_two_rank_selftest():
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_selftest_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        assert res[r] == [3.0, 4.0, 7.0, float(1 - r)]
