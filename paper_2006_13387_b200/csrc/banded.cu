@@ -338,10 +338,10 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
         const double* col = sb + (REV ? (cnt - 1 - q) : q) * S;
         const int jl = lane - u;
         double m[R];
-        m[0] = (jl >= 1 && jl <= bw) ? col[jl] : 0.0;
+        m[0] = lds_or_zero(col + jl, jl >= 1 && jl <= bw);
 #pragma unroll
-        for (int s = 1; s < R; ++s) m[s] = (jl + 32 * s <= bw) ? col[jl + 32 * s] : 0.0;
-        const double d = col[0];
+        for (int s = 1; s < R; ++s) m[s] = lds_or_zero(col + jl + 32 * s, jl + 32 * s <= bw);
+        const double d = lds_or_zero(col, true);
         if (lane == u) dsave = d;
 #pragma unroll
         for (int c = 0; c < NR; ++c) {

@@ -114,6 +114,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// shared-memory load of a double, 0.0 when !pred: zero and predicated load
+// into the same register (the C ternary compiles to zero + load into a
+// temporary + two predicated moves).  volatile: stays between the mbarrier
+// wait and the refill of the stage it reads (both volatile asm).
+__device__ __forceinline__ double lds_or_zero(const double* p, bool pred) {
+  double v;
+  asm volatile(
+      "{\n"
+      ".reg .pred q;\n"
+      "setp.ne.u32 q, %2, 0;\n"
+      "mov.b64 %0, 0;\n"
+      "@q ld.shared.f64 %0, [%1];\n"
+      "}\n"
+      : "=d"(v)
+      : "r"(smem_u32(p)), "r"((uint32_t)pred));
+  return v;
+}
+
 // global -> shared bulk copy; bytes and both addresses multiples of 16
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
