@@ -836,8 +836,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->heat_dir.assign(o->heat_dirichlet_nodes, o->heat_dirichlet_nodes + o->n_heat_dirichlet);
   pc->opts.heat_dirichlet_nodes = nullptr;
   pc->opts.snapshots = nullptr;
-  if (o->randomized && (!o->snapshots || o->n_snapshots < 1 || o->n_snapshots + 1 > kEigBlock - 2))
-    throw Error(MS_E_INVALID, "randomized eigensolver needs 1..13 snapshots and the forcings array");
+  if (o->randomized && (!o->snapshots || o->n_snapshots < 1 || o->n_snapshots + 3 > 32))
+    throw Error(MS_E_INVALID, "randomized eigensolver needs 1..29 snapshots and the forcings array");
   DBuf<int> fail;
   fail.alloc(1);
 
@@ -1059,7 +1059,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       if (!hLc.p || hLc.n < (size_t)foff) {
         hLc.alloc(foff);
         hLr.alloc(foff);
-        work.alloc((size_t)nk * (2 * kEigBlock + (el ? 6 : 0)) * NLd);
+        const int wb = o->randomized ? randomized_block(o->n_snapshots) : kEigBlock;
+        work.alloc((size_t)nk * (2 * wb + (el ? 6 : 0)) * NLd);
         evecs.alloc((size_t)nk * kNeig * NLd);
       }
       hsysd.upload(hs.data(), nk, st);

@@ -149,6 +149,26 @@ __device__ __forceinline__ void block_sum_multi(double (&v)[P + 1], int nv, doub
   __syncthreads();
 }
 
+template <int NV>
+__device__ __forceinline__ void block_sum_nv(double (&v)[NV], int nv, double* red, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    if (t < nv) {
+      double x = warp_sum(v[t]);
+      if (lane == 0) red[t * 8 + wid] = x;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kEigThreads / 32; ++w) s += red[threadIdx.x * 8 + w];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
 // The P columns of W (column-major, length n) solved in place, one warp per
 // column: forward sweep on Lc, backward on Lr, each warp with its own
 // register window and no block barrier between steps (band_sweep,
@@ -169,19 +189,20 @@ __device__ void band_solve_cols(const BandSys& s, const double* __restrict__ Lc,
   __syncthreads();
 }
 
-// cyclic Jacobi on the P x P symmetric matrix A (row stride P+1), one warp;
+// cyclic Jacobi on the B x B symmetric matrix A (row stride B+1), one warp;
 // relative-threshold rotations keep small eigenvalues of graded matrices
 // accurate.  On exit: ritz ascending, V columns in the same order.
+template <int B = P>
 __device__ void jacobi_warp(double* A, double* V, double* ritz, int* order) {
   const int lane = threadIdx.x & 31;
-  constexpr int LD = P + 1;
-  if (lane < P)
-    for (int j = 0; j < P; ++j) V[lane * LD + j] = (lane == j) ? 1.0 : 0.0;
+  constexpr int LD = B + 1;
+  if (lane < B)
+    for (int j = 0; j < B; ++j) V[lane * LD + j] = (lane == j) ? 1.0 : 0.0;
   __syncwarp();
   for (int sweep = 0; sweep < 60; ++sweep) {
     bool rotated = false;
-    for (int p = 0; p < P - 1; ++p)
-      for (int q = p + 1; q < P; ++q) {
+    for (int p = 0; p < B - 1; ++p)
+      for (int q = p + 1; q < B; ++q) {
         const double app = A[p * LD + p], aqq = A[q * LD + q], apq = A[p * LD + q];
         if (apq == 0.0 || fabs(apq) <= 1e-17 * sqrt(fabs(app) * fabs(aqq))) continue;
         rotated = true;
@@ -189,7 +210,7 @@ __device__ void jacobi_warp(double* A, double* V, double* ritz, int* order) {
         const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
         const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
         __syncwarp();
-        if (lane < P && lane != p && lane != q) {
+        if (lane < B && lane != p && lane != q) {
           const double alp = A[lane * LD + p], alq = A[lane * LD + q];
           const double nlp = c * alp - s * alq, nlq = s * alp + c * alq;
           A[lane * LD + p] = nlp;
@@ -197,7 +218,7 @@ __device__ void jacobi_warp(double* A, double* V, double* ritz, int* order) {
           A[lane * LD + q] = nlq;
           A[q * LD + lane] = nlq;
         }
-        if (lane < P) {
+        if (lane < B) {
           const double vlp = V[lane * LD + p], vlq = V[lane * LD + q];
           V[lane * LD + p] = c * vlp - s * vlq;
           V[lane * LD + q] = s * vlp + c * vlq;
@@ -214,15 +235,15 @@ __device__ void jacobi_warp(double* A, double* V, double* ritz, int* order) {
     if (!rotated) break;
   }
   if (lane == 0) {
-    for (int i = 0; i < P; ++i) order[i] = i;
-    for (int i = 0; i < P; ++i)  // selection sort (stable on ties by index)
-      for (int j = i + 1; j < P; ++j)
+    for (int i = 0; i < B; ++i) order[i] = i;
+    for (int i = 0; i < B; ++i)  // selection sort (stable on ties by index)
+      for (int j = i + 1; j < B; ++j)
         if (A[order[j] * LD + order[j]] < A[order[i] * LD + order[i]]) {
           const int t = order[i];
           order[i] = order[j];
           order[j] = t;
         }
-    for (int i = 0; i < P; ++i) ritz[i] = A[order[i] * LD + order[i]];
+    for (int i = 0; i < B; ++i) ritz[i] = A[order[i] * LD + order[i]];
   }
   __syncwarp();
 }
@@ -483,28 +504,29 @@ void launch_subspace(const Grid& g, const double* E, const uint8_t* hdir, const 
 // F -= MZ (Z^T F)/G; U = deflate(B^-1 F); 3 x { U = orth(U); U = deflate(B^-1 M U) };
 // Q = orthonormal basis of [U, Z] (1e-10 rank cut); Rayleigh-Ritz on (Q^T K Q,
 // Q^T M Q).  Z = 1 on free nodes, deflate(X) = X - Z (MZ^T X)/G.
+template <int B = P>
 __device__ void cgs2_euclid(double* cols, int ncols, int n, double* red, double* dots,
                             double* keep_flag) {
   // in place Euclidean CGS2 of `ncols` columns; zeroes columns that vanish
-  double v[P + 1];
+  double v[B + 1];
   for (int c = 0; c < ncols; ++c) {
     double* w = cols + (int64_t)c * n;
     double nrm0 = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) nrm0 += w[i] * w[i];
 #pragma unroll
-    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
     v[0] = nrm0;
-    block_sum_multi(v, 1, red, dots);
+    block_sum_nv<B + 1>(v, 1, red, dots);
     nrm0 = dots[0];
     for (int rep = 0; rep < 2; ++rep) {
 #pragma unroll
-      for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+      for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
 #pragma unroll
-        for (int l = 0; l < P; ++l)
+        for (int l = 0; l < B; ++l)
           if (l < c) v[l] += cols[(int64_t)l * n + i] * w[i];
       }
-      block_sum_multi(v, P + 1, red, dots);
+      block_sum_nv<B + 1>(v, B + 1, red, dots);
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         double x = w[i];
         for (int l = 0; l < c; ++l) x -= dots[l] * cols[(int64_t)l * n + i];
@@ -515,9 +537,9 @@ __device__ void cgs2_euclid(double* cols, int ncols, int n, double* red, double*
     double nrm = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) nrm += w[i] * w[i];
 #pragma unroll
-    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
     v[0] = nrm;
-    block_sum_multi(v, 1, red, dots);
+    block_sum_nv<B + 1>(v, 1, red, dots);
     const bool ok = dots[0] > 1e-20 * nrm0 && dots[0] > 0.0;
     const double inv = ok ? 1.0 / sqrt(dots[0]) : 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] *= inv;
@@ -526,7 +548,7 @@ __device__ void cgs2_euclid(double* cols, int ncols, int n, double* red, double*
   }
 }
 
-template <int T>
+template <int T, int B>
 __global__ void __launch_bounds__(kEigThreads)
     k_randomized(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir,
                  HeatParam hp, EigBatch eb, const double* __restrict__ F, int ns, int nlx) {
@@ -535,20 +557,20 @@ __global__ void __launch_bounds__(kEigThreads)
   const BandSys s = eb.sys[kb];
   const int n = s.n, S = s.bw + 1;
   const int nex = 2 * eb.mex, ney = 2 * eb.mey;
-  constexpr int LD = P + 1;
+  constexpr int LD = B + 1;
   double* sE = sm;
   double* win = sE + nex * ney;
-  double* red = win + S * P;
-  double* dots = red + (P + 1) * 8;
-  double* Am = dots + (P + 1);
-  double* Vm = Am + P * LD;
-  double* ritz = Vm + P * LD;
-  double* keep = ritz + P;  // P flags
-  double* misc = keep + P;
+  double* red = win + S * B;
+  double* dots = red + (B + 1) * 8;
+  double* Am = dots + (B + 1);
+  double* Vm = Am + B * LD;
+  double* ritz = Vm + B * LD;
+  double* keep = ritz + B;  // B flags
+  double* misc = keep + B;
   int* order = reinterpret_cast<int*>(misc + 4);
-  uint8_t* dir = reinterpret_cast<uint8_t*>(order + P);
+  uint8_t* dir = reinterpret_cast<uint8_t*>(order + B);
   __shared__ double hlap[16], hmel[16];
-  __shared__ double Lm[P][P + 1], Cm[P][P + 1];
+  __shared__ double Lm[B][B + 1], Cm[B][B + 1];
   if (threadIdx.x < 16) {
     hlap[threadIdx.x] = hp.lap[threadIdx.x];
     hmel[threadIdx.x] = hp.mel[threadIdx.x];
@@ -562,28 +584,28 @@ __global__ void __launch_bounds__(kEigThreads)
   }
   __syncthreads();
   const EigCtx ctx{s, n, nex, ney, sE, dir, hlap, hmel};
-  double* X = eb.work + (int64_t)kb * 2 * P * n;  // cols 0..P-3: basis; P-2: MZ; P-1: Z
-  double* W = X + (int64_t)P * n;                 // solve workspace
-  double* Zc = X + (int64_t)(P - 1) * n;
-  double* MZ = X + (int64_t)(P - 2) * n;
-  double v[P + 1];
+  double* X = eb.work + (int64_t)kb * 2 * B * n;  // cols 0..B-3: basis; B-2: MZ; B-1: Z
+  double* W = X + (int64_t)B * n;                 // solve workspace
+  double* Zc = X + (int64_t)(B - 1) * n;
+  double* MZ = X + (int64_t)(B - 2) * n;
+  double v[B + 1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) Zc[i] = dir[i] ? 0.0 : 1.0;
   __syncthreads();
   double G;
   {
 #pragma unroll
-    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const double mz = dir[i] ? 0.0 : stencil(ctx, Zc, i, hmel);
       MZ[i] = mz;
       v[0] += Zc[i] * mz;
     }
-    block_sum_multi(v, 1, red, dots);
+    block_sum_nv<B + 1>(v, 1, red, dots);
     G = dots[0];
   }
   // forcings (lexicographic node index in F -> band order)
   const double* Fk = F + (int64_t)kb * ns * (nlx * (n / nlx));
-  for (int t = threadIdx.x; t < n * P; t += blockDim.x) {
+  for (int t = threadIdx.x; t < n * B; t += blockDim.x) {
     const int c = t / n, i = t % n;
     double val = 0.0;
     if (c < ns && !dir[i]) {
@@ -597,12 +619,12 @@ __global__ void __launch_bounds__(kEigThreads)
   // F -= MZ (Z^T F) / G
   {
 #pragma unroll
-    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x)
 #pragma unroll
-      for (int c = 0; c < P; ++c)
+      for (int c = 0; c < B; ++c)
         if (c < ns) v[c] += Zc[i] * W[(int64_t)c * n + i];
-    block_sum_multi(v, P + 1, red, dots);
+    block_sum_nv<B + 1>(v, B + 1, red, dots);
     for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
       const int c = t / n, i = t % n;
       W[t] -= MZ[i] * (dots[c] / G);
@@ -611,12 +633,12 @@ __global__ void __launch_bounds__(kEigThreads)
   }
   auto deflate = [&]() {
 #pragma unroll
-    for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+    for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x)
 #pragma unroll
-      for (int c = 0; c < P; ++c)
+      for (int c = 0; c < B; ++c)
         if (c < ns) v[c] += MZ[i] * W[(int64_t)c * n + i];
-    block_sum_multi(v, P + 1, red, dots);
+    block_sum_nv<B + 1>(v, B + 1, red, dots);
     for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
       const int c = t / n, i = t % n;
       W[t] -= Zc[i] * (dots[c] / G);
@@ -626,7 +648,7 @@ __global__ void __launch_bounds__(kEigThreads)
   band_solve_cols<T>(s, eb.Lc, eb.Lr, W, ns);
   deflate();
   for (int pass = 1; pass < 4; ++pass) {
-    cgs2_euclid(W, ns, n, red, dots, nullptr);
+    cgs2_euclid<B>(W, ns, n, red, dots, nullptr);
     for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
       const int c = t / n, i = t % n;
       X[t] = dir[i] ? 0.0 : stencil(ctx, W + (int64_t)c * n, i, hmel);
@@ -644,7 +666,7 @@ __global__ void __launch_bounds__(kEigThreads)
     X[t] = (c < ns) ? W[t] : Zc[i];
   }
   __syncthreads();
-  cgs2_euclid(X, m0, n, red, dots, keep);
+  cgs2_euclid<B>(X, m0, n, red, dots, keep);
   int m = 0;
   if (threadIdx.x == 0) {
     // compact kept columns to the front (order preserved)
@@ -666,15 +688,15 @@ __global__ void __launch_bounds__(kEigThreads)
     const double* coef = pass == 0 ? hlap : hmel;
     for (int c = 0; c < m; ++c) {
 #pragma unroll
-      for (int l = 0; l < P + 1; ++l) v[l] = 0.0;
+      for (int l = 0; l < B + 1; ++l) v[l] = 0.0;
       const double* xc = X + (int64_t)c * n;
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double ax = dir[i] ? 0.0 : stencil(ctx, xc, i, coef);
 #pragma unroll
-        for (int l = 0; l < P; ++l)
+        for (int l = 0; l < B; ++l)
           if (l <= c) v[l] += ax * X[(int64_t)l * n + i];
       }
-      block_sum_multi(v, c + 1, red, dots);
+      block_sum_nv<B + 1>(v, c + 1, red, dots);
       if (threadIdx.x <= c) {
         if (pass == 0)
           Am[threadIdx.x * LD + c] = Am[c * LD + threadIdx.x] = dots[threadIdx.x];
@@ -685,7 +707,7 @@ __global__ void __launch_bounds__(kEigThreads)
     }
   }
   // generalized m x m eigenproblem: Mr = L L^T, C = L^-1 Kr L^-T (thread 0),
-  // Jacobi on C padded to P x P with a huge diagonal
+  // Jacobi on C padded to B x B with a huge diagonal
   if (threadIdx.x == 0) {
     for (int i = 0; i < m; ++i)
       for (int j = 0; j <= i; ++j) {
@@ -706,14 +728,14 @@ __global__ void __launch_bounds__(kEigThreads)
         for (int q = 0; q < j; ++q) a -= Am[i * LD + q] * Lm[j][q];
         Am[i * LD + j] = a / Lm[j][j];  // reuse Am as C (row i done before being read)
       }
-    for (int i = 0; i < P; ++i)
-      for (int j = 0; j < P; ++j)
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < B; ++j)
         if (i >= m || j >= m) Am[i * LD + j] = (i == j) ? 1e300 : 0.0;
     for (int i = 0; i < m; ++i)
       for (int j = 0; j < i; ++j) Am[i * LD + j] = Am[j * LD + i] = 0.5 * (Am[i * LD + j] + Am[j * LD + i]);
   }
   __syncthreads();
-  if (threadIdx.x < 32) jacobi_warp(Am, Vm, ritz, order);
+  if (threadIdx.x < 32) jacobi_warp<B>(Am, Vm, ritz, order);
   __syncthreads();
   // Ritz vectors: x = Q (L^-T y), y = Vm[:, order[c]]
   if (threadIdx.x == 0) {
@@ -774,26 +796,39 @@ void launch_rand_sigma(const Grid& g, const double* E, const uint8_t* hdir, cons
   MS_CUDA(cudaGetLastError());
 }
 
+// block size of the randomized solvers: 16 while the snapshots fit next to
+// the kernel candidates (the common n_max + 5 = 11), else 32
+int randomized_block(int ns) { return ns + 3 <= kEigBlock ? kEigBlock : 32; }
+
 template <int T>
 struct RandomizedLaunch {
-  static void run(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
-                  const double* F, int ns, int nlx, size_t smem, cudaStream_t st) {
-    MS_CUDA(cudaFuncSetAttribute(k_randomized<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_randomized<T><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, nlx);
+  template <int B>
+  static void go(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
+                 const double* F, int ns, int nlx, int max_bw, cudaStream_t st) {
+    const int NLy = 2 * b.mey + 1;
+    const size_t smem = sizeof(double) * ((size_t)(2 * b.mex) * (2 * b.mey) + (size_t)(max_bw + 1) * B +
+                                          (B + 1) * 8 + (B + 1) + 2 * B * (B + 1) + 2 * B + 4) +
+                        sizeof(int) * B + (size_t)nlx * NLy + 16;
+    MS_CUDA(cudaFuncSetAttribute(k_randomized<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_randomized<T, B><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, nlx);
     MS_CUDA(cudaGetLastError());
+  }
+  static void run(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
+                  const double* F, int ns, int nlx, int max_bw, cudaStream_t st) {
+    if (randomized_block(ns) == kEigBlock)
+      go<kEigBlock>(g, E, hdir, hp, b, F, ns, nlx, max_bw, st);
+    else
+      go<32>(g, E, hdir, hp, b, F, ns, nlx, max_bw, st);
   }
 };
 
 void launch_randomized(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
                        const EigBatch& b, const double* F, int ns, cudaStream_t st) {
   if (b.nk == 0) return;
-  if (ns + 1 > P - 2) throw Error(-1, "too many snapshots for the randomized eigensolver (<= 13)");
+  if (ns + 3 > 32) throw Error(-1, "too many snapshots for the randomized eigensolver (<= 29)");
   const int NLx = 2 * b.mex + 1, NLy = 2 * b.mey + 1;
   const int max_bw = std::min(NLx, NLy) + 1;
-  const size_t smem = sizeof(double) * ((size_t)(2 * b.mex) * (2 * b.mey) + (size_t)(max_bw + 1) * P +
-                                        (P + 1) * 8 + (P + 1) + 2 * P * (P + 1) + 2 * P + 4) +
-                      sizeof(int) * P + (size_t)NLx * NLy + 16;
-  band_dispatch<RandomizedLaunch>(max_bw, g, E, hdir, hp, b, F, ns, NLx, smem, st);
+  band_dispatch<RandomizedLaunch>(max_bw, g, E, hdir, hp, b, F, ns, NLx, max_bw, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -894,26 +929,6 @@ void launch_compact_psi(const EigBatch& b, int NLx, const int* nsel, const int64
 // (spectral.py:37-45, assembly.py:262-273) -- are M-orthonormalised, locked
 // and deflated, so the iteration only resolves the remaining kNeig - 3 pairs.
 
-template <int NV>
-__device__ __forceinline__ void block_sum_nv(double (&v)[NV], int nv, double* red, double* out) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int t = 0; t < NV; ++t) {
-    if (t < nv) {
-      double x = warp_sum(v[t]);
-      if (lane == 0) red[t * 8 + wid] = x;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < nv) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kEigThreads / 32; ++w) s += red[threadIdx.x * 8 + w];
-    out[threadIdx.x] = s;
-  }
-  __syncthreads();
-}
-
 struct EigCtxE {
   BandSys s;
   int n, nex, ney;
@@ -1010,28 +1025,32 @@ struct ElSmem {
 };
 constexpr int kElNV = P + 3;  // reduction width: P block columns + 3 kernel modes
 
+template <int B = P>
 __device__ __forceinline__ ElSmem el_smem(double* sm, int nex, int ney, int S, int NL) {
+  constexpr int NV = B + 3;
   ElSmem m;
   m.sE = sm;
   m.win = m.sE + nex * ney;
-  m.red = m.win + S * P;
-  m.dots = m.red + kElNV * 8;
-  m.Am = m.dots + kElNV;
-  m.Vm = m.Am + P * (P + 1);
-  m.ritz = m.Vm + P * (P + 1);
-  m.ritz_old = m.ritz + P;
-  m.misc = m.ritz_old + P;
+  m.red = m.win + S * B;
+  m.dots = m.red + NV * 8;
+  m.Am = m.dots + NV;
+  m.Vm = m.Am + B * (B + 1);
+  m.ritz = m.Vm + B * (B + 1);
+  m.ritz_old = m.ritz + B;
+  m.misc = m.ritz_old + B;
   m.order = reinterpret_cast<int*>(m.misc + 4);
-  m.dirn = reinterpret_cast<uint8_t*>(m.order + P);
+  m.dirn = reinterpret_cast<uint8_t*>(m.order + B);
   (void)NL;
   return m;
 }
 
+template <int B = P>
 static size_t el_smem_bytes(int mex, int mey, int max_bw) {
+  constexpr int NV = B + 3;
   const int NL = (2 * mex + 1) * (2 * mey + 1);
-  return sizeof(double) * ((size_t)(2 * mex) * (2 * mey) + (size_t)(max_bw + 1) * P + kElNV * 8 + kElNV +
-                           2 * P * (P + 1) + 2 * P + 4) +
-         sizeof(int) * P + (size_t)NL + 16;
+  return sizeof(double) * ((size_t)(2 * mex) * (2 * mey) + (size_t)(max_bw + 1) * B + NV * 8 + NV +
+                           2 * B * (B + 1) + 2 * B + 4) +
+         sizeof(int) * B + (size_t)NL + 16;
 }
 
 // M-orthonormal rigid-body modes Zo (3 columns) and MZo = M Zo, CGS2 in the M
@@ -1367,7 +1386,7 @@ void launch_rand_sigma_el(const Grid& g, const double* E, const uint8_t* hdir, c
   MS_CUDA(cudaGetLastError());
 }
 
-template <int KJ>
+template <int KJ, int B>
 __global__ void __launch_bounds__(kEigThreads)
     k_randomized_el(Grid g, const double* __restrict__ E, const uint8_t* __restrict__ hdir, ElastParam ep,
                     EigBatch eb, const double* __restrict__ F, int ns, int nlx) {
@@ -1376,10 +1395,10 @@ __global__ void __launch_bounds__(kEigThreads)
   const BandSys s = eb.sys[kb];
   const int n = s.n, S = s.bw + 1, NLn = n / 2;
   const int nex = 2 * eb.mex, ney = 2 * eb.mey;
-  constexpr int LD = P + 1;
-  const ElSmem m = el_smem(sm, nex, ney, S, NLn);
-  __shared__ double ske[64], smel[16], Gi[9], keep[P];
-  __shared__ double Lm[P][P + 1], Cm[P][P + 1];
+  constexpr int LD = B + 1;
+  const ElSmem m = el_smem<B>(sm, nex, ney, S, NLn);
+  __shared__ double ske[64], smel[16], Gi[9], keep[B];
+  __shared__ double Lm[B][B + 1], Cm[B][B + 1];
   if (threadIdx.x < 64) ske[threadIdx.x] = ep.ke[threadIdx.x];
   if (threadIdx.x < 16) smel[threadIdx.x] = ep.mel[threadIdx.x];
   for (int t = threadIdx.x; t < nex * ney; t += blockDim.x)
@@ -1391,14 +1410,14 @@ __global__ void __launch_bounds__(kEigThreads)
   }
   __syncthreads();
   const EigCtxE ctx{s, n, nex, ney, m.sE, m.dirn, ske, smel};
-  double* X = eb.work + (int64_t)kb * (2 * P + 6) * n;
-  double* W = X + (int64_t)P * n;
-  double* Z = W + (int64_t)P * n;
+  double* X = eb.work + (int64_t)kb * (2 * B + 6) * n;
+  double* W = X + (int64_t)B * n;
+  double* Z = W + (int64_t)B * n;
   double* MZ = Z + 3 * (int64_t)n;
-  double v[kElNV];
+  double v[(B + 3)];
   auto zero_v = [&]() {
 #pragma unroll
-    for (int l = 0; l < kElNV; ++l) v[l] = 0.0;
+    for (int l = 0; l < (B + 3); ++l) v[l] = 0.0;
   };
   // Z on the free dofs (rotation about the neighbourhood centre), MZ, G^-1
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1463,7 +1482,7 @@ __global__ void __launch_bounds__(kEigThreads)
   // forcings: [ns][2 NL] x-plane then y-plane (lexicographic) -> band order
   const int NLd = 2 * NLn;
   const double* Fk = F + (int64_t)kb * ns * NLd;
-  for (int t = threadIdx.x; t < n * P; t += blockDim.x) {
+  for (int t = threadIdx.x; t < n * B; t += blockDim.x) {
     const int c = t / n, i = t % n;
     double val = 0.0;
     if (c < ns && !m.dirn[i >> 1]) {
@@ -1478,7 +1497,7 @@ __global__ void __launch_bounds__(kEigThreads)
   band_solve_cols<KJ>(s, eb.Lc, eb.Lr, W, ns);
   project(Z, MZ);  // deflate
   for (int pass = 1; pass < 4; ++pass) {
-    cgs2_euclid(W, ns, n, m.red, m.dots, nullptr);
+    cgs2_euclid<B>(W, ns, n, m.red, m.dots, nullptr);
     for (int t = threadIdx.x; t < n * ns; t += blockDim.x) {
       const int c = t / n, i = t % n;
       X[t] = m.dirn[i >> 1] ? 0.0 : el_stencil(ctx, W + (int64_t)c * n, i, true);
@@ -1496,7 +1515,7 @@ __global__ void __launch_bounds__(kEigThreads)
     X[t] = (c < ns) ? W[t] : Z[(int64_t)(c - ns) * n + i];
   }
   __syncthreads();
-  cgs2_euclid(X, m0, n, m.red, m.dots, keep);
+  cgs2_euclid<B>(X, m0, n, m.red, m.dots, keep);
   if (threadIdx.x == 0) {
     int q = 0;
     for (int c = 0; c < m0; ++c)
@@ -1519,7 +1538,7 @@ __global__ void __launch_bounds__(kEigThreads)
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double ax = m.dirn[i >> 1] ? 0.0 : el_stencil(ctx, xc, i, ps == 1);
 #pragma unroll
-        for (int l = 0; l < P; ++l)
+        for (int l = 0; l < B; ++l)
           if (l <= c) v[l] += ax * X[(int64_t)l * n + i];
       }
       block_sum_nv(v, c + 1, m.red, m.dots);
@@ -1552,15 +1571,15 @@ __global__ void __launch_bounds__(kEigThreads)
         for (int q = 0; q < j; ++q) a -= m.Am[i * LD + q] * Lm[j][q];
         m.Am[i * LD + j] = a / Lm[j][j];
       }
-    for (int i = 0; i < P; ++i)
-      for (int j = 0; j < P; ++j)
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < B; ++j)
         if (i >= mq || j >= mq) m.Am[i * LD + j] = (i == j) ? 1e300 : 0.0;
     for (int i = 0; i < mq; ++i)
       for (int j = 0; j < i; ++j)
         m.Am[i * LD + j] = m.Am[j * LD + i] = 0.5 * (m.Am[i * LD + j] + m.Am[j * LD + i]);
   }
   __syncthreads();
-  if (threadIdx.x < 32) jacobi_warp(m.Am, m.Vm, m.ritz, m.order);
+  if (threadIdx.x < 32) jacobi_warp<B>(m.Am, m.Vm, m.ritz, m.order);
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int c = 0; c < kNeig && c < mq; ++c) {
@@ -1592,21 +1611,29 @@ __global__ void __launch_bounds__(kEigThreads)
 
 template <int KJ>
 struct RandElLaunch {
-  static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
-                  const double* F, int ns, int nlx, size_t smem, cudaStream_t st) {
-    MS_CUDA(cudaFuncSetAttribute(k_randomized_el<KJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_randomized_el<KJ><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, F, ns, nlx);
+  template <int B>
+  static void go(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
+                 const double* F, int ns, int nlx, int max_bw, cudaStream_t st) {
+    const size_t smem = el_smem_bytes<B>(b.mex, b.mey, max_bw);
+    if (smem > 200 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
+    MS_CUDA(cudaFuncSetAttribute(k_randomized_el<KJ, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_randomized_el<KJ, B><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, F, ns, nlx);
     MS_CUDA(cudaGetLastError());
+  }
+  static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
+                  const double* F, int ns, int nlx, int max_bw, cudaStream_t st) {
+    if (randomized_block(ns) == kEigBlock)
+      go<kEigBlock>(g, E, hdir, ep, b, F, ns, nlx, max_bw, st);
+    else
+      go<32>(g, E, hdir, ep, b, F, ns, nlx, max_bw, st);
   }
 };
 
 void launch_randomized_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
                           const EigBatch& b, int max_bw, const double* F, int ns, cudaStream_t st) {
   if (b.nk == 0) return;
-  if (ns + 3 > P) throw Error(-1, "too many snapshots for the randomized elasticity eigensolver (<= 13)");
-  const size_t smem = el_smem_bytes(b.mex, b.mey, max_bw);
-  if (smem > 200 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
-  band_dispatch<RandElLaunch>(max_bw, g, E, hdir, ep, b, F, ns, 2 * b.mex + 1, smem, st);
+  if (ns + 3 > 32) throw Error(-1, "too many snapshots for the randomized elasticity eigensolver (<= 29)");
+  band_dispatch<RandElLaunch>(max_bw, g, E, hdir, ep, b, F, ns, 2 * b.mex + 1, max_bw, st);
 }
 
 }  // namespace msgpu

@@ -82,6 +82,10 @@ void launch_rand_sigma_el(const Grid& g, const double* E, const uint8_t* hdir, c
 void launch_compact_psi_el(const EigBatch& b, int NLx, const int* nsel, const int64_t* psioff,
                            double* psi, cudaStream_t st);
 
+// block size of the randomized solvers for `ns` snapshots (16, or 32 above 13);
+// their work buffers hold (2 B [+ 6 for elasticity]) * n doubles per centre
+int randomized_block(int ns);
+
 // gap / fixed selection on device (spectral.py:161-186)
 void launch_select(int n_centers, const double* evals, int n_max, double threshold, int fixed,
                    int* nsel, cudaStream_t st);

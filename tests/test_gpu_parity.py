@@ -462,3 +462,30 @@ def test_growing_maxit_reuses_preconditioner_safely():
     mesh2, op2, pre2 = setup_spec(spec)
     x2, rep2 = G.pcg_solve(op2, b, pre2, tol=1e-14, maxit=100)
     assert np.array_equal(x, x2) and np.array_equal(rep.alphas, rep2.alphas)
+
+
+@pytest.mark.parametrize("tag", ["EH+Rot;Rand", "EE;Rand"])
+def test_randomized_with_many_snapshots_matches_oracle(tag):
+    """15 snapshots (32-column block) on the reference's cell at eta 1 against
+    the oracle's restatement of solve_local_eig_randomized."""
+    g = load_golden("ref_bench100_eta1.npz")
+    mesh_o = O.mesh_for(100, 100)
+    op_o = O.elasticity_operator(mesh_o, g["E"], 0.3, O.whole_node_dofs(mesh_o, g["dirichlet_nodes"]))
+    prob = O.OracleProblem(mesh_o, op_o, g["E"], 0.3, g["b"], g["dirichlet_nodes"])
+    elastic = tag.startswith("EE")
+    P = O.build_two_level(prob, H=10, level1_mode="neighborhoods", enrich=not elastic,
+                          eig_solver=O.randomized_solver(n_snapshots=15),
+                          eig_kind="elasticity" if elastic else "heat")
+    mesh = G.build_fine_mesh(100, 100)
+    coeff = G.CoefficientField(g["E"], 0.3, float(g["E"].min()), 1.0)
+    op = G.ElasticityOperator(mesh, coeff, g["free_dofs"])
+    part = G.build_coarse_partition(mesh, 10, 10)
+    pre = G.build_preconditioner(tag, op, mesh, part, coeff, g["dirichlet_nodes"], G.EigOptions(n_snapshots=15))
+    assert pre.coarse_dim == P.coarse_dim
+    assert np.array_equal(np.array(pre.mode_counts), np.array(P.info["mode_counts"]))
+    r = g["apply_r"]
+    assert rel(pre.apply(r), P.apply(r)) <= 1e-7
+    x, rep = G.pcg_solve(op, g["b"], pre, tol=1e-8, maxit=2000)
+    xo, repo = O.pcg(op_o.matrix, prob.b, P, tol=1e-8, maxit=2000)
+    assert abs(rep.iterations - repo.iterations) <= 1
+    assert rel(x, xo) <= 1e-7
