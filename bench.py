@@ -51,9 +51,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", type=int, default=3, choices=(3, 4, 5),
-                    help="BASELINE config: 3 (headline, 2048^2), 4 (4096x2048 MBB, eta 1e9), "
-                         "5 (1024^2 50-step sequence with rebuild every step)")
+    ap.add_argument("--config", type=int, default=3, choices=(1, 2, 3, 4, 5),
+                    help="BASELINE config: 1 (64^2 inclusions), 2 (512^2 channels, --eta sweep), 3 (headline, "
+                         "2048^2), 4 (4096x2048 MBB, eta 1e9), 5 (1024^2 50-step sequence with rebuild every step)")
+    ap.add_argument("--eta", type=float, default=None, help="contrast for config 2 (1e2, 1e4, 1e6 or 1e8; default 1e6)")
     ap.add_argument("--n", "--mesh-n", dest="n", type=int, default=None, help="override the mesh size (nx; ny = nx/2 for config 4)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -234,6 +235,10 @@ def run_ours(args):
     if args.config == 4:
         nx = args.n or 4096
         spec = configs.config4(seed=args.seed, nx=nx, ny=nx // 2)
+    elif args.config == 1:
+        spec = configs.config1(seed=args.seed)
+    elif args.config == 2:
+        spec = configs.config2(seed=args.seed, eta=args.eta or 1e6, n=args.n or 512)
     else:
         spec = configs.config3(seed=args.seed, n=args.n or 2048)
     t_gen = time.perf_counter() - t0
@@ -344,11 +349,16 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": (f"config3: {spec.nx}^2 Q1 plane stress, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
-                                f"filtered-noise tanh density 40%, SIMP p=3, eta=1e6, cantilever, {args.variant}, rtol 1e-8")
-                   if args.config == 3 else
-                   (f"config4: {spec.nx}x{spec.ny} Q1 MBB beam, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
-                    f"filtered-noise tanh density 50%, SIMP p=3, eta=1e9, {args.variant}, rtol 1e-8"),
+        "config": {"workload": {
+                       3: (f"config3: {spec.nx}^2 Q1 plane stress, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
+                           f"filtered-noise tanh density 40%, SIMP p=3, eta=1e6, cantilever, {args.variant}, rtol 1e-8"),
+                       4: (f"config4: {spec.nx}x{spec.ny} Q1 MBB beam, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
+                           f"filtered-noise tanh density 50%, SIMP p=3, eta=1e9, {args.variant}, rtol 1e-8"),
+                       1: (f"config1: {spec.nx}^2 Q1, {spec.Nx}x{spec.Ny} subdomains of {spec.H}^2, overlap {spec.delta}, "
+                           f"40 random square inclusions, SIMP p=3, eta=1e6, cantilever, {args.variant}, rtol 1e-8"),
+                       2: (f"config2: {spec.nx}^2 Q1, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, random channels "
+                           f"+ inclusions, eta={spec.E_max / spec.E_min:g}, cantilever, {args.variant}, rtol 1e-8"),
+                   }[args.config],
                    "n_free": n_free, "iterations_per_step": it_step, "maxit": args.maxit, "converged": bool(conv), "coarse_dim": info["coarse_dim"],
                    "n_subdomains": info["n_subdomains"], "mode_counts_hist": np.bincount(info["mode_counts"], minlength=7).tolist(),
                    "l2": "inputs larger than L2 (level-1 factors %.1f GB)" % (F2 / 1e9),
