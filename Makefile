@@ -1,17 +1,25 @@
 # Builds the sm_100a C-ABI library in-tree (travels to the GPU box with gpurun).
+# One object per source so `make -j` compiles them in parallel; the ptxas
+# resource report of every kernel goes to build/ptxas/*.log (and /tmp/ptxas.log).
 NVCC ?= nvcc
 ARCH ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS ?= -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 SRC := $(wildcard paper_2006_13387_b200/csrc/*.cu)
 HDR := $(wildcard paper_2006_13387_b200/csrc/*.cuh) include/msgpu.h
+OBJ := $(patsubst paper_2006_13387_b200/csrc/%.cu,build/obj/%.o,$(SRC))
 LIB := paper_2006_13387_b200/libmsgpu.so
 
 all: $(LIB)
 
-$(LIB): $(SRC) $(HDR)
-	$(NVCC) $(ARCH) $(NVFLAGS) -shared $(SRC) -o $@ -ldl 2> /tmp/ptxas.log || (cat /tmp/ptxas.log; false)
+build/obj/%.o: paper_2006_13387_b200/csrc/%.cu $(HDR)
+	@mkdir -p build/obj build/ptxas
+	$(NVCC) $(ARCH) $(NVFLAGS) -c $< -o $@ 2> build/ptxas/$*.log || (cat build/ptxas/$*.log; false)
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared $(OBJ) -o $@ -ldl
+	@cat build/ptxas/*.log > /tmp/ptxas.log
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(OBJ)
 
 .PHONY: all clean
