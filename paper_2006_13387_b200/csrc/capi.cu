@@ -192,6 +192,7 @@ struct Prof {
     if (!e) e = make();
     return e;
   }
+  bool timing(unsigned bits) const { return on && (mask & bits) != 0u; }
   cudaEvent_t begin(int comp, int it, cudaStream_t st) {
     if (!on || !((mask >> comp) & 1u)) return nullptr;
     cudaEvent_t a = it >= 0 ? slot(comp, it, 0) : get();
@@ -233,6 +234,10 @@ struct Prof {
 struct ms_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
+  // side branch of the preconditioner apply: the coarse restriction + solve
+  // run here, concurrently with the level-1 sweeps on `st` (single rank)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::string err;
   Prof prof;
   std::unique_ptr<Comm> comm;  // multi-GPU strips (world > 1)
@@ -525,15 +530,70 @@ static void coarse_solve(ms_precond* pc, const int* done, cudaStream_t st) {
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
 // `restricted`: the cell restriction partials of r were already produced
 // (fused into the residual update); only their reduction remains.
+static int overlap_coarse() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_OVERLAP");
+    v = (e && std::string(e) == "1") ? 1 : 0;  // opt-in: MS_OVERLAP=1
+  }
+  return v;
+}
+
+// coarse branch: f0 = R0 r (cell partials unless already fused), y0 = K0^-1 f0
+static void coarse_restrict(ms_precond* pc, const double* r, const int* done, int it, bool restricted, bool dist,
+                            cudaStream_t st) {
+  ms_problem* P = pc->prob;
+  Prof& pf = P->ctx->prof;
+  cudaEvent_t a = pf.begin(MS_PROF_RESTRICT, it, st);
+  if (!restricted) launch_restrict_cells(P->g, pc->C0, pc->C1, pc->cd, r, done, st);
+  if (dist) {
+    exchange_rpart(pc);
+    MS_CUDA(cudaMemsetAsync(pc->f0.p, 0, pc->N_c * sizeof(double), st));
+  }
+  launch_restrict_reduce(pc->cd, pc->f0.p, done, st, pc->kc0, pc->kc1);
+  if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
+  pf.end(MS_PROF_RESTRICT, it, st, a);
+}
+
+static void coarse_branch(ms_precond* pc, const double* r, const int* done, int it, bool restricted, bool dist,
+                          cudaStream_t st) {
+  coarse_restrict(pc, r, done, it, restricted, dist, st);
+  Prof& pf = pc->prob->ctx->prof;
+  cudaEvent_t a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
+  coarse_solve(pc, done, st);
+  pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
+}
+
+// precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
+// `restricted`: the cell restriction partials of r were already produced
+// (fused into the residual update); only their reduction remains.
+// With MS_OVERLAP=1, on one rank, the coarse branch forks onto ctx->st2 and
+// runs concurrently with the level-1 sweeps.  Both are HBM streams and the
+// sweeps already run at ~93% of peak, so the fork only pays when the SYMV's
+// slack outweighs the sweeps' slowdown: measured -1.1% per iteration on one
+// B200 and +1.0% on another (config 3), hence opt-in.  With a communicator the
+// apply stays on one stream: collectives of one communicator must not run
+// concurrently.
 static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgScalars* sc,
                                double* beta_hist, int it = -1, bool restricted = false) {
   ms_problem* P = pc->prob;
-  const cudaStream_t st = P->ctx->st;
-  Prof& pf = P->ctx->prof;
+  ms_ctx* ctx = P->ctx;
+  const cudaStream_t st = ctx->st;
+  Prof& pf = ctx->prof;
   const int* done = sc ? &sc->done : nullptr;
   cudaEvent_t a;
-  const bool dist = P->ctx->world() > 1;
+  const bool dist = ctx->world() > 1;
   const int ns = pc->s1 - pc->s0;
+  // a per-component profile times the branch serialized (its events would
+  // otherwise measure the branch stretched across the concurrent sweeps)
+  const bool fork = pc->has_coarse && ns > 0 && !dist && overlap_coarse() != 0 &&
+                    !pf.timing((1u << MS_PROF_RESTRICT) | (1u << MS_PROF_COARSE_SOLVE));
+  if (fork) {
+    MS_CUDA(cudaEventRecord(ctx->fork, st));
+    MS_CUDA(cudaStreamWaitEvent(ctx->st2, ctx->fork, 0));
+    coarse_branch(pc, r, done, it, restricted, dist, ctx->st2);
+    MS_CUDA(cudaEventRecord(ctx->join, ctx->st2));
+  }
   if (ns > 0) {
     a = pf.begin(MS_PROF_LEVEL1, it, st);
     if (pc->dense)
@@ -543,20 +603,10 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
     pf.end(MS_PROF_LEVEL1, it, st, a);
     if (dist) exchange_ybuf(pc);
   }
-  if (pc->has_coarse) {
-    a = pf.begin(MS_PROF_RESTRICT, it, st);
-    if (!restricted) launch_restrict_cells(P->g, pc->C0, pc->C1, pc->cd, r, done, st);
-    if (dist) {
-      exchange_rpart(pc);
-      MS_CUDA(cudaMemsetAsync(pc->f0.p, 0, pc->N_c * sizeof(double), st));
-    }
-    launch_restrict_reduce(pc->cd, pc->f0.p, done, st, pc->kc0, pc->kc1);
-    if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
-    pf.end(MS_PROF_RESTRICT, it, st, a);
-    a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
-    coarse_solve(pc, done, st);
-    pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
-  }
+  if (fork)
+    MS_CUDA(cudaStreamWaitEvent(st, ctx->join, 0));
+  else if (pc->has_coarse)
+    coarse_branch(pc, r, done, it, restricted, dist, st);
   a = pf.begin(MS_PROF_COMBINE, it, st);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
                  pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st, pc->C0, pc->C1);
@@ -602,6 +652,13 @@ int ms_ctx_create(int device, ms_ctx** out) {
   c = new ms_ctx();
   c->device = device;
   MS_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;  // the short coarse branch gets SM slots first as level-1 CTAs retire
+    MS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    MS_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi));
+  }
+  MS_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  MS_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   *out = c;
   MS_API_END(c)
 }
@@ -717,6 +774,9 @@ int ms_ctx_destroy(ms_ctx* ctx) {
   if (!ctx) return MS_OK;
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamDestroy(ctx->st);
+  if (ctx->st2) cudaStreamDestroy(ctx->st2);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
   delete ctx;
   return MS_OK;
 }

@@ -109,3 +109,40 @@ def test_krylov_report_behaviour(rng, tmp_path):
     report.write_residual_csv(path)
     rows = path.read_text().strip().splitlines()
     assert rows[0] == "iteration,relative_residual" and len(rows) == len(report.residuals) + 1
+
+
+_OVERLAP_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2006_13387_b200 as G
+mesh = G.build_fine_mesh(64, 64)
+part = G.build_coarse_partition(mesh, 4, 4)
+rng = np.random.default_rng(7)
+E = np.where(rng.random(mesh.n_elements) < 0.3, 1.0, 1e-4)
+coeff = G.CoefficientField(E, 0.3, 1e-4, 1.0)
+op = G.assemble_elasticity(mesh, coeff, mesh.boundary_nodes())
+pre = G.build_preconditioner("EH+Rot", op, mesh, part, coeff, mesh.boundary_nodes())
+b = rng.standard_normal(op.n_free)
+x, rep = G.pcg_solve(op, b, pre, tol=1e-8)
+np.save(sys.argv[2], np.concatenate([x, np.asarray(rep.residuals), pre.apply(b)]))
+"""
+
+
+def test_coarse_branch_overlap_is_bit_identical(tmp_path):
+    """The coarse restriction + SYMV forked onto a second stream (opt-in,
+    MS_OVERLAP=1) gives the same bits as the serial apply."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    script = tmp_path / "ov.py"
+    script.write_text(_OVERLAP_SCRIPT)
+    out = {}
+    for ov in ("1", "0"):
+        env = dict(os.environ, MS_OVERLAP=ov)
+        subprocess.run([sys.executable, str(script), root, str(tmp_path / f"ov{ov}.npy")], check=True, env=env,
+                       timeout=600)
+        out[ov] = np.load(tmp_path / f"ov{ov}.npy")
+    assert np.array_equal(out["0"], out["1"])
