@@ -193,7 +193,7 @@ def run_reference(args):
     best["value"] = v
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config3 recipe, bounded CPU sample at {args.cpu_sample_n}^2 of the 2048^2 workload",
                    "rtol": 1e-8},
