@@ -149,8 +149,8 @@ constexpr int kCellThreads = 256;
 #ifndef MS_CB_MINB
 #define MS_CB_MINB 6
 #endif
-template <bool UPD, bool VEC>
-__global__ void __launch_bounds__(kCellThreads, MS_CR_MINB)
+template <bool UPD, bool VEC, int NU, int MINB>
+__global__ void __launch_bounds__(kCellThreads, MINB)
     k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, int J0, double* __restrict__ x,
                     const double* __restrict__ p, double* __restrict__ r,
                     const double* __restrict__ q, PcgScalars* sc, double* partials,
@@ -175,33 +175,68 @@ __global__ void __launch_bounds__(kCellThreads, MS_CR_MINB)
   double acc[13];
 #pragma unroll
   for (int v = 0; v < 13; ++v) acc[v] = 0.0;  // [4 corners][x, y, rot] + ||r||^2
-  for (int t = threadIdx.x; t < w * hgt; t += kCellThreads) {
-    const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
-    const int64_t n = (int64_t)b * g.nnx + a;
-    double rx = r[n], ry = r[n + nn];
-    if (UPD) {
-      x[n] += alpha * p[n];
-      x[n + nn] += alpha * p[n + nn];
-      rx -= alpha * q[n];
-      ry -= alpha * q[n + nn];
-      r[n] = rx;
-      r[n + nn] = ry;
-      acc[12] += rx * rx + ry * ry;
-    }
-    if (!VEC && has_coarse) {
-      const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n;
-      const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n;
-      const double2 c4a = __ldg(c2), c4b = __ldg(c2 + 1), p4a = __ldg(p2), p4b = __ldg(p2 + 1);
-      const double ch4[4] = {c4a.x, c4a.y, c4b.x, c4b.y};
-      const double ps4[4] = {p4a.x, p4a.y, p4b.x, p4b.y};
+  // NU nodes per thread in flight: all their loads are issued before the first
+  // is consumed; per-node arithmetic and accumulation order do not depend on NU.
+  const int total = w * hgt;
+  for (int t0 = threadIdx.x; t0 < total; t0 += NU * kCellThreads) {
+    int a[NU], b[NU];
+    int64_t n[NU];
+    bool ok[NU];
+    double rx[NU], ry[NU], px[NU], py[NU], qx[NU], qy[NU], xx[NU], xy[NU];
+    double2 c4[NU][2], p4[NU][2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int I = ci + (c & 1), J = cj + (c >> 1);
-        double ex, ey;
-        rot_xy(cd, I, J, a, b, ex, ey);
-        acc[3 * c] += ps4[c] * rx;
-        acc[3 * c + 1] += ps4[c] * ry;
-        acc[3 * c + 2] += __dmul_rn(ch4[c], ex) * rx + __dmul_rn(ch4[c], ey) * ry;
+    for (int u = 0; u < NU; ++u) {
+      const int t = t0 + u * kCellThreads;
+      ok[u] = t < total;
+      const int tt = ok[u] ? t : 0;
+      b[u] = b_lo + tt / w;
+      a[u] = a_lo + tt - (tt / w) * w;
+      n[u] = (int64_t)b[u] * g.nnx + a[u];
+      rx[u] = ok[u] ? r[n[u]] : 0.0;
+      ry[u] = ok[u] ? r[n[u] + nn] : 0.0;
+      if (UPD) {
+        xx[u] = ok[u] ? x[n[u]] : 0.0;
+        xy[u] = ok[u] ? x[n[u] + nn] : 0.0;
+        px[u] = ok[u] ? p[n[u]] : 0.0;
+        py[u] = ok[u] ? p[n[u] + nn] : 0.0;
+        qx[u] = ok[u] ? q[n[u]] : 0.0;
+        qy[u] = ok[u] ? q[n[u] + nn] : 0.0;
+      }
+      c4[u][0] = c4[u][1] = p4[u][0] = p4[u][1] = make_double2(0.0, 0.0);
+      if (!VEC && has_coarse && ok[u]) {
+        const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n[u];
+        const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n[u];
+        c4[u][0] = __ldg(c2);
+        c4[u][1] = __ldg(c2 + 1);
+        p4[u][0] = __ldg(p2);
+        p4[u][1] = __ldg(p2 + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      if (!ok[u]) continue;
+      double rxu = rx[u], ryu = ry[u];
+      if (UPD) {
+        x[n[u]] = xx[u] + alpha * px[u];
+        x[n[u] + nn] = xy[u] + alpha * py[u];
+        rxu -= alpha * qx[u];
+        ryu -= alpha * qy[u];
+        r[n[u]] = rxu;
+        r[n[u] + nn] = ryu;
+        acc[12] += rxu * rxu + ryu * ryu;
+      }
+      if (!VEC && has_coarse) {
+        const double ch4[4] = {c4[u][0].x, c4[u][0].y, c4[u][1].x, c4[u][1].y};
+        const double ps4[4] = {p4[u][0].x, p4[u][0].y, p4[u][1].x, p4[u][1].y};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int I = ci + (c & 1), J = cj + (c >> 1);
+          double ex, ey;
+          rot_xy(cd, I, J, a[u], b[u], ex, ey);
+          acc[3 * c] += ps4[c] * rxu;
+          acc[3 * c + 1] += ps4[c] * ryu;
+          acc[3 * c + 2] += __dmul_rn(ch4[c], ex) * rxu + __dmul_rn(ch4[c], ey) * ryu;
+        }
       }
     }
   }
@@ -306,25 +341,41 @@ __global__ void __launch_bounds__(kCellThreads, MS_CR_MINB)
   }
 }
 
+static int restrict_nu() {
+  static int v = [] {
+    const char* e = getenv("MS_RESTRICT_NU");  // A/B knob: 1 = one node per thread in flight
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return v;
+}
+
 void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const double* p, double* r,
                             const double* q, const CoarseDev& cd, PcgScalars* sc,
                             double* partials, double* res_hist, cudaStream_t st) {
+  const dim3 grid(cd.Nx, J1 - J0);
   if (cd.vec)
-    k_cell_restrict<true, true><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc,
-                                                                             partials, res_hist, nullptr);
+    k_cell_restrict<true, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+                                                                  res_hist, nullptr);
+  else if (restrict_nu() == 2)
+    k_cell_restrict<true, false, 2, 2><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+                                                                      res_hist, nullptr);
   else
-    k_cell_restrict<true, false><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc,
-                                                                              partials, res_hist, nullptr);
+    k_cell_restrict<true, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+                                                                   res_hist, nullptr);
   MS_CUDA(cudaGetLastError());
 }
 
 void launch_restrict_cells(const Grid& g, int J0, int J1, const CoarseDev& cd, const double* r,
                            const int* done, cudaStream_t st) {
+  const dim3 grid(cd.Nx, J1 - J0);
   if (cd.vec)
-    k_cell_restrict<false, true><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(
+    k_cell_restrict<false, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(
+        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+  else if (restrict_nu() == 2)
+    k_cell_restrict<false, false, 2, 2><<<grid, kCellThreads, 0, st>>>(
         g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
   else
-    k_cell_restrict<false, false><<<dim3(cd.Nx, J1 - J0), kCellThreads, 0, st>>>(
+    k_cell_restrict<false, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(
         g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
   MS_CUDA(cudaGetLastError());
 }
