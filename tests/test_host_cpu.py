@@ -181,3 +181,31 @@ def test_randomized_forcings_follow_reference_dof_order(kind):
         full = np.zeros((F.shape[2], 11))
         full[K.free_dofs] = ref
         assert np.array_equal(F[k].T, full)
+
+
+def test_condition_estimate_helpers_follow_reference():
+    """krylov.py:38-70: the Lanczos tridiagonal is bitwise the reference's loop;
+    long solves take the two extreme Ritz values by bisection, which agree with
+    the full spectrum to round-off."""
+    import scipy.linalg as sla
+
+    from paper_2006_13387_b200 import krylov as K
+
+    rng = np.random.default_rng(7)
+    for k in (1, 2, 3, 40, 600, 3000):
+        a = list(rng.uniform(0.05, 1.0, k))
+        b = list(rng.uniform(0.0, 0.95, max(k - 1, 0)))
+        d, e = K._lanczos_tridiagonal(a, b)
+        dr, er = np.empty(k), np.empty(max(k - 1, 0))
+        for j in range(k):  # the reference's loop
+            dr[j] = 1.0 / a[j]
+            if j > 0:
+                dr[j] += b[j - 1] / a[j - 1]
+            if j < k - 1:
+                er[j] = np.sqrt(b[j]) / a[j]
+        assert np.array_equal(d, dr) and np.array_equal(e, er)
+        lo, hi = K._ritz_extremes(a, b)
+        w = sla.eigh_tridiagonal(dr, er, eigvals_only=True) if k > 1 else dr
+        assert lo == pytest.approx(w[0], rel=1e-10) and hi == pytest.approx(w[-1], rel=1e-12)
+    assert K._ritz_extremes([], []) == (None, None)
+    assert K._ritz_extremes([1.0, float("nan")], [0.5]) == (None, None)
