@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo exit=$? >> gpurun_out/bench.log
+timeout 1200 python -m pytest tests/test_dist.py tests/test_gpu_behaviour.py -q > gpurun_out/pytest_dist.log 2>&1; echo exit=$? >> gpurun_out/pytest_dist.log

@@ -454,12 +454,15 @@ static void exchange_rows(ms_problem* P, double* v, int k) {
   if (!c || c->world == 1 || k <= 0) return;
   const HaloPlan h = halo_plan(P->b_lo, row_hi(P), P->g.ny, k, c->rank, c->world);
   const int64_t rowb = (int64_t)P->g.nnx * sizeof(double);
+  // both planes and both neighbours in one group (one NCCL launch per halo)
+  Xfer x[4];
   for (int plane = 0; plane < 2; ++plane) {
     char* base = reinterpret_cast<char*>(v + plane * P->g.n_nodes);
-    c->sendrecv2(base + h.send_lo[0] * rowb, h.send_n[0] * rowb, h.dst[0], base + h.recv_lo[0] * rowb,
-                 h.recv_n[0] * rowb, h.src[0], base + h.send_lo[1] * rowb, h.send_n[1] * rowb, h.dst[1],
-                 base + h.recv_lo[1] * rowb, h.recv_n[1] * rowb, h.src[1], P->ctx->st);
+    for (int q = 0; q < 2; ++q)
+      x[plane * 2 + q] = {base + h.send_lo[q] * rowb, (size_t)(h.send_n[q] * rowb), h.dst[q],
+                          base + h.recv_lo[q] * rowb, (size_t)(h.recv_n[q] * rowb), h.src[q]};
   }
+  c->sendrecv(x, 4, P->ctx->st);
 }
 
 // every rank ends with every rank's owned rows (solution / operator output)

@@ -72,13 +72,12 @@ struct NcclComm : Comm {
   void broadcast(void* buf, size_t bytes, int root, cudaStream_t st) override {
     MS_NCCL(nccl().broadcast(buf, buf, bytes, ncclUint8, root, comm, st));
   }
-  void sendrecv2(const void* s0, size_t sb0, int dst0, void* r0, size_t rb0, int src0, const void* s1,
-                 size_t sb1, int dst1, void* r1, size_t rb1, int src1, cudaStream_t st) override {
+  void sendrecv(const Xfer* x, int n, cudaStream_t st) override {
     MS_NCCL(nccl().groupStart());
-    if (dst0 >= 0 && sb0) MS_NCCL(nccl().send(s0, sb0, ncclUint8, dst0, comm, st));
-    if (src0 >= 0 && rb0) MS_NCCL(nccl().recv(r0, rb0, ncclUint8, src0, comm, st));
-    if (dst1 >= 0 && sb1) MS_NCCL(nccl().send(s1, sb1, ncclUint8, dst1, comm, st));
-    if (src1 >= 0 && rb1) MS_NCCL(nccl().recv(r1, rb1, ncclUint8, src1, comm, st));
+    for (int i = 0; i < n; ++i) {
+      if (x[i].dst >= 0 && x[i].sb) MS_NCCL(nccl().send(x[i].s, x[i].sb, ncclUint8, x[i].dst, comm, st));
+      if (x[i].src >= 0 && x[i].rb) MS_NCCL(nccl().recv(x[i].r, x[i].rb, ncclUint8, x[i].src, comm, st));
+    }
     MS_NCCL(nccl().groupEnd());
   }
   bool capturable() const override { return true; }
@@ -97,11 +96,11 @@ struct CallbackComm : Comm {
     MS_CUDA(cudaStreamSynchronize(st));
     check(cb.broadcast(cb.user, buf, (int64_t)bytes, root), "broadcast");
   }
-  void sendrecv2(const void* s0, size_t sb0, int dst0, void* r0, size_t rb0, int src0, const void* s1,
-                 size_t sb1, int dst1, void* r1, size_t rb1, int src1, cudaStream_t st) override {
+  void sendrecv(const Xfer* x, int n, cudaStream_t st) override {
     MS_CUDA(cudaStreamSynchronize(st));
-    check(cb.sendrecv(cb.user, s0, (int64_t)sb0, dst0, r0, (int64_t)rb0, src0), "sendrecv");
-    check(cb.sendrecv(cb.user, s1, (int64_t)sb1, dst1, r1, (int64_t)rb1, src1), "sendrecv");
+    for (int i = 0; i < n; ++i)
+      check(cb.sendrecv(cb.user, x[i].s, (int64_t)x[i].sb, x[i].dst, x[i].r, (int64_t)x[i].rb, x[i].src),
+            "sendrecv");
   }
   bool capturable() const override { return false; }
 };

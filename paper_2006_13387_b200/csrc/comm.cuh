@@ -11,17 +11,31 @@
 
 namespace msgpu {
 
+// one point-to-point exchange: send `sb` bytes from s to rank `dst` and receive
+// `rb` bytes into r from rank `src` (either side may be -1 / 0 bytes)
+struct Xfer {
+  const void* s;
+  size_t sb;
+  int dst;
+  void* r;
+  size_t rb;
+  int src;
+};
+
 // All operations are stream-ordered on `st` and act on device buffers.
 struct Comm {
   int rank = 0, world = 1;
   virtual ~Comm() = default;
   virtual void allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
   virtual void broadcast(void* buf, size_t bytes, int root, cudaStream_t st) = 0;
-  // send `sbytes` from sbuf to rank `dst` and receive `rbytes` into rbuf from
-  // rank `src` (either may be -1), as one group
-  virtual void sendrecv2(const void* s0, size_t sb0, int dst0, void* r0, size_t rb0, int src0,
-                         const void* s1, size_t sb1, int dst1, void* r1, size_t rb1, int src1,
-                         cudaStream_t st) = 0;
+  // all n exchanges as one group (NCCL: one ncclGroupStart/End); messages
+  // between a pair of ranks match in list order
+  virtual void sendrecv(const Xfer* x, int n, cudaStream_t st) = 0;
+  void sendrecv2(const void* s0, size_t sb0, int dst0, void* r0, size_t rb0, int src0, const void* s1,
+                 size_t sb1, int dst1, void* r1, size_t rb1, int src1, cudaStream_t st) {
+    const Xfer x[2] = {{s0, sb0, dst0, r0, rb0, src0}, {s1, sb1, dst1, r1, rb1, src1}};
+    sendrecv(x, 2, st);
+  }
   // may the operations be captured into a CUDA graph
   virtual bool capturable() const = 0;
 };
