@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_dist.py tests/test_gpu_behaviour.py -q > gpurun_out/pytest_dist.log 2>&1; echo exit=$? >> gpurun_out/pytest_dist.log
+( echo "== prev"; MSGPU_LIB=$PWD/build/libmsgpu_prev.so timeout 600 python tests/diag_dist_bitid.py; echo "== new"; timeout 600 python tests/diag_dist_bitid.py ) > gpurun_out/dist_bitid.log 2>&1

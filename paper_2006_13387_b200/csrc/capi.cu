@@ -543,8 +543,11 @@ static int overlap_coarse() {
 }
 
 // coarse branch: f0 = R0 r (cell partials unless already fused), y0 = K0^-1 f0
+// `rr_hist` != nullptr (multi-rank PCG iteration): the rank's ||r||^2 partial
+// rides in slot N_c of the f0 allreduce instead of its own collective, and is
+// finalised (residual, convergence flag) right after it.
 static void coarse_restrict(ms_precond* pc, const double* r, const int* done, int it, bool restricted, bool dist,
-                            cudaStream_t st) {
+                            cudaStream_t st, double* rr_hist = nullptr) {
   ms_problem* P = pc->prob;
   Prof& pf = P->ctx->prof;
   cudaEvent_t a = pf.begin(MS_PROF_RESTRICT, it, st);
@@ -554,13 +557,22 @@ static void coarse_restrict(ms_precond* pc, const double* r, const int* done, in
     MS_CUDA(cudaMemsetAsync(pc->f0.p, 0, pc->N_c * sizeof(double), st));
   }
   launch_restrict_reduce(pc->cd, pc->f0.p, done, st, pc->kc0, pc->kc1);
-  if (dist) P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c, st);
+  if (dist) {
+    PcgScalars* sc = P->sc.p;
+    if (rr_hist)
+      MS_CUDA(cudaMemcpyAsync(pc->f0.p + pc->N_c, &sc->part[PART_RR], sizeof(double), cudaMemcpyDeviceToDevice, st));
+    P->ctx->comm->allreduce_sum(pc->f0.p, pc->N_c + (rr_hist ? 1 : 0), st);
+    if (rr_hist) {
+      MS_CUDA(cudaMemcpyAsync(&sc->part[PART_RR], pc->f0.p + pc->N_c, sizeof(double), cudaMemcpyDeviceToDevice, st));
+      launch_finalize(sc, PART_RR, rr_hist, st);
+    }
+  }
   pf.end(MS_PROF_RESTRICT, it, st, a);
 }
 
 static void coarse_branch(ms_precond* pc, const double* r, const int* done, int it, bool restricted, bool dist,
-                          cudaStream_t st) {
-  coarse_restrict(pc, r, done, it, restricted, dist, st);
+                          cudaStream_t st, double* rr_hist = nullptr) {
+  coarse_restrict(pc, r, done, it, restricted, dist, st, rr_hist);
   Prof& pf = pc->prob->ctx->prof;
   cudaEvent_t a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
   coarse_solve(pc, done, st);
@@ -578,7 +590,8 @@ static void coarse_branch(ms_precond* pc, const double* r, const int* done, int 
 // apply stays on one stream: collectives of one communicator must not run
 // concurrently.
 static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgScalars* sc,
-                               double* beta_hist, int it = -1, bool restricted = false) {
+                               double* beta_hist, int it = -1, bool restricted = false,
+                               double* rr_hist = nullptr) {
   ms_problem* P = pc->prob;
   ms_ctx* ctx = P->ctx;
   const cudaStream_t st = ctx->st;
@@ -609,7 +622,7 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
   if (fork)
     MS_CUDA(cudaStreamWaitEvent(st, ctx->join, 0));
   else if (pc->has_coarse)
-    coarse_branch(pc, r, done, it, restricted, dist, st);
+    coarse_branch(pc, r, done, it, restricted, dist, st, rr_hist);
   a = pf.begin(MS_PROF_COMBINE, it, st);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
                  pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st, pc->C0, pc->C1);
@@ -1275,7 +1288,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     fail.zero(st);
     dense_spd_inverse(N, K0.p, pc->K0inv.p, inv_work.p, fail.p, st);
     check_fail(fail, st, "coarse operator: basis is rank deficient, K0");
-    pc->f0.alloc(N);
+    pc->f0.alloc(N + 1);  // + the ||r||^2 slot of the multi-rank PCG allreduce
     pc->y0.alloc(N);
     pc->part.alloc((size_t)packed_tiles(nt) * 2 * kTile);
     if ((size_t)N * N <= (size_t)4096 * 4096) {
@@ -1519,12 +1532,18 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     else
       launch_pcg_update(n, P->x.p, pnew, P->r.p, P->q.p, P->sc.p, P->partials.p, P->hres.p, st);
     pf.end(MS_PROF_UPDATE, i, st, a);
+    // multi-rank with a coarse space: ||r||^2 is summed inside the f0 allreduce
+    // (one collective fewer per iteration); the level-1 sweeps of the converged
+    // iteration then still run, their output unused
+    const bool rr_in_f0 = dist && fused;
     if (dist) {
-      dist_finalize(P, PART_RR, P->hres.p);
-      exchange_rows(P, P->r.p, pc->halo_rows);  // level-1 subdomains reach delta rows out
+      if (!rr_in_f0) dist_finalize(P, PART_RR, P->hres.p);
+      // level-1 subdomains reach delta rows out; without a preconditioner the
+      // next matvec needs r (= z) on one halo row
+      exchange_rows(P, P->r.p, pc ? pc->halo_rows : 1);
     }
     if (pc) {
-      precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, i, fused);
+      precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, i, fused, rr_in_f0 ? P->hres.p : nullptr);
     } else {
       a = pf.begin(MS_PROF_COMBINE, i, st);
       launch_rz(n, P->r.p, P->r.p, P->sc.p, P->partials.p, P->hbeta.p, st);
