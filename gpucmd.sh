@@ -1,2 +1,14 @@
-mkdir -p gpurun_out
-( echo "== prev"; MSGPU_LIB=$PWD/build/libmsgpu_prev.so timeout 600 python tests/diag_dist_bitid.py; echo "== new"; timeout 600 python tests/diag_dist_bitid.py ) > gpurun_out/dist_bitid.log 2>&1
+mkdir -p gpurun_out; O=gpurun_out/ab4.log; : > $O
+P=$PWD/build/libmsgpu_prev.so
+MSGPU_LIB=$P timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
+timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
+for v in prev new prev new; do
+  echo "== bench $v" >> $O
+  if [ $v = prev ]; then export MSGPU_LIB=$P; else unset MSGPU_LIB; fi
+  timeout 300 python bench.py --maxit 400 --e2e-steps 0 --no-cpu-baseline --no-parity --steps 3 --warmup 3 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+  if l.startswith('{'):
+    d=json.loads(l); k=d['roofline']['kernel_ms_per_launch']; print('%.4g'%d['value'], '%.4f'%(d['ms_per_step']/d['config']['iterations_per_step']), {a:round(b*1000,1) for a,b in k.items()}, d['clocks']['sm_mhz'])
+" >> $O
+done

@@ -78,9 +78,19 @@ __device__ __forceinline__ bool grid_reduce_last(double blockval, double* partia
   if (!am_last) return false;
   __threadfence();
   const unsigned int nb = gridDim.x * gridDim.y;
-  // fixed order: thread i sums partials i, i+T, ...; then block tree
+  // fixed order: thread i sums partials i, i+T, ...; then block tree.  L2
+  // loads (ld.global.cg: other CTAs' partials, published by their fences),
+  // 8 in flight per thread; the sum order is unchanged.
   double s = 0.0;
-  for (unsigned int i = threadIdx.x; i < nb; i += blockDim.x) s += ((volatile double*)partials)[i];
+  unsigned int i = threadIdx.x;
+  for (; i + 7 * blockDim.x < nb; i += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(partials + i + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; i < nb; i += blockDim.x) s += __ldcg(partials + i);
   s = block_sum(s, sh);
   if (threadIdx.x == 0) {
     *out = s;
