@@ -149,14 +149,20 @@ constexpr int kCellThreads = 256;
 #ifndef MS_CB_MINB
 #define MS_CB_MINB 6
 #endif
-template <bool UPD, bool VEC, int NU, int MINB>
-__global__ void __launch_bounds__(kCellThreads, MINB)
+#ifndef MS_CR2_TPB
+#define MS_CR2_TPB 128
+#endif
+#ifndef MS_CR2_MINB
+#define MS_CR2_MINB 4
+#endif
+template <bool UPD, bool VEC, int NU, int MINB, int TPB = kCellThreads>
+__global__ void __launch_bounds__(TPB, MINB)
     k_cell_restrict(Grid g, CoarseDev cd, int has_coarse, int J0, double* __restrict__ x,
                     const double* __restrict__ p, double* __restrict__ r,
                     const double* __restrict__ q, PcgScalars* sc, double* partials,
                     double* res_hist, const int* done) {
   if (UPD ? sc->done : (done && *(volatile const int*)done)) return;
-  __shared__ double sred[13 * (kCellThreads / 32)];
+  __shared__ double sred[13 * (TPB / 32)];
   const int64_t nn = g.n_nodes;
   const int ci = blockIdx.x, cj = J0 + blockIdx.y, Nx = cd.Nx, Ny = cd.Ny;
   const int mx = g.nx / Nx, my = g.ny / Ny;
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(kCellThreads, MINB)
   // NU nodes per thread in flight: all their loads are issued before the first
   // is consumed; per-node arithmetic and accumulation order do not depend on NU.
   const int total = w * hgt;
-  for (int t0 = threadIdx.x; t0 < total; t0 += NU * kCellThreads) {
+  for (int t0 = threadIdx.x; t0 < total; t0 += NU * TPB) {
     int a[NU], b[NU];
     int64_t n[NU];
     bool ok[NU];
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(kCellThreads, MINB)
     double2 c4[NU][2], p4[NU][2];
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
-      const int t = t0 + u * kCellThreads;
+      const int t = t0 + u * TPB;
       ok[u] = t < total;
       const int tt = ok[u] ? t : 0;
       b[u] = b_lo + tt / w;
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(kCellThreads, MINB)
 #pragma unroll
   for (int v = 0; v < 13; ++v) {
     const double s = warp_sum(acc[v]);
-    if (lane == 0) sred[v * (kCellThreads / 32) + warp] = s;
+    if (lane == 0) sred[v * (TPB / 32) + warp] = s;
   }
   __syncthreads();
   double* rp = cd.rpart + ((int64_t)cj * Nx + ci) * 4 * kSlots;
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(kCellThreads, MINB)
   if (threadIdx.x < 13) {
     double s = 0.0;
 #pragma unroll
-    for (int w2 = 0; w2 < kCellThreads / 32; ++w2) s += sred[threadIdx.x * (kCellThreads / 32) + w2];
+    for (int w2 = 0; w2 < TPB / 32; ++w2) s += sred[threadIdx.x * (TPB / 32) + w2];
     if (threadIdx.x == 12) {
       rrblk = s;
     } else if (!VEC && has_coarse) {
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(kCellThreads, MINB)
       const int I = ci + (c & 1), J = cj + (c >> 1);
       psk[c] = cok[c] ? cd.psi + __ldg(cd.psioff + (J - 1) * (Nx - 1) + (I - 1)) : cd.psi;
     }
-    for (int t = threadIdx.x; t < w * hgt; t += kCellThreads) {
+    for (int t = threadIdx.x; t < w * hgt; t += TPB) {
       const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
       const int64_t n = (int64_t)b * g.nnx + a;
       const double rx = r[n], ry = r[n + nn];
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(kCellThreads, MINB)
       const double* psk = cd.psi + __ldg(cd.psioff + k);
       for (int m = 1; m < cns[c]; ++m) {
         double sx = 0.0, sy = 0.0;
-        for (int t = threadIdx.x; t < w * hgt; t += kCellThreads) {
+        for (int t = threadIdx.x; t < w * hgt; t += TPB) {
           const int b = b_lo + t / w, a = a_lo + t - (t / w) * w;
           const int64_t n = (int64_t)b * g.nnx + a;
           const int ln = (a - (I - 1) * cd.mex) + (b - (J - 1) * cd.mey) * cd.NLx;
@@ -357,7 +363,7 @@ void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const doub
     k_cell_restrict<true, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
                                                                   res_hist, nullptr);
   else if (restrict_nu() == 2)
-    k_cell_restrict<true, false, 2, 2><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+    k_cell_restrict<true, false, 2, MS_CR2_MINB, MS_CR2_TPB><<<grid, MS_CR2_TPB, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
                                                                       res_hist, nullptr);
   else
     k_cell_restrict<true, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
