@@ -1,10 +1,13 @@
-mkdir -p gpurun_out; O=gpurun_out/ab4.log; : > $O
-P=$PWD/build/libmsgpu_prev.so
-MSGPU_LIB=$P timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
-timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
+mkdir -p gpurun_out; O=gpurun_out/ab7.log; : > $O
+for v in prev new; do
+  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
+  echo "== $v" >> $O
+  timeout 300 python tests/diag_bitid.py 1 64 5000 >> $O 2>&1
+  timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
+done
 for v in prev new prev new; do
+  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
   echo "== bench $v" >> $O
-  if [ $v = prev ]; then export MSGPU_LIB=$P; else unset MSGPU_LIB; fi
   timeout 300 python bench.py --maxit 400 --e2e-steps 0 --no-cpu-baseline --no-parity --steps 3 --warmup 3 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
