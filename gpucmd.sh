@@ -1,17 +1,2 @@
-mkdir -p gpurun_out; O=gpurun_out/ab7.log; : > $O
-for v in prev new; do
-  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
-  echo "== $v" >> $O
-  timeout 300 python tests/diag_bitid.py 1 64 5000 >> $O 2>&1
-  timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
-done
-for v in prev new prev new; do
-  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
-  echo "== bench $v" >> $O
-  timeout 300 python bench.py --maxit 400 --e2e-steps 0 --no-cpu-baseline --no-parity --steps 3 --warmup 3 2>&1 | python -c "
-import sys,json
-for l in sys.stdin:
-  if l.startswith('{'):
-    d=json.loads(l); k=d['roofline']['kernel_ms_per_launch']; print('%.4g'%d['value'], '%.4f'%(d['ms_per_step']/d['config']['iterations_per_step']), {a:round(b*1000,1) for a,b in k.items()}, d['clocks']['sm_mhz'])
-" >> $O
-done
+mkdir -p gpurun_out
+( timeout 900 python tests/diag_fullsolve.py 2048 EH+Rot; timeout 900 python tests/diag_fullsolve.py 2048 HH+Rot ) > gpurun_out/fullsolve.log 2>&1

@@ -124,12 +124,12 @@ class TwoLevelPreconditioner:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value and _lib.alive():
-            try:
+        try:  # at interpreter exit the module globals may already be torn down
+            if h is not None and h.value and _lib.alive():
                 _lib.load().ms_precond_destroy(h)
-            except Exception:
-                pass
-            self.handle = None
+        except Exception:
+            pass
+        self.handle = None
 
 
 def randomized_forcings(mesh, part, dirichlet_nodes, n_snapshots, seed, kind="diffusion"):
