@@ -1,2 +1,9 @@
-mkdir -p gpurun_out
-( timeout 900 python tests/diag_fullsolve.py 2048 EH+Rot; timeout 900 python tests/diag_fullsolve.py 2048 HH+Rot ) > gpurun_out/fullsolve.log 2>&1
+mkdir -p gpurun_out; O=gpurun_out/ab9.log; : > $O
+for v in prev new prev new; do
+  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
+  echo "== $v" >> $O
+  timeout 300 python tests/diag_bitid.py 1 64 5000 >> $O 2>&1
+  timeout 300 python tests/diag_bitid.py 3 512 300 >> $O 2>&1
+  timeout 300 python tests/diag_bitid.py 5 256 300 >> $O 2>&1
+  timeout 600 python tests/diag_build.py 2>&1 | grep -v Warn >> $O
+done

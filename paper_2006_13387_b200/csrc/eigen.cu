@@ -189,6 +189,38 @@ __device__ void band_solve_cols(const BandSys& s, const double* __restrict__ Lc,
   __syncthreads();
 }
 
+// As band_solve_cols for an even number of columns, two per warp sharing each
+// band read: a column pair is interleaved into `scratch` (2 n doubles per
+// pair, free while the solve runs), swept with NR = 2 and copied back.  The
+// arithmetic of each column is that of the one-column sweep (bit-identical).
+template <int T>
+__device__ void band_solve_cols2(const BandSys& s, const double* __restrict__ Lc,
+                                 const double* __restrict__ Lr, double* W, double* scratch, int ncols) {
+  __syncthreads();  // W complete, scratch free
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int n = s.n;
+  for (int pr = warp; 2 * pr < ncols; pr += nw) {
+    double* y0 = W + (int64_t)(2 * pr) * n;
+    double* y1 = y0 + n;
+    double* yi = scratch + (int64_t)pr * 2 * n;
+    for (int i = lane; i < n; i += 32) {
+      yi[2 * i] = y0[i];
+      yi[2 * i + 1] = y1[i];
+    }
+    __syncwarp();
+    band_sweep<T, 2, kPD, false>(Lc + s.foff, n, s.bw, yi, lane);
+    __syncwarp();
+    band_sweep<T, 2, kPD, true>(Lr + s.foff, n, s.bw, yi, lane);
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      y0[i] = yi[2 * i];
+      y1[i] = yi[2 * i + 1];
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
 // cyclic Jacobi on the B x B symmetric matrix A (row stride B+1), one warp;
 // relative-threshold rotations keep small eigenvalues of graded matrices
 // accurate.  On exit: ritz ascending, V columns in the same order.
@@ -314,8 +346,9 @@ __global__ void __launch_bounds__(kEigThreads)
       W[t] = dir[i] ? 0.0 : stencil(ctx, X + (int64_t)c * n, i, hmel);
     }
     __syncthreads();
-    // (2) W <- (K + sigma M)^{-1} W
-    band_solve_cols<T>(s, eb.Lc, eb.Lr, W, P);
+    // (2) W <- (K + sigma M)^{-1} W (X is dead until (3) rewrites it: scratch)
+    static_assert(P % 2 == 0, "column pairs");
+    band_solve_cols2<T>(s, eb.Lc, eb.Lr, W, X, P);
     // (3) M-orthonormalise W into X (CGS2 against the constant and earlier columns)
     for (int c = 0; c < P; ++c) {
       double* w = W + (int64_t)c * n;
