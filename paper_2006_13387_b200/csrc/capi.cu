@@ -8,9 +8,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -32,6 +35,87 @@ namespace {
 std::mutex g_err_mu;
 std::string g_err;
 
+// Device block cache.  A released block is kept (after a device
+// synchronisation, which cudaFree would also perform, so no stream can still
+// be using it) and handed to a later allocation of between half its size and
+// its size on the same device: repeated builds -- config 5 rebuilds the
+// preconditioner every step -- stop paying cudaMalloc/cudaFree of gigabytes.
+// At most MS_CACHE_BYTES (default 32 GiB) stay cached; a failed cudaMalloc
+// returns the device's cached blocks to the driver and retries.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> idle;         // (device, bytes) -> block
+  std::unordered_map<void*, std::pair<int, size_t>> owned;  // every block we allocated
+  size_t cached = 0, limit = 0;
+  BlockCache() {
+    const char* e = getenv("MS_CACHE_BYTES");
+    limit = e ? (size_t)strtoull(e, nullptr, 10) : ((size_t)32 << 30);
+  }
+  void flush(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = idle.begin(); it != idle.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        owned.erase(it->second);
+        cached -= it->first.second;
+        it = idle.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();  // never destroyed: no ordering issue at exit
+  return *c;
+}
+
+void* dev_alloc(size_t bytes, cudaError_t* err) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BlockCache& c = block_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.idle.lower_bound({dev, bytes});
+    if (it != c.idle.end() && it->first.first == dev && it->first.second <= 2 * bytes) {
+      void* p = it->second;
+      c.cached -= it->first.second;
+      c.idle.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c.flush(dev);
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *err = e;
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.owned[p] = {dev, bytes};
+  return p;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  BlockCache& c = block_cache();
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.owned.find(p);
+  if (it == c.owned.end() || c.cached + it->second.second > c.limit) {
+    if (it != c.owned.end()) c.owned.erase(it);
+    cudaFree(p);
+    return;
+  }
+  c.idle.insert({it->second, p});
+  c.cached += it->second.second;
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -41,20 +125,18 @@ struct DBuf {
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    dev_free(p);
     p = nullptr;
     n = 0;
   }
   void alloc(size_t count) {
     release();
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-    if (e != cudaSuccess) {
-      p = nullptr;
-      cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    p = static_cast<T*>(dev_alloc(count * sizeof(T), &e));
+    if (!p)
       throw Error(MS_E_NOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
                                   " bytes failed: " + cudaGetErrorString(e));
-    }
     n = count;
   }
   void zero(cudaStream_t st) { MS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st)); }
