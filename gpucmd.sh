@@ -1,11 +1,11 @@
-mkdir -p gpurun_out; O=gpurun_out/ab10.log; : > $O
-for v in prev new; do
-  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
-  echo "== $v" >> $O
-  timeout 600 python tests/diag_build.py 2>&1 | grep -v Warn >> $O
-  timeout 900 python bench.py --config 5 --steps 20 --no-cpu-baseline 2>&1 | grep '^{' | python -c "
+mkdir -p gpurun_out; O=gpurun_out/ab12.log; : > $O
+for v in prev t64 t128 prev t64 t128; do
+  export MSGPU_LIB=$PWD/build/libmsgpu_$v.so
+  echo "== bench $v" >> $O
+  timeout 300 python bench.py --maxit 400 --e2e-steps 0 --no-cpu-baseline --no-parity --steps 3 --warmup 3 2>&1 | python -c "
 import sys,json
-d=json.loads(sys.stdin.read()); c=d['config']; print('config5', '%.4g'%d['value'], 'ms/step %.1f'%d['ms_per_step'], 'build/step %.3f'%c['build_s_per_step'], 'solve/step %.3f'%c['solve_s_per_step'], sum(c['iterations']))" >> $O
+for l in sys.stdin:
+  if l.startswith('{'):
+    d=json.loads(l); k=d['roofline']['kernel_ms_per_launch']; print('%.4g'%d['value'], '%.4f'%(d['ms_per_step']/d['config']['iterations_per_step']), {a:round(b*1000,1) for a,b in k.items()}, d['clocks']['sm_mhz'])
+" >> $O
 done
-unset MSGPU_LIB
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
