@@ -171,6 +171,12 @@ int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_call
 int ms_comm_selftest(ms_ctx* ctx, double* out4);
 /* synchronous copy between host and/or device buffers (callback helpers) */
 int ms_copy(void* dst, const void* src, size_t bytes);
+/* device memory held by the library's block cache (released buffers kept for
+ * reuse, at most MS_CACHE_BYTES, default 32 GiB): *bytes = cached bytes of the
+ * current device; with release != 0 they are returned to the driver first
+ * (e.g. before a large allocation outside the library).  No reference
+ * counterpart: scipy has no device memory. */
+int ms_cache_trim(int release, size_t* bytes);
 /* node-row halo plan of rank `rank` owning rows [lo, hi] of 0..ny, depth k:
  * out12 = {send_lo, send_n, dst, recv_lo, recv_n, src} for slot 0 (towards the
  * previous rank) then slot 1 (towards the next); pure arithmetic, no CUDA */

@@ -19,4 +19,16 @@ from . import topopt
 from .topopt import (DensityFilter, OptimizeConfig, OptimizationResult, ReusePolicy,
                      compliance_and_sensitivity, oc_update, optimize)
 
+
+
+def release_cached_memory():
+    """Return the device memory kept by the library's block cache to the driver
+    (e.g. before large allocations outside this package); returns the bytes freed."""
+    from ._lib import cache_trim
+
+    held = cache_trim(False)
+    cache_trim(True)
+    return held
+
+
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -29,7 +29,7 @@ EXPORTS = (
     "ms_operator_apply", "ms_precond_build", "ms_precond_destroy", "ms_precond_apply",
     "ms_precond_apply_coarse", "ms_precond_info_get", "ms_precond_coarse_matrix", "ms_pcg_solve",
     "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
-    "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_comm_selftest", "ms_strip_rows", "ms_copy",
+    "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_comm_selftest", "ms_strip_rows", "ms_copy", "ms_cache_trim",
     "ms_halo_plan", "ms_ctx_set_profiling_mask", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
     "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot",
 )
@@ -134,6 +134,7 @@ def load(path: str | os.PathLike | None = None):
         "ms_comm_selftest": (C.c_int, [vp, dp]),
         "ms_strip_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, ip, ip]),
         "ms_copy": (C.c_int, [vp, vp, C.c_size_t]),
+        "ms_cache_trim": (C.c_int, [C.c_int, C.POINTER(C.c_size_t)]),
         "ms_halo_plan": (C.c_int, [C.c_int] * 6 + [ip]),
         "ms_filter_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(vp)]),
         "ms_filter_destroy": (C.c_int, [vp]),
@@ -189,3 +190,12 @@ def dptr(arr):
 
 def iptr(arr):
     return arr.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def cache_trim(release=False):
+    """Bytes of device memory held by the library's block cache on the current
+    device (released buffers kept for reuse); with release=True they are first
+    returned to the driver (ms_cache_trim)."""
+    out = C.c_size_t(0)
+    check(load().ms_cache_trim(1 if release else 0, C.byref(out)))
+    return int(out.value)

@@ -841,6 +841,22 @@ int ms_ctx_attach_callbacks(ms_ctx* ctx, int rank, int world, const ms_comm_call
   MS_API_END(ctx)
 }
 
+int ms_cache_trim(int release, size_t* bytes) {
+  MS_API_BEGIN
+  int dev = 0;
+  MS_CUDA(cudaGetDevice(&dev));
+  BlockCache& c = block_cache();
+  if (release) c.flush(dev);
+  if (bytes) {
+    std::lock_guard<std::mutex> lk(c.mu);
+    size_t b = 0;
+    for (const auto& kv : c.idle)
+      if (kv.first.first == dev) b += kv.first.second;
+    *bytes = b;
+  }
+  MS_API_END(nullptr)
+}
+
 int ms_copy(void* dst, const void* src, size_t bytes) {
   MS_API_BEGIN
   if (bytes && (!dst || !src)) throw Error(MS_E_INVALID, "null argument");

@@ -146,3 +146,29 @@ def test_coarse_branch_overlap_is_bit_identical(tmp_path):
                        timeout=600)
         out[ov] = np.load(tmp_path / f"ov{ov}.npy")
     assert np.array_equal(out["0"], out["1"])
+
+
+@pytest.mark.gpu
+def test_block_cache_reuses_and_releases_device_memory():
+    """Released C-ABI buffers are kept for reuse (a rebuild of the same
+    preconditioner is served from the cache) and returned on request."""
+    import paper_2006_13387_b200 as G
+    from paper_2006_13387_b200 import _lib, configs
+    from paper_2006_13387_b200.solve import setup_spec
+
+    spec = configs.config1(seed=0, n=64, H=16, delta=1)
+    G.release_cached_memory()
+    assert _lib.cache_trim(False) == 0
+    mesh, op, pre = setup_spec(spec)
+    x1, r1 = G.pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
+    del pre
+    held = _lib.cache_trim(False)
+    assert held > 0
+    pre = G.build_preconditioner("EH+Rot", op, mesh, G.build_coarse_partition(mesh, spec.Nx, spec.Ny), op.coeff,
+                                 spec.heat_dirichlet_nodes, G.EigOptions(), level1="blocks", delta=spec.delta)
+    assert _lib.cache_trim(False) < held  # the rebuild took its buffers from the cache
+    x2, r2 = G.pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
+    assert r1.iterations == r2.iterations and np.array_equal(x1, x2)
+    del pre, op
+    assert G.release_cached_memory() > 0
+    assert _lib.cache_trim(False) == 0
