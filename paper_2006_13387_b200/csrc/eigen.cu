@@ -193,6 +193,11 @@ __device__ void band_solve_cols(const BandSys& s, const double* __restrict__ Lc,
 // band read: a column pair is interleaved into `scratch` (2 n doubles per
 // pair, free while the solve runs), swept with NR = 2 and copied back.  The
 // arithmetic of each column is that of the one-column sweep (bit-identical).
+#ifndef MS_EIG_PD2
+#define MS_EIG_PD2 8
+#endif
+constexpr int kPD2 = MS_EIG_PD2;  // band columns prefetched ahead in the two-column sweeps
+
 template <int T>
 __device__ void band_solve_cols2(const BandSys& s, const double* __restrict__ Lc,
                                  const double* __restrict__ Lr, double* W, double* scratch, int ncols) {
@@ -208,9 +213,9 @@ __device__ void band_solve_cols2(const BandSys& s, const double* __restrict__ Lc
       yi[2 * i + 1] = y1[i];
     }
     __syncwarp();
-    band_sweep<T, 2, kPD, false>(Lc + s.foff, n, s.bw, yi, lane);
+    band_sweep<T, 2, kPD2, false>(Lc + s.foff, n, s.bw, yi, lane);
     __syncwarp();
-    band_sweep<T, 2, kPD, true>(Lr + s.foff, n, s.bw, yi, lane);
+    band_sweep<T, 2, kPD2, true>(Lr + s.foff, n, s.bw, yi, lane);
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
       y0[i] = yi[2 * i];
