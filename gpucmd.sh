@@ -1,7 +1,5 @@
-mkdir -p gpurun_out; O=gpurun_out/ab13.log; : > $O
-for v in prev new prev new; do
-  case $v in prev) export MSGPU_LIB=$PWD/build/libmsgpu_prev.so;; new) unset MSGPU_LIB;; esac
-  echo "== $v" >> $O
-  timeout 300 python tests/diag_bitid.py 5 256 300 >> $O 2>&1
-  timeout 600 python tests/diag_build.py 2>&1 | grep -v Warn >> $O
-done
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo exit=$? >> gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo exit=$? >> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo exit=$? >> gpurun_out/bench_ref.log
