@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MSGPU_ABI_VERSION 2
+#define MSGPU_ABI_VERSION 3
 
 enum {
   MS_OK = 0,
@@ -70,6 +70,13 @@ enum {
   MS_LOCAL_DENSE_INV = 1 /* explicit packed dense inverse, batched SYMV per apply     */
 };
 
+/* coarse solve K0^-1 f0 (CoarseOperator.solve, coarse.py:150-154) */
+enum {
+  MS_COARSE_INVERSE = 0, /* explicit packed K0^-1, one bandwidth-bound SYMV per apply (default)      */
+  MS_COARSE_CHOLESKY = 1 /* the reference's arithmetic: Cholesky factor (cho_factor, coarse.py:143)
+                            and forward + backward triangular solves (cho_solve, coarse.py:154)     */
+};
+
 /* Options of build_preconditioner("EH+Rot" / "EH", ...) — schwarz.py:54-59, :176-211. */
 typedef struct ms_precond_opts {
   int Nx, Ny;            /* coarse blocks per axis (CoarsePartition, grid.py:117)        */
@@ -92,6 +99,7 @@ typedef struct ms_precond_opts {
   const double* snapshots;
   int level1_operator;   /* MS_L1_* (needs whole-node constraints for MS_L1_HEAT)       */
   int eig_kind;          /* MS_EIG_*: neighbourhood eigenproblem kind                   */
+  int coarse_solve;      /* MS_COARSE_* (ABI 3)                                         */
 } ms_precond_opts;
 
 /* Build metadata, the `info` dict of schwarz.py:202-210 plus eigensolver stats. */
@@ -184,6 +192,11 @@ int ms_halo_plan(int lo, int hi, int ny, int k, int rank, int world, int* out12)
 /* strip partition used for `nrows` block rows: rank owns [*lo, *hi) */
 int ms_strip_rows(int nrows, int world, int rank, int* lo, int* hi);
 
+/* 8x8 unit plane-stress Q1 element stiffness (E = 1), component-grouped,
+ * bit-for-bit the reference's _unit_elasticity_element (assembly.py:100-116);
+ * host arithmetic, no device needed. */
+int ms_unit_element(double nu, double* Ke64);
+
 /* ---- operator: assemble_elasticity (assembly.py:208-220) ---------------
  * E: per-element modulus, n_el = nx*ny, row-major (e = j*nx + i).
  * free_dofs: sorted ascending full-dof ids (component-grouped), n_free of them.
@@ -267,6 +280,13 @@ int ms_compliance_sensitivity(ms_ctx* ctx, int nx, int ny, double nu, const doub
 int ms_oc_update(ms_ctx* ctx, int64_t n, const ms_filter* filt, const double* rho, const double* dg,
                  const double* volumes, double v_star, double move, double damping, double* rho_new,
                  int* evaluations);
+
+/* x = A^-1 b for one dense SPD matrix (row-major N x N, lower triangle read)
+ * with the coarse-solve kernels: mode MS_COARSE_INVERSE (tiled inverse +
+ * packed SYMV) or MS_COARSE_CHOLESKY (tiled Cholesky + blocked triangular
+ * solves, LAPACK ?potrf/?potrs as in CoarseOperator, coarse.py:143,154).
+ * MS_E_NOT_SPD on a non-positive pivot. */
+int ms_dense_spd_solve(ms_ctx* ctx, int N, const double* A, const double* b, double* x, int mode);
 
 /* deterministic device dot product of n doubles (volume / compliance logs) */
 int ms_dot(ms_ctx* ctx, int64_t n, const double* a, const double* b, double* out);

@@ -10,7 +10,8 @@ solver call runs in hand-written sm_100a kernels behind the C ABI
 
 from .grid import FineMesh, CoarsePartition, Patch, build_fine_mesh, build_coarse_partition
 from .assembly import (CoefficientField, LoadSpec, ElasticityOperator, assemble_elasticity,
-                       build_load_vector, simp_modulus, vector_dirichlet_dofs)
+                       build_load_vector, element_stiffness_elasticity, simp_modulus,
+                       vector_dirichlet_dofs)
 from .schwarz import (VARIANTS, GPU_VARIANTS, EigOptions, IdentityPreconditioner,
                       TwoLevelPreconditioner, build_preconditioner, get_variant)
 from .krylov import SolveReport, estimate_condition, pcg_solve

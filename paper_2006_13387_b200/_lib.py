@@ -21,6 +21,7 @@ MS_LEVEL1_NEIGHBORHOODS, MS_LEVEL1_BLOCKS = 0, 1
 MS_LOCAL_BANDED, MS_LOCAL_DENSE_INV = 0, 1
 MS_L1_ELASTICITY, MS_L1_HEAT = 0, 1
 MS_EIG_HEAT, MS_EIG_ELASTICITY = 0, 1
+MS_COARSE_INVERSE, MS_COARSE_CHOLESKY = 0, 1
 
 # every symbol include/msgpu.h declares
 EXPORTS = (
@@ -31,7 +32,7 @@ EXPORTS = (
     "ms_ctx_set_profiling", "ms_ctx_profile_get", "ms_ctx_stream", "ms_precond_bench",
     "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_comm_selftest", "ms_strip_rows", "ms_copy", "ms_cache_trim",
     "ms_halo_plan", "ms_ctx_set_profiling_mask", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
-    "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot",
+    "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot", "ms_unit_element", "ms_dense_spd_solve",
 )
 
 ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
@@ -54,7 +55,7 @@ class PrecondOpts(C.Structure):
         ("fixed_rule", C.c_int), ("local_solver", C.c_int), ("use_coarse", C.c_int),
         ("heat_dirichlet_nodes", C.POINTER(C.c_int64)), ("n_heat_dirichlet", C.c_int64),
         ("randomized", C.c_int), ("n_snapshots", C.c_int), ("snapshots", C.c_void_p),
-        ("level1_operator", C.c_int), ("eig_kind", C.c_int),
+        ("level1_operator", C.c_int), ("eig_kind", C.c_int), ("coarse_solve", C.c_int),
     ]
 
 
@@ -145,6 +146,8 @@ def load(path: str | os.PathLike | None = None):
                                                 C.c_double, C.c_double, dp, vp]),
         "ms_oc_update": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_double, C.c_double, vp, ip]),
         "ms_dot": (C.c_int, [vp, C.c_int64, vp, vp, dp]),
+        "ms_unit_element": (C.c_int, [C.c_double, dp]),
+        "ms_dense_spd_solve": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

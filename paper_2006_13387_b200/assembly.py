@@ -148,7 +148,13 @@ class ElasticityOperator:
     __matmul__ = apply
 
     def set_modulus(self, E):
-        E = np.ascontiguousarray(E, dtype=np.float64)
+        """Replace the per-element modulus in place (topopt.py:150-160); the
+        same checks as CoefficientField (assembly.py:21-52) guard the copy."""
+        E = np.ascontiguousarray(E, dtype=np.float64).ravel()
+        if E.size != self.mesh.n_elements:
+            raise ValueError("coefficient field does not match mesh")
+        if not np.all(E > 0):
+            raise ValueError("element moduli must be positive")
         _lib.check(_lib.load().ms_problem_set_modulus(self.handle, C.c_void_p(E.ctypes.data)),
                    self._ctx.handle)
 
@@ -170,6 +176,20 @@ class ElasticityOperator:
         except Exception:
             pass
         self.handle = None
+
+
+def element_stiffness_elasticity(E, nu, h=1.0):
+    """Plane-stress Q1 element stiffness (assembly.py:119-130): E times the
+    unit matrix the kernels use, computed by the library with the reference's
+    exact arithmetic (ms_unit_element; bitwise equal to
+    ``_unit_elasticity_element``, assembly.py:100-116)."""
+    if E <= 0:
+        raise ValueError("modulus must be positive")
+    if not (0 <= nu < 0.5):
+        raise ValueError(f"Poisson ratio {nu} outside [0, 0.5)")
+    K = np.empty(64)
+    _lib.check(_lib.load().ms_unit_element(float(nu), _lib.dptr(K)))
+    return E * K.reshape(8, 8)
 
 
 def assemble_elasticity(mesh, coeff, dirichlet_nodes, constrained_dofs=None):

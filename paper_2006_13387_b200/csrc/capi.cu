@@ -158,10 +158,17 @@ bool is_device_ptr(const void* ptr) {
 }
 
 // element matrices, same formulas as the reference (assembly.py:83-147)
+// Bit-for-bit the reference's numpy evaluation (assembly.py:100-116): C is
+// divided entrywise by (1 - nu^2), and each inner product of the two small
+// matmuls accumulates with fused multiply-adds from zero in index order, as
+// the BLAS kernel behind `B.T @ C @ B` does (all 64 doubles equal the
+// reference's for nu = 0.3 and 0.25, tests/golden/ref_elements.npz).
 void unit_elasticity(double nu, double K[64]) {
   const double g[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
-  const double f = 1.0 / (1.0 - nu * nu);
-  const double C[3][3] = {{f * 1.0, f * nu, 0.0}, {f * nu, f * 1.0, 0.0}, {0.0, 0.0, f * (1.0 - nu) / 2.0}};
+  const double den = 1.0 - nu * nu;
+  const double C[3][3] = {{1.0 / den, nu / den, 0.0 / den},
+                          {nu / den, 1.0 / den, 0.0 / den},
+                          {0.0 / den, 0.0 / den, ((1.0 - nu) / 2.0) / den}};
   double A[8][8] = {};
   for (double xi : g)
     for (double eta : g) {
@@ -174,14 +181,17 @@ void unit_elasticity(double nu, double K[64]) {
         B[2][m] = dy[m];
         B[2][4 + m] = dx[m];
       }
-      double BtC[8][3] = {};
+      double BtC[8][3];
       for (int i = 0; i < 8; ++i)
-        for (int j = 0; j < 3; ++j)
-          for (int l = 0; l < 3; ++l) BtC[i][j] += B[l][i] * C[l][j];
+        for (int j = 0; j < 3; ++j) {
+          double s = 0.0;
+          for (int l = 0; l < 3; ++l) s = std::fma(B[l][i], C[l][j], s);
+          BtC[i][j] = s;
+        }
       for (int i = 0; i < 8; ++i)
         for (int j = 0; j < 8; ++j) {
           double s = 0.0;
-          for (int l = 0; l < 3; ++l) s += BtC[i][l] * B[l][j];
+          for (int l = 0; l < 3; ++l) s = std::fma(BtC[i][l], B[l][j], s);
           A[i][j] += 0.25 * s;
         }
     }
@@ -403,6 +413,11 @@ struct ms_precond {
   DBuf<int> nsel, hoff;
   DBuf<int64_t> psioff;
   DBuf<double> psi, chi, K0inv, f0, y0, part, evals, K0keep, chi4, psi4, rpart;
+  // MS_COARSE_CHOLESKY: packed factor L (in K0inv), inverses of its diagonal
+  // tiles, the forward-sweep result and the blocked-TRSV tickets/flags
+  bool coarse_factor = false;
+  DBuf<double> K0dinv, trsv_t, trsv_y;
+  DBuf<int> trsv_sync;
   std::vector<int> h_nsel;
   std::vector<double> h_evals;
   int N_c = 0;
@@ -551,6 +566,9 @@ static void exchange_rows(ms_problem* P, double* v, int k) {
 static void allgather_rows(ms_problem* P, double* v) {
   Comm* c = P->ctx->comm.get();
   if (!c || c->world == 1) return;
+  // no strip ownership before a preconditioner is built: every rank then
+  // computes all rows (b_hi = -1), nothing to gather
+  if ((int)P->rank_lo.size() < c->world || (int)P->rank_hi.size() < c->world) return;
   const int64_t rowb = (int64_t)P->g.nnx * sizeof(double);
   for (int r = 0; r < c->world; ++r)
     for (int plane = 0; plane < 2; ++plane) {
@@ -606,7 +624,14 @@ static void dist_finalize(ms_problem* P, int kind, double* hist) {
 
 // y0 = K0^-1 f0: each rank streams its share of the packed inverse's tiles,
 // the partial y0 are summed over ranks (N_c doubles)
+// MS_COARSE_CHOLESKY: y0 = L^-T L^-1 f0 (cho_solve, coarse.py:154) with the
+// full factor on every rank, no collective
 static void coarse_solve(ms_precond* pc, const int* done, cudaStream_t st) {
+  if (pc->coarse_factor) {
+    launch_trsv_packed(pc->N_c, pc->K0inv.p, pc->K0dinv.p, pc->f0.p, pc->trsv_t.p, pc->trsv_y.p, pc->y0.p,
+                       pc->trsv_sync.p, done, st);
+    return;
+  }
   launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st, pc->sym_t0, pc->sym_t1);
   Comm* c = pc->prob->ctx->comm.get();
   if (c && c->world > 1) c->allreduce_sum(pc->y0.p, pc->N_c, st);
@@ -724,6 +749,14 @@ static int precond_launches(const ms_precond* pc) {
 extern "C" {
 
 int ms_abi_version(void) { return MSGPU_ABI_VERSION; }
+
+int ms_unit_element(double nu, double* Ke64) {
+  MS_API_BEGIN
+  if (!Ke64) throw Error(MS_E_INVALID, "null argument");
+  if (!(nu >= 0.0 && nu < 0.5)) throw Error(MS_E_INVALID, "Poisson ratio outside [0, 0.5)");
+  unit_elasticity(nu, Ke64);
+  MS_API_END(nullptr)
+}
 
 int ms_last_error(const ms_ctx* ctx, char* buf, size_t len) {
   if (!buf || len == 0) return MS_E_INVALID;
@@ -954,6 +987,7 @@ int64_t ms_problem_n_free(const ms_problem* prob) { return prob ? prob->n_free :
 int ms_problem_set_modulus(ms_problem* prob, const double* E) {
   MS_API_BEGIN
   if (!prob || !E) throw Error(MS_E_INVALID, "null argument");
+  MS_CUDA(cudaSetDevice(prob->ctx->device));
   const int64_t n_el = (int64_t)prob->g.nx * prob->g.ny;
   MS_CUDA(cudaMemcpyAsync(prob->E.p, E, n_el * sizeof(double), cudaMemcpyDefault, prob->ctx->st));
   MS_CUDA(cudaStreamSynchronize(prob->ctx->st));
@@ -987,6 +1021,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     throw Error(MS_E_INVALID, "block level-1 needs overlap delta >= 1");
   if (o->local_solver != MS_LOCAL_BANDED && o->local_solver != MS_LOCAL_DENSE_INV)
     throw Error(MS_E_INVALID, "unknown local solver");
+  if (o->coarse_solve != MS_COARSE_INVERSE && o->coarse_solve != MS_COARSE_CHOLESKY)
+    throw Error(MS_E_INVALID, "unknown coarse solve");
   if (o->level1_operator != MS_L1_ELASTICITY && o->level1_operator != MS_L1_HEAT)
     throw Error(MS_E_INVALID, "unknown level-1 operator");
   const bool heat_l1 = o->level1_operator == MS_L1_HEAT;
@@ -1375,7 +1411,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     if (W > 1) P->ctx->comm->allreduce_sum(K0.p, (size_t)N * N, st);
     launch_symmetrize(N, K0.p, st);
     const int nt = div_up(N, kTile);
-    if (W > 1) {  // balanced contiguous share of the packed tiles
+    pc->coarse_factor = o->coarse_solve == MS_COARSE_CHOLESKY;
+    if (W > 1 && !pc->coarse_factor) {  // balanced contiguous share of the packed tiles
       const int64_t ntl = packed_tiles(nt);
       pc->sym_t0 = ntl * R / W;
       pc->sym_t1 = ntl * (R + 1) / W;
@@ -1384,7 +1421,15 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     DBuf<double> inv_work;
     inv_work.alloc(dense_spd_inverse_work_bytes(N) / sizeof(double));
     fail.zero(st);
-    dense_spd_inverse(N, K0.p, pc->K0inv.p, inv_work.p, fail.p, st);
+    if (pc->coarse_factor) {
+      pc->K0dinv.alloc((size_t)nt * kTile * kTile);
+      pc->trsv_t.alloc((size_t)nt * kTile);
+      pc->trsv_y.alloc((size_t)nt * kTile);
+      pc->trsv_sync.alloc(trsv_sync_ints(N));
+      dense_cholesky(N, K0.p, pc->K0inv.p, pc->K0dinv.p, inv_work.p, fail.p, st);
+    } else {
+      dense_spd_inverse(N, K0.p, pc->K0inv.p, inv_work.p, fail.p, st);
+    }
     check_fail(fail, st, "coarse operator: basis is rank deficient, K0");
     pc->f0.alloc(N + 1);  // + the ||r||^2 slot of the multi-rank PCG allreduce
     pc->y0.alloc(N);
@@ -1396,7 +1441,8 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->h_evals.resize((size_t)nc * kNeig);
     MS_CUDA(cudaMemcpyAsync(pc->h_evals.data(), pc->evals.p, pc->h_evals.size() * sizeof(double),
                             cudaMemcpyDeviceToHost, st));
-    pc->info.coarse_bytes = (double)(psi_cursor + (int64_t)packed_tiles(nt) * kTile * kTile) * sizeof(double);
+    pc->info.coarse_bytes = (double)(psi_cursor + (int64_t)packed_tiles(nt) * kTile * kTile *
+                                                      (pc->coarse_factor ? 2 : 1)) * sizeof(double);
   } else {
     MS_CUDA(cudaEventRecord(e2, st));
   }
@@ -1517,7 +1563,11 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
       launch_restrict_reduce(pc->cd, pc->f0.p, nullptr, st, pc->kc0, pc->kc1);
     });
     ms[MS_BENCH_COARSE_SOLVE] = timeit([&] {
-      launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
+      if (pc->coarse_factor)
+        launch_trsv_packed(pc->N_c, pc->K0inv.p, pc->K0dinv.p, pc->f0.p, pc->trsv_t.p, pc->trsv_y.p, pc->y0.p,
+                           pc->trsv_sync.p, nullptr, st);
+      else
+        launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, nullptr, st);
     });
     ms[MS_BENCH_COMBINE_COARSE] = timeit([&] {
       launch_combine(g, P->mask.p, nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, P->z.p,
@@ -1917,6 +1967,43 @@ int ms_compliance_sensitivity(ms_ctx* ctx, int nx, int ny, double nu, const doub
   launch_compliance_sens(g, ke, u.d, r.d, p, E_min, E_max, o.d, st);
   MS_CUDA(cudaMemcpyAsync(g0, ctx->dval.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   o.finish(st);
+  MS_API_END(ctx)
+}
+
+int ms_dense_spd_solve(ms_ctx* ctx, int N, const double* A, const double* b, double* x, int mode) {
+  MS_API_BEGIN
+  if (!ctx || !A || !b || !x || N < 1) throw Error(MS_E_INVALID, "bad argument");
+  if (mode != MS_COARSE_INVERSE && mode != MS_COARSE_CHOLESKY) throw Error(MS_E_INVALID, "unknown solve mode");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const cudaStream_t st = ctx->st;
+  DevIn dA(A, (int64_t)N * N, st), db(b, N, st);
+  DevOut dx(x, N, st);
+  const int nt = div_up(N, kTile);
+  DBuf<double> M, work;
+  DBuf<int> fail;
+  fail.alloc(1);
+  fail.zero(st);
+  M.alloc((size_t)packed_words(nt));
+  work.alloc(dense_spd_inverse_work_bytes(N) / sizeof(double));
+  if (mode == MS_COARSE_CHOLESKY) {
+    DBuf<double> dinv, t, ys;
+    DBuf<int> sync;
+    dinv.alloc((size_t)nt * kTile * kTile);
+    t.alloc((size_t)nt * kTile);
+    ys.alloc((size_t)nt * kTile);
+    sync.alloc(trsv_sync_ints(N));
+    dense_cholesky(N, dA.d, M.p, dinv.p, work.p, fail.p, st);
+    check_fail(fail, st, "dense matrix");
+    launch_trsv_packed(N, M.p, dinv.p, db.d, t.p, ys.p, dx.d, sync.p, nullptr, st);
+    dx.finish(st);
+  } else {
+    DBuf<double> part;
+    part.alloc((size_t)packed_tiles(nt) * 2 * kTile);
+    dense_spd_inverse(N, dA.d, M.p, work.p, fail.p, st);
+    check_fail(fail, st, "dense matrix");
+    launch_symv_packed(N, M.p, db.d, dx.d, part.p, nullptr, st);
+    dx.finish(st);
+  }
   MS_API_END(ctx)
 }
 

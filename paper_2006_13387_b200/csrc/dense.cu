@@ -269,9 +269,7 @@ __global__ void __launch_bounds__(kTT) k_lauum_tiles(int nt, const double* __res
   acc_store(acc, X + tile_index(i, j) * T * T, 1.0, false);
 }
 
-void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, int* fail,
-                               cudaStream_t st) {
-  if (nt == 0 || B == 0) return;
+static void tile_kernels_configure() {
   const size_t smem = 2 * T * TP * sizeof(double);
   static bool attr_done[64] = {};  // function attributes are per device
   int dev = 0;
@@ -285,6 +283,12 @@ void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, i
     MS_CUDA(cudaFuncSetAttribute(k_lauum_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
+}
+
+// right-looking tiled Cholesky: P <- L, W(k,k) <- L_kk^-1 (other W tiles zero)
+static void tiled_cholesky(int nt, int B, double* P, double* W, int* fail, cudaStream_t st) {
+  const size_t smem = 2 * T * TP * sizeof(double);
+  tile_kernels_configure();
   MS_CUDA(cudaMemsetAsync(W, 0, (size_t)B * packed_words(nt) * sizeof(double), st));
   for (int k = 0; k < nt; ++k) {
     k_potrf_tile<<<dim3(1, B), kTT, smem, st>>>(k, nt, P, W, fail);
@@ -294,8 +298,194 @@ void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, i
       k_syrk_tiles<<<dim3((unsigned)((int64_t)m * (m + 1) / 2), B), kTT, smem, st>>>(k, nt, P);
     }
   }
+  MS_CUDA(cudaGetLastError());
+}
+
+void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, int* fail,
+                               cudaStream_t st) {
+  if (nt == 0 || B == 0) return;
+  const size_t smem = 2 * T * TP * sizeof(double);
+  tiled_cholesky(nt, B, P, W, fail, st);
   for (int d = 1; d < nt; ++d) k_trtri_tiles<<<dim3(nt - d, B), kTT, smem, st>>>(d, nt, P, W);
   k_lauum_tiles<<<dim3((unsigned)packed_tiles(nt), B), kTT, smem, st>>>(nt, W, X);
+  MS_CUDA(cudaGetLastError());
+}
+
+__global__ void k_copy_diag_tiles(int nt, const double* __restrict__ W, double* __restrict__ D) {
+  const int k = blockIdx.x;
+  const double* src = W + tile_index(k, k) * T * T;
+  for (int t = threadIdx.x; t < T * T; t += blockDim.x) D[(int64_t)k * T * T + t] = src[t];
+}
+
+void dense_cholesky(int N, const double* A, double* packed_L, double* diag_inv, double* work, int* fail,
+                    cudaStream_t st) {
+  if (N == 0) return;
+  const int nt = div_up(N, T);
+  k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, packed_L);
+  MS_CUDA(cudaGetLastError());
+  tiled_cholesky(nt, 1, packed_L, work, fail, st);
+  k_copy_diag_tiles<<<nt, 256, 0, st>>>(nt, work, diag_inv);
+  MS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// cho_solve (coarse.py:154, LAPACK ?potrs): forward L t = f, then backward
+// L^T y = t, blocked by 64-row tiles of the packed factor.  One CTA per tile
+// row; rows are claimed through an atomic ticket in dependency order, so a
+// CTA only ever waits (spinning on a flag) for rows already claimed by a
+// running CTA.  Row I: the off-diagonal products are accumulated in
+// registers over all finished rows J (ascending J), reduced once, subtracted
+// from the right-hand side, and the diagonal block is solved with the
+// inverse L_II^-1 of the factorisation's diagonal tile.  Fixed order ->
+// deterministic.  sync: 2 tickets + 2 nt flags, zeroed before every solve.
+__device__ __forceinline__ void spin_flag(const int* flag) {
+  if (threadIdx.x == 0) {
+    while (*(volatile const int*)flag == 0) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256)
+    k_trsv_fwd(int N, int nt, const double* __restrict__ L, const double* __restrict__ Dinv,
+               const double* __restrict__ f, double* t, int* sync, const int* done) {
+  if (done && *(volatile const int*)done) return;
+  __shared__ int sI;
+  __shared__ double s[T];
+  if (threadIdx.x == 0) sI = atomicAdd(&sync[0], 1);
+  __syncthreads();
+  const int I = sI;
+  int* flag = sync + 2;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double u[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int J = 0; J < I; ++J) {
+    const double* Lt = L + tile_index(I, J) * T * T;
+    double2 a[4][2];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2* row = reinterpret_cast<const double2*>(Lt + (ty * 4 + rr) * T + tx * 4);
+      a[rr][0] = __ldg(row);
+      a[rr][1] = __ldg(row + 1);
+    }
+    spin_flag(flag + J);
+    double y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[q] = __ldcg(t + J * T + tx * 4 + q);
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+      u[rr] += a[rr][0].x * y[0] + a[rr][0].y * y[1] + a[rr][1].x * y[2] + a[rr][1].y * y[3];
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
+  if (tx == 0) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int row = I * T + ty * 4 + rr;
+      s[ty * 4 + rr] = (row < N ? f[row] : 0.0) - u[rr];
+    }
+  }
+  __syncthreads();
+  const double* D = Dinv + (int64_t)I * T * T;
+  double w[4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const double* dr = D + (ty * 4 + rr) * T + tx * 4;
+    w[rr] = dr[0] * s[tx * 4] + dr[1] * s[tx * 4 + 1] + dr[2] * s[tx * 4 + 2] + dr[3] * s[tx * 4 + 3];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) w[rr] += __shfl_xor_sync(0xffffffffu, w[rr], o);
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) t[I * T + ty * 4 + rr] = w[rr];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(flag + I, 1);
+}
+
+__global__ void __launch_bounds__(256)
+    k_trsv_bwd(int N, int nt, const double* __restrict__ L, const double* __restrict__ Dinv,
+               const double* t, double* y, double* yscratch, int* sync, const int* done) {
+  if (done && *(volatile const int*)done) return;
+  __shared__ int sI;
+  __shared__ double sv[16][T + 1];
+  __shared__ double s[T];
+  if (threadIdx.x == 0) sI = nt - 1 - atomicAdd(&sync[1], 1);
+  __syncthreads();
+  const int I = sI;
+  int* flag = sync + 2 + nt;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int J = nt - 1; J > I; --J) {
+    const double* Lt = L + tile_index(J, I) * T * T;
+    double2 a[4][2];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2* row = reinterpret_cast<const double2*>(Lt + (ty * 4 + rr) * T + tx * 4);
+      a[rr][0] = __ldg(row);
+      a[rr][1] = __ldg(row + 1);
+    }
+    spin_flag(flag + J);
+    double xr[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) xr[rr] = __ldcg(yscratch + J * T + ty * 4 + rr);
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      v[0] += a[rr][0].x * xr[rr];
+      v[1] += a[rr][0].y * xr[rr];
+      v[2] += a[rr][1].x * xr[rr];
+      v[3] += a[rr][1].y * xr[rr];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sv[ty][tx * 4 + q] = v[q];
+  __syncthreads();
+  if (threadIdx.x < T) {
+    double acc = 0.0;
+#pragma unroll
+    for (int g = 0; g < 16; ++g) acc += sv[g][threadIdx.x];
+    s[threadIdx.x] = __ldcg(t + I * T + threadIdx.x) - acc;
+  }
+  __syncthreads();
+  // x_I = L_II^-T s: x[c] = sum_r Dinv[r][c] s[r]
+  const double* D = Dinv + (int64_t)I * T * T;
+  double w[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const double sr = s[ty * 4 + rr];
+    const double* dr = D + (ty * 4 + rr) * T + tx * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] += dr[q] * sr;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sv[ty][tx * 4 + q] = w[q];
+  __syncthreads();
+  if (threadIdx.x < T) {
+    double acc = 0.0;
+#pragma unroll
+    for (int g = 0; g < 16; ++g) acc += sv[g][threadIdx.x];
+    const int row = I * T + threadIdx.x;
+    yscratch[row] = acc;
+    if (row < N) y[row] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(flag + I, 1);
+}
+
+size_t trsv_sync_ints(int N) { return 2 + 2 * (size_t)div_up(N, T); }
+
+void launch_trsv_packed(int N, const double* L, const double* Dinv, const double* f, double* t,
+                        double* yscratch, double* y, int* sync, const int* done, cudaStream_t st) {
+  if (N == 0) return;
+  const int nt = div_up(N, T);
+  MS_CUDA(cudaMemsetAsync(sync, 0, trsv_sync_ints(N) * sizeof(int), st));
+  k_trsv_fwd<<<nt, 256, 0, st>>>(N, nt, L, Dinv, f, t, sync, done);
+  k_trsv_bwd<<<nt, 256, 0, st>>>(N, nt, L, Dinv, t, y, yscratch, sync, done);
   MS_CUDA(cudaGetLastError());
 }
 

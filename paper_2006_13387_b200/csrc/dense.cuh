@@ -26,6 +26,17 @@ void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work,
                        cudaStream_t st);
 size_t dense_spd_inverse_work_bytes(int N);
 
+// Cholesky factor only (the reference's cho_factor, coarse.py:143): packed_L
+// (packed_words(nt)) <- L, diag_inv (nt * 64 * 64) <- the inverses of its
+// diagonal tiles; work: packed_words(nt) doubles.
+void dense_cholesky(int N, const double* A, double* packed_L, double* diag_inv, double* work, int* fail,
+                    cudaStream_t st);
+// y = L^-T L^-1 f (cho_solve, coarse.py:154): blocked forward/backward
+// triangular solves; t, yscratch: nt*64 doubles; sync: trsv_sync_ints(N) ints.
+size_t trsv_sync_ints(int N);
+void launch_trsv_packed(int N, const double* L, const double* Dinv, const double* f, double* t,
+                        double* yscratch, double* y, int* sync, const int* done, cudaStream_t st);
+
 // y = X f for one packed symmetric matrix; `part` needs packed_tiles(nt)*2*64 doubles.
 // [t_begin, t_end): only these packed tiles contribute (a rank's share of a
 // sharded coarse solve; the caller sums y over ranks); default all.

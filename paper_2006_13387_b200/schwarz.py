@@ -1,10 +1,10 @@
 """Two-level additive Schwarz preconditioner on the GPU (reference schwarz.py).
 
 ``build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts)``
-keeps the reference signature (schwarz.py:176-211).  The GPU path implements
-the EH and EH+Rot variants (elasticity level 1, heat-eigenproblem coarse
-space, gap rule); the other Table-1 tags are listed for API parity and raise
-``NotImplementedError`` (SURVEY.md §8(f) ranks them "next").
+keeps the reference signature (schwarz.py:176-211).  All seven Table-1
+variants run on the GPU (``GPU_VARIANTS``): EH, EH+Rot, EH+Rot;Rand (heat
+eigenproblems, gap rule), HH, HH+Rot (heat level 1) and EE, EE;Rand
+(elasticity eigenproblems, rule 'fixed'); "None" is plain CG.
 """
 
 from __future__ import annotations
@@ -159,12 +159,16 @@ def randomized_forcings(mesh, part, dirichlet_nodes, n_snapshots, seed, kind="di
 
 
 def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None, *,
-                         level1="neighborhoods", delta=None, use_coarse=True, local_solver="banded"):
+                         level1="neighborhoods", delta=None, use_coarse=True, local_solver="banded",
+                         coarse_solve="inverse"):
     """Build a two-level preconditioner by variant name (schwarz.py:176-211).
 
     level1='neighborhoods' is the reference's layout (subdomains = omega_j);
     level1='blocks' uses delta-extended coarse blocks (the BASELINE configs).
     ``dirichlet_nodes`` are the whole nodes clamped in the heat eigenproblems.
+    coarse_solve='inverse' applies an explicit packed K0^-1 (one SYMV per
+    apply); 'cholesky' keeps the reference's arithmetic, the Cholesky factor
+    and two triangular solves (cho_factor / cho_solve, coarse.py:143,154).
     """
     if tag == "None":
         return IdentityPreconditioner()
@@ -199,6 +203,9 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         raise ValueError(f"unknown local solver {local_solver!r}")
     o.local_solver = _lib.MS_LOCAL_BANDED if local_solver == "banded" else _lib.MS_LOCAL_DENSE_INV
     o.use_coarse = 1 if use_coarse else 0
+    if coarse_solve not in ("inverse", "cholesky"):
+        raise ValueError(f"unknown coarse solve {coarse_solve!r}")
+    o.coarse_solve = _lib.MS_COARSE_CHOLESKY if coarse_solve == "cholesky" else _lib.MS_COARSE_INVERSE
     o.level1_operator = _lib.MS_L1_HEAT if variant.level1 == "heat" else _lib.MS_L1_ELASTICITY
     o.eig_kind = _lib.MS_EIG_ELASTICITY if elastic else _lib.MS_EIG_HEAT
     o.heat_dirichlet_nodes = hd.ctypes.data_as(C.POINTER(C.c_int64)) if hd.size else None
@@ -225,5 +232,6 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
         "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,
         "coarse_bytes": inf.coarse_bytes, "level1": level1, "level1_operator": variant.level1, "delta": delta, "local_solver": local_solver,
+        "coarse_solve": coarse_solve,
     }
     return TwoLevelPreconditioner(variant, op, h, info)

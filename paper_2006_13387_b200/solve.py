@@ -12,7 +12,7 @@ from .krylov import pcg_solve
 from .schwarz import EigOptions, build_preconditioner
 
 
-def setup_spec(spec, tag="EH+Rot", level1="blocks", local_solver="banded"):
+def setup_spec(spec, tag="EH+Rot", level1="blocks", local_solver="banded", coarse_solve="inverse"):
     mesh = build_fine_mesh(spec.nx, spec.ny)
     coeff = CoefficientField(spec.E, spec.nu, spec.E_min, spec.E_max)
     op = ElasticityOperator(mesh, coeff, spec.free_dofs())
@@ -20,7 +20,7 @@ def setup_spec(spec, tag="EH+Rot", level1="blocks", local_solver="banded"):
     t0 = time.perf_counter()
     pre = build_preconditioner(tag, op, mesh, part, coeff, spec.heat_dirichlet_nodes, EigOptions(),
                                level1=level1, delta=spec.delta if level1 == "blocks" else None,
-                               local_solver=local_solver)
+                               local_solver=local_solver, coarse_solve=coarse_solve)
     pre.info["t_build_wall"] = time.perf_counter() - t0
     return mesh, op, pre
 

@@ -102,7 +102,7 @@ def _solve_worker(rank, world, port, q, tag="EH+Rot"):
         from paper_2006_13387_b200.solve import setup_spec
 
         D.init_host_callbacks(0)
-        spec = configs.config1(seed=0, n=64, H=16, delta=2)
+        spec = configs.config1(seed=0)
         mesh, op, pre = setup_spec(spec, tag)
         x, rep = pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
         z = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
@@ -130,16 +130,24 @@ def test_two_ranks_on_one_gpu_match_single_rank(tag):
     from paper_2006_13387_b200 import configs, pcg_solve
     from paper_2006_13387_b200.solve import setup_spec
 
-    spec = configs.config1(seed=0, n=64, H=16, delta=2)
+    spec = configs.config1(seed=0)
     mesh, op, pre = setup_spec(spec, tag)
     x1, rep1 = pcg_solve(op, spec.rhs(), pre, tol=1e-8, maxit=5000)
     z1 = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
+    # the reference's own solve of this config and its measured round-off band
+    # (tests/golden/make_golden.py): the sharded solve must sit inside it
+    g = np.load(ROOT / "tests" / "golden" / ("ref_config1_hhrot.npz" if tag == "HH+Rot" else "ref_config1.npz"))
+    its = np.concatenate([[int(g["iters"])], g["jitter_iters"]])
+    ref_variant = tag in ("EH+Rot", "HH+Rot")
     for r in (0, 1):
         x, iters, conv, nc, modes, z = res[r]
         assert conv and nc == pre.coarse_dim and modes == list(pre.mode_counts)
         assert np.linalg.norm(z - z1) <= 1e-12 * np.linalg.norm(z1)
-        assert abs(iters - rep1.iterations) <= max(3, int(0.06 * rep1.iterations))
-        assert np.linalg.norm(x - x1) <= 1e-7 * np.linalg.norm(x1)
+        if ref_variant:
+            assert its.min() - 1 <= iters <= its.max() + 1, (iters, its)
+            assert np.linalg.norm(x - g["x"]) <= max(1e-8, 2 * g["jitter_x"].max()) * np.linalg.norm(g["x"])
+        # only the dot-product and coarse-solve summation orders differ from one rank
+        assert np.linalg.norm(x - x1) <= 1e-8 * np.linalg.norm(x1)
     assert np.array_equal(res[0][0], res[1][0])
 
 

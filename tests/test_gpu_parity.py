@@ -176,18 +176,35 @@ def test_deterministic_solves():
     assert np.array_equal(x1, x2) and r1.iterations == r2.iterations
 
 
-@pytest.mark.parametrize("name,tag", [("ref_config1.npz", "EH+Rot"), ("ref_mbb_64x32.npz", "EH+Rot"),
-                                      ("ref_config2_n128.npz", "EH+Rot"), ("ref_config3_n128.npz", "EH+Rot"),
-                                      ("ref_config1_hhrot.npz", "HH+Rot"),
-                                      ("ref_config2_n128_eta1e2.npz", "EH+Rot"),
-                                      ("ref_config2_n128_eta1e8.npz", "EH+Rot"),
-                                      ("ref_config5_n128_step3.npz", "EH+Rot")])
-def test_baseline_config_against_reference(name, tag):
+def reference_band(g):
+    """The reference's own round-off band recorded by make_golden.py: its
+    iteration count and those of >= 8 perturbed re-runs (level-1 order
+    reversed / permuted, b(1 +- 2^-52), explicit or lower-factor K0 solve,
+    other SuperLU orderings), the largest solution spread among them, and
+    the largest true residual ||b - A x|| / ||b|| the reference reached."""
+    its = np.concatenate([[int(g["iters"])], g["jitter_iters"]])
+    return (int(its.min()), int(its.max()), float(g["jitter_x"].max()),
+            float(max(g["true_residual"], g["jitter_true_residual"].max())))
+
+
+BASELINE_CASES = [("ref_config1.npz", "EH+Rot"), ("ref_mbb_64x32.npz", "EH+Rot"),
+                  ("ref_config2_n128.npz", "EH+Rot"), ("ref_config3_n128.npz", "EH+Rot"),
+                  ("ref_config1_hhrot.npz", "HH+Rot"),
+                  ("ref_config2_n128_eta1e2.npz", "EH+Rot"),
+                  ("ref_config2_n128_eta1e8.npz", "EH+Rot"),
+                  ("ref_config5_n128_step3.npz", "EH+Rot"),
+                  ("ref_config5_n64_step0.npz", "EH+Rot"), ("ref_config5_n64_step1.npz", "EH+Rot"),
+                  ("ref_config5_n64_step2.npz", "EH+Rot")]
+
+
+@pytest.mark.parametrize("coarse_solve", ["inverse", "cholesky"])
+@pytest.mark.parametrize("name,tag", BASELINE_CASES)
+def test_baseline_config_against_reference(name, tag, coarse_solve):
     g = load_golden(name)
     spec = spec_from_golden(g)
     from paper_2006_13387_b200.solve import setup_spec
 
-    mesh, op, pre = setup_spec(spec, tag)
+    mesh, op, pre = setup_spec(spec, tag, coarse_solve=coarse_solve)
     assert pre.coarse_dim == int(g["coarse_dim"])
     assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
     z = pre.apply(g["apply_r"])
@@ -195,31 +212,21 @@ def test_baseline_config_against_reference(name, tag):
     # 2.2e-7 at eta 1e8)
     eta = spec.E_max / spec.E_min
     assert rel(z, g["apply_z"]) <= max(1e-7, 1e-14 * eta)
-    x, rep = G.pcg_solve(op, spec.rhs(), pre, tol=float(g["tol"]), maxit=5000)
-    # Iteration counts of these ill-conditioned solves (kappa ~ 1e7, hundreds to
-    # thousands of iterations) are chaotic under round-off: the reference moves
-    # by its jitter band (reversed level-1 order, b*(1+2^-52)), and changing only
-    # the summation order inside our own kernels moved config-3-128 between
-    # 2271 and 2356 iterations.  Accept max(3 x jitter width, 6%).  The early
-    # trajectory, before round-off amplification, must agree tightly.
-    ref_it = int(g["iters"])
-    width = max(1, int(np.abs(g["jitter_iters"] - ref_it).max()))
-    tol_it = max(3 * width, int(np.ceil(0.06 * ref_it)))
-    assert rep.converged and abs(rep.iterations - ref_it) <= tol_it, (rep.iterations, ref_it, g["jitter_iters"])
+    x, rep = G.pcg_solve(op, spec.rhs(), pre, tol=float(g["tol"]), maxit=int(g["maxit"]))
+    # Iterations: inside the reference's own measured band, +-1 (north star
+    # +-1 around a count that round-off alone moves by the band's width)
+    lo, hi, x_spread, true_res = reference_band(g)
+    assert rep.converged and lo - 1 <= rep.iterations <= hi + 1, (rep.iterations, lo, hi, int(g["iters"]))
     k = min(15, len(g["residuals"]) - 1)
     assert np.allclose(rep.residuals[:k], g["residuals"][:k], rtol=1e-5), "early PCG trajectory differs"
-    # The reference's own PCG solution sits ~1e-8 from the exact one on these
-    # ill-conditioned configs, so parity is judged against the direct solve:
-    # the GPU solution must be as accurate as the reference's (x2 slack), and
-    # within 1e-8 of the reference wherever the reference is that accurate.
+    # Solution: within 1e-8 of the reference's, or of twice the reference's
+    # own spread under the same perturbations when that is larger
+    assert rel(x, g["x"]) <= max(1e-8, 2.0 * x_spread), (rel(x, g["x"]), x_spread)
+    # and as converged as the reference: true residual no worse than the
+    # worst the reference band reached (x2)
     prob = O.problem_from_spec(spec)
-    import scipy.sparse.linalg as spla
-
-    x_dir = spla.spsolve(prob.op.matrix.tocsc(), prob.b)
-    e_ref = rel(g["x"], x_dir)
-    e_gpu = rel(x, x_dir)
-    assert e_gpu <= max(1e-8, 2.0 * e_ref), (e_gpu, e_ref)
-    assert rel(x, g["x"]) <= max(1e-8, 3.0 * e_ref, 10 * float(g["jitter_x"].max()))
+    r_true = float(np.linalg.norm(prob.b - prob.op.matrix @ x) / np.linalg.norm(prob.b))
+    assert r_true <= 2.0 * true_res, (r_true, true_res)
 
 
 @pytest.mark.parametrize("name,tag", [("ref_bench100_hhrot_eta1.npz", "HH+Rot"),
@@ -272,13 +279,18 @@ def test_level1_only_matches_oracle(rng):
         assert rel(pre.apply(r), P.apply(r)) <= 1e-8
 
 
-def test_coarse_apply_matches_oracle(rng):
+@pytest.mark.parametrize("coarse_solve", ["inverse", "cholesky"])
+def test_coarse_apply_matches_oracle(rng, coarse_solve):
+    """R0^T K0^-1 R0 r against the oracle's cho_solve (coarse.py:150-158) with
+    the explicit packed inverse and with the factor + blocked triangular
+    solves; both against each other to K0's round-off."""
     spec = configs.config3(seed=2, n=64, H=16, delta=2, eta=1e4)
     prob = O.problem_from_spec(spec)
     Po = O.build_two_level(prob, H=16, delta=2, level1_mode="blocks")
     from paper_2006_13387_b200.solve import setup_spec
 
-    mesh, op, pre = setup_spec(spec)
+    mesh, op, pre = setup_spec(spec, coarse_solve=coarse_solve)
+    assert pre.info["coarse_solve"] == coarse_solve
     assert pre.coarse_dim == Po.coarse_dim
     assert pre.mode_counts == Po.info["mode_counts"]
     for _ in range(3):
@@ -286,10 +298,44 @@ def test_coarse_apply_matches_oracle(rng):
         assert rel(pre.apply_coarse(r), Po.coarse.apply(r)) <= 1e-8
 
 
-def test_config5_sequence_rebuild_matches_oracle():
-    """Config-5 shape at 64^2: density sequence, set_modulus + full rebuild per step."""
-    import scipy.sparse.linalg as spla
+@pytest.mark.parametrize("mode", ["inverse", "cholesky"])
+@pytest.mark.parametrize("N", [1, 37, 64, 65, 200, 1000])
+def test_dense_spd_solve_kernels(N, mode, rng):
+    """The two coarse-solve forms on dense SPD matrices of order N (single
+    element, ragged last tile, exact tiles, many tiles): x = A^-1 b to
+    cond * eps against LAPACK cho_solve; non-SPD input raises ValueError
+    (the reference's CoarseOperator, coarse.py:142-147)."""
+    import ctypes as C
 
+    import scipy.linalg as sla
+
+    from paper_2006_13387_b200 import _lib
+    from paper_2006_13387_b200._context import default_context
+
+    Q, _ = np.linalg.qr(rng.standard_normal((N, N)))
+    A = (Q * np.logspace(0, 6, N)) @ Q.T
+    A = np.ascontiguousarray(0.5 * (A + A.T))
+    b = rng.standard_normal(N)
+    x = np.empty(N)
+    ctx = default_context()
+    code = _lib.MS_COARSE_CHOLESKY if mode == "cholesky" else _lib.MS_COARSE_INVERSE
+    lib = _lib.load()
+    _lib.check(lib.ms_dense_spd_solve(ctx.handle, N, C.c_void_p(A.ctypes.data), C.c_void_p(b.ctypes.data),
+                                      C.c_void_p(x.ctypes.data), code), ctx.handle)
+    xr = sla.cho_solve(sla.cho_factor(A), b)
+    assert rel(x, xr) <= 1e-16 * np.linalg.cond(A) * 50
+    bad = A.copy()
+    bad[N // 2, N // 2] = -1.0
+    with pytest.raises(ValueError):
+        _lib.check(lib.ms_dense_spd_solve(ctx.handle, N, C.c_void_p(bad.ctypes.data), C.c_void_p(b.ctypes.data),
+                                          C.c_void_p(x.ctypes.data), code), ctx.handle)
+
+
+def test_config5_sequence_rebuild_in_place():
+    """Config-5 shape at 64^2: the density sequence driven through set_modulus
+    and a full rebuild per step on ONE operator gives the same coarse spaces and
+    solves as fresh operators (the steps' reference parity is in
+    test_baseline_config_against_reference, ref_config5_n64_step*)."""
     n, H, delta = 64, 16, 2
     base = configs.config5(seed=1, step=0, n=n, H=H, delta=delta)
     mesh = G.build_fine_mesh(n, n)
@@ -305,17 +351,16 @@ def test_config5_sequence_rebuild_matches_oracle():
         pre = G.build_preconditioner("EH+Rot", op, mesh, part, coeff, base.heat_dirichlet_nodes,
                                      level1="blocks", delta=delta)
         x, rep = G.pcg_solve(op, base.rhs(), pre, tol=1e-8, maxit=5000)
-        spec = configs.ProblemSpec(name="c5", nx=n, ny=n, E=E, E_min=base.E_min, E_max=1.0,
-                                   constrained_dofs=base.constrained_dofs,
-                                   heat_dirichlet_nodes=base.heat_dirichlet_nodes,
-                                   load_full=base.load_full, H=H, delta=delta)
-        prob = O.problem_from_spec(spec)
-        P = O.build_two_level(prob, H=H, delta=delta, level1_mode="blocks")
-        xo, repo = O.pcg(prob.op.matrix, prob.b, P, tol=1e-8, maxit=5000)
-        assert pre.coarse_dim == P.coarse_dim and pre.mode_counts == P.info["mode_counts"], k
-        assert rep.converged and abs(rep.iterations - repo.iterations) <= max(3, int(0.06 * repo.iterations))
-        x_dir = spla.spsolve(prob.op.matrix.tocsc(), prob.b)
-        assert rel(x, x_dir) <= max(1e-8, 2.0 * rel(xo, x_dir)), k
+        g = load_golden(f"ref_config5_n64_step{k}.npz")
+        assert np.array_equal(g["E"], E)
+        op2 = G.ElasticityOperator(mesh, coeff, base.free_dofs())
+        pre2 = G.build_preconditioner("EH+Rot", op2, mesh, part, coeff, base.heat_dirichlet_nodes,
+                                      level1="blocks", delta=delta)
+        x2, rep2 = G.pcg_solve(op2, base.rhs(), pre2, tol=1e-8, maxit=5000)
+        assert pre.coarse_dim == int(g["coarse_dim"]) and pre.mode_counts == list(g["mode_counts"])
+        assert np.array_equal(x, x2) and rep.iterations == rep2.iterations, k
+    with pytest.raises(ValueError):
+        op.set_modulus(np.ones(5))
 
 
 def test_profiling_and_graph_paths_agree():
@@ -353,8 +398,9 @@ def test_dense_inverse_local_solver_matches_banded(rng):
         assert rel(pre_d.apply(r), pre_b.apply(r)) <= 1e-8
     assert rel(pre_d.apply(g["apply_r"]), g["apply_z"]) <= 1e-7
     x, rep = G.pcg_solve(op_d, spec.rhs(), pre_d, tol=1e-8, maxit=5000)
-    ref_it = int(g["iters"])
-    assert rep.converged and abs(rep.iterations - ref_it) <= max(3, int(0.06 * ref_it))
+    lo, hi, x_spread, _ = reference_band(g)
+    assert rep.converged and lo - 1 <= rep.iterations <= hi + 1, (rep.iterations, lo, hi)
+    assert rel(x, g["x"]) <= max(1e-8, 2.0 * x_spread)
 
 
 @pytest.mark.parametrize("eta", ["1", "1e+06"])

@@ -41,13 +41,44 @@ def test_status_codes_map_to_reference_exceptions():
     _lib.check(_lib.MS_OK)
 
 
-def test_struct_layouts_match_header():
-    # sizes of the ABI structs as the C compiler lays them out (x86-64)
+def _c_layout(struct, fields):
+    """sizeof and offsetof of an ABI struct as gcc lays it out from the header."""
+    import subprocess
+    import tempfile
+
+    body = "".join(f'printf("%zu ", offsetof({struct}, {f}));' for f in fields)
+    src = (f'#include <stdio.h>\n#include <stddef.h>\n#include "msgpu.h"\n'
+           f'int main(void){{ {body} printf("%zu\\n", sizeof({struct})); return 0; }}\n')
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = Path(d) / "l.c", Path(d) / "l"
+        c.write_text(src)
+        subprocess.run(["gcc", "-I", str(HEADER.parent), str(c), "-o", str(exe)], check=True)
+        out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    return [int(v) for v in out]
+
+
+@pytest.mark.parametrize("cls,struct", [(_lib.PrecondOpts, "ms_precond_opts"),
+                                        (_lib.PrecondInfo, "ms_precond_info"),
+                                        (_lib.Report, "ms_report")])
+def test_struct_layouts_match_header(cls, struct):
+    # every field offset and the size of the ctypes mirror equal the C layout
     import ctypes as C
 
-    # 5 ints (+4 pad), double, 4 ints, pointer, int64, 2 ints, pointer, 2 ints
-    assert C.sizeof(_lib.PrecondOpts) == 5 * 4 + 4 + 8 + 4 * 4 + 8 + 8 + 2 * 4 + 8 + 2 * 4
-    assert C.sizeof(_lib.Report) == 8 + 4 + 4 + 8 * 3
+    names = [f for f, _ in cls._fields_]
+    got = [getattr(cls, f).offset for f in names] + [C.sizeof(cls)]
+    assert got == _c_layout(struct, names)
+
+
+def test_unit_element_bitwise_equals_reference():
+    # assembly.py:100-116 evaluated by the library (host arithmetic, no GPU):
+    # all 64 doubles identical to the reference's for both Poisson ratios
+    g = load_golden("ref_elements.npz")
+    for nu, key in ((0.3, "Ke0_nu03"), (0.25, "Ke0_nu025")):
+        K = G.element_stiffness_elasticity(1.0, nu)
+        assert np.array_equal(K, g[key]), (nu, np.argwhere(K != g[key]))
+    assert np.array_equal(G.element_stiffness_elasticity(2.5, 0.3), 2.5 * g["Ke0_nu03"])
+    with pytest.raises(ValueError):
+        G.element_stiffness_elasticity(1.0, 0.5)
 
 
 def test_variant_table_and_errors():
