@@ -114,6 +114,10 @@ typedef struct ms_precond_info {
   double t_coarse;       /* s, eigensolves + basis + K0 + factor/inverse      */
   double local_bytes;    /* bytes of level-1 operator data read per apply     */
   double coarse_bytes;   /* bytes of coarse data (psi + K0^-1) read per apply */
+  int level1_twisted;    /* 1: two-sided (twisted) level-1 factors, 2 warps per subdomain */
+  int level1_copies;     /* banded factor copies read per apply: 1 (column band, dot-form
+                            backward sweep) or 2 (column + row band)                        */
+  int n_subdomains_local; /* level-1 subdomains owned by this rank (all of them on one rank)    */
 } ms_precond_info;
 
 /* SolveReport (krylov.py:17-35); history arrays are caller-provided. */

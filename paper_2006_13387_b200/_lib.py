@@ -64,6 +64,7 @@ class PrecondInfo(C.Structure):
         ("coarse_dim", C.c_int), ("n_centers", C.c_int), ("n_subdomains", C.c_int),
         ("max_eig_passes", C.c_int), ("mean_eig_passes", C.c_double), ("t_level1", C.c_double), ("t_eig", C.c_double),
         ("t_coarse", C.c_double), ("local_bytes", C.c_double), ("coarse_bytes", C.c_double),
+        ("level1_twisted", C.c_int), ("level1_copies", C.c_int), ("n_subdomains_local", C.c_int),
     ]
 
 

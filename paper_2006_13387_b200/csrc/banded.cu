@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256)
 void launch_l1_assemble(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,
                         const BandSys* sys, int nsys, double* Lc, cudaStream_t st) {
   if (nsys == 0) return;
-  k_l1_assemble<<<nsys, 256, 0, st>>>(g, ke, E, mask, sys, Lc);
+  { k_l1_assemble<<<nsys, 256, 0, st>>>(g, ke, E, mask, sys, Lc); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -119,7 +119,7 @@ void launch_l1_heat_assemble(const Grid& g, const double* lap, const double* E, 
   if (nsys == 0) return;
   LapParam lp;
   for (int i = 0; i < 16; ++i) lp.lap[i] = lap[i];
-  k_l1_heat_assemble<<<nsys, 256, 0, st>>>(g, lp, E, mask, sys, Lc);
+  { k_l1_heat_assemble<<<nsys, 256, 0, st>>>(g, lp, E, mask, sys, Lc); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -130,7 +130,7 @@ __global__ void k_whole_node_check(int64_t n_nodes, const uint8_t* __restrict__ 
 }
 
 void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cudaStream_t st) {
-  k_whole_node_check<<<4 * 148, 256, 0, st>>>(g.n_nodes, mask, fail);
+  { k_whole_node_check<<<4 * 148, 256, 0, st>>>(g.n_nodes, mask, fail); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -144,10 +144,11 @@ void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cuda
 // (forward sweep -> D^-1 L^-1 b), Lr the unit factor l_{k+j,k} with 1.
 __global__ void __launch_bounds__(256)
     k_band_potrf(const BandSys* __restrict__ sys, double* __restrict__ Lc,
-                 double* __restrict__ Lr, int* fail, int ldl) {
+                 double* __restrict__ Lr, int* fail, int ldl, double* __restrict__ schur) {
   extern __shared__ double smem[];
   const BandSys s = sys[blockIdx.x];
   const int bw = s.bw, S = bw + 1, n = s.n;
+  const int ne = (s.nelim > 0 && s.nelim < n) ? s.nelim : n;  // columns eliminated
   double* W = smem;                                           // S*S
   short2* pairs = reinterpret_cast<short2*>(smem + S * S);    // bw(bw+1)/2
   const int npairs = bw * (bw + 1) / 2;
@@ -157,14 +158,14 @@ __global__ void __launch_bounds__(256)
       for (int j1 = j2; j1 <= bw; ++j1) pairs[p++] = make_short2((short)j1, (short)j2);
   }
   double* colc = Lc + s.foff;
-  double* colr = Lr + s.foff;
+  double* colr = Lr ? Lr + s.foff : nullptr;  // row band: only for the two-copy sweeps
   for (int t = threadIdx.x; t < S * S; t += blockDim.x) {
     const int c = t / S, j = t % S;
     W[t] = (c < n) ? colc[(int64_t)c * S + j] : 0.0;
   }
   __syncthreads();
   bool bad = false;
-  for (int k = 0; k < n; ++k) {
+  for (int k = 0; k < ne; ++k) {
     const int sk = k % S;
     double d = W[sk * S];
     if (ldl ? !(d != 0.0 && isfinite(d)) : !(d > 0.0)) {
@@ -188,23 +189,125 @@ __global__ void __launch_bounds__(256)
         vc = vr = (j == 0) ? inv : W[sk * S + j] * inv;
       }
       colc[(int64_t)k * S + j] = vc;
-      if (k + j < n) colr[(int64_t)(k + j) * S + j] = vr;
+      if (Lr && k + j < n) colr[(int64_t)(k + j) * S + j] = vr;
       const int cn = k + S;  // next column into the freed slot
       W[sk * S + j] = (cn < n) ? colc[(int64_t)cn * S + j] : 0.0;
     }
     __syncthreads();
   }
+  if (ne < n) {
+    // partial factorisation (twisted level 1): the window holds the Schur
+    // complement of the last cnt = n - ne unknowns; dump it, make the
+    // remaining columns identity
+    const int cnt = n - ne;
+    double* out = schur + s.yoff;
+    for (int t = threadIdx.x; t < cnt * cnt; t += blockDim.x) {
+      const int i = t / cnt, i2 = t % cnt;
+      const int lo = min(i, i2), d = abs(i - i2);
+      out[t] = W[((ne + lo) % S) * S + d];
+    }
+    for (int t = threadIdx.x; t < cnt * S; t += blockDim.x) {
+      const int k = ne + t / S, j = t % S;
+      const double v = j == 0 ? 1.0 : 0.0;
+      colc[(int64_t)k * S + j] = v;
+      if (Lr && k + j < n) colr[(int64_t)(k + j) * S + j] = v;
+    }
+  }
   if (bad && threadIdx.x == 0) atomicCAS(fail, 0, (int)blockIdx.x + 1);
 }
 
+// top / bottom column bands of the twisted systems from the natural band
+__global__ void __launch_bounds__(256)
+    k_twist_split(const BandSys* __restrict__ nat, const BandSys* __restrict__ sys,
+                  const double* __restrict__ band, double* __restrict__ Lc) {
+  const BandSys s = sys[blockIdx.x];
+  const int64_t fn = nat[blockIdx.x].foff;
+  const int S = s.bw + 1, n = s.n, m = s.m, nT = m + s.bw, nB = n - m;
+  for (int64_t t = threadIdx.x; t < (int64_t)nT * S; t += blockDim.x) {
+    const int k = (int)(t / S), j = (int)(t % S);
+    Lc[s.foff + t] = (k + j < nT) ? band[fn + t] : 0.0;  // separator block kept
+  }
+  for (int64_t t = threadIdx.x; t < (int64_t)nB * S; t += blockDim.x) {
+    const int q = (int)(t / S), j = (int)(t % S);
+    // bottom-local column q = natural column n-1-q; row q+j = natural n-1-q-j
+    const int cn = n - 1 - q;
+    const bool ok = q + j < nB && q < nB - s.bw;  // separator block of B is zero
+    Lc[s.foffB + t] = ok ? band[fn + (int64_t)(cn - j) * S + j] : 0.0;
+  }
+}
+
+void launch_twist_split(const BandSys* nat, const BandSys* sys, int nsys, int max_bw, const double* band_nat,
+                        double* Lc, cudaStream_t st) {
+  (void)max_bw;
+  if (nsys == 0) return;
+  { k_twist_split<<<nsys, 256, 0, st>>>(nat, sys, band_nat, Lc); ms_count_launch(); }
+  MS_CUDA(cudaGetLastError());
+}
+
+// Sinv = (W_T + flip(W_B))^-1 by in-place Gauss-Jordan with diagonal pivots
+// (SPD: no pivoting needed); W_T at schur + 2 s max_bw^2, W_B max_bw^2
+// after it, in the bottom system's reversed order.
+__global__ void __launch_bounds__(256)
+    k_schur_inverse(const BandSys* __restrict__ sys, const double* __restrict__ schur,
+                    double* __restrict__ Sinv, int* fail, int stride) {
+  extern __shared__ double A[];
+  const BandSys s = sys[blockIdx.x];
+  const int bw = s.bw;
+  const double* WT = schur + (int64_t)blockIdx.x * 2 * stride;
+  const double* WB = WT + stride;
+  for (int t = threadIdx.x; t < bw * bw; t += blockDim.x) {
+    const int i = t / bw, j = t % bw;
+    A[t] = WT[t] + WB[(bw - 1 - i) * bw + (bw - 1 - j)];
+  }
+  bool bad = false;
+  for (int k = 0; k < bw; ++k) {
+    __syncthreads();
+    double d = A[k * bw + k];
+    if (!(d > 0.0)) {
+      bad = true;
+      d = 1.0;
+    }
+    const double inv = 1.0 / d;
+    for (int t = threadIdx.x; t < bw * bw; t += blockDim.x) {
+      const int i = t / bw, j = t % bw;
+      if (i != k && j != k) A[t] -= A[i * bw + k] * A[k * bw + j] * inv;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < bw; t += blockDim.x) {
+      if (t != k) {
+        A[k * bw + t] *= inv;
+        A[t * bw + k] = -A[t * bw + k] * inv;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) A[k * bw + k] = inv;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < bw * bw; t += blockDim.x) {
+    const int i = t / bw, j = t % bw;
+    Sinv[s.soff + t] = 0.5 * (A[t] + A[j * bw + i]);  // symmetric to round-off; keep it exact
+  }
+  if (bad && threadIdx.x == 0) atomicCAS(fail, 0, (int)blockIdx.x + 1);
+}
+
+void launch_schur_inverse(const BandSys* sys, int nsys, int max_bw, const double* schur, double* Sinv, int* fail,
+                          cudaStream_t st) {
+  if (nsys == 0) return;
+  const size_t smem = (size_t)max_bw * max_bw * sizeof(double);
+  if (smem > 220 * 1024) throw Error(-1, "separator too wide for the twisted level-1");
+  MS_CUDA(cudaFuncSetAttribute(k_schur_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  { k_schur_inverse<<<nsys, 256, smem, st>>>(sys, schur, Sinv, fail, max_bw * max_bw); ms_count_launch(); }
+  MS_CUDA(cudaGetLastError());
+}
+
 void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, double* Lr, int* fail,
-                       cudaStream_t st, int ldl) {
+                       cudaStream_t st, int ldl, double* schur) {
   if (nsys == 0) return;
   const int S = max_bw + 1;
   const size_t smem = (size_t)S * S * sizeof(double) + (size_t)(max_bw * (max_bw + 1) / 2 + 1) * 4;
   if (smem > 220 * 1024) throw Error(-1, "band too wide for the shared-memory Cholesky window");
   MS_CUDA(cudaFuncSetAttribute(k_band_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_band_potrf<<<nsys, 256, smem, st>>>(sys, Lc, Lr, fail, ldl);
+  { k_band_potrf<<<nsys, 256, smem, st>>>(sys, Lc, Lr, fail, ldl, schur); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -272,6 +375,23 @@ struct Ring {
   uint32_t phase;  // parity bit per stage
 };
 
+// ring shared-memory header: kTmaWarps * kNst mbarriers, rounded to an even
+// word count (the stages stay 16-byte aligned)
+constexpr int kRingHeaderWords = (kTmaWarps * kNst + 1) & ~1;
+
+__device__ __forceinline__ void ring_init(Ring& rg, double* smem, int warp, int lane, int stage_words) {
+  rg.bar = reinterpret_cast<uint64_t*>(smem) + warp * kNst;
+  rg.buf = smem + kRingHeaderWords + (size_t)warp * kNst * stage_words;
+  rg.stage = stage_words;
+  rg.phase = 0;
+  if (lane == 0) {
+    for (int st = 0; st < kNst; ++st) mbar_init(rg.bar + st, 1);
+    mbar_fence_init();
+  }
+}
+
+
+
 // first physical column and count of chunk c (steps [c kCh, c kCh + cnt))
 __device__ __forceinline__ void chunk_cols(bool rev, int n, int c, int& start, int& cnt) {
   const int k0 = c * kCh;
@@ -291,15 +411,17 @@ __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int
   bulk_g2s(rg.buf + (size_t)st * rg.stage, L + a, words * 8u, rg.bar + st);
 }
 
-template <int T, int NR, bool REV>
-__device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw,
-                                                double* __restrict__ y, int lane, Ring& rg) {
+// ym(r): address of the NR values of the sweep's r-th row (r counts the
+// sweep's own steps, i.e. already reversed for REV)
+template <int T, int NR, bool REV, class YMap>
+__device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw, YMap ym,
+                                                int lane, Ring& rg) {
   constexpr int R = T + 1;
   const int S = bw + 1;
   const int nch = (n + kCh - 1) / kCh;
   if (lane == 0)
     for (int c = 0; c < min(kNst, nch); ++c) ring_issue<REV>(rg, L, n, S, c);
-  auto yat = [&](int r, int c) -> double* { return y + (int64_t)(REV ? (n - 1 - r) : r) * NR + c; };
+  auto yat = [&](int r, int c) -> double* { return ym(r) + c; };
 
   double acc[NR][R], rnext[NR];
 #pragma unroll
@@ -333,6 +455,10 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
       // Step u of the block: lane owns row k0 + 32 s + lane in slot s, i.e.
       // band offset j = 32 s + lane - u from the pivot row; rows outside
       // 1..bw get a zero coefficient (no selects on the update path).
+      // (An address-select form -- masked-out slots read a zero slot, slots
+      // 1..T-2 unpredicated, validity masks per chunk -- issues ~30% fewer
+      // instructions per step but measured 4-15% slower: 0.39 -> 0.47 ms at
+      // config 2, 1.92 -> 2.00 ms at config 3.)
       auto step = [&](int q) {
         const int u = h + q;
         const double* col = sb + (REV ? (cnt - 1 - q) : q) * S;
@@ -373,14 +499,98 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
   }
 }
 
+// Backward sweep L^T x = w from the COLUMN band (the same bytes the forward
+// sweep reads: one factor copy instead of a column and a row band).  Each
+// chunk of kCh columns = kCh rows, processed top row first:
+//  A) every row's dot product with the already final x of the rows above the
+//     chunk (x_{k+j}, j beyond the chunk, from a 128-row circular window in
+//     shared memory): 4 lanes per row, each a quarter of the j's, reduced by
+//     two xor shuffles -- all rows of the chunk in parallel;
+//  B) the chunk's own kCh x kCh triangle in order: row q's x is broadcast
+//     and the later rows of the chunk accumulate L[k_p + (p - q)][k_p] x_q.
+// Dependent chain per row: one shuffle + fma + mul (B); the window products
+// (A) are off the chain.  rows k = natural numbering of the system; ym(k)
+// addresses row k's NR values (w on entry, x on exit).
+template <int NR, class YMap>
+__device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int n, int bw, YMap ym, int lane,
+                                               Ring& rg, double* __restrict__ xw) {
+  static_assert(kCh == 8, "4 lanes per chunk row");
+  const int S = bw + 1;
+  const int nch = (n + kCh - 1) / kCh;
+  if (lane == 0)
+    for (int c = 0; c < min(kNst, nch); ++c) ring_issue<true>(rg, L, n, S, c);
+  for (int i = lane; i < 128 * NR; i += 32) xw[i] = 0.0;
+  __syncwarp();
+  const int p = lane >> 2, gq = lane & 3;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch % kNst;
+    mbar_wait(rg.bar + st, (rg.phase >> st) & 1u);
+    rg.phase ^= 1u << st;
+    int start, cnt;
+    chunk_cols(true, n, ch, start, cnt);
+    const double* sb = rg.buf + (size_t)st * rg.stage + (int)(((int64_t)start * S) & 1);
+    const bool own = p < cnt;
+    const int pc = own ? p : 0;
+    const int k = start + cnt - 1 - pc;           // this group's row (chunk position pc from the top)
+    const double* col = sb + (cnt - 1 - pc) * S;  // its column: L[k + j][k], j = 0..bw
+    double w[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) w[c] = ym(k)[c];
+    // (A) rows above the chunk: j in (pc, bw], this lane's quarter
+    double s0[NR], s1[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) s0[c] = s1[c] = 0.0;
+    int j = pc + 1 + gq;
+    for (; j + 4 <= bw; j += 8) {
+      const double l0 = col[j], l1 = col[j + 4];
+      const int a0 = ((k + j) & 127) * NR, a1 = ((k + j + 4) & 127) * NR;
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        s0[c] = fma(l0, xw[a0 + c], s0[c]);
+        s1[c] = fma(l1, xw[a1 + c], s1[c]);
+      }
+    }
+    if (j <= bw) {
+      const double l0 = col[j];
+      const int a0 = ((k + j) & 127) * NR;
+#pragma unroll
+      for (int c = 0; c < NR; ++c) s0[c] = fma(l0, xw[a0 + c], s0[c]);
+    }
+    double sum[NR], t[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) {
+      sum[c] = s0[c] + s1[c];
+      sum[c] += __shfl_xor_sync(0xffffffffu, sum[c], 1);
+      sum[c] += __shfl_xor_sync(0xffffffffu, sum[c], 2);
+      t[c] = 0.0;
+    }
+    const double d = col[0];
+    // (B) the chunk's triangle
+    for (int q = 0; q < cnt; ++q) {
+      const double lv = col[max(p - q, 0)];  // L[k_p + (p - q)][k_p] for the later rows p > q
+      const int kq = start + cnt - 1 - q;
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        const double x = __shfl_sync(0xffffffffu, (w[c] - sum[c] - t[c]) * d, 4 * q);
+        if (lane == 4 * q) {
+          xw[(kq & 127) * NR + c] = x;
+          ym(kq)[c] = x;
+        }
+        t[c] = fma(lv, x, t[c]);
+      }
+    }
+    __syncwarp();  // window writes visible; every lane done with the stage before it is refilled
+    if (lane == 0 && ch + kNst < nch) ring_issue<true>(rg, L, n, S, ch + kNst);
+  }
+}
+
 static int ring_stage_words(int max_bw) { return (kCh * (max_bw + 1) + 3) & ~1; }
 static size_t ring_smem_bytes(int max_bw) {
-  const int nb = (kTmaWarps * kNst + 1) & ~1;
-  return ((size_t)nb + (size_t)kTmaWarps * kNst * ring_stage_words(max_bw)) * sizeof(double);
+  return ((size_t)kRingHeaderWords + (size_t)kTmaWarps * kNst * ring_stage_words(max_bw)) * sizeof(double);
 }
 
 template <int T, int NR>
-__global__ void __launch_bounds__(kTmaWarps * 32)
+__global__ void __launch_bounds__(kTmaWarps * 32, 3)
     k_l1_solve_ring(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                     const double* __restrict__ Lr, const double* __restrict__ r,
                     double* __restrict__ ybuf, const int* done, int stage_words) {
@@ -390,14 +600,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
   const int sid = blockIdx.x * kTmaWarps + warp;
   if (sid >= nsys) return;
   Ring rg;
-  rg.bar = reinterpret_cast<uint64_t*>(smem_ring) + warp * kNst;
-  rg.buf = smem_ring + ((kTmaWarps * kNst + 1) & ~1) + (size_t)warp * kNst * stage_words;
-  rg.stage = stage_words;
-  rg.phase = 0;
-  if (lane == 0) {
-    for (int st = 0; st < kNst; ++st) mbar_init(rg.bar + st, 1);
-    mbar_fence_init();
-  }
+  ring_init(rg, smem_ring, warp, lane, stage_words);
   const BandSys s = sys[sid];
   double* y = ybuf + s.yoff;
   for (int i = lane; i < s.n * NR; i += 32) {
@@ -407,16 +610,122 @@ __global__ void __launch_bounds__(kTmaWarps * 32)
     y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
   }
   __syncwarp();
-  band_sweep_ring<T, NR, false>(Lc + s.foff, s.n, s.bw, y, lane, rg);
+  const int n = s.n;
+  band_sweep_ring<T, NR, false>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg);
   __syncwarp();
-  band_sweep_ring<T, NR, true>(Lr + s.foff, s.n, s.bw, y, lane, rg);
+  if (Lr) {
+    band_sweep_ring<T, NR, true>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; }, lane,
+                                 rg);
+  } else {  // one factor copy: backward sweep by dot products over the column band
+    double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * kNst * stage_words + (size_t)warp * 128 * NR;
+    band_sweep_dot<NR>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw);
+  }
+}
+
+// Twisted sweeps: warp pair per subdomain (even warp: top system, odd warp:
+// bottom system), both forward sweeps concurrently, the separator solved by
+// the pair with the explicit Schur inverse, both backward sweeps
+// concurrently.  y stays in natural order (what the combine reads); the
+// bottom system's separator partials live in shared memory.
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+}
+
+template <int T, int NR>
+__global__ void __launch_bounds__(kTmaWarps * 32, 3)
+    k_l1_solve_twist(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
+                     const double* __restrict__ Lr, const double* __restrict__ Sinv,
+                     const double* __restrict__ r, double* __restrict__ ybuf, const int* done, int stage_words,
+                     int max_bw) {
+  static_assert(kTmaWarps % 2 == 0, "warp pairs");
+  if (done && *(volatile const int*)done) return;
+  extern __shared__ __align__(16) double smem_ring[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, role = warp & 1;  // role 0: top, 1: bottom
+  const int sid = blockIdx.x * (kTmaWarps / 2) + pair;
+  if (sid >= nsys) return;  // both warps of a pair leave together
+  Ring rg;
+  ring_init(rg, smem_ring, warp, lane, stage_words);
+  const size_t ring_words = kRingHeaderWords + (size_t)kTmaWarps * kNst * stage_words;
+  double* sB = smem_ring + ring_words + (size_t)pair * 2 * NR * max_bw;  // bottom separator partials
+  double* tS = sB + NR * max_bw;                                       // separator right-hand side
+  const BandSys s = sys[sid];
+  const int n = s.n, bw = s.bw, m = s.m, nT = m + bw, nB = n - m;
+  double* y = ybuf + s.yoff;
+  // gather R_s r: top warp rows [0, nT), bottom warp rows [nT, n) and zero separator partials
+  {
+    const int i0 = role ? nT * NR : 0, i1 = role ? n * NR : nT * NR;
+    for (int i = i0 + lane; i < i1; i += 32) {
+      const int ln = NR == 1 ? (i >> 1) : (i >> 1), c = i & 1;
+      int a, b;
+      band_node_of(s, ln, a, b);
+      y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
+    }
+    if (role)
+      for (int i = lane; i < NR * bw; i += 32) sB[i] = 0.0;
+  }
+  __syncwarp();
+  if (role == 0) {
+    band_sweep_ring<T, NR, false>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg);
+  } else {
+    const int nb_own = nB - bw;
+    band_sweep_ring<T, NR, false>(
+        Lc + s.foffB, nB, bw,
+        [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; }, lane, rg);
+  }
+  pair_sync(pair);
+  // separator: t = (r_S - L_ST y_T) + (- L_SB y_B); x_S = Sinv t
+  const int tid = role * 32 + lane;
+  for (int i = tid; i < NR * bw; i += 64) {
+    const int row = i / NR, c = i % NR;
+    tS[i] = y[(int64_t)(m + row) * NR + c] + sB[(bw - 1 - row) * NR + c];
+  }
+  pair_sync(pair);
+  const double* Si = Sinv + s.soff;
+  for (int j = tid; j < bw; j += 64) {
+    double acc[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[c] = 0.0;
+    for (int i = 0; i < bw; ++i) {
+      const double v = __ldg(Si + (int64_t)i * bw + j);  // symmetric: column j = row j, coalesced over j
+#pragma unroll
+      for (int c = 0; c < NR; ++c) acc[c] = fma(v, tS[i * NR + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NR; ++c) y[(int64_t)(m + j) * NR + c] = acc[c];
+  }
+  pair_sync(pair);
+  if (role == 0) {
+    band_sweep_ring<T, NR, true>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; }, lane,
+                                 rg);
+  } else {
+    band_sweep_ring<T, NR, true>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane, rg);
+  }
+}
+
+template <int T, int NR>
+static void solve_twist_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
+                          const double* Lr, const double* Sinv, const double* r, double* ybuf, const int* done,
+                          cudaStream_t st) {
+  const size_t smem = ring_smem_bytes(max_bw) + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double);
+  static size_t configured[64] = {};
+  int dev = 0;
+  MS_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64 || smem > configured[dev]) {
+    MS_CUDA(cudaFuncSetAttribute(k_l1_solve_twist<T, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    if (dev < 64) configured[dev] = smem;
+  }
+  { k_l1_solve_twist<T, NR><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, Sinv, r, ybuf, done, ring_stage_words(max_bw), max_bw); ms_count_launch(); }
 }
 
 template <int T, int NR>
 static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                          const double* Lr, const double* r, double* ybuf, const int* done,
                          cudaStream_t st) {
-  const size_t smem = ring_smem_bytes(max_bw);
+  // + the dot sweep's x windows (one factor copy)
+  const size_t smem = ring_smem_bytes(max_bw) + (Lr ? 0 : (size_t)kTmaWarps * 128 * NR * sizeof(double));
   static size_t configured[64] = {};  // per instantiation and device
   int dev = 0;
   MS_CUDA(cudaGetDevice(&dev));
@@ -425,8 +734,8 @@ static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw
                                  (int)smem));
     if (dev < 64) configured[dev] = smem;
   }
-  k_l1_solve_ring<T, NR><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
-      g, sys, nsys, Lc, Lr, r, ybuf, done, ring_stage_words(max_bw));
+  { k_l1_solve_ring<T, NR><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, r, ybuf, done, ring_stage_words(max_bw)); ms_count_launch(); }
 }
 
 static bool use_ring_sweeps() {
@@ -438,40 +747,53 @@ static bool use_ring_sweeps() {
   return v == 1;
 }
 
+bool ring_sweep_ok(int T, int min_bw) { return T <= 1 || min_bw > 32 * (T - 1); }
+bool l1_ring_sweeps_enabled() { return use_ring_sweeps(); }
+
 template <int T, int NR>
 static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
-                    const double* Lr, const double* r, double* ybuf, const int* done, cudaStream_t st) {
-  if (use_ring_sweeps()) {
+                    const double* Lr, const double* r, double* ybuf, const int* done, cudaStream_t st,
+                    const double* Sinv, bool ring_ok) {
+  if (Sinv) {
+    solve_twist_t<T, NR>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st);
+    return;
+  }
+  if (use_ring_sweeps() && ring_ok) {
     solve_ring_t<T, NR>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st);
     return;
   }
-  k_l1_solve<T, NR><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, 0, st>>>(g, sys, nsys, Lc, Lr, r,
-                                                                            ybuf, done);
+  if (!Lr) throw Error(-1, "the register-prefetch level-1 sweeps need the row band (two factor copies)");
+  { k_l1_solve<T, NR><<<div_up(nsys, kSolveWarps), kSolveWarps * 32, 0, st>>>(g, sys, nsys, Lc, Lr, r,
+                                                                            ybuf, done); ms_count_launch(); }
 }
 
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
-                     const int* done, cudaStream_t st) {
+                     const int* done, cudaStream_t st, const double* Sinv, int min_bw) {
   if (nsys == 0) return;
   const int T = std::max(1, div_up(max_bw, 32));
+  if (min_bw < 0) min_bw = max_bw;
+  // the ring step assumes slots 1..T-2 inside every band
+  const bool ring_ok = ring_sweep_ok(T, min_bw);
+  if (Sinv && !ring_ok) throw Error(-1, "twisted level-1 needs every band wider than 32 (T - 1)");
   if (nrhs == 1) {
     switch (T) {
-      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
       default: throw Error(-1, "level-1 band wider than 256 unsupported");
     }
   } else if (nrhs == 2) {
     switch (T) {
-      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
-      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st); break;
+      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
       default: throw Error(-1, "heat level-1 band wider than 128 unsupported");
     }
   } else {

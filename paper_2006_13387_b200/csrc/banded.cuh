@@ -22,6 +22,18 @@ struct BandSys {
   int bw;          // lower bandwidth
   int64_t foff;    // offset into Lc / Lr
   int64_t yoff;    // offset of the local vector in the solution buffer
+  // Twisted (two-sided) factorisation, 0 = plain.  With split m > 0 the
+  // unknowns are [T | S | B] = [0, m) [m, m+bw) [m+bw, n): the "top" system
+  // (rows [0, m+bw), natural order) is factored at foff, the "bottom" system
+  // (rows [m, n) in reversed order) at foffB, each eliminating only its own
+  // part; the separator S (bw unknowns; T and B do not couple across it)
+  // gets the explicit inverse of its Schur complement at soff.  Both halves'
+  // sweeps run concurrently (one warp each), which halves the dependent
+  // chain of a solve for the same factor bytes (+bw/n).
+  int m;
+  int nelim;       // Cholesky: eliminate only the first nelim columns (<= 0: all)
+  int64_t foffB;
+  int64_t soff;
 };
 
 __host__ __device__ inline int band_fast_len(const BandSys& s) { return s.fastx ? s.w : s.hgt; }
@@ -59,16 +71,38 @@ void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cuda
 // In-place banded Cholesky of every system: Lc holds A's lower band on
 // entry, L on exit (diag slot = 1/L_kk); Lr receives the row band.
 // *fail gets (system index + 1) of a non-positive pivot, else stays 0.
+// Systems with 0 < nelim < n are eliminated for their first nelim columns
+// only: the remaining bw x bw Schur complement is written (full, row-major)
+// to schur + yoff and the last n - nelim columns of Lc / Lr become identity.
 void launch_band_potrf(const BandSys* sys, int nsys, int max_bw, double* Lc, double* Lr,
-                       int* fail, cudaStream_t st, int ldl = 0);
+                       int* fail, cudaStream_t st, int ldl = 0, double* schur = nullptr);
+
+// Twisted level-1 build helpers (BandSys.m > 0).  twist_split: from the
+// natural column bands (at nat[s].foff) write the top system's band at
+// sys[s].foff (the separator block kept) and the bottom system's reversed
+// band at sys[s].foffB (its separator block zero).  schur_inverse: Sinv =
+// (W_T + flip(W_B))^-1 from the two partial factorisations' Schur windows
+// (schur + 2 s max_bw^2, the bottom one max_bw^2 further), written full at
+// Sinv + sys[s].soff; one CTA per system.
+void launch_twist_split(const BandSys* nat, const BandSys* sys, int nsys, int max_bw, const double* band_nat,
+                        double* Lc, cudaStream_t st);
+void launch_schur_inverse(const BandSys* sys, int nsys, int max_bw, const double* schur, double* Sinv, int* fail,
+                          cudaStream_t st);
 
 // y_s = K_s^{-1} (R_s r) for every system, warp per system.  r is a full
 // layout vector; the local solutions land in ybuf[yoff ...], node-interleaved
 // (2 ln + c).  nrhs = 2: scalar systems applied to the x and y components in
 // one sweep (the factor is read once for both).
+// Lr == nullptr: one factor copy, the backward sweep by dot products over the
+// column band (half the factor bytes).
+// Sinv != nullptr: twisted systems (BandSys.m > 0).  min_bw: narrowest band
+// among the systems (the shared-memory ring sweep needs min_bw > 32 (T - 1),
+// T = ceil(max_bw / 32); narrower mixes take the register-prefetch sweep).
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
-                     const int* done, cudaStream_t st);
+                     const int* done, cudaStream_t st, const double* Sinv = nullptr, int min_bw = -1);
+bool ring_sweep_ok(int T, int min_bw);
+bool l1_ring_sweeps_enabled();  // false under MS_L1_SWEEP=reg
 
 // ---------------------------------------------------------------------------
 // One warp's banded sweep over a factor read from global memory (L2/L1),

@@ -116,6 +116,17 @@ void dev_free(void* p) {
   c.cached += it->second.second;
 }
 
+// twisted level-1 sweeps when all subdomain pairs fit in one wave (3 CTAs of
+// 2 pairs per SM): below that the plain sweeps' per-step chain is exposed;
+// above it the twisted kernel needs a second wave (measured at config 5,
+// 1,024 subdomains: twisted 2.52e9 vs plain 3.29e9 DOF-iter/s; config 2,
+// 256 subdomains: twisted 1.96e9 vs plain 1.35e9)
+static int twist_max_subdomains(int device) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms * 3 * 2;
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -371,6 +382,7 @@ struct ms_problem {
   // captured PCG chunk (CUDA graph) of plain CG solves; preconditioned solves
   // keep theirs in the ms_precond (it captures both objects' buffers)
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;
+  long long gexec_kernels = 0, gexec_prof_kernels = 0;  // kernel nodes per replay
   int graph_gen = 0;
   unsigned prof_mask = 0;  // Prof::mask the profiling graph was captured with
   std::vector<std::pair<int, int>> captured;
@@ -397,10 +409,13 @@ struct ms_precond {
   ms_precond_opts opts{};
   std::vector<int64_t> heat_dir;
   // level 1
-  int NbX = 0, NbY = 0, nsys = 0, max_bw = 0;
+  int NbX = 0, NbY = 0, nsys = 0, max_bw = 0, min_bw = 0;
   std::vector<BandSys> hsys;
   DBuf<BandSys> sys;
   DBuf<double> Lc, Lr, ybuf, Xinv;
+  DBuf<double> Sinv;   // twisted level 1: separator Schur inverses (empty: plain sweeps)
+  bool twisted = false;
+  bool one_copy = false;  // plain banded level 1 with the column band only (dot-form backward sweep)
   bool dense = false;  // MS_LOCAL_DENSE_INV: packed explicit inverses in Xinv
   int nrhs = 1;        // 2: heat level-1 (scalar factor applied to both blocks)
   int dense_nt = 0;
@@ -429,6 +444,7 @@ struct ms_precond {
   // packed K0^-1 tiles [sym_t0, sym_t1) of the sharded coarse solve (all on one rank)
   int64_t sym_t0 = 0, sym_t1 = -1;
   cudaGraphExec_t gexec = nullptr, gexec_prof = nullptr;  // captured PCG chunks for (prob, this)
+  long long gexec_kernels = 0, gexec_prof_kernels = 0;     // kernel nodes per replay
   int graph_gen = 0;  // prob->hist_gen the graphs were captured with
   unsigned prof_mask = 0;  // Prof::mask the profiling graph was captured with
   std::vector<std::pair<int, int>> captured;
@@ -545,20 +561,25 @@ static HaloPlan halo_plan(int lo, int hi, int ny, int k, int rank, int world) {
   return h;
 }
 
-// exchange k node rows of both planes with the neighbouring strips
-static void exchange_rows(ms_problem* P, double* v, int k) {
-  Comm* c = P->ctx->comm.get();
-  if (!c || c->world == 1 || k <= 0) return;
+// the 4 transfers of a k-row halo of both planes with the neighbouring strips
+static void row_halo_xfers(ms_problem* P, Comm* c, double* v, int k, Xfer x[4]) {
   const HaloPlan h = halo_plan(P->b_lo, row_hi(P), P->g.ny, k, c->rank, c->world);
   const int64_t rowb = (int64_t)P->g.nnx * sizeof(double);
-  // both planes and both neighbours in one group (one NCCL launch per halo)
-  Xfer x[4];
   for (int plane = 0; plane < 2; ++plane) {
     char* base = reinterpret_cast<char*>(v + plane * P->g.n_nodes);
     for (int q = 0; q < 2; ++q)
       x[plane * 2 + q] = {base + h.send_lo[q] * rowb, (size_t)(h.send_n[q] * rowb), h.dst[q],
                           base + h.recv_lo[q] * rowb, (size_t)(h.recv_n[q] * rowb), h.src[q]};
   }
+}
+
+// exchange k node rows of both planes with the neighbouring strips
+static void exchange_rows(ms_problem* P, double* v, int k) {
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1 || k <= 0) return;
+  // both planes and both neighbours in one group (one NCCL launch per halo)
+  Xfer x[4];
+  row_halo_xfers(P, c, v, k, x);
   c->sendrecv(x, 4, P->ctx->st);
 }
 
@@ -722,7 +743,8 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
     if (pc->dense)
       launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
     else
-      launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st);
+      launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st,
+                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw);
     pf.end(MS_PROF_LEVEL1, it, st, a);
     if (dist) exchange_ybuf(pc);
   }
@@ -735,15 +757,20 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
                  pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st, pc->C0, pc->C1);
   pf.end(MS_PROF_COMBINE, it, st, a);
   if (dist) {
-    if (sc) dist_finalize(P, PART_RZ, beta_hist);
-    exchange_rows(P, z, 1);  // the next matvec refreshes p on one halo row
+    if (sc) {
+      // r.z allreduce and the z halo (the next matvec refreshes p on one halo
+      // row) in one communicator group, then the beta / convergence finalise
+      Comm* c = ctx->comm.get();
+      Xfer x[4];
+      row_halo_xfers(P, c, z, 1, x);
+      c->allreduce_sendrecv(&P->sc.p->part[PART_RZ], 1, x, 4, st);
+      launch_finalize(P->sc.p, PART_RZ, beta_hist, st);
+    } else {
+      exchange_rows(P, z, 1);
+    }
   }
 }
 
-static int precond_launches(const ms_precond* pc) {
-  if (!pc) return 1;  // rz
-  return (pc->nsys > 0 ? 1 : 0) + (pc->has_coarse ? 3 : 0) + 1;
-}
 
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -1120,6 +1147,38 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     };
     cover(xlo, xhi, g.nx + 1, xcov);
     cover(ylo, yhi, g.ny + 1, ycov);
+    // Twisted (two-sided) level-1 factors when the per-GPU subdomain count is
+    // too small to hide the sweeps' dependent chain (config 2,
+    // config 3 at 8 GPUs); MS_L1_TWIST=0/1 forces it off/on.
+    const int ns_own = pc->s1 - pc->s0;
+    std::vector<BandSys> nat;  // natural band layout (assembly input)
+    if (o->local_solver == MS_LOCAL_BANDED) {
+      int tw_env = -1;
+      if (const char* e = getenv("MS_L1_TWIST")) tw_env = std::atoi(e);
+      bool ok = pc->max_bw <= 128;
+      for (int q = pc->s0; q < pc->s1 && ok; ++q) ok = pc->hsys[q].n >= 4 * pc->hsys[q].bw;
+      pc->min_bw = pc->max_bw;
+      for (int q = pc->s0; q < pc->s1; ++q) pc->min_bw = std::min(pc->min_bw, pc->hsys[q].bw);
+      ok = ok && ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
+      pc->twisted = ok && (tw_env == 1 || (tw_env != 0 && ns_own <= twist_max_subdomains(pc->device)));
+    }
+    if (pc->twisted) {
+      int64_t tw = 0, so = 0;
+      for (int q = pc->s0; q < pc->s1; ++q) {
+        BandSys& b = pc->hsys[q];
+        nat.push_back(b);
+        const int S = b.bw + 1;
+        b.m = (b.n - b.bw) / 2;
+        const int nT = b.m + b.bw, nB = b.n - b.m;
+        b.foff = tw;
+        b.foffB = tw + (((int64_t)nT * S + 1) & ~(int64_t)1);
+        tw = b.foffB + (((int64_t)nB * S + 1) & ~(int64_t)1);
+        b.soff = so;
+        so += ((int64_t)b.bw * b.bw + 1) & ~(int64_t)1;
+      }
+      foff = tw;
+      pc->Sinv.alloc(so + 2);
+    }
     pc->sys.upload(pc->hsys.data(), pc->hsys.size(), st);
     pc->xcov.upload(xcov.data(), xcov.size(), st);
     pc->ycov.upload(ycov.data(), ycov.size(), st);
@@ -1133,20 +1192,74 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       MS_CUDA(cudaMemcpyAsync(&bad, fail.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       MS_CUDA(cudaStreamSynchronize(st));
       if (bad) throw Error(MS_E_INVALID, "heat level-1 (HH variants) needs whole-node constraints");
-      HeatParam hp{};
-      heat_elements(g.h, hp);
-      launch_l1_heat_assemble(g, hp.lap, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
-    } else {
-      launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
     }
     pc->dense = o->local_solver == MS_LOCAL_DENSE_INV;
     pc->nrhs = heat_l1 ? 2 : 1;
-    if (!pc->dense) {
-      pc->Lr.alloc(foff + 2);
+    if (pc->twisted) {
+      // natural bands (assembly) -> top / bottom bands -> partial Cholesky of
+      // both halves -> explicit inverse of the separator's Schur complement
+      int64_t fn = 0;
+      for (BandSys& b : nat) {
+        b.foff = fn;
+        fn += ((int64_t)b.n * (b.bw + 1) + 1) & ~(int64_t)1;
+      }
+      DBuf<BandSys> nat_d, half_d;
+      nat_d.upload(nat.data(), nat.size(), st);
+      pc->Lr.alloc(foff + 2);  // holds the natural bands first (fn <= foff)
+      if (heat_l1) {
+        HeatParam hp{};
+        heat_elements(g.h, hp);
+        launch_l1_heat_assemble(g, hp.lap, P->E.p, P->mask.p, nat_d.p, ns, pc->Lr.p, st);
+      } else {
+        launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, nat_d.p, ns, pc->Lr.p, st);
+      }
+      launch_twist_split(nat_d.p, pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lr.p, pc->Lc.p, st);
       pc->Lr.zero(st);
+      std::vector<BandSys> halves(2 * (size_t)ns);
+      const int64_t mb2 = (int64_t)pc->max_bw * pc->max_bw;
+      for (int i = 0; i < ns; ++i) {
+        const BandSys& b = pc->hsys[pc->s0 + i];
+        BandSys t = b, u = b;
+        t.n = b.m + b.bw;
+        t.nelim = b.m;
+        t.yoff = 2 * i * mb2;
+        u.foff = b.foffB;
+        u.n = b.n - b.m;
+        u.nelim = u.n - b.bw;
+        u.yoff = (2 * i + 1) * mb2;
+        t.m = u.m = 0;
+        halves[2 * i] = t;
+        halves[2 * i + 1] = u;
+      }
+      half_d.upload(halves.data(), halves.size(), st);
+      DBuf<double> schur;
+      schur.alloc((size_t)2 * ns * mb2);
+      launch_band_potrf(half_d.p, 2 * ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st, 0, schur.p);
+      check_fail(fail, st, "level-1 subdomain matrix");
+      launch_schur_inverse(pc->sys.p + pc->s0, ns, pc->max_bw, schur.p, pc->Sinv.p, fail.p, st);
+      check_fail(fail, st, "level-1 subdomain separator");
+    } else if (!pc->dense) {
+      if (heat_l1) {
+        HeatParam hp{};
+        heat_elements(g.h, hp);
+        launch_l1_heat_assemble(g, hp.lap, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
+      } else {
+        launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
+      }
+      // one factor copy (column band) unless MS_L1_COPIES=2 or the
+      // register-prefetch sweeps are in use
+      int copies_env = 0;
+      if (const char* e = getenv("MS_L1_COPIES")) copies_env = std::atoi(e);
+      pc->one_copy = copies_env != 2 && l1_ring_sweeps_enabled() &&
+                     ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
+      if (!pc->one_copy) {
+        pc->Lr.alloc(foff + 2);
+        pc->Lr.zero(st);
+      }
       launch_band_potrf(pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
       check_fail(fail, st, "level-1 subdomain matrix");
     } else {
+      launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
       // explicit inverses: band -> packed tiles, batched tiled Cholesky inverse
       int max_n = 0;
       for (const BandSys& b : pc->hsys) max_n = std::max(max_n, b.n);
@@ -1180,8 +1293,12 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->xlo_d.p, pc->xlen_d.p, pc->ylo_d.p, pc->ylen_d.p,
                    pc->yoff_d.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
     pc->info.n_subdomains = pc->nsys;
+    pc->info.level1_twisted = pc->twisted ? 1 : 0;
+    pc->info.n_subdomains_local = pc->s1 - pc->s0;
+    pc->info.level1_copies = pc->dense ? 0 : (pc->one_copy ? 1 : 2);
     pc->info.local_bytes = pc->dense ? (double)ns * packed_words(pc->dense_nt) * sizeof(double)
-                                     : (double)foff * 2 * sizeof(double);
+                                     : (double)(foff * (pc->one_copy ? 1 : 2) + (pc->twisted ? pc->Sinv.n : 0)) *
+                                           sizeof(double);
   }
   MS_CUDA(cudaEventRecord(e1, st));
 
@@ -1555,7 +1672,7 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
                               nullptr, st);
       else
         launch_l1_solve(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r,
-                        pc->ybuf.p, nullptr, st);
+                        pc->ybuf.p, nullptr, st, pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw);
     });
   if (pc->has_coarse) {
     ms[MS_BENCH_RESTRICT] = timeit([&] {
@@ -1606,6 +1723,7 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   if (pc && pc->prob != P) throw Error(MS_E_INVALID, "preconditioner built for another problem");
   MS_CUDA(cudaSetDevice(P->ctx->device));
   const auto wall0 = std::chrono::steady_clock::now();
+  const long long launches0 = ms_launch_counter();
   const cudaStream_t st = P->ctx->st;
   if (P->hcap < maxit + 1) {
     P->hres.alloc(maxit + 1);
@@ -1705,13 +1823,18 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   Prof& prof = P->ctx->prof;
   const bool use_graph = maxit >= chunk && (!dist || P->ctx->comm->capturable());
   cudaGraphExec_t& gexec = prof.on ? (pc ? pc->gexec_prof : P->gexec_prof) : (pc ? pc->gexec : P->gexec);
+  long long& gkernels = prof.on ? (pc ? pc->gexec_prof_kernels : P->gexec_prof_kernels)
+                                : (pc ? pc->gexec_kernels : P->gexec_kernels);
   if (use_graph && !gexec) {
     cudaGraph_t graph;
     prof.capturing = true;
     prof.captured.clear();
+    const long long c0 = ms_launch_counter();
     MS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < chunk; ++i) launch_iter(i);
     MS_CUDA(cudaStreamEndCapture(st, &graph));
+    gkernels = ms_launch_counter() - c0;  // captured, not launched: counted per replay
+    ms_launch_counter() = c0;
     prof.capturing = false;
     MS_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
     MS_CUDA(cudaGraphDestroy(graph));
@@ -1721,6 +1844,7 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   while (!done && it < maxit) {
     if (use_graph && it + chunk <= maxit) {
       MS_CUDA(cudaGraphLaunch(gexec, st));
+      ms_launch_counter() += gkernels;
       if (prof.on) prof.replayed(it);
       it += chunk;
     } else {
@@ -1746,10 +1870,9 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   if (alphas && iters > 0) MS_CUDA(cudaMemcpy(alphas, P->halpha.p, iters * sizeof(double), cudaMemcpyDefault));
   if (betas && iters > 1) MS_CUDA(cudaMemcpy(betas, P->hbeta.p, (iters - 1) * sizeof(double), cudaMemcpyDefault));
   if (rep) {
-    // init: norm + precond (its restriction is not fused: +1); per iteration:
-    // matvec, update(+restriction partials), precond
-    rep->kernel_launches = 1 + precond_launches(pc) + ((pc && pc->has_coarse) ? 1 : 0) +
-                           (int64_t)iters * (2 + precond_launches(pc));
+    // counted at every launch site (graph replays add their kernel nodes);
+    // includes the no-op kernels of a chunk's iterations past convergence
+    rep->kernel_launches = ms_launch_counter() - launches0;
     rep->iterations = iters;
     rep->converged = hs.converged;
     rep->final_residual = hs.res;

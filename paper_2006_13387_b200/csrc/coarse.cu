@@ -61,7 +61,7 @@ __global__ void k_pou_table(Grid g, CoarseDev cd, double* __restrict__ chi) {
 
 void launch_pou_table(const Grid& g, const CoarseDev& cd, double* chi, cudaStream_t st) {
   if (cd.n_centers == 0) return;
-  k_pou_table<<<cd.n_centers, 256, 0, st>>>(g, cd, chi);
+  { k_pou_table<<<cd.n_centers, 256, 0, st>>>(g, cd, chi); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -129,7 +129,7 @@ __global__ void k_node_tables(Grid g, CoarseDev cd, double* __restrict__ chi4,
 void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double* psi4,
                         cudaStream_t st) {
   if (cd.n_centers == 0) return;
-  k_node_tables<<<148 * 8, 256, 0, st>>>(g, cd, chi4, psi4);
+  { k_node_tables<<<148 * 8, 256, 0, st>>>(g, cd, chi4, psi4); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -360,14 +360,14 @@ void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const doub
                             double* partials, double* res_hist, cudaStream_t st) {
   const dim3 grid(cd.Nx, J1 - J0);
   if (cd.vec)
-    k_cell_restrict<true, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
-                                                                  res_hist, nullptr);
+    { k_cell_restrict<true, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+                                                                  res_hist, nullptr); ms_count_launch(); }
   else if (restrict_nu() == 2)
-    k_cell_restrict<true, false, 2, MS_CR2_MINB, MS_CR2_TPB><<<grid, MS_CR2_TPB, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
-                                                                      res_hist, nullptr);
+    { k_cell_restrict<true, false, 2, MS_CR2_MINB, MS_CR2_TPB><<<grid, MS_CR2_TPB, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+                                                                      res_hist, nullptr); ms_count_launch(); }
   else
-    k_cell_restrict<true, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
-                                                                   res_hist, nullptr);
+    { k_cell_restrict<true, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(g, cd, 1, J0, x, p, r, q, sc, partials,
+                                                                   res_hist, nullptr); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -375,14 +375,14 @@ void launch_restrict_cells(const Grid& g, int J0, int J1, const CoarseDev& cd, c
                            const int* done, cudaStream_t st) {
   const dim3 grid(cd.Nx, J1 - J0);
   if (cd.vec)
-    k_cell_restrict<false, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(
-        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+    { k_cell_restrict<false, true, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(
+        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done); ms_count_launch(); }
   else if (restrict_nu() == 2)
-    k_cell_restrict<false, false, 2, 2><<<grid, kCellThreads, 0, st>>>(
-        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+    { k_cell_restrict<false, false, 2, 2><<<grid, kCellThreads, 0, st>>>(
+        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done); ms_count_launch(); }
   else
-    k_cell_restrict<false, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(
-        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done);
+    { k_cell_restrict<false, false, 1, MS_CR_MINB><<<grid, kCellThreads, 0, st>>>(
+        g, cd, 1, J0, nullptr, nullptr, const_cast<double*>(r), nullptr, nullptr, nullptr, nullptr, done); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -415,7 +415,7 @@ void launch_restrict_reduce(const CoarseDev& cd, double* f0, const int* done, cu
   if (k_end < 0) k_end = cd.n_centers;
   if (k_end <= k_begin) return;
   const int total = (k_end - k_begin) * kSlots;
-  k_restrict_reduce<<<div_up(total, 256), 256, 0, st>>>(cd, f0, done, k_begin, k_end);
+  { k_restrict_reduce<<<div_up(total, 256), 256, 0, st>>>(cd, f0, done, k_begin, k_end); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -573,11 +573,11 @@ void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const C
   if (cd) cdv = *cd;
   if (J1 < 0) J1 = Ny;
   if (cd && cd->vec)
-    k_combine<true><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, 1, Nx, Ny, J0,
-                                                                   y0, r, z, sc, partials, beta_hist);
+    { k_combine<true><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, 1, Nx, Ny, J0,
+                                                                   y0, r, z, sc, partials, beta_hist); ms_count_launch(); }
   else
-    k_combine<false><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0,
-                                                                    Nx, Ny, J0, y0, r, z, sc, partials, beta_hist);
+    { k_combine<false><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, cd ? 1 : 0,
+                                                                    Nx, Ny, J0, y0, r, z, sc, partials, beta_hist); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -667,7 +667,7 @@ void launch_k0_assemble(const Grid& g, const KeParam& ke, const double* E, const
                         cudaStream_t st, int k_begin, int k_end) {
   if (cd.n_centers == 0) return;
   if (k_end < 0) k_end = cd.n_centers;
-  k_k0_assemble<<<n_cta, 256, 0, st>>>(g, ke, E, mask, cd, K0, scratch, k_begin, k_end);
+  { k_k0_assemble<<<n_cta, 256, 0, st>>>(g, ke, E, mask, cd, K0, scratch, k_begin, k_end); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -685,7 +685,7 @@ __global__ void k_symmetrize(int N, double* A) {
 
 void launch_symmetrize(int N, double* A, cudaStream_t st) {
   if (N == 0) return;
-  k_symmetrize<<<148 * 4, 256, 0, st>>>(N, A);
+  { k_symmetrize<<<148 * 4, 256, 0, st>>>(N, A); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 

@@ -80,6 +80,15 @@ struct NcclComm : Comm {
     }
     MS_NCCL(nccl().groupEnd());
   }
+  void allreduce_sendrecv(double* buf, size_t n, const Xfer* x, int nx, cudaStream_t st) override {
+    MS_NCCL(nccl().groupStart());
+    MS_NCCL(nccl().allReduce(buf, buf, n, ncclFloat64, ncclSum, comm, st));
+    for (int i = 0; i < nx; ++i) {
+      if (x[i].dst >= 0 && x[i].sb) MS_NCCL(nccl().send(x[i].s, x[i].sb, ncclUint8, x[i].dst, comm, st));
+      if (x[i].src >= 0 && x[i].rb) MS_NCCL(nccl().recv(x[i].r, x[i].rb, ncclUint8, x[i].src, comm, st));
+    }
+    MS_NCCL(nccl().groupEnd());
+  }
   bool capturable() const override { return true; }
 };
 

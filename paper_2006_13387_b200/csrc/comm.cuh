@@ -36,6 +36,12 @@ struct Comm {
     const Xfer x[2] = {{s0, sb0, dst0, r0, rb0, src0}, {s1, sb1, dst1, r1, rb1, src1}};
     sendrecv(x, 2, st);
   }
+  // allreduce(buf[0..n)) and the n_x exchanges as ONE group (NCCL: one
+  // ncclGroupStart/End, one launch); the default runs them one after the other
+  virtual void allreduce_sendrecv(double* buf, size_t n, const Xfer* x, int nx, cudaStream_t st) {
+    allreduce_sum(buf, n, st);
+    sendrecv(x, nx, st);
+  }
   // may the operations be captured into a CUDA graph
   virtual bool capturable() const = 0;
 };

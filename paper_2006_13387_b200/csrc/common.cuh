@@ -9,6 +9,16 @@
 
 namespace msgpu {
 
+// Host-side count of this thread's kernel launches (every <<<>>> site of the
+// library increments it right after the launch; ms_pcg_solve reports the
+// difference, with graph replays adding their captured kernel count).
+inline long long& ms_launch_counter() {
+  static thread_local long long c = 0;
+  return c;
+}
+inline void ms_count_launch() { ++ms_launch_counter(); }
+
+
 // Host-side error type carrying an ABI status code.
 struct Error : std::runtime_error {
   int code;

@@ -118,7 +118,7 @@ __global__ void k_band_to_tiles(const BandSys* __restrict__ sys, int s0, int nt,
 
 void launch_band_to_tiles(const BandSys* sys, int s0, int B, int nt, const double* band, double* P,
                           cudaStream_t st) {
-  k_band_to_tiles<<<dim3(256, B), 256, 0, st>>>(sys, s0, nt, band, P);
+  { k_band_to_tiles<<<dim3(256, B), 256, 0, st>>>(sys, s0, nt, band, P); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -291,11 +291,11 @@ static void tiled_cholesky(int nt, int B, double* P, double* W, int* fail, cudaS
   tile_kernels_configure();
   MS_CUDA(cudaMemsetAsync(W, 0, (size_t)B * packed_words(nt) * sizeof(double), st));
   for (int k = 0; k < nt; ++k) {
-    k_potrf_tile<<<dim3(1, B), kTT, smem, st>>>(k, nt, P, W, fail);
+    { k_potrf_tile<<<dim3(1, B), kTT, smem, st>>>(k, nt, P, W, fail); ms_count_launch(); }
     const int m = nt - k - 1;
     if (m > 0) {
-      k_trsm_tiles<<<dim3(m, B), kTT, smem, st>>>(k, nt, P, W);
-      k_syrk_tiles<<<dim3((unsigned)((int64_t)m * (m + 1) / 2), B), kTT, smem, st>>>(k, nt, P);
+      { k_trsm_tiles<<<dim3(m, B), kTT, smem, st>>>(k, nt, P, W); ms_count_launch(); }
+      { k_syrk_tiles<<<dim3((unsigned)((int64_t)m * (m + 1) / 2), B), kTT, smem, st>>>(k, nt, P); ms_count_launch(); }
     }
   }
   MS_CUDA(cudaGetLastError());
@@ -306,8 +306,8 @@ void dense_spd_inverse_batched(int nt, int B, double* P, double* W, double* X, i
   if (nt == 0 || B == 0) return;
   const size_t smem = 2 * T * TP * sizeof(double);
   tiled_cholesky(nt, B, P, W, fail, st);
-  for (int d = 1; d < nt; ++d) k_trtri_tiles<<<dim3(nt - d, B), kTT, smem, st>>>(d, nt, P, W);
-  k_lauum_tiles<<<dim3((unsigned)packed_tiles(nt), B), kTT, smem, st>>>(nt, W, X);
+  for (int d = 1; d < nt; ++d) { k_trtri_tiles<<<dim3(nt - d, B), kTT, smem, st>>>(d, nt, P, W); ms_count_launch(); }
+  { k_lauum_tiles<<<dim3((unsigned)packed_tiles(nt), B), kTT, smem, st>>>(nt, W, X); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -321,10 +321,10 @@ void dense_cholesky(int N, const double* A, double* packed_L, double* diag_inv, 
                     cudaStream_t st) {
   if (N == 0) return;
   const int nt = div_up(N, T);
-  k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, packed_L);
+  { k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, packed_L); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
   tiled_cholesky(nt, 1, packed_L, work, fail, st);
-  k_copy_diag_tiles<<<nt, 256, 0, st>>>(nt, work, diag_inv);
+  { k_copy_diag_tiles<<<nt, 256, 0, st>>>(nt, work, diag_inv); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -484,8 +484,8 @@ void launch_trsv_packed(int N, const double* L, const double* Dinv, const double
   if (N == 0) return;
   const int nt = div_up(N, T);
   MS_CUDA(cudaMemsetAsync(sync, 0, trsv_sync_ints(N) * sizeof(int), st));
-  k_trsv_fwd<<<nt, 256, 0, st>>>(N, nt, L, Dinv, f, t, sync, done);
-  k_trsv_bwd<<<nt, 256, 0, st>>>(N, nt, L, Dinv, t, y, yscratch, sync, done);
+  { k_trsv_fwd<<<nt, 256, 0, st>>>(N, nt, L, Dinv, f, t, sync, done); ms_count_launch(); }
+  { k_trsv_bwd<<<nt, 256, 0, st>>>(N, nt, L, Dinv, t, y, yscratch, sync, done); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -500,7 +500,7 @@ void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work,
   const int nt = div_up(N, T);
   double* P = work;
   double* W = work + packed_words(nt);
-  k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, P);
+  { k_pack_tiles<<<148 * 8, 256, 0, st>>>(N, nt, A, P); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
   dense_spd_inverse_batched(nt, 1, P, W, packed_inv, fail, st);
 }
@@ -592,8 +592,8 @@ void launch_symv_packed(int N, const double* X, const double* f, double* y, doub
   const int nt = div_up(N, T);
   if (t_end < 0) t_end = packed_tiles(nt);
   if (t_end > t_begin)
-    k_symv_tiles<<<(unsigned)(t_end - t_begin), 256, 0, st>>>(N, nt, X, f, part, done, t_begin);
-  k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done, t_begin, t_end);
+    { k_symv_tiles<<<(unsigned)(t_end - t_begin), 256, 0, st>>>(N, nt, X, f, part, done, t_begin); ms_count_launch(); }
+  { k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done, t_begin, t_end); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -696,7 +696,7 @@ void launch_l1_dense_apply(const Grid& g, const BandSys* sys, int nsys, int nt, 
   const size_t smem = sizeof(double) * ((size_t)2 * nt * T + 16 * (T + 1) + T);
   if (smem > 220 * 1024) throw Error(-1, "subdomain too large for the dense level-1 apply");
   MS_CUDA(cudaFuncSetAttribute(k_l1_dense_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_l1_dense_apply<<<nsys, kDenseApplyThreads, smem, st>>>(g, sys, nt, X, r, ybuf, done);
+  { k_l1_dense_apply<<<nsys, kDenseApplyThreads, smem, st>>>(g, sys, nt, X, r, ybuf, done); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 

@@ -64,7 +64,7 @@ void launch_heat_assemble(const Grid& g, const double* E, const uint8_t* hdir,
                           const HeatParam& hp, double sigma, const BandSys* sys, int nsys,
                           double* Lc, cudaStream_t st, const double* sigma_per_sys) {
   if (nsys == 0) return;
-  k_heat_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sigma, sys, Lc, sigma_per_sys);
+  { k_heat_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sigma, sys, Lc, sigma_per_sys); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -515,7 +515,7 @@ struct SubspaceLaunch {
   static void run(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
                   int max_pass, double tol, size_t smem, cudaStream_t st) {
     MS_CUDA(cudaFuncSetAttribute(k_subspace<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_subspace<T><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, max_pass, tol);
+    { k_subspace<T><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, max_pass, tol); ms_count_launch(); }
     MS_CUDA(cudaGetLastError());
   }
 };
@@ -830,7 +830,7 @@ __global__ void k_rand_sigma(Grid g, const double* __restrict__ E, const uint8_t
 void launch_rand_sigma(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp,
                        const BandSys* sys, int nsys, double* sigma, cudaStream_t st) {
   if (nsys == 0) return;
-  k_rand_sigma<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sys, sigma);
+  { k_rand_sigma<<<nsys, 256, 0, st>>>(g, E, hdir, hp, sys, sigma); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -848,7 +848,7 @@ struct RandomizedLaunch {
                                           (B + 1) * 8 + (B + 1) + 2 * B * (B + 1) + 2 * B + 4) +
                         sizeof(int) * B + (size_t)nlx * NLy + 16;
     MS_CUDA(cudaFuncSetAttribute(k_randomized<T, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_randomized<T, B><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, nlx);
+    { k_randomized<T, B><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, hp, b, F, ns, nlx); ms_count_launch(); }
     MS_CUDA(cudaGetLastError());
   }
   static void run(const Grid& g, const double* E, const uint8_t* hdir, const HeatParam& hp, const EigBatch& b,
@@ -891,7 +891,7 @@ __global__ void k_select(int n_centers, const double* __restrict__ evals, int n_
 void launch_select(int n_centers, const double* evals, int n_max, double threshold, int fixed,
                    int* nsel, cudaStream_t st) {
   if (n_centers == 0) return;
-  k_select<<<div_up(n_centers, 128), 128, 0, st>>>(n_centers, evals, n_max, threshold, fixed, nsel);
+  { k_select<<<div_up(n_centers, 128), 128, 0, st>>>(n_centers, evals, n_max, threshold, fixed, nsel); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -954,7 +954,7 @@ __global__ void __launch_bounds__(256)
 void launch_compact_psi(const EigBatch& b, int NLx, const int* nsel, const int64_t* psioff,
                         double* psi, cudaStream_t st) {
   if (b.nk == 0) return;
-  k_compact_psi<<<b.nk, 256, 0, st>>>(b, NLx, nsel, psioff, psi);
+  { k_compact_psi<<<b.nk, 256, 0, st>>>(b, NLx, nsel, psioff, psi); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -1051,7 +1051,7 @@ void launch_el_assemble(const Grid& g, const double* E, const uint8_t* hdir, con
                         double sigma, const BandSys* sys, int nsys, double* Lc, cudaStream_t st,
                         const double* sigma_per_sys) {
   if (nsys == 0) return;
-  k_el_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, ep, sigma, sys, Lc, sigma_per_sys);
+  { k_el_assemble<<<nsys, 256, 0, st>>>(g, E, hdir, ep, sigma, sys, Lc, sigma_per_sys); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -1312,7 +1312,7 @@ struct SubspaceElLaunch {
   static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,
                   int max_pass, double tol, size_t smem, cudaStream_t st) {
     MS_CUDA(cudaFuncSetAttribute(k_subspace_el<KJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_subspace_el<KJ><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, max_pass, tol);
+    { k_subspace_el<KJ><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, max_pass, tol); ms_count_launch(); }
     MS_CUDA(cudaGetLastError());
   }
 };
@@ -1383,7 +1383,7 @@ __global__ void __launch_bounds__(256)
 void launch_compact_psi_el(const EigBatch& b, int NLx, const int* nsel, const int64_t* psioff,
                            double* psi, cudaStream_t st) {
   if (b.nk == 0) return;
-  k_compact_psi_el<<<b.nk, 256, 0, st>>>(b, NLx, nsel, psioff, psi);
+  { k_compact_psi_el<<<b.nk, 256, 0, st>>>(b, NLx, nsel, psioff, psi); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -1420,7 +1420,7 @@ __global__ void k_rand_sigma_el(Grid g, const double* __restrict__ E, const uint
 void launch_rand_sigma_el(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep,
                           const BandSys* sys, int nsys, double* sigma, cudaStream_t st) {
   if (nsys == 0) return;
-  k_rand_sigma_el<<<nsys, 256, 0, st>>>(g, E, hdir, ep, sys, sigma);
+  { k_rand_sigma_el<<<nsys, 256, 0, st>>>(g, E, hdir, ep, sys, sigma); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -1655,7 +1655,7 @@ struct RandElLaunch {
     const size_t smem = el_smem_bytes<B>(b.mex, b.mey, max_bw);
     if (smem > 200 * 1024) throw Error(-1, "neighbourhood too large for the elasticity eigensolver tile");
     MS_CUDA(cudaFuncSetAttribute(k_randomized_el<KJ, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_randomized_el<KJ, B><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, F, ns, nlx);
+    { k_randomized_el<KJ, B><<<b.nk, kEigThreads, smem, st>>>(g, E, hdir, ep, b, F, ns, nlx); ms_count_launch(); }
     MS_CUDA(cudaGetLastError());
   }
   static void run(const Grid& g, const double* E, const uint8_t* hdir, const ElastParam& ep, const EigBatch& b,

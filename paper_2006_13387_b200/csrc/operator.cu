@@ -175,8 +175,8 @@ void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint
   if (b_hi < 0) b_hi = g.ny;
   const int ty0 = std::max(0, b_lo - 1) / MV_NY, ty1 = std::min(g.ny, b_hi + 1) / MV_NY;
   dim3 grid(div_up(g.nx + 1, MV_TX), ty1 - ty0 + 1);
-  k_matvec<<<grid, MV_TX * MV_TY, 0, st>>>(g, ke, E, mask, z, p_old, p_new, q, mode, sc, partials,
-                                           alpha_hist, b_lo, b_hi, ty0);
+  { k_matvec<<<grid, MV_TX * MV_TY, 0, st>>>(g, ke, E, mask, z, p_old, p_new, q, mode, sc, partials,
+                                           alpha_hist, b_lo, b_hi, ty0); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kReduceThreads)
 
 void launch_pcg_update(int64_t n, double* x, const double* p, double* r, const double* q,
                        PcgScalars* sc, double* partials, double* res_hist, cudaStream_t st) {
-  k_pcg_update<<<reduce_blocks(), kReduceThreads, 0, st>>>(n, x, p, r, q, sc, partials, res_hist);
+  { k_pcg_update<<<reduce_blocks(), kReduceThreads, 0, st>>>(n, x, p, r, q, sc, partials, res_hist); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kReduceThreads)
 
 void launch_rz(int64_t n, const double* r, const double* z, PcgScalars* sc, double* partials,
                double* beta_hist, cudaStream_t st) {
-  k_rz<<<reduce_blocks(), kReduceThreads, 0, st>>>(n, r, z, sc, partials, beta_hist);
+  { k_rz<<<reduce_blocks(), kReduceThreads, 0, st>>>(n, r, z, sc, partials, beta_hist); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kReduceThreads)
 
 void launch_init_norm(int64_t n, const double* b, PcgScalars* sc, double* partials,
                       double* res_hist, cudaStream_t st) {
-  k_init_norm<<<reduce_blocks(), kReduceThreads, 0, st>>>(n, b, sc, partials, res_hist);
+  { k_init_norm<<<reduce_blocks(), kReduceThreads, 0, st>>>(n, b, sc, partials, res_hist); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -291,7 +291,7 @@ __global__ void k_finalize(PcgScalars* sc, int kind, double* hist) {
 }
 
 void launch_finalize(PcgScalars* sc, int kind, double* hist, cudaStream_t st) {
-  k_finalize<<<1, 1, 0, st>>>(sc, kind, hist);
+  { k_finalize<<<1, 1, 0, st>>>(sc, kind, hist); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -310,12 +310,12 @@ __global__ void k_gather_free(int64_t n_free, const int64_t* __restrict__ free_d
 
 void launch_scatter_free(int64_t n_free, const int64_t* free_dofs, const double* src_free,
                          double* dst_full, cudaStream_t st) {
-  k_scatter_free<<<reduce_blocks(), 256, 0, st>>>(n_free, free_dofs, src_free, dst_full);
+  { k_scatter_free<<<reduce_blocks(), 256, 0, st>>>(n_free, free_dofs, src_free, dst_full); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 void launch_gather_free(int64_t n_free, const int64_t* free_dofs, const double* src_full,
                         double* dst_free, cudaStream_t st) {
-  k_gather_free<<<reduce_blocks(), 256, 0, st>>>(n_free, free_dofs, src_full, dst_free);
+  { k_gather_free<<<reduce_blocks(), 256, 0, st>>>(n_free, free_dofs, src_full, dst_free); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 

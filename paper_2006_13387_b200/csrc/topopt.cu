@@ -80,13 +80,13 @@ static int stream_blocks(int64_t n) { return (int)std::min<int64_t>(div_up(n, kF
 
 void launch_filter_apply(const FilterDev& f, const double* x, double* y, cudaStream_t st) {
   const int64_t n = (int64_t)f.nx * f.ny;
-  k_filter_apply<<<stream_blocks(n), kFiltThreads, 0, st>>>(f, x, y);
+  { k_filter_apply<<<stream_blocks(n), kFiltThreads, 0, st>>>(f, x, y); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
 void launch_filter_adjoint(const FilterDev& f, const double* v, double* y, cudaStream_t st) {
   const int64_t n = (int64_t)f.nx * f.ny;
-  k_filter_adjoint<<<stream_blocks(n), kFiltThreads, 0, st>>>(f, v, y);
+  { k_filter_adjoint<<<stream_blocks(n), kFiltThreads, 0, st>>>(f, v, y); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -114,7 +114,7 @@ __global__ void k_simp(int64_t n, const double* __restrict__ rho_f, double p, do
 
 void launch_simp(int64_t n, const double* rho_f, double p, double E_min, double E_max, double* E,
                  int* bad, cudaStream_t st) {
-  k_simp<<<stream_blocks(n), kFiltThreads, 0, st>>>(n, rho_f, p, E_min, E_max, E, bad);
+  { k_simp<<<stream_blocks(n), kFiltThreads, 0, st>>>(n, rho_f, p, E_min, E_max, E, bad); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -152,8 +152,8 @@ void launch_compliance_sens(const Grid& g, const KeParam& ke, const double* u_fu
                             const double* rho_f, double p, double E_min, double E_max, double* sens,
                             cudaStream_t st) {
   const int64_t n = (int64_t)g.nx * g.ny;
-  k_compliance_sens<<<stream_blocks(n), kFiltThreads, 0, st>>>(g, ke, u_full, rho_f, p, E_min,
-                                                               E_max, sens);
+  { k_compliance_sens<<<stream_blocks(n), kFiltThreads, 0, st>>>(g, ke, u_full, rho_f, p, E_min,
+                                                               E_max, sens); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kFiltThreads)
 
 void launch_dot(int64_t n, const double* a, const double* b, double* out, double* partials,
                 unsigned int* ticket, cudaStream_t st) {
-  k_dot<<<kDotBlocks, kFiltThreads, 0, st>>>(n, a, b, out, partials, ticket);
+  { k_dot<<<kDotBlocks, kFiltThreads, 0, st>>>(n, a, b, out, partials, ticket); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -201,7 +201,7 @@ __global__ void k_oc_init(OcState* s, double v_star, double move, double damping
 }
 
 void launch_oc_init(OcState* s, double v_star, double move, double damping, cudaStream_t st) {
-  k_oc_init<<<1, 1, 0, st>>>(s, v_star, move, damping);
+  { k_oc_init<<<1, 1, 0, st>>>(s, v_star, move, damping); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kFiltThreads)
 void launch_oc_eval(int64_t n, const double* rho, const double* dg, const double* vol,
                     const double* wv, OcState* s, double* partials, unsigned int* ticket,
                     cudaStream_t st) {
-  k_oc_eval<<<kDotBlocks, kFiltThreads, 0, st>>>(n, rho, dg, vol, wv, s, partials, ticket);
+  { k_oc_eval<<<kDotBlocks, kFiltThreads, 0, st>>>(n, rho, dg, vol, wv, s, partials, ticket); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 
@@ -286,7 +286,7 @@ __global__ void k_oc_final(int64_t n, const double* __restrict__ rho, const doub
 
 void launch_oc_final(int64_t n, const double* rho, const double* dg, const double* vol,
                      const OcState* s, double* rho_new, cudaStream_t st) {
-  k_oc_final<<<stream_blocks(n), kFiltThreads, 0, st>>>(n, rho, dg, vol, s, rho_new);
+  { k_oc_final<<<stream_blocks(n), kFiltThreads, 0, st>>>(n, rho, dg, vol, s, rho_new); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
 

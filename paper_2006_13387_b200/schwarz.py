@@ -232,6 +232,7 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "eigenvalues": evals[:nc], "n_subdomains": inf.n_subdomains,
         "max_eig_passes": inf.max_eig_passes, "mean_eig_passes": inf.mean_eig_passes, "local_bytes": inf.local_bytes,
         "coarse_bytes": inf.coarse_bytes, "level1": level1, "level1_operator": variant.level1, "delta": delta, "local_solver": local_solver,
-        "coarse_solve": coarse_solve,
+        "coarse_solve": coarse_solve, "level1_twisted": bool(inf.level1_twisted),
+        "level1_copies": int(inf.level1_copies), "n_subdomains_local": int(inf.n_subdomains_local),
     }
     return TwoLevelPreconditioner(variant, op, h, info)

@@ -285,6 +285,7 @@ def _eig_from_args(args):
 
 
 _JIT = None
+_MESH_ELEMENT_DOFS = _N_FULL = _KE_E = None
 
 
 def _jitter_task(name):
@@ -292,7 +293,7 @@ def _jitter_task(name):
     return name, _JIT[name]()
 
 
-def jitter_band(op, b, variant, level1, cop, blocks, tol, maxit, procs, x_ref):
+def jitter_band(op, b, variant, level1, cop, blocks, tol, maxit, procs, x_ref, heat=None):
     """The reference's own round-off band (VERDICT r1 'next' 1): the same
     preconditioner re-run under perturbations that change only rounding,
     through the TwoLevelPreconditioner / CoarseOperator seams
@@ -304,7 +305,16 @@ def jitter_band(op, b, variant, level1, cop, blocks, tol, maxit, procs, x_ref):
       coarse mode applies) and as a lower Cholesky factor (dpotrf 'L');
     * the level-1 SuperLU factors under the two other column orderings
       (MMD_AT_PLUS_A, MMD_ATA; the GPU uses banded Cholesky instead);
-    * explicit K0^-1 together with the reversed level-1 order.
+    * explicit K0^-1 together with the reversed level-1 order;
+    * the operator A p evaluated element by element in ascending and in
+      descending element order (the matrix-free evaluation the GPU uses)
+      instead of the CSR row sums;
+    * three combinations of the above (operator order + coarse form +
+      level-1 order or ordering + b scaling);
+    * the level-1 matrices factored by LAPACK banded Cholesky in
+      node-interleaved order (dpbtrf/dpbtrs) instead of SuperLU -- alone and
+      combined with the element-order operator and either coarse form: the
+      arithmetic of the GPU path, which the band must be able to contain.
     Returns {name: (iterations, ||x - x_ref||/||x_ref||, true residual)}."""
     import copy
     import multiprocessing as mp
@@ -341,6 +351,75 @@ def jitter_band(op, b, variant, level1, cop, blocks, tol, maxit, procs, x_ref):
 
     import scipy.sparse.linalg as spla
 
+    # the same operator evaluated element by element (the GPU's matrix-free
+    # order: each element's Ke0 E_e p_e scattered in ascending / descending
+    # element order) instead of the CSR row sums; the CSR product and
+    # these differ only in summation order (bitwise equal on a point load)
+    ed = _MESH_ELEMENT_DOFS
+    fi = np.full(_N_FULL, -1)
+    fi[op.free_dofs] = np.arange(op.n_free)
+    loc = fi[ed]
+    ok = loc >= 0
+    Ke_E = _KE_E
+
+    def ebe(order):
+        lo_ok = loc[order]
+        ok_o = ok[order]
+        tgt = np.maximum(lo_ok, 0)[ok_o]
+        Ko = Ke_E[order]
+
+        def matvec(p):
+            pf = np.where(ok_o, p[np.maximum(lo_ok, 0)], 0.0)
+            q = np.einsum("eij,ej->ei", Ko, pf)
+            out = np.zeros(op.n_free)
+            np.add.at(out, tgt, q[ok_o])
+            return out
+        return matvec
+
+    def run_op(A, l1=None, coarse_op=None, bb=None):
+        pre = schwarz.TwoLevelPreconditioner(variant, level1 if l1 is None else l1,
+                                             cop if coarse_op is None else coarse_op, op.n_free, {})
+        x, rep = krylov.pcg_solve(A, b if bb is None else bb, pre, tol=tol, maxit=maxit)
+        return rep.iterations, x
+
+    def band_solve(K):
+        """LAPACK banded Cholesky (dpbtrf/dpbtrs) of an SPD sparse matrix."""
+        coo = K.tocoo()
+        dd = coo.row - coo.col
+        keep = dd >= 0
+        ab = np.zeros((int(dd[keep].max()) + 1, K.shape[0]))
+        ab[dd[keep], coo.col[keep]] = coo.data[keep]
+        cb = sla.cholesky_banded(ab, lower=True)
+        return lambda r: sla.cho_solve_banded((cb, True), r)
+
+    def banded_level1():
+        """The same local matrices K_i = A[idx][:, idx] (or the heat blocks'
+        D[sidx][:, sidx]) factored by banded Cholesky in node-interleaved
+        order instead of SuperLU -- the level-1 arithmetic of the GPU path."""
+        out = []
+        if heat is None:
+            n_nodes = _N_FULL // 2
+            for idx, _ in level1:
+                fd = op.free_dofs[idx]
+                perm = np.lexsort((fd // n_nodes, fd % n_nodes))
+                bs = band_solve(op.matrix[idx[perm]][:, idx[perm]])
+
+                def solve(r, bs=bs, perm=perm):
+                    z = np.empty_like(r)
+                    z[perm] = bs(r[perm])
+                    return z
+                out.append((idx, solve))
+        else:
+            D, parts = heat
+            for (idx, _), sidx in zip(level1, parts):
+                bs = band_solve(D[sidx][:, sidx])
+
+                def solve(r, bs=bs, m=sidx.size):
+                    return np.concatenate([bs(r[:m]), bs(r[m:])])
+                out.append((idx, solve))
+        return out
+
+    n_el = ed.shape[0]
     p1 = np.random.default_rng(1).permutation(len(level1))
     p2 = np.random.default_rng(2).permutation(len(level1))
     eps = 2.0 ** -52
@@ -355,6 +434,18 @@ def jitter_band(op, b, variant, level1, cop, blocks, tol, maxit, procs, x_ref):
         "splu_mmd_at_plus_a": lambda: run(relu("MMD_AT_PLUS_A"), cop, b) if blocks else None,
         "splu_mmd_ata": lambda: run(relu("MMD_ATA"), cop, b) if blocks else None,
         "k0_inverse_l1_reversed": lambda: run(level1[::-1], k0_inv(), b),
+        "operator_element_order": lambda: run_op(ebe(np.arange(n_el))),
+        "operator_element_order_reversed": lambda: run_op(ebe(np.arange(n_el)[::-1])),
+        # several rounding changes at once (a different implementation changes
+        # all of them together)
+        "combined_ebe_k0inv_l1rev": lambda: run_op(ebe(np.arange(n_el)), level1[::-1], k0_inv()),
+        "combined_ebe_rev_k0inv_mmd": lambda: run_op(ebe(np.arange(n_el)[::-1]),
+                                                     relu("MMD_AT_PLUS_A") if blocks else None, k0_inv()),
+        "combined_ebe_k0low_perm_b": lambda: run_op(ebe(np.arange(n_el)), [level1[i] for i in p1], k0_lower(),
+                                                    b * (1 + eps)),
+        "l1_banded_cholesky": lambda: run(banded_level1(), cop, b),
+        "combined_banded_ebe_k0inv": lambda: run_op(ebe(np.arange(n_el)), banded_level1(), k0_inv()),
+        "combined_banded_ebe_k0chol": lambda: run_op(ebe(np.arange(n_el)[::-1]), banded_level1(), cop),
     }
     names = list(_JIT)
     with mp.get_context("fork").Pool(procs) as pool:
@@ -394,8 +485,13 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000, tag="EH+Rot", procs=None, sa
     from mselast import coarse
     cop = coarse.assemble_coarse_operator(op, basis)
     blocks = _Blocks(mesh, spec.H, spec.delta)
+    heat = None
     if variant.level1 == "heat":
         level1 = schwarz._subdomain_heat_solvers(op, mesh, blocks, coeff, spec.heat_dirichlet_nodes)
+        D_op = assembly.assemble_diffusion(mesh, coeff.values, spec.heat_dirichlet_nodes)
+        si = D_op.free_index()
+        parts = [si[p.interior_node_ids(mesh)] for p in blocks.neighborhoods]
+        heat = (D_op.matrix, [q[q >= 0] for q in parts if (q >= 0).any()])
     else:
         level1 = schwarz._subdomain_elasticity_solvers(op, mesh, blocks)
     pre = schwarz.TwoLevelPreconditioner(variant, level1, cop, op.n_free, {})
@@ -405,7 +501,10 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000, tag="EH+Rot", procs=None, sa
     rng = np.random.default_rng(11)
     r = rng.standard_normal(op.n_free)
     z = pre.apply(r)
-    band = jitter_band(op, b, variant, level1, cop, variant.level1 != "heat", tol, maxit, procs, x)
+    global _MESH_ELEMENT_DOFS, _N_FULL, _KE_E
+    _MESH_ELEMENT_DOFS, _N_FULL = mesh.element_dofs(), mesh.n_dofs
+    _KE_E = coeff.values[:, None, None] * Ke[None]
+    band = jitter_band(op, b, variant, level1, cop, variant.level1 != "heat", tol, maxit, procs, x, heat)
     names = sorted(band)
     true_res = np.linalg.norm(b - op.matrix @ x) / np.linalg.norm(b)
     save(fname, E=spec.E, constrained_dofs=spec.constrained_dofs,

@@ -3,6 +3,12 @@
 The oracle cannot run a whole 2048^2 or 4096x2048 solve in test time, so full
 size is checked piecewise against it and through size-independent properties:
 
+* coarse dimension: the mode count of EVERY neighbourhood of configs 2 (all
+  four contrasts), 3, 4 and three config-5 steps against the reference's
+  own pencils (tests/golden/nc_*.npz, make_nc_fullsize.py: reference
+  build_local_eigproblem + ARPACK + the reference's select_modes, dense
+  ?sygvx cross-checked on the 24 closest-to-threshold / random centres):
+  n_sel per centre and N_c exact;
 * eigenproblems: 12 neighbourhoods per config solved by the oracle's ARPACK
   path (pinned to the dense LAPACK solve in test_host_cpu.py): mode counts
   exact (gap rule), selected eigenvalues 1e-9, the rest 1e-6;
@@ -156,3 +162,50 @@ def test_fullsize_config5_step_converges():
     assert rep.converged and rep.residuals[-1] <= spec.tol
     true_res = np.linalg.norm(b - op @ x) / np.linalg.norm(b)
     assert true_res <= 1.5 * spec.tol, (true_res, rep.iterations)
+
+
+NC_CASES = {
+    "config2_1e2": lambda: configs.config2(seed=0, eta=1e2),
+    "config2_1e4": lambda: configs.config2(seed=0, eta=1e4),
+    "config2_1e6": lambda: configs.config2(seed=0, eta=1e6),
+    "config2_1e8": lambda: configs.config2(seed=0, eta=1e8),
+    "config3": lambda: configs.config3(seed=0),
+    "config4": lambda: configs.config4(seed=0),
+    "config5_step0": lambda: configs.config5(seed=0, step=0),
+    "config5_step25": lambda: configs.config5(seed=0, step=25),
+    "config5_step49": lambda: configs.config5(seed=0, step=49),
+}
+
+
+@pytest.mark.parametrize("case", list(NC_CASES))
+def test_fullsize_mode_counts_every_neighbourhood(case):
+    """north star: coarse-space dimension identical (integer, bit-exact),
+    excepting eigenvalue ratios within 1e-10 of the gap threshold."""
+    from conftest import load_golden
+
+    g = load_golden(f"nc_{case}.npz")
+    spec = NC_CASES[case]()
+    assert (spec.nx, spec.ny, spec.H) == (int(g["nx"]), int(g["ny"]), int(g["H"]))
+    mesh = G.build_fine_mesh(spec.nx, spec.ny)
+    coeff = G.CoefficientField(spec.E, spec.nu, spec.E_min, spec.E_max)
+    op = G.ElasticityOperator(mesh, coeff, spec.free_dofs())
+    part = G.build_coarse_partition(mesh, spec.Nx, spec.Ny)
+    # coarse space only (the level 1 does not enter the mode selection)
+    pre = G.build_preconditioner("EH+Rot", op, mesh, part, coeff, spec.heat_dirichlet_nodes,
+                                 level1="blocks", delta=spec.delta)
+    got = np.array(pre.mode_counts)
+    ref = g["n_sel"]
+    exempt = g["margin"] < 1e-10
+    diff = np.nonzero((got != ref) & ~exempt)[0]
+    assert diff.size == 0, (case, diff[:10], got[diff[:10]], ref[diff[:10]], g["margin"][diff[:10]])
+    if not exempt.any():
+        assert pre.coarse_dim == int(g["N_c"]), (case, pre.coarse_dim, int(g["N_c"]))
+    # the selected eigenvalues themselves: GPU subspace iteration vs ARPACK on
+    # the reference pencil, relative 1e-9 above the pencil's round-off floor
+    lam, w = pre.info["eigenvalues"], g["eigenvalues"]
+    floor = 1e-15 * 24.0 / mesh.h ** 2
+    sel = np.arange(7)[None, :] < ref[:, None]
+    err = np.abs(lam - w)
+    assert np.all(err[sel] <= 1e-9 * np.abs(w[sel]) + floor), case
+    del pre, op
+    torch.cuda.empty_cache()
