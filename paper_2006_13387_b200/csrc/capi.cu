@@ -1246,11 +1246,12 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       } else {
         launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
       }
-      // one factor copy (column band) unless MS_L1_COPIES=2 or the
-      // register-prefetch sweeps are in use
-      int copies_env = 0;
+      // one factor copy (column band, dot-form backward sweep) on request
+      // (MS_L1_COPIES=1): half the factor bytes, but the backward sweep is
+      // issue-bound (config 3: level 1 2.48 ms vs 1.97 ms with both bands)
+      int copies_env = 2;
       if (const char* e = getenv("MS_L1_COPIES")) copies_env = std::atoi(e);
-      pc->one_copy = copies_env != 2 && l1_ring_sweeps_enabled() &&
+      pc->one_copy = copies_env == 1 && l1_ring_sweeps_enabled() &&
                      ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
       if (!pc->one_copy) {
         pc->Lr.alloc(foff + 2);
