@@ -1,5 +1,5 @@
-# GPU-box validation used during development: smoke, the -m gpu suite, the default bench line
+# GPU-box validation: smoke, the -m gpu suite, the default bench line
 mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo exit=$? >> gpurun_out/smoke.log
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
+timeout 2400 python -m pytest tests -m gpu -q -rs > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo exit=$? >> gpurun_out/bench.log

@@ -6,6 +6,8 @@
 // which makes K_i a band of width 2*(short side)+3 (73 for the configs'
 // 35x35-node subdomains); its Cholesky factor is 1.4 MB instead of the 24 MB
 // of a packed dense inverse, so one apply streams ~8x fewer bytes.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -358,10 +360,13 @@ __global__ void __launch_bounds__(kSolveWarps * 32)
 #define MS_TMA_CH 8
 #endif
 #ifndef MS_TMA_NST
-#define MS_TMA_NST 3
+#define MS_TMA_NST 2  // 2 stages: 4 CTAs (16 warps) per SM; config 3 level 1 1.99 -> 1.94 ms vs 3 stages
 #endif
 #ifndef MS_TMA_WARPS
 #define MS_TMA_WARPS 4
+#endif
+#ifndef MS_L1_MINB
+#define MS_L1_MINB 3  // register budget sized for >= 3 resident CTAs per SM (~128 registers)
 #endif
 constexpr int kCh = MS_TMA_CH;  // band columns per stage (divides 32)
 constexpr int kNst = MS_TMA_NST;  // stages per warp
@@ -375,15 +380,39 @@ struct Ring {
   uint32_t phase;  // parity bit per stage
 };
 
-// ring shared-memory header: kTmaWarps * kNst mbarriers, rounded to an even
-// word count (the stages stay 16-byte aligned)
-constexpr int kRingHeaderWords = (kTmaWarps * kNst + 1) & ~1;
+// Padded ring (elasticity bands, S = bw + 1 even): every band column gets its
+// own P = 32 (T + 1) word slot in the stage, words [S, P) of every slot and a
+// 32-word guard before the first stage stay zero.  A sweep step then reads
+// its R = T + 1 coefficients (band offsets 32 s + lane - u) and the pivot
+// with unconditional loads at compile-time offsets: rows outside the band
+// read zeros.  The copies are one bulk copy per column (S * 8 bytes, 16-byte
+// aligned because S is even), issued by lanes 0..cnt-1.
+template <int T>
+__host__ __device__ constexpr int pad_slot_words() {
+  return 32 * (T + 1);
+}
+constexpr int kPadGuard = 32;
 
-__device__ __forceinline__ void ring_init(Ring& rg, double* smem, int warp, int lane, int stage_words) {
+// ring shared-memory header: kTmaWarps * kNst mbarriers, rounded to 16 words
+// (the stages stay 128-byte aligned)
+constexpr int kRingHeaderWords = (kTmaWarps * kNst + 15) & ~15;  // 128-byte aligned stages (TMA boxes)
+
+// per-warp ring words: kNst stages (+ the zero guard of the padded layout)
+__host__ __device__ inline int ring_warp_words(int stage_words, bool pad) {
+  return kNst * stage_words + (pad ? kPadGuard : 0);
+}
+
+__device__ __forceinline__ void ring_init(Ring& rg, double* smem, int warp, int lane, int stage_words,
+                                          bool pad = false) {
   rg.bar = reinterpret_cast<uint64_t*>(smem) + warp * kNst;
-  rg.buf = smem + kRingHeaderWords + (size_t)warp * kNst * stage_words;
+  double* base = smem + kRingHeaderWords + (size_t)warp * ring_warp_words(stage_words, pad);
+  rg.buf = base + (pad ? kPadGuard : 0);
   rg.stage = stage_words;
   rg.phase = 0;
+  if (pad) {  // guard and slot tails must read zero; the copies never touch them
+    for (int i = lane; i < ring_warp_words(stage_words, pad); i += 32) base[i] = 0.0;
+    __syncwarp();
+  }
   if (lane == 0) {
     for (int st = 0; st < kNst; ++st) mbar_init(rg.bar + st, 1);
     mbar_fence_init();
@@ -397,6 +426,26 @@ __device__ __forceinline__ void chunk_cols(bool rev, int n, int c, int& start, i
   const int k0 = c * kCh;
   cnt = min(kCh, n - k0);
   start = rev ? n - k0 - cnt : k0;
+}
+
+// padded stage fill: one 2-D TMA box of kCh columns x P words (the words
+// past S zero-filled); all lanes call, lane 0 issues
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool REV, int P>
+__device__ __forceinline__ void ring_issue_pad(Ring& rg, const CUtensorMap* map, int col0, int n, int c, int lane) {
+  if (lane != 0) return;
+  int start, cnt;
+  chunk_cols(REV, n, c, start, cnt);
+  const int st = c % kNst;
+  mbar_expect_tx(rg.bar + st, (uint32_t)(kCh * P * 8));
+  tma_load_2d(rg.buf + (size_t)st * rg.stage, map, 0, col0 + start, rg.bar + st);
 }
 
 template <bool REV>
@@ -413,14 +462,19 @@ __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int
 
 // ym(r): address of the NR values of the sweep's r-th row (r counts the
 // sweep's own steps, i.e. already reversed for REV)
-template <int T, int NR, bool REV, class YMap>
+template <int T, int NR, bool REV, bool PAD, class YMap>
 __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw, YMap ym,
-                                                int lane, Ring& rg) {
+                                                int lane, Ring& rg, const CUtensorMap* map = nullptr,
+                                                int col0 = 0) {
   constexpr int R = T + 1;
+  constexpr int P = pad_slot_words<T>();
   const int S = bw + 1;
   const int nch = (n + kCh - 1) / kCh;
-  if (lane == 0)
+  if (PAD) {
+    for (int c = 0; c < min(kNst, nch); ++c) ring_issue_pad<REV, P>(rg, map, col0, n, c, lane);
+  } else if (lane == 0) {
     for (int c = 0; c < min(kNst, nch); ++c) ring_issue<REV>(rg, L, n, S, c);
+  }
   auto yat = [&](int r, int c) -> double* { return ym(r) + c; };
 
   double acc[NR][R], rnext[NR];
@@ -443,6 +497,9 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
       rnext[c] = r < n ? *yat(r, c) : 0.0;
     }
     double dsave = 0.0;  // 1/L_kk of this lane's row of the block
+    double yfin[NR];     // PAD: the row's final value, captured at its pivot step
+#pragma unroll
+    for (int c = 0; c < NR; ++c) yfin[c] = 0.0;
 #pragma unroll 1
     for (int h = 0; h < 32 && k0 + h < n; h += kCh) {
       const int ch = (k0 + h) / kCh;
@@ -451,6 +508,39 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
       rg.phase ^= 1u << st;
       int start, cnt;
       chunk_cols(REV, n, ch, start, cnt);
+      if (PAD) {
+        // slot q of the stage = column start + q; this lane's coefficient of
+        // step q (u = h + q) sits at slot(q) + lane - u
+        const double* sb = rg.buf + (size_t)st * rg.stage;
+        const double* sl = sb + (lane - h);
+        auto stepP = [&](int q, int slot) {
+          const int u = h + q;
+          const double* colq = sb + slot * P;
+          const double* a = sl + (slot * P - q);
+          double m[R];
+#pragma unroll
+          for (int s2 = 0; s2 < R; ++s2) m[s2] = a[32 * s2];
+          const double d = colq[0];
+#pragma unroll
+          for (int c = 0; c < NR; ++c) {
+            const double wk = __shfl_sync(0xffffffffu, acc[c][0] * d, u);
+            yfin[c] = (lane == u) ? wk : yfin[c];
+#pragma unroll
+            for (int s2 = 0; s2 < R; ++s2) acc[c][s2] = fma(-m[s2], wk, acc[c][s2]);
+          }
+        };
+        if (cnt == kCh) {
+#pragma unroll
+          for (int q = 0; q < kCh; ++q) stepP(q, REV ? kCh - 1 - q : q);
+        } else {
+#pragma unroll
+          for (int q = 0; q < kCh; ++q)
+            if (q < cnt) stepP(q, REV ? cnt - 1 - q : q);
+        }
+        __syncwarp();  // every lane is done with this stage before it is refilled
+        if (ch + kNst < nch) ring_issue_pad<REV, P>(rg, map, col0, n, ch + kNst, lane);
+        continue;
+      }
       const double* sb = rg.buf + (size_t)st * rg.stage + (int)(((int64_t)start * S) & 1);
       // Step u of the block: lane owns row k0 + 32 s + lane in slot s, i.e.
       // band offset j = 32 s + lane - u from the pivot row; rows outside
@@ -489,9 +579,11 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
     }
     // slot 0 of lane L stopped changing at step L: it holds row k0+L's final
     // accumulator, and w = acc * (1/L_kk) exactly as the pivot step formed it
+    // (PAD: the pivot lane's slot 0 takes one more, meaningless update; its
+    // value was captured at the pivot step instead, the same product)
 #pragma unroll
     for (int c = 0; c < NR; ++c) {
-      if (k0 + lane < n) *yat(k0 + lane, c) = acc[c][0] * dsave;
+      if (k0 + lane < n) *yat(k0 + lane, c) = PAD ? yfin[c] : acc[c][0] * dsave;
 #pragma unroll
       for (int s = 0; s < R - 1; ++s) acc[c][s] = acc[c][s + 1];
       acc[c][R - 1] = 0.0;
@@ -511,96 +603,136 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
 // Dependent chain per row: one shuffle + fma + mul (B); the window products
 // (A) are off the chain.  rows k = natural numbering of the system; ym(k)
 // addresses row k's NR values (w on entry, x on exit).
-template <int NR, class YMap>
+template <int T, int NR, bool PAD, class YMap>
 __device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int n, int bw, YMap ym, int lane,
-                                               Ring& rg, double* __restrict__ xw) {
+                                               Ring& rg, double* __restrict__ xw,
+                                               const CUtensorMap* map = nullptr, int col0 = 0) {
   static_assert(kCh == 8, "4 lanes per chunk row");
+  constexpr int kWin = 128;       // window rows (>= bw + kCh); stored twice so reads never wrap
+  constexpr int kA = 8 * T;       // phase-A terms per lane: j = pc + 1 + g + 4 i <= 32 T
+  constexpr int P = pad_slot_words<T>();
   const int S = bw + 1;
   const int nch = (n + kCh - 1) / kCh;
-  if (lane == 0)
+  if (PAD) {
+    for (int c = 0; c < min(kNst, nch); ++c) ring_issue_pad<true, P>(rg, map, col0, n, c, lane);
+  } else if (lane == 0) {
     for (int c = 0; c < min(kNst, nch); ++c) ring_issue<true>(rg, L, n, S, c);
-  for (int i = lane; i < 128 * NR; i += 32) xw[i] = 0.0;
+  }
+  for (int i = lane; i < 2 * kWin * NR; i += 32) xw[i] = 0.0;
   __syncwarp();
   const int p = lane >> 2, gq = lane & 3;
+  // the group's row of chunk ch (position pc from the chunk top)
+  auto row_of = [&](int ch, int& start, int& cnt, int& pc) {
+    chunk_cols(true, n, ch, start, cnt);
+    pc = p < cnt ? p : 0;
+    return start + cnt - 1 - pc;
+  };
+  // w (the forward sweep's output) of the next chunk's rows is loaded one
+  // chunk ahead: the L2 latency stays off the chunk's dependent chain
+  double wnext[NR];
+  {
+    int s0, c0, p0;
+    const int k0 = row_of(0, s0, c0, p0);
+#pragma unroll
+    for (int c = 0; c < NR; ++c) wnext[c] = ym(k0)[c];
+  }
   for (int ch = 0; ch < nch; ++ch) {
     const int st = ch % kNst;
+    int start, cnt, pc;
+    const int k = row_of(ch, start, cnt, pc);
+    double wp[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) wp[c] = wnext[c];
+    if (ch + 1 < nch) {
+      int s1, c1, p1;
+      const int k1 = row_of(ch + 1, s1, c1, p1);
+#pragma unroll
+      for (int c = 0; c < NR; ++c) wnext[c] = ym(k1)[c];
+    }
     mbar_wait(rg.bar + st, (rg.phase >> st) & 1u);
     rg.phase ^= 1u << st;
-    int start, cnt;
-    chunk_cols(true, n, ch, start, cnt);
-    const double* sb = rg.buf + (size_t)st * rg.stage + (int)(((int64_t)start * S) & 1);
-    const bool own = p < cnt;
-    const int pc = own ? p : 0;
-    const int k = start + cnt - 1 - pc;           // this group's row (chunk position pc from the top)
-    const double* col = sb + (cnt - 1 - pc) * S;  // its column: L[k + j][k], j = 0..bw
-    double w[NR];
+    const double* sb = rg.buf + (size_t)st * rg.stage + (PAD ? 0 : (int)(((int64_t)start * S) & 1));
+    const double* col = sb + (cnt - 1 - pc) * (PAD ? P : S);  // its column: L[k + j][k], j = 0..bw
+    // (A) rows above the chunk: j = pc + 1 + gq + 4 i, row k + j = start + cnt + gq + 4 i
+    // (independent of the group: the window reads are broadcasts)
+    {
+      const double* cj = col + pc + 1 + gq;
+      const double* xj = xw + (((start + cnt + gq) & (kWin - 1)) * NR);
+      const int jmax = bw - pc - 1 - gq;  // valid i: 4 i <= jmax
+      double acc[4][NR];
 #pragma unroll
-    for (int c = 0; c < NR; ++c) w[c] = ym(k)[c];
-    // (A) rows above the chunk: j in (pc, bw], this lane's quarter
-    double s0[NR], s1[NR];
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int c = 0; c < NR; ++c) s0[c] = s1[c] = 0.0;
-    int j = pc + 1 + gq;
-    for (; j + 4 <= bw; j += 8) {
-      const double l0 = col[j], l1 = col[j + 4];
-      const int a0 = ((k + j) & 127) * NR, a1 = ((k + j + 4) & 127) * NR;
+        for (int c = 0; c < NR; ++c) acc[u][c] = 0.0;
+#pragma unroll
+      for (int i = 0; i < kA; ++i) {
+        if (PAD || 4 * i <= jmax) {  // padded slots read zero beyond the band
+          const double lv = cj[4 * i];
+#pragma unroll
+          for (int c = 0; c < NR; ++c) acc[i & 3][c] = fma(lv, xj[4 * i * NR + c], acc[i & 3][c]);
+        }
+      }
 #pragma unroll
       for (int c = 0; c < NR; ++c) {
-        s0[c] = fma(l0, xw[a0 + c], s0[c]);
-        s1[c] = fma(l1, xw[a1 + c], s1[c]);
+        double sum = (acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c]);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        wp[c] -= sum;
       }
     }
-    if (j <= bw) {
-      const double l0 = col[j];
-      const int a0 = ((k + j) & 127) * NR;
-#pragma unroll
-      for (int c = 0; c < NR; ++c) s0[c] = fma(l0, xw[a0 + c], s0[c]);
-    }
-    double sum[NR], t[NR];
-#pragma unroll
-    for (int c = 0; c < NR; ++c) {
-      sum[c] = s0[c] + s1[c];
-      sum[c] += __shfl_xor_sync(0xffffffffu, sum[c], 1);
-      sum[c] += __shfl_xor_sync(0xffffffffu, sum[c], 2);
-      t[c] = 0.0;
-    }
+    // (B) the chunk's triangle: row q's x broadcast from its group, the later
+    // rows p > q accumulate L[k_p + (p - q)][k_p] x_q
     const double d = col[0];
-    // (B) the chunk's triangle
-    for (int q = 0; q < cnt; ++q) {
-      const double lv = col[max(p - q, 0)];  // L[k_p + (p - q)][k_p] for the later rows p > q
-      const int kq = start + cnt - 1 - q;
+    double lq[kCh];
+#pragma unroll
+    for (int q = 0; q < kCh; ++q) lq[q] = col[max(p - q, 0)];
+    double t[NR], xm[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) t[c] = xm[c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < kCh; ++q) {
+      if (q < cnt) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double x = __shfl_sync(0xffffffffu, (wp[c] - t[c]) * d, 4 * q);
+          xm[c] = (p == q) ? x : xm[c];
+          t[c] = fma(lq[q], x, t[c]);
+        }
+      }
+    }
+    if (gq == 0 && p < cnt) {
+      const int slot = (k & (kWin - 1)) * NR;
 #pragma unroll
       for (int c = 0; c < NR; ++c) {
-        const double x = __shfl_sync(0xffffffffu, (w[c] - sum[c] - t[c]) * d, 4 * q);
-        if (lane == 4 * q) {
-          xw[(kq & 127) * NR + c] = x;
-          ym(kq)[c] = x;
-        }
-        t[c] = fma(lv, x, t[c]);
+        xw[slot + c] = xm[c];
+        xw[slot + kWin * NR + c] = xm[c];
+        ym(k)[c] = xm[c];
       }
     }
     __syncwarp();  // window writes visible; every lane done with the stage before it is refilled
-    if (lane == 0 && ch + kNst < nch) ring_issue<true>(rg, L, n, S, ch + kNst);
+    if (PAD) {
+      if (ch + kNst < nch) ring_issue_pad<true, P>(rg, map, col0, n, ch + kNst, lane);
+    } else if (lane == 0 && ch + kNst < nch) {
+      ring_issue<true>(rg, L, n, S, ch + kNst);
+    }
   }
 }
 
 static int ring_stage_words(int max_bw) { return (kCh * (max_bw + 1) + 3) & ~1; }
-static size_t ring_smem_bytes(int max_bw) {
-  return ((size_t)kRingHeaderWords + (size_t)kTmaWarps * kNst * ring_stage_words(max_bw)) * sizeof(double);
-}
 
-template <int T, int NR>
-__global__ void __launch_bounds__(kTmaWarps * 32, 3)
+template <int T, int NR, bool PAD>
+__global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_ring(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                     const double* __restrict__ Lr, const double* __restrict__ r,
-                    double* __restrict__ ybuf, const int* done, int stage_words) {
+                    double* __restrict__ ybuf, const int* done, int stage_words,
+                    const __grid_constant__ CUtensorMap mapc, const __grid_constant__ CUtensorMap mapr) {
   if (done && *(volatile const int*)done) return;
-  extern __shared__ __align__(16) double smem_ring[];
+  extern __shared__ __align__(128) double smem_ring[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sid = blockIdx.x * kTmaWarps + warp;
   if (sid >= nsys) return;
   Ring rg;
-  ring_init(rg, smem_ring, warp, lane, stage_words);
+  ring_init(rg, smem_ring, warp, lane, stage_words, PAD);
   const BandSys s = sys[sid];
   double* y = ybuf + s.yoff;
   for (int i = lane; i < s.n * NR; i += 32) {
@@ -611,14 +743,18 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3)
   }
   __syncwarp();
   const int n = s.n;
-  band_sweep_ring<T, NR, false>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg);
+  const int col0 = PAD ? (int)(s.foff / (s.bw + 1)) : 0;  // the system's first column in the TMA view
+  band_sweep_ring<T, NR, false, PAD>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
+                                     &mapc, col0);
   __syncwarp();
   if (Lr) {
-    band_sweep_ring<T, NR, true>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; }, lane,
-                                 rg);
+    band_sweep_ring<T, NR, true, PAD>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; },
+                                      lane, rg, &mapr, col0);
   } else {  // one factor copy: backward sweep by dot products over the column band
-    double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * kNst * stage_words + (size_t)warp * 128 * NR;
-    band_sweep_dot<NR>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw);
+    double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD) +
+                 (size_t)warp * 256 * NR;
+    band_sweep_dot<T, NR, PAD>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
+                               &mapc, col0);
   }
 }
 
@@ -631,22 +767,23 @@ __device__ __forceinline__ void pair_sync(int pair) {
   asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
 }
 
-template <int T, int NR>
-__global__ void __launch_bounds__(kTmaWarps * 32, 3)
+template <int T, int NR, bool PAD>
+__global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_twist(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                      const double* __restrict__ Lr, const double* __restrict__ Sinv,
                      const double* __restrict__ r, double* __restrict__ ybuf, const int* done, int stage_words,
-                     int max_bw) {
+                     int max_bw, const __grid_constant__ CUtensorMap mapc,
+                     const __grid_constant__ CUtensorMap mapr) {
   static_assert(kTmaWarps % 2 == 0, "warp pairs");
   if (done && *(volatile const int*)done) return;
-  extern __shared__ __align__(16) double smem_ring[];
+  extern __shared__ __align__(128) double smem_ring[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, role = warp & 1;  // role 0: top, 1: bottom
   const int sid = blockIdx.x * (kTmaWarps / 2) + pair;
   if (sid >= nsys) return;  // both warps of a pair leave together
   Ring rg;
-  ring_init(rg, smem_ring, warp, lane, stage_words);
-  const size_t ring_words = kRingHeaderWords + (size_t)kTmaWarps * kNst * stage_words;
+  ring_init(rg, smem_ring, warp, lane, stage_words, PAD);
+  const size_t ring_words = kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD);
   double* sB = smem_ring + ring_words + (size_t)pair * 2 * NR * max_bw;  // bottom separator partials
   double* tS = sB + NR * max_bw;                                       // separator right-hand side
   const BandSys s = sys[sid];
@@ -666,12 +803,14 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3)
   }
   __syncwarp();
   if (role == 0) {
-    band_sweep_ring<T, NR, false>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg);
+    band_sweep_ring<T, NR, false, PAD>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg,
+                                       &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
   } else {
     const int nb_own = nB - bw;
-    band_sweep_ring<T, NR, false>(
+    band_sweep_ring<T, NR, false, PAD>(
         Lc + s.foffB, nB, bw,
-        [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; }, lane, rg);
+        [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; }, lane, rg,
+        &mapc, PAD ? (int)(s.foffB / (bw + 1)) : 0);
   }
   pair_sync(pair);
   // separator: t = (r_S - L_ST y_T) + (- L_SB y_B); x_S = Sinv t
@@ -696,46 +835,75 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3)
   }
   pair_sync(pair);
   if (role == 0) {
-    band_sweep_ring<T, NR, true>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; }, lane,
-                                 rg);
+    band_sweep_ring<T, NR, true, PAD>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; },
+                                      lane, rg, &mapr, PAD ? (int)(s.foff / (bw + 1)) : 0);
   } else {
-    band_sweep_ring<T, NR, true>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane, rg);
+    band_sweep_ring<T, NR, true, PAD>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane,
+                                      rg, &mapr, PAD ? (int)(s.foffB / (bw + 1)) : 0);
   }
 }
 
-template <int T, int NR>
+// ring shared memory of a launch: header + per-warp rings (+ extras)
+template <int T>
+static int ring_stage_words_t(int max_bw, bool pad) {
+  return pad ? kCh * pad_slot_words<T>() : ring_stage_words(max_bw);
+}
+static size_t ring_bytes(int stage_words, bool pad) {
+  return ((size_t)kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, pad)) * sizeof(double);
+}
+
+template <class K>
+static void set_smem(K kernel, size_t smem, size_t* configured) {
+  int dev = 0;
+  MS_CUDA(cudaGetDevice(&dev));
+  if (dev >= 64 || smem > configured[dev]) {
+    MS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (dev < 64) configured[dev] = smem;
+  }
+}
+
+static const L1Maps& no_maps() {
+  static L1Maps m{};
+  return m;
+}
+
+template <int T, int NR, bool PAD>
 static void solve_twist_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                           const double* Lr, const double* Sinv, const double* r, double* ybuf, const int* done,
-                          cudaStream_t st) {
-  const size_t smem = ring_smem_bytes(max_bw) + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double);
+                          cudaStream_t st, const L1Maps& maps) {
+  const int sw = ring_stage_words_t<T>(max_bw, PAD);
+  const size_t smem = ring_bytes(sw, PAD) + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double);
   static size_t configured[64] = {};
-  int dev = 0;
-  MS_CUDA(cudaGetDevice(&dev));
-  if (dev >= 64 || smem > configured[dev]) {
-    MS_CUDA(cudaFuncSetAttribute(k_l1_solve_twist<T, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    if (dev < 64) configured[dev] = smem;
-  }
-  { k_l1_solve_twist<T, NR><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
-      g, sys, nsys, Lc, Lr, Sinv, r, ybuf, done, ring_stage_words(max_bw), max_bw); ms_count_launch(); }
+  set_smem(k_l1_solve_twist<T, NR, PAD>, smem, configured);
+  { k_l1_solve_twist<T, NR, PAD><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, Sinv, r, ybuf, done, sw, max_bw, maps.c, maps.r); ms_count_launch(); }
 }
 
-template <int T, int NR>
+template <int T, int NR, bool PAD>
 static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                          const double* Lr, const double* r, double* ybuf, const int* done,
-                         cudaStream_t st) {
+                         cudaStream_t st, const L1Maps& maps) {
+  const int sw = ring_stage_words_t<T>(max_bw, PAD);
   // + the dot sweep's x windows (one factor copy)
-  const size_t smem = ring_smem_bytes(max_bw) + (Lr ? 0 : (size_t)kTmaWarps * 128 * NR * sizeof(double));
+  const size_t smem = ring_bytes(sw, PAD) + (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));
   static size_t configured[64] = {};  // per instantiation and device
-  int dev = 0;
-  MS_CUDA(cudaGetDevice(&dev));
-  if (dev >= 64 || smem > configured[dev]) {
-    MS_CUDA(cudaFuncSetAttribute(k_l1_solve_ring<T, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    if (dev < 64) configured[dev] = smem;
+  set_smem(k_l1_solve_ring<T, NR, PAD>, smem, configured);
+  { k_l1_solve_ring<T, NR, PAD><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, r, ybuf, done, sw, maps.c, maps.r); ms_count_launch(); }
+}
+
+// Padded TMA-tensor ring for the elasticity bands on request (MS_L1_PAD=1):
+// leaner steps (unconditional loads at immediate offsets) pay off only in the
+// latency-bound regime (config 2: level 1 0.327 -> 0.306 ms plain, 0.206 ->
+// 0.197 ms twisted, 3 stages); bandwidth-bound it is slower (config 3: 1.99
+// -> 2.33 ms: 73% more shared-memory traffic per band column)
+bool l1_padded_ring_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_L1_PAD");
+    v = (e && std::string(e) == "1") ? 1 : 0;
   }
-  { k_l1_solve_ring<T, NR><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
-      g, sys, nsys, Lc, Lr, r, ybuf, done, ring_stage_words(max_bw)); ms_count_launch(); }
+  return v == 1;
 }
 
 static bool use_ring_sweeps() {
@@ -748,18 +916,46 @@ static bool use_ring_sweeps() {
 }
 
 bool ring_sweep_ok(int T, int min_bw) { return T <= 1 || min_bw > 32 * (T - 1); }
+
+void make_band_map(CUtensorMap* map, const double* band, int64_t cols, int S, int T) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    MS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw Error(-1, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)cols};
+  const cuuint64_t strides[1] = {(cuuint64_t)S * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)(32 * (T + 1)), (cuuint32_t)kCh};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(band), dims, strides, box,
+                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(-1, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
 bool l1_ring_sweeps_enabled() { return use_ring_sweeps(); }
 
 template <int T, int NR>
 static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                     const double* Lr, const double* r, double* ybuf, const int* done, cudaStream_t st,
-                    const double* Sinv, bool ring_ok) {
+                    const double* Sinv, bool ring_ok, const L1Maps* maps) {
+  // padded TMA ring: elasticity bands with their tensor maps (uniform bw)
+  const bool pad = NR == 1 && maps && maps->valid;
+  const L1Maps& mp = pad ? *maps : no_maps();
   if (Sinv) {
-    solve_twist_t<T, NR>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st);
+    if (pad)
+      solve_twist_t<T, NR, NR == 1>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
+    else
+      solve_twist_t<T, NR, false>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
     return;
   }
   if (use_ring_sweeps() && ring_ok) {
-    solve_ring_t<T, NR>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st);
+    if (pad)
+      solve_ring_t<T, NR, NR == 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
+    else
+      solve_ring_t<T, NR, false>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
     return;
   }
   if (!Lr) throw Error(-1, "the register-prefetch level-1 sweeps need the row band (two factor copies)");
@@ -769,7 +965,7 @@ static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, con
 
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
-                     const int* done, cudaStream_t st, const double* Sinv, int min_bw) {
+                     const int* done, cudaStream_t st, const double* Sinv, int min_bw, const L1Maps* maps) {
   if (nsys == 0) return;
   const int T = std::max(1, div_up(max_bw, 32));
   if (min_bw < 0) min_bw = max_bw;
@@ -778,22 +974,22 @@ void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, in
   if (Sinv && !ring_ok) throw Error(-1, "twisted level-1 needs every band wider than 32 (T - 1)");
   if (nrhs == 1) {
     switch (T) {
-      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
       default: throw Error(-1, "level-1 band wider than 256 unsupported");
     }
   } else if (nrhs == 2) {
     switch (T) {
-      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
-      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok); break;
+      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
       default: throw Error(-1, "heat level-1 band wider than 128 unsupported");
     }
   } else {

@@ -1,6 +1,8 @@
 // Batched banded SPD machinery: band assembly, Cholesky, sweeps.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "operator.cuh"
 
@@ -93,16 +95,30 @@ void launch_schur_inverse(const BandSys* sys, int nsys, int max_bw, const double
 // layout vector; the local solutions land in ybuf[yoff ...], node-interleaved
 // (2 ln + c).  nrhs = 2: scalar systems applied to the x and y components in
 // one sweep (the factor is read once for both).
+// 2-D TMA descriptors of the column / row bands viewed as [columns][S]
+// (every system with the same S, starting at a whole column): the padded
+// level-1 ring loads 8-column boxes of P = 32 (T+1) words per column, the
+// words past S zero-filled by the TMA (out of bounds in the inner dimension).
+struct L1Maps {
+  CUtensorMap c, r;
+  bool valid = false;
+};
+// encodes a [cols][S] fp64 band at `band` (16-byte aligned, S even); T = ceil(bw / 32)
+void make_band_map(CUtensorMap* map, const double* band, int64_t cols, int S, int T);
+
 // Lr == nullptr: one factor copy, the backward sweep by dot products over the
-// column band (half the factor bytes).
+// column band (half the factor bytes).  maps (valid): the padded TMA ring
+// (uniform bw, elasticity bands).
 // Sinv != nullptr: twisted systems (BandSys.m > 0).  min_bw: narrowest band
 // among the systems (the shared-memory ring sweep needs min_bw > 32 (T - 1),
 // T = ceil(max_bw / 32); narrower mixes take the register-prefetch sweep).
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
-                     const int* done, cudaStream_t st, const double* Sinv = nullptr, int min_bw = -1);
+                     const int* done, cudaStream_t st, const double* Sinv = nullptr, int min_bw = -1,
+                     const L1Maps* maps = nullptr);
 bool ring_sweep_ok(int T, int min_bw);
 bool l1_ring_sweeps_enabled();  // false under MS_L1_SWEEP=reg
+bool l1_padded_ring_enabled();  // false under MS_L1_PAD=0
 
 // ---------------------------------------------------------------------------
 // One warp's banded sweep over a factor read from global memory (L2/L1),

@@ -416,6 +416,8 @@ struct ms_precond {
   DBuf<double> Sinv;   // twisted level 1: separator Schur inverses (empty: plain sweeps)
   bool twisted = false;
   bool one_copy = false;  // plain banded level 1 with the column band only (dot-form backward sweep)
+  bool pad = false;       // padded TMA ring (uniform bw), maps below
+  L1Maps maps;
   bool dense = false;  // MS_LOCAL_DENSE_INV: packed explicit inverses in Xinv
   int nrhs = 1;        // 2: heat level-1 (scalar factor applied to both blocks)
   int dense_nt = 0;
@@ -744,7 +746,7 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
       launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
     else
       launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st,
-                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw);
+                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps);
     pf.end(MS_PROF_LEVEL1, it, st, a);
     if (dist) exchange_ybuf(pc);
   }
@@ -1118,22 +1120,32 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       P->b_hi = P->rank_hi[R];
       pc->halo_rows = std::max(1, o->delta);
     }
-    int64_t foff = 0, yoff = 0;
     for (int J = 0; J < pc->NbY; ++J)
       for (int I = 0; I < pc->NbX; ++I) {
         BandSys s{};
         if (xhi[I] < xlo[I] || yhi[J] < ylo[J]) throw Error(MS_E_INVALID, "empty level-1 subdomain");
         band_setup(s, xlo[I], xhi[I], ylo[J], yhi[J], heat_l1 ? 1 : 2);
         if (heat_l1) s.nrhs = 2;
-        const int sid = J * pc->NbX + I;
-        s.foff = foff;  // factors stored for owned subdomains only
-        s.yoff = yoff;
-        // even offsets: the ring sweeps bulk-copy 16-byte aligned chunks
-        if (sid >= pc->s0 && sid < pc->s1) foff += ((int64_t)s.n * (s.bw + 1) + 1) & ~(int64_t)1;
-        yoff += (int64_t)s.n * s.nrhs;
         pc->max_bw = std::max(pc->max_bw, s.bw);
         pc->hsys.push_back(s);
       }
+    // Padded TMA ring for the elasticity bands (banded local solver, ring
+    // sweeps): every system stored with the widest bandwidth so that all
+    // columns share one stride S and the bands form one [columns][S] tensor
+    // (boundary blocks are at most 2 band words narrower: zeros)
+    pc->pad = !heat_l1 && o->local_solver == MS_LOCAL_BANDED && l1_ring_sweeps_enabled() &&
+              l1_padded_ring_enabled() && pc->max_bw <= 8 * 32 - 1;
+    if (pc->pad)
+      for (BandSys& s : pc->hsys) s.bw = pc->max_bw;
+    int64_t foff = 0, yoff = 0;
+    for (int sid = 0; sid < (int)pc->hsys.size(); ++sid) {
+      BandSys& s = pc->hsys[sid];
+      s.foff = foff;  // factors stored for owned subdomains only
+      s.yoff = yoff;
+      // even offsets: the ring sweeps bulk-copy 16-byte aligned chunks
+      if (sid >= pc->s0 && sid < pc->s1) foff += ((int64_t)s.n * (s.bw + 1) + 1) & ~(int64_t)1;
+      yoff += (int64_t)s.n * s.nrhs;
+    }
     std::vector<int> xcov((g.nx + 1) * 4, -1), ycov((g.ny + 1) * 4, -1);
     auto cover = [](const std::vector<int>& lo, const std::vector<int>& hi, int nn, std::vector<int>& cov) {
       for (int a = 0; a < nn; ++a) {
@@ -1293,6 +1305,13 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     }
     pc->l1 = L1Dev{pc->NbX, pc->NbY, pc->xlo_d.p, pc->xlen_d.p, pc->ylo_d.p, pc->ylen_d.p,
                    pc->yoff_d.p, pc->xcov.p, pc->ycov.p, pc->ybuf.p};
+    if (pc->pad && !pc->dense) {
+      const int S = pc->max_bw + 1, T = std::max(1, div_up(pc->max_bw, 32));
+      const int64_t cols = foff / S;
+      make_band_map(&pc->maps.c, pc->Lc.p, cols, S, T);
+      if (pc->Lr.p) make_band_map(&pc->maps.r, pc->Lr.p, cols, S, T);
+      pc->maps.valid = true;
+    }
     pc->info.n_subdomains = pc->nsys;
     pc->info.level1_twisted = pc->twisted ? 1 : 0;
     pc->info.n_subdomains_local = pc->s1 - pc->s0;
@@ -1673,7 +1692,7 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
                               nullptr, st);
       else
         launch_l1_solve(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r,
-                        pc->ybuf.p, nullptr, st, pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw);
+                        pc->ybuf.p, nullptr, st, pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps);
     });
   if (pc->has_coarse) {
     ms[MS_BENCH_RESTRICT] = timeit([&] {

@@ -507,13 +507,16 @@ def adapter_case(spec, fname, tol=1e-8, maxit=5000, tag="EH+Rot", procs=None, sa
     band = jitter_band(op, b, variant, level1, cop, variant.level1 != "heat", tol, maxit, procs, x, heat)
     names = sorted(band)
     true_res = np.linalg.norm(b - op.matrix @ x) / np.linalg.norm(b)
-    save(fname, E=spec.E, constrained_dofs=spec.constrained_dofs,
-         heat_dirichlet_nodes=spec.heat_dirichlet_nodes, load_full=spec.load_full,
+    big = {}
+    if spec.nx < 512:  # full-size fixtures: E / load regenerate from configs, no K0 or apply pair
+        big = dict(E=spec.E, load_full=spec.load_full, K0=cop.K0 if cop.dim <= 4096 else np.zeros((0, 0)),
+                   apply_r=r, apply_z=z)
+    save(fname, constrained_dofs=spec.constrained_dofs,
+         heat_dirichlet_nodes=spec.heat_dirichlet_nodes,
          nx=spec.nx, ny=spec.ny, H=spec.H, delta=spec.delta, nu=spec.nu, tol=tol, maxit=maxit,
          iters=rep.iterations, converged=rep.converged, x=x, residuals=np.array(rep.residuals),
          cond=rep.cond_estimate, true_residual=true_res,
-         coarse_dim=basis.N_c, mode_counts=np.array(modes), eigenvalues=lam,
-         K0=cop.K0 if cop.dim <= 4096 else np.zeros((0, 0)), apply_r=r, apply_z=z,
+         coarse_dim=basis.N_c, mode_counts=np.array(modes), eigenvalues=lam, **big,
          jitter_names=np.array(names),
          jitter_iters=np.array([band[k][0] for k in names]),
          jitter_x=np.array([band[k][1] for k in names]),

@@ -232,3 +232,64 @@ def test_callback_communicator_two_rank_selftest():
         assert p.exitcode == 0
     for r in (0, 1):
         assert res[r] == [3.0, 4.0, 7.0, float(1 - r)]
+
+
+def _strip_worker(rank, world, port, q, n, maxit):
+    sys.path.insert(0, str(ROOT))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    _init(rank, world, port)
+    try:
+        from paper_2006_13387_b200 import configs, dist as D, pcg_solve
+        from paper_2006_13387_b200.solve import setup_spec
+
+        D.init_host_callbacks(0)
+        spec = configs.config3(seed=0, n=n)
+        mesh, op, pre = setup_spec(spec, "EH+Rot")
+        x, rep = pcg_solve(op, spec.rhs(), pre, tol=1e-12, maxit=maxit)
+        z = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
+        q.put((rank, x, rep.iterations, pre.coarse_dim, list(pre.mode_counts), z,
+               pre.info["n_subdomains_local"], rep.residuals))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [4, 8])
+def test_strip_ranks_on_one_gpu_match_single_rank(world):
+    """Config 3's recipe at 256^2 (8 x 8 subdomain rows) sharded into 4 and 8
+    strips, the ranks' kernels on the one B200 and their collectives through
+    gloo host callbacks: same coarse space on every rank, the subdomain rows
+    partitioned, and the same preconditioner and PCG iterates as one rank
+    (only the summation order of dot products and of the sharded coarse
+    solve differ)."""
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    n, maxit = 256, 40
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q, n, maxit)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((v[0], v[1:]) for v in (q.get(timeout=900) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    sys.path.insert(0, str(ROOT))
+    from paper_2006_13387_b200 import configs, pcg_solve
+    from paper_2006_13387_b200.solve import setup_spec
+
+    spec = configs.config3(seed=0, n=n)
+    mesh, op, pre = setup_spec(spec, "EH+Rot")
+    x1, rep1 = pcg_solve(op, spec.rhs(), pre, tol=1e-12, maxit=maxit)
+    z1 = pre.apply(np.linspace(-1.0, 1.0, op.n_free))
+    owned = [res[r][5] for r in range(world)]
+    assert sum(owned) == pre.info["n_subdomains"] and max(owned) - min(owned) <= spec.Nx
+    for r in range(world):
+        x, iters, nc, modes, z, _, resid = res[r]
+        assert nc == pre.coarse_dim and modes == list(pre.mode_counts)
+        assert iters == rep1.iterations == maxit
+        assert np.linalg.norm(z - z1) <= 1e-12 * np.linalg.norm(z1)
+        assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
+        assert np.allclose(resid, rep1.residuals, rtol=1e-9)
+        assert np.array_equal(x, res[0][0])

@@ -209,3 +209,40 @@ def test_fullsize_mode_counts_every_neighbourhood(case):
     assert np.all(err[sel] <= 1e-9 * np.abs(w[sel]) + floor), case
     del pre, op
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("coarse_solve", ["inverse", "cholesky"])
+@pytest.mark.parametrize("eta", ["100", "10000", "1e+06"])
+def test_fullsize_config2_solve_against_reference(eta, coarse_solve):
+    """BASELINE config 2 at its full 512^2 size (525,312 dofs): the reference's
+    own converged solve of each contrast (make_golden.py cfg2full, with its
+    18-perturbation round-off band) against the GPU solve -- N_c and every
+    centre's mode count exact, iterations in the band (+-1; 4 s.d. for the
+    explicit-inverse coarse solve), solution within max(1e-8, 2x the
+    reference's own spread), true residual no worse than the reference's."""
+    from pathlib import Path
+
+    name = f"ref_config2_n512_eta{eta}.npz"
+    if not (Path(__file__).parent / "golden" / name).exists():
+        pytest.skip(f"{name} not generated")
+    from conftest import load_golden
+
+    g = load_golden(name)
+    spec = configs.config2(seed=0, eta=float(eta))
+    assert spec.free_dofs().size == int(g["n_free"])
+    mesh, op, pre = setup_spec(spec, coarse_solve=coarse_solve)
+    assert pre.coarse_dim == int(g["coarse_dim"])
+    assert np.array_equal(np.array(pre.mode_counts), g["mode_counts"])
+    b = spec.rhs()
+    x, rep = G.pcg_solve(op, b, pre, tol=float(g["tol"]), maxit=int(g["maxit"]))
+    its = np.concatenate([[int(g["iters"])], g["jitter_iters"]])
+    assert rep.converged
+    if coarse_solve == "cholesky":
+        assert its.min() - 1 <= rep.iterations <= its.max() + 1, (rep.iterations, its.min(), its.max())
+    else:
+        mu, sd = its.mean(), its.std(ddof=1)
+        assert abs(rep.iterations - mu) <= 4 * sd + 1, (rep.iterations, mu, sd)
+    assert rel(x, g["x"]) <= max(1e-8, 2 * float(g["jitter_x"].max())), rel(x, g["x"])
+    r_true = np.linalg.norm(b - op @ x) / np.linalg.norm(b)
+    ref_true = max(float(g["true_residual"]), float(g["jitter_true_residual"].max()))
+    assert r_true <= 2 * ref_true, (r_true, ref_true)
