@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--eta", type=float, default=None, help="contrast for config 2 (1e2, 1e4, 1e6 or 1e8; default 1e6)")
     ap.add_argument("--n", "--mesh-n", dest="n", type=int, default=None, help="override the mesh size (nx; ny = nx/2 for config 4)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ny", type=int, default=None,
+                    help="config 3: an n x ny strip of the recipe (2048 x 256 = one GPU's share of 8)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-n", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=40)
@@ -149,12 +151,12 @@ def make_spec(args):
         return configs.config1(seed=args.seed)
     if args.config == 2:
         return configs.config2(seed=args.seed, eta=args.eta or 1e6, n=args.n or 512)
-    return configs.config3(seed=args.seed, n=args.n or 2048)
+    return configs.config3(seed=args.seed, n=args.n or 2048, ny=args.ny)
 
 
 def workload_name(args, spec):
     return {
-        3: (f"config3: {spec.nx}^2 Q1 plane stress, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
+        3: (f"config3: {spec.nx}x{spec.ny} Q1 plane stress, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
             f"filtered-noise tanh density 40%, SIMP p=3, eta=1e6, cantilever, {args.variant}, rtol 1e-8"),
         4: (f"config4: {spec.nx}x{spec.ny} Q1 MBB beam, {spec.Nx}x{spec.Ny} subdomains of 32^2, overlap 2, "
             f"filtered-noise tanh density 50%, SIMP p=3, eta=1e9, {args.variant}, rtol 1e-8"),

@@ -236,12 +236,15 @@ def config2(seed=0, eta=1e6, n=512, H=32, delta=2):
                  cantilever_bcs(n, n), H, delta, eta=eta)
 
 
-def config3(seed=0, n=2048, H=32, delta=2, eta=1e6, volume=0.4):
-    """2048^2 filtered-noise tanh-projected density at 40% volume, eta 1e6."""
+def config3(seed=0, n=2048, H=32, delta=2, eta=1e6, volume=0.4, ny=None):
+    """2048^2 filtered-noise tanh-projected density at 40% volume, eta 1e6.
+    ny < n gives an n x ny strip of the same recipe (e.g. 2048 x 256: the
+    512 subdomains one GPU owns when config 3 is split over 8)."""
+    ny = ny or n
     rng = np.random.default_rng([3, seed])
-    rho = filtered_noise_density(rng, n, n, volume)
-    return _spec(f"config3[n={n},seed={seed}]", n, n, rho.reshape(n, n), 1.0 / eta,
-                 cantilever_bcs(n, n), H, delta, eta=eta)
+    rho = filtered_noise_density(rng, n, ny, volume)
+    name = f"config3[n={n},seed={seed}]" if ny == n else f"config3[{n}x{ny},seed={seed}]"
+    return _spec(name, n, ny, rho.reshape(ny, n), 1.0 / eta, cantilever_bcs(n, ny), H, delta, eta=eta)
 
 
 def config4(seed=0, nx=4096, ny=2048, H=32, delta=2, eta=1e9, volume=0.5):
