@@ -834,6 +834,16 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     for (int c = 0; c < NR; ++c) y[(int64_t)(m + j) * NR + c] = acc[c];
   }
   pair_sync(pair);
+  if (!Lr) {  // one factor copy: both backward sweeps by dot products over the column bands
+    double* xw = smem_ring + ring_words + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw + (size_t)warp * 256 * NR;
+    if (role == 0)
+      band_sweep_dot<T, NR, PAD>(Lc + s.foff, nT, bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
+                                 &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
+    else  // bottom-local row k = natural n - 1 - k (its separator rows now hold x_S)
+      band_sweep_dot<T, NR, PAD>(Lc + s.foffB, nB, bw, [&](int k) { return y + (int64_t)(n - 1 - k) * NR; }, lane,
+                                 rg, xw, &mapc, PAD ? (int)(s.foffB / (bw + 1)) : 0);
+    return;
+  }
   if (role == 0) {
     band_sweep_ring<T, NR, true, PAD>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; },
                                       lane, rg, &mapr, PAD ? (int)(s.foff / (bw + 1)) : 0);
@@ -872,7 +882,8 @@ static void solve_twist_t(const Grid& g, const BandSys* sys, int nsys, int max_b
                           const double* Lr, const double* Sinv, const double* r, double* ybuf, const int* done,
                           cudaStream_t st, const L1Maps& maps) {
   const int sw = ring_stage_words_t<T>(max_bw, PAD);
-  const size_t smem = ring_bytes(sw, PAD) + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double);
+  const size_t smem = ring_bytes(sw, PAD) + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double) +
+                      (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));  // dot-sweep windows
   static size_t configured[64] = {};
   set_smem(k_l1_solve_twist<T, NR, PAD>, smem, configured);
   { k_l1_solve_twist<T, NR, PAD><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(

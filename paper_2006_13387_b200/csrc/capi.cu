@@ -1207,6 +1207,15 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     }
     pc->dense = o->local_solver == MS_LOCAL_DENSE_INV;
     pc->nrhs = heat_l1 ? 2 : 1;
+    // one factor copy (column band, dot-form backward sweeps) on request
+    // (MS_L1_COPIES=1): half the factor bytes, but the backward sweep is
+    // issue-bound (config 3: level 1 2.12 ms vs 1.94 ms with both bands)
+    {
+      int copies_env = 2;
+      if (const char* e = getenv("MS_L1_COPIES")) copies_env = std::atoi(e);
+      pc->one_copy = !pc->dense && copies_env == 1 && l1_ring_sweeps_enabled() &&
+                     ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
+    }
     if (pc->twisted) {
       // natural bands (assembly) -> top / bottom bands -> partial Cholesky of
       // both halves -> explicit inverse of the separator's Schur complement
@@ -1217,16 +1226,21 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       }
       DBuf<BandSys> nat_d, half_d;
       nat_d.upload(nat.data(), nat.size(), st);
-      pc->Lr.alloc(foff + 2);  // holds the natural bands first (fn <= foff)
+      DBuf<double> natband;  // natural bands (fn <= foff words)
+      natband.alloc(fn + 2);
       if (heat_l1) {
         HeatParam hp{};
         heat_elements(g.h, hp);
-        launch_l1_heat_assemble(g, hp.lap, P->E.p, P->mask.p, nat_d.p, ns, pc->Lr.p, st);
+        launch_l1_heat_assemble(g, hp.lap, P->E.p, P->mask.p, nat_d.p, ns, natband.p, st);
       } else {
-        launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, nat_d.p, ns, pc->Lr.p, st);
+        launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, nat_d.p, ns, natband.p, st);
       }
-      launch_twist_split(nat_d.p, pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lr.p, pc->Lc.p, st);
-      pc->Lr.zero(st);
+      launch_twist_split(nat_d.p, pc->sys.p + pc->s0, ns, pc->max_bw, natband.p, pc->Lc.p, st);
+      natband.release();
+      if (!pc->one_copy) {
+        pc->Lr.alloc(foff + 2);
+        pc->Lr.zero(st);
+      }
       std::vector<BandSys> halves(2 * (size_t)ns);
       const int64_t mb2 = (int64_t)pc->max_bw * pc->max_bw;
       for (int i = 0; i < ns; ++i) {
@@ -1258,13 +1272,6 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       } else {
         launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
       }
-      // one factor copy (column band, dot-form backward sweep) on request
-      // (MS_L1_COPIES=1): half the factor bytes, but the backward sweep is
-      // issue-bound (config 3: level 1 2.48 ms vs 1.97 ms with both bands)
-      int copies_env = 2;
-      if (const char* e = getenv("MS_L1_COPIES")) copies_env = std::atoi(e);
-      pc->one_copy = copies_env == 1 && l1_ring_sweeps_enabled() &&
-                     ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
       if (!pc->one_copy) {
         pc->Lr.alloc(foff + 2);
         pc->Lr.zero(st);

@@ -578,14 +578,16 @@ def test_twisted_level1_matches_plain_sweeps(tag, rng, monkeypatch):
     assert v @ pre.apply(w) == pytest.approx(w @ pre.apply(v), rel=1e-9)
 
 
+@pytest.mark.parametrize("twist", ["0", "1"])
 @pytest.mark.parametrize("tag", ["EH+Rot", "HH+Rot"])
-def test_one_copy_level1_matches_two_copy(tag, rng, monkeypatch):
+def test_one_copy_level1_matches_two_copy(tag, twist, rng, monkeypatch):
     """One factor copy (backward sweep by dot products over the column band)
-    against the column + row band sweeps: same local solves to round-off."""
+    against the column + row band sweeps, plain and twisted: same local
+    solves to round-off."""
     from paper_2006_13387_b200.solve import setup_spec
 
     spec = configs.config1(seed=0, n=64, H=16, delta=2)
-    monkeypatch.setenv("MS_L1_TWIST", "0")
+    monkeypatch.setenv("MS_L1_TWIST", twist)
     out = {}
     for copies in ("2", "1"):
         monkeypatch.setenv("MS_L1_COPIES", copies)
