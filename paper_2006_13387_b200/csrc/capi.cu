@@ -1895,7 +1895,10 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   const int iters = hs.iter;
   if (residuals) MS_CUDA(cudaMemcpy(residuals, P->hres.p, (iters + 1) * sizeof(double), cudaMemcpyDefault));
   if (alphas && iters > 0) MS_CUDA(cudaMemcpy(alphas, P->halpha.p, iters * sizeof(double), cudaMemcpyDefault));
-  if (betas && iters > 1) MS_CUDA(cudaMemcpy(betas, P->hbeta.p, (iters - 1) * sizeof(double), cudaMemcpyDefault));
+  // the reference records beta after every non-final iteration: k - 1 on
+  // convergence, k when maxit stops an unconverged solve (krylov.py:123-127)
+  const int nbeta = hs.converged ? iters - 1 : iters;
+  if (betas && nbeta > 0) MS_CUDA(cudaMemcpy(betas, P->hbeta.p, nbeta * sizeof(double), cudaMemcpyDefault));
   if (rep) {
     // counted at every launch site (graph replays add their kernel nodes);
     // includes the no-op kernels of a chunk's iterations past convergence

@@ -21,6 +21,7 @@ struct PcgScalars {
   int converged;
   int first;       // next z.r reduction starts the recurrence (beta = 0)
   int dist;        // multi-rank: reductions leave partials in part[], finalised after allreduce
+  int stop_after_beta;  // maxit reached unconverged: finish this iteration's z and beta, then stop
   double part[4];  // per-rank partial sums: [PART_PQ], [PART_RR], [PART_RZ]
   unsigned int tickets[8];
 };
@@ -44,7 +45,9 @@ __device__ __forceinline__ void fin_res(PcgScalars* sc, double rr, double* res_h
     sc->converged = 1;
     sc->done = 1;
   } else if (sc->iter >= sc->maxit) {
-    sc->done = 1;
+    // the reference still forms z = M r and beta of the last iteration
+    // before leaving the loop (krylov.py:123-127): stop after the beta
+    sc->stop_after_beta = 1;
   }
 }
 __device__ __forceinline__ void fin_beta(PcgScalars* sc, double rz, double* beta_hist) {
@@ -56,6 +59,7 @@ __device__ __forceinline__ void fin_beta(PcgScalars* sc, double rz, double* beta
     if (beta_hist) beta_hist[sc->iter - 1] = sc->beta;
   }
   sc->rz = rz;
+  if (sc->stop_after_beta) sc->done = 1;
 }
 
 // multi-rank: finalize one allreduced partial (kind = PART_*)

@@ -104,6 +104,8 @@ def test_maxit_reports_unconverged(rng):
     _, _, op = gpu_problem(nx, nx, E, 0.3, op_o.free_dofs)
     _, rep = G.pcg_solve(op, rng.standard_normal(op_o.n_free), None, tol=1e-14, maxit=3)
     assert not rep.converged and rep.iterations == 3
+    # the reference records a beta after every unconverged iteration (krylov.py:123-127)
+    assert len(rep.alphas) == 3 and len(rep.betas) == 3 and np.all(np.isfinite(rep.betas))
 
 
 def test_zero_rhs_and_bad_tolerance():
