@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_ring(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                     const double* __restrict__ Lr, const double* __restrict__ r,
                     double* __restrict__ ybuf, const int* done, int stage_words,
-                    const __grid_constant__ CUtensorMap mapc, const __grid_constant__ CUtensorMap mapr) {
+                    const __grid_constant__ CUtensorMap mapc, const __grid_constant__ CUtensorMap mapr,
+                    int fwd_only) {
   if (done && *(volatile const int*)done) return;
   extern __shared__ __align__(128) double smem_ring[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -746,6 +747,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   const int col0 = PAD ? (int)(s.foff / (s.bw + 1)) : 0;  // the system's first column in the TMA view
   band_sweep_ring<T, NR, false, PAD>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
                                      &mapc, col0);
+  if (fwd_only) return;  // the backward sweep follows in k_l1_bwd_window
   __syncwarp();
   if (Lr) {
     band_sweep_ring<T, NR, true, PAD>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; },
@@ -853,6 +855,147 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-copy backward sweep in axpy form from the COLUMN band: x = L^-T w.
+// Pivot k (descending) updates the rows k - j with L[k][k-j] = col_{k-j}[j],
+// so every lane reads its own row's column at band offset j = 32 s + lane - u
+// (consecutive lanes: stride S - 1 words, no bank conflicts), and the columns
+// of the last bw + 1 pivots must stay in shared memory: one warp per CTA
+// streams its band through a deep ring of kWCh-column chunks; a chunk is
+// refilled right after its own pivots (its columns' last use), the chunks a
+// pivot reaches down to are waited for before its chunk starts.  The forward
+// sweep ran before in k_l1_solve_ring (fwd_only).  Half the factor bytes of
+// the two-band sweeps; the deep ring caps residency at 4 warps per SM.
+constexpr int kWCh = 4;
+static bool use_window_bwd();
+
+__host__ __device__ inline int win_stages(int bw) { return (bw + 3 + 12 + kWCh - 1) / kWCh + 1; }  // + ~12 rows of prefetch
+__host__ __device__ inline int win_stage_words(int bw) { return (kWCh * (bw + 1) + 3) & ~1; }
+__host__ __device__ inline int win_header_words(int nst) { return (nst + 15) & ~15; }
+
+template <int T>
+__global__ void __launch_bounds__(32, 4)
+    k_l1_bwd_window(const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
+                    double* __restrict__ ybuf, const int* done, int nst, int stage_words) {
+  if (done && *(volatile const int*)done) return;
+  extern __shared__ __align__(128) double smw[];
+  const int lane = threadIdx.x;
+  const int sid = blockIdx.x;
+  if (sid >= nsys) return;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smw);
+  double* buf = smw + win_header_words(nst);
+  const BandSys s = sys[sid];
+  const int n = s.n, bw = s.bw, S = bw + 1;
+  const double* L = Lc + s.foff;
+  double* y = ybuf + s.yoff;
+  const int nch = (n + kWCh - 1) / kWCh;
+  // REV chunk c: columns [start, start + cnt), the highest first
+  auto chunk = [&](int c, int& start, int& cnt) {
+    const int k0 = c * kWCh;
+    cnt = min(kWCh, n - k0);
+    start = n - k0 - cnt;
+  };
+  auto issue = [&](int c) {
+    int start, cnt;
+    chunk(c, start, cnt);
+    const int64_t w0 = (int64_t)start * S;
+    const int64_t a = w0 & ~(int64_t)1;
+    const uint32_t words = (uint32_t)((cnt * S + (int)(w0 - a) + 1) & ~1);
+    const int st = c % nst;
+    mbar_expect_tx(bar + st, words * 8u);
+    bulk_g2s(buf + (size_t)st * stage_words, L + a, words * 8u, bar + st);
+  };
+  // shared address of column `col` (its chunk is resident)
+  auto colp = [&](int col) -> const double* {
+    const int c = (n - 1 - col) / kWCh;
+    int start, cnt;
+    chunk(c, start, cnt);
+    return buf + (size_t)(c % nst) * stage_words + (int)(((int64_t)start * S) & 1) + (col - start) * S;
+  };
+  if (lane == 0) {
+    for (int st = 0; st < nst; ++st) mbar_init(bar + st, 1);
+    mbar_fence_init();
+    for (int c = 0; c < min(nst, nch); ++c) issue(c);
+  }
+  __syncwarp();
+  uint64_t phase = 0;
+  int waited = 0;
+  const int ahead = (bw + kWCh - 1) / kWCh + 1;  // chunks below a pivot chunk its updates reach
+  constexpr int R = T + 1;
+  // REV numbering: sweep row r = natural row n - 1 - r
+  auto yat = [&](int r) -> double* { return y + (n - 1 - r); };
+  double acc[R], rnext;
+#pragma unroll
+  for (int sl = 0; sl < R - 1; ++sl) {
+    const int r = 32 * sl + lane;
+    acc[sl] = r < n ? *yat(r) : 0.0;
+  }
+  acc[R - 1] = 0.0;
+  rnext = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane) : 0.0;
+  for (int r0 = 0; r0 < n; r0 += 32) {
+    acc[R - 1] = rnext;
+    {
+      const int r = r0 + 32 * R + lane;
+      rnext = r < n ? *yat(r) : 0.0;
+    }
+    // this lane's rows in the block's slots and their columns' bases:
+    // coefficient of pivot u for slot sl = col_{row}[32 sl + lane - u]
+    const double* base[R];
+    bool rowok[R];
+    double dsave = 0.0;
+#pragma unroll 1
+    for (int h = 0; h < 32 && r0 + h < n; h += kWCh) {
+      const int ch = (r0 + h) / kWCh;
+      const int need = min(ch + ahead, nch - 1);
+      while (waited <= need) {
+        const int st = waited % nst;
+        mbar_wait(bar + st, (uint32_t)((phase >> st) & 1u));
+        phase ^= 1ull << st;
+        ++waited;
+      }
+      if (h == 0) {  // slot bases once per block (their chunks are resident now)
+#pragma unroll
+        for (int sl = 0; sl < R; ++sl) {
+          const int col = n - 1 - (r0 + 32 * sl + lane);
+          rowok[sl] = col >= 0 && col < n;
+          base[sl] = (rowok[sl] ? colp(col) : buf) + 32 * sl + lane;
+        }
+      }
+      int start, cnt;
+      chunk(ch, start, cnt);
+      const double* pcol = colp(start + cnt - 1);  // pivot columns: pcol - q S
+      auto step = [&](int q) {
+        const int u = h + q;
+        double m[R];
+#pragma unroll
+        for (int sl = 0; sl < R; ++sl) {
+          const int j = 32 * sl + lane - u;
+          m[sl] = lds_or_zero(base[sl] - u, rowok[sl] && j >= 1 && j <= bw);
+        }
+        const double d = lds_or_zero(pcol - q * S, true);
+        if (lane == u) dsave = d;
+        const double wk = __shfl_sync(0xffffffffu, acc[0] * d, u);
+#pragma unroll
+        for (int sl = 0; sl < R; ++sl) acc[sl] = fma(-m[sl], wk, acc[sl]);
+      };
+      if (cnt == kWCh) {
+#pragma unroll
+        for (int q = 0; q < kWCh; ++q) step(q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kWCh; ++q)
+          if (q < cnt) step(q);
+      }
+      __syncwarp();  // chunk ch's pivots are done: its columns are dead
+      if (lane == 0 && ch + nst < nch) issue(ch + nst);
+    }
+    if (r0 + lane < n) *yat(r0 + lane) = acc[0] * dsave;
+#pragma unroll
+    for (int sl = 0; sl < R - 1; ++sl) acc[sl] = acc[sl + 1];
+    acc[R - 1] = 0.0;
+  }
+}
+
 // ring shared memory of a launch: header + per-warp rings (+ extras)
 template <int T>
 static int ring_stage_words_t(int max_bw, bool pad) {
@@ -899,8 +1042,16 @@ static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw
   const size_t smem = ring_bytes(sw, PAD) + (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));
   static size_t configured[64] = {};  // per instantiation and device
   set_smem(k_l1_solve_ring<T, NR, PAD>, smem, configured);
+  const bool window = !Lr && NR == 1 && use_window_bwd();
   { k_l1_solve_ring<T, NR, PAD><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
-      g, sys, nsys, Lc, Lr, r, ybuf, done, sw, maps.c, maps.r); ms_count_launch(); }
+      g, sys, nsys, Lc, Lr, r, ybuf, done, sw, maps.c, maps.r, window ? 1 : 0); ms_count_launch(); }
+  if (window) {
+    const int nst = win_stages(max_bw), wsw = win_stage_words(max_bw);
+    const size_t wsmem = ((size_t)win_header_words(nst) + (size_t)nst * wsw) * sizeof(double);
+    static size_t wconf[64] = {};
+    set_smem(k_l1_bwd_window<T>, wsmem, wconf);
+    { k_l1_bwd_window<T><<<nsys, 32, wsmem, st>>>(sys, nsys, Lc, ybuf, done, nst, wsw); ms_count_launch(); }
+  }
 }
 
 // Padded TMA-tensor ring for the elasticity bands on request (MS_L1_PAD=1):
@@ -913,6 +1064,18 @@ bool l1_padded_ring_enabled() {
   if (v < 0) {
     const char* e = getenv("MS_L1_PAD");
     v = (e && std::string(e) == "1") ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// one factor copy, plain level 1: backward sweep in axpy form from a deep
+// shared-memory window of the column band (default), or the dot-product form
+// (MS_L1_BWD=dot)
+static bool use_window_bwd() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_L1_BWD");
+    v = (e && std::string(e) == "dot") ? 0 : 1;
   }
   return v == 1;
 }
