@@ -18,27 +18,45 @@
 namespace msgpu {
 
 constexpr int T = kTile;
-constexpr int TP = T + 1;  // shared-memory tile pitch (padding: transposed stores are conflict-free)
-constexpr int kTT = 256;   // threads per tile CTA (16 x 16, 4 x 4 outputs each)
+constexpr int TP = T + 4;  // shared-memory tile pitch: the DMMA fragment loads are bank-conflict free
+constexpr int kTT = 256;   // threads per tile CTA (8 warps)
 
+// 64x64 tile products on the FP64 tensor cores (DMMA, mma.sync m8n8k4):
+// warp w owns rows 32 (w / 4) + 8 rb + g and columns 16 (w % 4) + 8 cb +
+// 2 t + e of the tile (g = lane / 4, t = lane % 4), i.e. 4 x 2 m8n8 blocks.
 struct TileAcc {
-  double v[4][4];
+  double v[4][2][2];
 };
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void frag_pos(int rb, int cb, int e, int& row, int& col) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  row = 32 * (w >> 2) + 8 * rb + (lane >> 2);
+  col = 16 * (w & 3) + 8 * cb + 2 * (lane & 3) + e;
+}
 
 // acc += sA * sB where sA[r][q], sB[q][c] are 64x64 row-major in smem (pitch TP)
 __device__ __forceinline__ void tile_mma(TileAcc& acc, const double* sA, const double* sB) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const double* pa = sA + (32 * (w >> 2) + g) * TP + t;
+  const double* pb = sB + t * TP + 16 * (w & 3) + g;
 #pragma unroll 4
-  for (int q = 0; q < T; ++q) {
-    double a[4], b[4];
+  for (int k = 0; k < T; k += 4) {
+    double a[4], b[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = sA[(ty + 16 * i) * TP + q];
+    for (int rb = 0; rb < 4; ++rb) a[rb] = pa[8 * rb * TP + k];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sB[q * TP + tx + 16 * j];
+    for (int cb = 0; cb < 2; ++cb) b[cb] = pb[k * TP + 8 * cb];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int rb = 0; rb < 4; ++rb)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc.v[i][j] += a[i] * b[j];
+      for (int cb = 0; cb < 2; ++cb) dmma_8x8x4(acc.v[rb][cb], a[rb], b[cb]);
   }
 }
 
@@ -57,18 +75,35 @@ __device__ __forceinline__ void acc_zero(TileAcc& a) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) a.v[i][j] = 0.0;
+    for (int j = 0; j < 2; ++j) a.v[i][j][0] = a.v[i][j][1] = 0.0;
 }
 
 __device__ __forceinline__ void acc_store(const TileAcc& a, double* g, double scale, bool add) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int idx = (ty + 16 * i) * T + tx + 16 * j;
-      g[idx] = add ? g[idx] + scale * a.v[i][j] : scale * a.v[i][j];
-    }
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int row, col;
+        frag_pos(i, j, e, row, col);
+        const int idx = row * T + col;
+        g[idx] = add ? g[idx] + scale * a.v[i][j][e] : scale * a.v[i][j][e];
+      }
+}
+
+// the accumulator into a shared-memory tile (pitch TP)
+__device__ __forceinline__ void acc_to_smem(const TileAcc& a, double* s) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int row, col;
+        frag_pos(i, j, e, row, col);
+        s[row * TP + col] = a.v[i][j][e];
+      }
 }
 
 __device__ __forceinline__ void tile_ij(int64_t t, int& i, int& j) {
@@ -231,13 +266,7 @@ __global__ void __launch_bounds__(kTT) k_trtri_tiles(int d, int nt, const double
     tile_mma(acc, sA, sB);
   }
   __syncthreads();
-  {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) sB[(ty + 16 * a) * TP + tx + 16 * b] = acc.v[a][b];
-  }
+  acc_to_smem(acc, sB);
   tile_load(sA, W + tile_index(i, i) * T * T, false);
   __syncthreads();
   TileAcc out;
