@@ -416,6 +416,7 @@ struct ms_precond {
   DBuf<double> Sinv;   // twisted level 1: separator Schur inverses (empty: plain sweeps)
   bool twisted = false;
   bool one_copy = false;  // plain banded level 1 with the column band only (dot-form backward sweep)
+  bool bitwise = false;   // multi-rank results bit-identical to one rank (MS_DIST_BITWISE=1)
   bool pad = false;       // padded TMA ring (uniform bw), maps below
   L1Maps maps;
   bool dense = false;  // MS_LOCAL_DENSE_INV: packed explicit inverses in Xinv
@@ -638,6 +639,24 @@ static void exchange_rpart(ms_precond* pc) {
                prev >= 0 ? rowd * sizeof(double) : 0, prev, P->ctx->st);
 }
 
+// bitwise mode: the block partials of one dot product sit in their global
+// slots on every rank (zero where another rank owns the block); summing the
+// arrays over ranks is exact, and the fixed-order reduction with the
+// producing kernel's block size gives the one-rank value bit for bit
+static void dist_zero_partials(ms_problem* P, int nb) {
+  MS_CUDA(cudaMemsetAsync(P->partials.p, 0, (size_t)nb * sizeof(double), P->ctx->st));
+}
+static void dist_reduce_bitwise(ms_problem* P, int kind, int nb, int threads, double* hist,
+                                const Xfer* x = nullptr, int nx = 0) {
+  Comm* c = P->ctx->comm.get();
+  if (nx)
+    c->allreduce_sendrecv(P->partials.p, nb, x, nx, P->ctx->st);
+  else
+    c->allreduce_sum(P->partials.p, nb, P->ctx->st);
+  launch_reduce_partials(P->partials.p, nb, threads, &P->sc.p->part[kind], P->ctx->st);
+  launch_finalize(P->sc.p, kind, hist, P->ctx->st);
+}
+
 static void dist_finalize(ms_problem* P, int kind, double* hist) {
   Comm* c = P->ctx->comm.get();
   if (!c || c->world == 1) return;
@@ -657,7 +676,7 @@ static void coarse_solve(ms_precond* pc, const int* done, cudaStream_t st) {
   }
   launch_symv_packed(pc->N_c, pc->K0inv.p, pc->f0.p, pc->y0.p, pc->part.p, done, st, pc->sym_t0, pc->sym_t1);
   Comm* c = pc->prob->ctx->comm.get();
-  if (c && c->world > 1) c->allreduce_sum(pc->y0.p, pc->N_c, st);
+  if (c && c->world > 1 && !pc->bitwise) c->allreduce_sum(pc->y0.p, pc->N_c, st);  // bitwise: replicated
 }
 
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
@@ -755,10 +774,16 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
   else if (pc->has_coarse)
     coarse_branch(pc, r, done, it, restricted, dist, st, rr_hist);
   a = pf.begin(MS_PROF_COMBINE, it, st);
+  const bool bitwise = dist && sc && pc->bitwise;
+  if (bitwise) dist_zero_partials(P, pc->opts.Nx * pc->opts.Ny);
   launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, pc->has_coarse ? &pc->cd : nullptr,
                  pc->opts.Nx, pc->opts.Ny, pc->y0.p, r, z, sc, P->partials.p, beta_hist, st, pc->C0, pc->C1);
   pf.end(MS_PROF_COMBINE, it, st, a);
-  if (dist) {
+  if (bitwise) {
+    Xfer x[4];
+    row_halo_xfers(P, ctx->comm.get(), z, 1, x);
+    dist_reduce_bitwise(P, PART_RZ, pc->opts.Nx * pc->opts.Ny, combine_threads(), beta_hist, x, 4);
+  } else if (dist) {
     if (sc) {
       // r.z allreduce and the z halo (the next matvec refreshes p on one halo
       // row) in one communicator group, then the beta / convergence finalise
@@ -1071,6 +1096,10 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
   pc->device = P->ctx->device;
   pc->st = P->ctx->st;
   pc->opts = *o;
+  if (W > 1) {
+    const char* e = getenv("MS_DIST_BITWISE");
+    pc->bitwise = e && std::string(e) == "1";
+  }
   if (o->heat_dirichlet_nodes && o->n_heat_dirichlet > 0)
     pc->heat_dir.assign(o->heat_dirichlet_nodes, o->heat_dirichlet_nodes + o->n_heat_dirichlet);
   pc->opts.heat_dirichlet_nodes = nullptr;
@@ -1556,7 +1585,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     launch_symmetrize(N, K0.p, st);
     const int nt = div_up(N, kTile);
     pc->coarse_factor = o->coarse_solve == MS_COARSE_CHOLESKY;
-    if (W > 1 && !pc->coarse_factor) {  // balanced contiguous share of the packed tiles
+    if (W > 1 && !pc->coarse_factor && !pc->bitwise) {  // balanced contiguous share of the packed tiles
       const int64_t ntl = packed_tiles(nt);
       pc->sym_t0 = ntl * R / W;
       pc->sym_t1 = ntl * (R + 1) / W;
@@ -1792,6 +1821,7 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
   hs.maxit = maxit;
   hs.first = 1;
   hs.dist = dist ? 1 : 0;
+  hs.bitwise = (dist && pc && pc->bitwise) ? 1 : 0;
   hs.done = maxit == 0 ? 1 : 0;
   MS_CUDA(cudaMemcpyAsync(P->sc.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
   cudaEvent_t t0, t1;
@@ -1812,13 +1842,19 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     double* pold = (i & 1) ? P->p1.p : P->p0.p;
     double* pnew = (i & 1) ? P->p0.p : P->p1.p;
     Prof& pf = P->ctx->prof;
+    const bool bitwise = dist && pc && pc->bitwise;
     cudaEvent_t a = pf.begin(MS_PROF_MATVEC, i, st);
+    if (bitwise) dist_zero_partials(P, matvec_partial_slots(P->g));
     launch_matvec(P->g, P->ke, P->E.p, P->mask.p, zp, pold, pnew, P->q.p, MV_PCG, P->sc.p,
                   P->partials.p, P->halpha.p, st, P->b_lo, row_hi(P));
     pf.end(MS_PROF_MATVEC, i, st, a);
-    if (dist) dist_finalize(P, PART_PQ, P->halpha.p);
+    if (bitwise)
+      dist_reduce_bitwise(P, PART_PQ, matvec_partial_slots(P->g), matvec_threads(), P->halpha.p);
+    else if (dist)
+      dist_finalize(P, PART_PQ, P->halpha.p);
     a = pf.begin(MS_PROF_UPDATE, i, st);
     const bool fused = pc && pc->has_coarse;
+    if (bitwise) dist_zero_partials(P, pc->opts.Nx * pc->opts.Ny);
     if (fused)  // residual update + coarse restriction partials in one pass
       launch_update_restrict(P->g, pc->C0, pc->C1, P->x.p, pnew, P->r.p, P->q.p, pc->cd, P->sc.p,
                              P->partials.p, P->hres.p, st);
@@ -1828,9 +1864,12 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     // multi-rank with a coarse space: ||r||^2 is summed inside the f0 allreduce
     // (one collective fewer per iteration); the level-1 sweeps of the converged
     // iteration then still run, their output unused
-    const bool rr_in_f0 = dist && fused;
+    const bool rr_in_f0 = dist && fused && !bitwise;
     if (dist) {
-      if (!rr_in_f0) dist_finalize(P, PART_RR, P->hres.p);
+      if (bitwise)
+        dist_reduce_bitwise(P, PART_RR, pc->opts.Nx * pc->opts.Ny, update_restrict_threads(pc->cd), P->hres.p);
+      else if (!rr_in_f0)
+        dist_finalize(P, PART_RR, P->hres.p);
       // level-1 subdomains reach delta rows out; without a preconditioner the
       // next matvec needs r (= z) on one halo row
       exchange_rows(P, P->r.p, pc ? pc->halo_rows : 1);

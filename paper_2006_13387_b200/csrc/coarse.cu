@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(TPB, MINB)
   if (!UPD) return;
   __syncthreads();
   double tot;
-  if (grid_reduce_last(threadIdx.x == 0 ? rrblk : 0.0, partials, &sc->tickets[1], &tot, sred)) {
+  if (grid_reduce_dist(threadIdx.x == 0 ? rrblk : 0.0, partials, (J0 + blockIdx.y) * gridDim.x + blockIdx.x,
+                       sc->dist && sc->bitwise, &sc->tickets[1], &tot, sred)) {
     if (threadIdx.x == 0) {
       if (sc->dist)
         sc->part[PART_RR] = tot;
@@ -355,6 +356,9 @@ static int restrict_nu() {
   return v;
 }
 
+int update_restrict_threads(const CoarseDev& cd) {
+  return (!cd.vec && restrict_nu() == 2) ? MS_CR2_TPB : kCellThreads;
+}
 void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const double* p, double* r,
                             const double* q, const CoarseDev& cd, PcgScalars* sc,
                             double* partials, double* res_hist, cudaStream_t st) {
@@ -554,7 +558,8 @@ __global__ void __launch_bounds__(kCombineThreads, MS_CB_MINB)
   if (!sc) return;
   const double bs = block_sum(dot, sred);
   double tot;
-  if (grid_reduce_last(bs, partials, &sc->tickets[2], &tot, sred)) {
+  if (grid_reduce_dist(bs, partials, (J0 + blockIdx.y) * gridDim.x + blockIdx.x, sc->dist && sc->bitwise,
+                       &sc->tickets[2], &tot, sred)) {
     if (threadIdx.x == 0) {
       if (sc->dist)
         sc->part[PART_RZ] = tot;
@@ -563,6 +568,8 @@ __global__ void __launch_bounds__(kCombineThreads, MS_CB_MINB)
     }
   }
 }
+
+int combine_threads() { return kCombineThreads; }
 
 void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
                     int Nx, int Ny, const double* y0, const double* r, double* z, PcgScalars* sc,

@@ -58,6 +58,10 @@ void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double
 // fused x += alpha p, r -= alpha q, ||r||^2 -> convergence, and restriction
 // partial sums per coarse cell; then f0 = sum of the 4 cell partials per centre
 // cells of coarse block rows [J0, J1) (the caller's strip)
+// block sizes of the fused update + restriction and of the combine (their
+// one-rank finishing blocks reduce the dot-product partials with them)
+int update_restrict_threads(const CoarseDev& cd);
+int combine_threads();
 void launch_update_restrict(const Grid& g, int J0, int J1, double* x, const double* p, double* r,
                             const double* q, const CoarseDev& cd, PcgScalars* sc,
                             double* partials, double* res_hist, cudaStream_t st);

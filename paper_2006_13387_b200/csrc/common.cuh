@@ -70,6 +70,22 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return t;
 }
 
+// fixed-order sum of nb partials by one block: thread i sums partials i,
+// i+T, ... (L2 loads, 8 in flight per thread), then the block tree
+__device__ __forceinline__ double reduce_partials_fixed(const double* partials, unsigned int nb, double* sh) {
+  double s = 0.0;
+  unsigned int i = threadIdx.x;
+  for (; i + 7 * blockDim.x < nb; i += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(partials + i + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; i < nb; i += blockDim.x) s += __ldcg(partials + i);
+  return block_sum(s, sh);
+}
+
 // "Last block finishes" deterministic grid reduction: every block writes its
 // partial; the last one to arrive (atomic ticket) sums all partials in index
 // order.  Returns true in the finishing block (all threads), with *out set.
@@ -87,26 +103,27 @@ __device__ __forceinline__ bool grid_reduce_last(double blockval, double* partia
   __syncthreads();
   if (!am_last) return false;
   __threadfence();
-  const unsigned int nb = gridDim.x * gridDim.y;
-  // fixed order: thread i sums partials i, i+T, ...; then block tree.  L2
-  // loads (ld.global.cg: other CTAs' partials, published by their fences),
-  // 8 in flight per thread; the sum order is unchanged.
-  double s = 0.0;
-  unsigned int i = threadIdx.x;
-  for (; i + 7 * blockDim.x < nb; i += 8 * blockDim.x) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcg(partials + i + u * blockDim.x);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s += v[u];
-  }
-  for (; i < nb; i += blockDim.x) s += __ldcg(partials + i);
-  s = block_sum(s, sh);
+  const double s = reduce_partials_fixed(partials, gridDim.x * gridDim.y, sh);
   if (threadIdx.x == 0) {
     *out = s;
     *ticket = 0u;  // re-arm for the next launch
   }
   return true;
+}
+
+// Bitwise multi-rank mode (MS_DIST_BITWISE): every block writes its partial
+// to its GLOBAL slot (the block's index in the one-rank grid); the ranks'
+// partial arrays (zero where another rank owns the block) are summed
+// exactly by an allreduce and reduced by k_reduce_partials with the same
+// fixed order and block size as the one-rank finishing block.
+__device__ __forceinline__ bool grid_reduce_dist(double blockval, double* partials, unsigned int gidx,
+                                                 bool global_slots, unsigned int* ticket, double* out,
+                                                 double* sh) {
+  if (global_slots) {
+    if (threadIdx.x == 0) partials[gidx] = blockval;
+    return false;
+  }
+  return grid_reduce_last(blockval, partials, ticket, out, sh);
 }
 
 // ---- bulk async copy (TMA engine, 1-D) + mbarrier helpers (sm_90+/sm_100a) ----

@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
   if (mode != MV_PCG) return;
   const double bs = block_sum(dot, sred);
   double tot;
-  if (grid_reduce_last(bs, partials, &sc->tickets[0], &tot, sred)) {
+  if (grid_reduce_dist(bs, partials, (blockIdx.y + tile_y0) * gridDim.x + blockIdx.x, sc->dist && sc->bitwise,
+                       &sc->tickets[0], &tot, sred)) {
     if (threadIdx.x == 0) {
       if (sc->dist)
         sc->part[PART_PQ] = tot;
@@ -166,6 +167,20 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
         fin_alpha(sc, tot, alpha_hist);
     }
   }
+}
+
+int matvec_partial_slots(const Grid& g) { return div_up(g.nx + 1, MV_TX) * (g.ny / MV_NY + 1); }
+int matvec_threads() { return MV_TX * MV_TY; }
+
+__global__ void k_reduce_partials(const double* __restrict__ partials, int nb, double* out) {
+  __shared__ double sh[32];
+  const double s = reduce_partials_fixed(partials, (unsigned)nb, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+void launch_reduce_partials(const double* partials, int nb, int threads, double* out, cudaStream_t st) {
+  { k_reduce_partials<<<1, threads, 0, st>>>(partials, nb, out); ms_count_launch(); }
+  MS_CUDA(cudaGetLastError());
 }
 
 void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint8_t* mask,

@@ -22,6 +22,7 @@ struct PcgScalars {
   int first;       // next z.r reduction starts the recurrence (beta = 0)
   int dist;        // multi-rank: reductions leave partials in part[], finalised after allreduce
   int stop_after_beta;  // maxit reached unconverged: finish this iteration's z and beta, then stop
+  int bitwise;     // multi-rank: block partials in global slots (bit-identical to one rank)
   double part[4];  // per-rank partial sums: [PART_PQ], [PART_RR], [PART_RZ]
   unsigned int tickets[8];
 };
@@ -64,6 +65,11 @@ __device__ __forceinline__ void fin_beta(PcgScalars* sc, double rz, double* beta
 
 // multi-rank: finalize one allreduced partial (kind = PART_*)
 void launch_finalize(PcgScalars* sc, int kind, double* hist, cudaStream_t st);
+// *out = fixed-order sum of nb partials with `threads` threads (bitwise multi-rank mode)
+void launch_reduce_partials(const double* partials, int nb, int threads, double* out, cudaStream_t st);
+// the one-rank grid of the fused matvec: global partial slots and block size
+int matvec_partial_slots(const Grid& g);
+int matvec_threads();
 
 // Element stiffness of the unit modulus Q1 plane-stress element, passed by
 // value (kernel parameter space is a broadcast constant bank).

@@ -234,9 +234,12 @@ def test_callback_communicator_two_rank_selftest():
         assert res[r] == [3.0, 4.0, 7.0, float(1 - r)]
 
 
-def _strip_worker(rank, world, port, q, n, maxit):
+def _strip_worker(rank, world, port, q, n, maxit, bitwise=False):
     sys.path.insert(0, str(ROOT))
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ["MS_L1_TWIST"] = "1"
+    if bitwise:
+        os.environ["MS_DIST_BITWISE"] = "1"
     _init(rank, world, port)
     try:
         from paper_2006_13387_b200 import configs, dist as D, pcg_solve
@@ -254,21 +257,25 @@ def _strip_worker(rank, world, port, q, n, maxit):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [4, 8])
-def test_strip_ranks_on_one_gpu_match_single_rank(world):
-    """Config 3's recipe at 256^2 (8 x 8 subdomain rows) sharded into 4 and 8
-    strips, the ranks' kernels on the one B200 and their collectives through
-    gloo host callbacks: same coarse space on every rank, the subdomain rows
-    partitioned, and the same preconditioner and PCG iterates as one rank
-    (only the summation order of dot products and of the sharded coarse
-    solve differ)."""
+@pytest.mark.parametrize("bitwise", [False, True])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_strip_ranks_on_one_gpu_match_single_rank(world, bitwise, monkeypatch):
+    """Config 3's recipe at 256^2 (8 x 8 subdomain rows) sharded into 2, 4 and
+    8 strips, the ranks' kernels on the one B200 and their collectives
+    through gloo host callbacks: same coarse space on every rank, the
+    subdomain rows partitioned, and the same preconditioner and PCG iterates
+    as one rank.  Default mode: only the summation order of the dot products
+    and of the sharded coarse solve differ (tolerances).  MS_DIST_BITWISE=1:
+    dot products from global block slots and a replicated coarse solve --
+    the iterates are bit-identical to one rank."""
     if not torch.cuda.is_available():  # pragma: no cover
         pytest.skip("no CUDA device")
     n, maxit = 256, 40
+    monkeypatch.setenv("MS_L1_TWIST", "1")
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q, n, maxit)) for r in range(world)]
+    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q, n, maxit, bitwise)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict((v[0], v[1:]) for v in (q.get(timeout=900) for _ in range(world)))
@@ -289,7 +296,11 @@ def test_strip_ranks_on_one_gpu_match_single_rank(world):
         x, iters, nc, modes, z, _, resid = res[r]
         assert nc == pre.coarse_dim and modes == list(pre.mode_counts)
         assert iters == rep1.iterations == maxit
+        if bitwise:
+            assert np.array_equal(x, x1), np.abs(x - x1).max()
+            assert np.array_equal(np.asarray(resid), np.asarray(rep1.residuals))
+        else:
+            assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
+            assert np.allclose(resid, rep1.residuals, rtol=1e-9)
         assert np.linalg.norm(z - z1) <= 1e-12 * np.linalg.norm(z1)
-        assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
-        assert np.allclose(resid, rep1.residuals, rtol=1e-9)
         assert np.array_equal(x, res[0][0])
