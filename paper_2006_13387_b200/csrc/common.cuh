@@ -169,6 +169,16 @@ __device__ __forceinline__ double lds_or_zero(const double* p, bool pred) {
   return v;
 }
 
+// 8-byte asynchronous global -> shared copy (cp.async, LDGSTS); ok == false
+// zero-fills the destination (src must still be a valid address)
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
 // global -> shared bulk copy; bytes and both addresses multiples of 16
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

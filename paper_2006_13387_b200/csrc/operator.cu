@@ -32,6 +32,11 @@ constexpr int MV_RPT = MV_NY / MV_TY;  // nodes per thread
 #ifndef MS_MV_MINB
 #define MS_MV_MINB 5
 #endif
+// cp.async (LDGSTS) tile loads instead of register-staged loads: measured
+// slower (config 3 matvec 0.099 -> 0.106 ms; 0.118 ms at 6 CTAs/SM), off
+#ifndef MS_MV_ASYNC
+#define MS_MV_ASYNC 0
+#endif
 __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
     k_matvec(Grid g, KeParam ke, const double* __restrict__ E, const uint8_t* __restrict__ mask,
              const double* __restrict__ z, const double* __restrict__ p_old,
@@ -41,16 +46,55 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
   __shared__ double sp[2][MV_NY + 2][MV_TX + 2];
   __shared__ double sE[MV_NY + 1][MV_TX + 1];
   __shared__ double sred[MV_TX * MV_TY / 32];
+#if MS_MV_ASYNC
+  __shared__ double so[2][MV_NY + 2][MV_TX + 2];  // p_old (PCG mode; sp receives z first)
+#endif
 
   const int a0 = blockIdx.x * MV_TX, b0 = (blockIdx.y + tile_y0) * MV_NY;
   const int tid = threadIdx.x;
   const double beta = (mode == MV_PCG) ? sc->beta : 0.0;
   const int64_t nn = g.n_nodes;
 
+  constexpr int kPT = (MV_NY + 2) * (MV_TX + 2);
+#if MS_MV_ASYNC
+  // Tile loads as asynchronous global->shared copies (cp.async, zero-filled
+  // outside the domain): no register staging, every element of the tile in
+  // flight at once; then p = z + beta p_old in shared memory.
+  {
+    constexpr int kET2 = (MV_NY + 1) * (MV_TX + 1);
+    for (int t = tid; t < kPT; t += MV_TX * MV_TY) {
+      const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
+      const int a = a0 + lx - 1, b = b0 + ly - 1;
+      const bool ok = a >= 0 && a <= g.nx && b >= 0 && b <= g.ny;
+      const int64_t n = ok ? (int64_t)b * g.nnx + a : 0;
+      double* dx = (mode == MV_PCG) ? &so[0][ly][lx] : &sp[0][ly][lx];
+      double* dy = (mode == MV_PCG) ? &so[1][ly][lx] : &sp[1][ly][lx];
+      cp_async8(dx, p_old + n, ok);
+      cp_async8(dy, p_old + n + nn, ok);
+      if (mode == MV_PCG) {
+        cp_async8(&sp[0][ly][lx], z + n, ok);
+        cp_async8(&sp[1][ly][lx], z + n + nn, ok);
+      }
+    }
+    for (int t = tid; t < kET2; t += MV_TX * MV_TY) {
+      const int ly = t / (MV_TX + 1), lx = t - ly * (MV_TX + 1);
+      const int i = a0 + lx - 1, j = b0 + ly - 1;
+      const bool ok = i >= 0 && i < g.nx && j >= 0 && j < g.ny;
+      cp_async8(&sE[ly][lx], E + (ok ? (int64_t)j * g.nx + i : 0), ok);
+    }
+    cp_async_wait_all();
+    if (mode == MV_PCG) {
+      for (int t = tid; t < kPT; t += MV_TX * MV_TY) {  // own elements only: no barrier needed before
+        const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
+        sp[0][ly][lx] = sp[0][ly][lx] + beta * so[0][ly][lx];
+        sp[1][ly][lx] = sp[1][ly][lx] + beta * so[1][ly][lx];
+      }
+    }
+  }
+#else
   // Tile loads: every global load of the thread is issued before the first
   // shared-memory store (compile-time trip counts, predicated), so each
   // thread keeps ~25 loads in flight instead of one dependent chain.
-  constexpr int kPT = (MV_NY + 2) * (MV_TX + 2);
   constexpr int kPIt = (kPT + MV_TX * MV_TY - 1) / (MV_TX * MV_TY);
   constexpr int kET = (MV_NY + 1) * (MV_TX + 1);
   constexpr int kEIt = (kET + MV_TX * MV_TY - 1) / (MV_TX * MV_TY);
@@ -97,6 +141,7 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
       }
     }
   }
+#endif
   __syncthreads();
 
   const int tx = tid % MV_TX, ty = tid / MV_TX;
