@@ -72,6 +72,7 @@ def parse():
                     help="reference arm: PCG iterations per timed step (full-size config, all host cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the iters-vs-reference solves (golden fixtures)")
+    ap.add_argument("--no-share", action="store_true", help="skip the per-GPU-share strips (config 3, N=1)")
     ap.add_argument("--variant", default="EH+Rot", choices=("EH+Rot", "EH", "EH+Rot;Rand", "HH+Rot", "HH", "EE",
                                                             "EE;Rand"),
                     help="preconditioner variant (Table 1 tags); the headline is EH+Rot")
@@ -209,6 +210,39 @@ def cpu_sample(args, threads):
                    f"({t:.2f} s); build {t_build:.1f} s excluded (ARPACK eigensolves)"),
         "kind": "port", "iterations": rep.iterations, "t_solve_s": t,
     }
+
+
+def per_gpu_share(args, spec):
+    """One GPU's share of config 3 split over W GPUs (strips of nx x ny/W,
+    the same recipe): level-1 kernel time and the PCG iteration time of a
+    capped solve on this GPU.  Not a scaling measurement (no collectives, one
+    GPU); it shows what the per-GPU kernels sustain when the subdomain count
+    per GPU shrinks (twisted level 1 below one wave)."""
+    import torch
+
+    from paper_2006_13387_b200 import configs, pcg_solve
+    from paper_2006_13387_b200.solve import setup_spec
+
+    out = {}
+    for W in (2, 4, 8):
+        ny = spec.ny // W
+        sub = configs.config3(seed=args.seed, n=spec.nx, ny=ny)
+        mesh, op, pre = setup_spec(sub, args.variant)
+        comp = pre.bench_components(reps=10)
+        b = torch.tensor(sub.rhs(), device="cuda")
+        pcg_solve(op, b, pre, tol=sub.tol, maxit=64, record=False)
+        torch.cuda.synchronize()
+        _, rep = pcg_solve(op, b, pre, tol=sub.tol, maxit=200, record=False)
+        S = level1_dofs(sub)
+        l1_bytes = pre.info["local_bytes"] + 2 * S * 8
+        pk, _ = peaks()
+        out[f"W{W}"] = {"strip": f"{sub.nx}x{sub.ny}", "subdomains": pre.info["n_subdomains"],
+                        "level1_twisted": pre.info["level1_twisted"],
+                        "level1_ms": comp["level1"], "level1_hbm_frac": l1_bytes / (comp["level1"] * 1e-3) / 1e9 / float(pk["hbm_gbs"]),
+                        "ms_per_iteration": rep.timings["solve"] * 1e3 / max(rep.iterations, 1)}
+        del pre, op
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_reference(args):
@@ -447,6 +481,8 @@ def run_ours(args):
         line["per_rank"] = every
     else:
         line["per_rank"] = [mine]
+    if world == 1 and args.config == 3 and not args.no_share:
+        line["per_gpu_share"] = per_gpu_share(args, spec)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_sample(args, 1)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -15,9 +15,10 @@ worker processes so the host's cores are used:
   process (threaded BLAS);
 * level 1 (schwarz.py:97-109): every worker owns a contiguous run of the
   delta-blocks (a strip of subdomain rows), factors them with SuperLU and
-  applies them; the per-worker partial sums are added in worker order, which
-  reproduces the sequential loop's summation order (z[idx] += solve(r[idx]),
-  schwarz.py:80-81) bit for bit;
+  solves them into its slice of a shared buffer; the main process then adds
+  the local solutions in the reference's subdomain order (z[idx] +=
+  solve(r[idx]), schwarz.py:80-81), so the sum is the sequential loop's bit
+  for bit;
 * the operator ``A @ p`` (krylov.py:114) by row blocks of the same CSR matrix
   (each row's dot product unchanged);
 * PCG itself (krylov.py:81-134) in the main process.
@@ -52,21 +53,19 @@ def _eig_task(k):
     return O.lowest_eigenpairs_arpack(K, M, min(7, K.n_free))
 
 
-def _worker(conn, A, rows, l1_specs, p, q, r, zpart, ranges):
-    """Serve 'mv' (q[rows] = A[rows] p) and 'l1' (zpart = sum of the owned
-    subdomain solves) until 'quit'."""
+def _worker(conn, A, rows, l1_specs, offs, p, q, r, ysh):
+    """Serve 'mv' (q[rows] = A[rows] p) and 'l1' (the owned subdomains'
+    solves into their slices of ysh) until 'quit'."""
     Arow = A[rows[0]:rows[1]]
-    solvers = [(idx, spla.splu(A[idx][:, idx].tocsc()).solve) for idx in l1_specs]
+    solvers = [(idx, o, spla.splu(A[idx][:, idx].tocsc()).solve) for idx, o in zip(l1_specs, offs)]
     conn.send("ready")
     while True:
         cmd = conn.recv()
         if cmd == "mv":
             q[rows[0]:rows[1]] = Arow @ p
         elif cmd == "l1":
-            for a, b in ranges:
-                zpart[a:b] = 0.0
-            for idx, solve in solvers:
-                zpart[idx] += solve(r[idx])
+            for idx, o, solve in solvers:
+                ysh[o:o + idx.size] = solve(r[idx])
         elif cmd == "quit":
             conn.send("bye")
             return
@@ -115,25 +114,19 @@ class ParallelReference:
             if idx.size:
                 specs.append(idx)
         self.n_subdomains = len(specs)
+        self.specs = specs
+        self.offs = np.concatenate([[0], np.cumsum([v.size for v in specs])]).astype(np.int64)
         self.p, self.q, self.r = _shared(n), _shared(n), _shared(n)
-        self.zpart = [_shared(n) for _ in range(procs)]
+        self.ysh = _shared(int(self.offs[-1]))
         cut = [round(i * len(specs) / procs) for i in range(procs + 1)]
         rcut = [round(i * n / procs) for i in range(procs + 1)]
-        nx_free = int(np.searchsorted(op.free_dofs, mesh.n_nodes))  # x-dofs first, then y
         ctx = mp.get_context("fork")
-        self.conns, self.procs_, self.ranges = [], [], []
+        self.conns, self.procs_ = [], []
         for w in range(procs):
-            mine = specs[cut[w]:cut[w + 1]]
-            if mine:
-                allidx = np.concatenate(mine)
-                xs, ys = allidx[allidx < nx_free], allidx[allidx >= nx_free]
-                rng = [(int(v.min()), int(v.max()) + 1) for v in (xs, ys) if v.size]
-            else:
-                rng = []
-            self.ranges.append(rng)
             a, b = ctx.Pipe()
-            pr = ctx.Process(target=_worker, args=(b, op.matrix, (rcut[w], rcut[w + 1]), mine, self.p, self.q,
-                                                   self.r, self.zpart[w], rng), daemon=True)
+            pr = ctx.Process(target=_worker, args=(b, op.matrix, (rcut[w], rcut[w + 1]), specs[cut[w]:cut[w + 1]],
+                                                   self.offs[cut[w]:cut[w + 1]], self.p, self.q, self.r,
+                                                   self.ysh), daemon=True)
             pr.start()
             self.conns.append(a)
             self.procs_.append(pr)
@@ -161,9 +154,9 @@ class ParallelReference:
         self.r[:] = r
         self._all("l1")
         z = np.zeros(self.n_free)
-        for w in range(self.procs):
-            for a, b in self.ranges[w]:
-                z[a:b] += self.zpart[w][a:b]
+        y, offs = self.ysh, self.offs
+        for i, idx in enumerate(self.specs):  # the reference's summation order
+            z[idx] += y[offs[i]:offs[i + 1]]
         z += self.coarse.apply(r)
         return z
 

@@ -603,10 +603,17 @@ static void allgather_rows(ms_problem* P, double* v) {
 
 // level-1 solutions of the neighbours' boundary subdomain rows (their overlap
 // reaches into my strip)
+static void ybuf_xfers(ms_precond* pc, Comm* c, Xfer x[2]);
 static void exchange_ybuf(ms_precond* pc) {
   ms_problem* P = pc->prob;
   Comm* c = P->ctx->comm.get();
   if (!c || c->world == 1) return;
+  Xfer x[2];
+  ybuf_xfers(pc, c, x);
+  c->sendrecv(x, 2, P->ctx->st);
+}
+// the level-1 boundary subdomain-row solutions to and from the neighbours
+static void ybuf_xfers(ms_precond* pc, Comm* c, Xfer x[2]) {
   const int r = c->rank, W = c->world;
   const int prev = r > 0 ? r - 1 : -1, next = r < W - 1 ? r + 1 : -1;
   auto seg = [&](int J, int64_t& off, int64_t& bytes) {
@@ -621,22 +628,29 @@ static void exchange_ybuf(ms_precond* pc) {
   if (prev >= 0) seg(pc->J0 - 1, o_pl, b_pl); else o_pl = b_pl = 0;
   if (next >= 0) seg(pc->J1, o_nf, b_nf); else o_nf = b_nf = 0;
   double* y = pc->ybuf.p;
-  c->sendrecv2(y + o_first, prev >= 0 ? b_first : 0, prev, y + o_nf, b_nf, next,
-               y + o_last, next >= 0 ? b_last : 0, next, y + o_pl, b_pl, prev, P->ctx->st);
+  x[0] = {y + o_first, (size_t)(prev >= 0 ? b_first : 0), prev, y + o_nf, (size_t)b_nf, next};
+  x[1] = {y + o_last, (size_t)(next >= 0 ? b_last : 0), next, y + o_pl, (size_t)b_pl, prev};
 }
 
 // restriction partials of the cell row below my lowest centre row (prev's last)
-static void exchange_rpart(ms_precond* pc) {
-  ms_problem* P = pc->prob;
-  Comm* c = P->ctx->comm.get();
-  if (!c || c->world == 1) return;
+// the restriction partials of the coarse-cell row below each strip (its
+// centres' f0 rows need the 4 cells around them)
+static void rpart_xfers(ms_precond* pc, Comm* c, Xfer x[2]) {
   const int r = c->rank, W = c->world;
   const int prev = r > 0 ? r - 1 : -1, next = r < W - 1 ? r + 1 : -1;
   const int64_t rowd = (int64_t)pc->cd.Nx * 4 * kSlots;
   double* rp = pc->rpart.p;
-  c->sendrecv2(nullptr, 0, -1, nullptr, 0, -1, rp + (pc->C1 - 1) * rowd,
-               next >= 0 ? rowd * sizeof(double) : 0, next, rp + (pc->C0 - 1) * rowd,
-               prev >= 0 ? rowd * sizeof(double) : 0, prev, P->ctx->st);
+  x[0] = {nullptr, 0, -1, nullptr, 0, -1};
+  x[1] = {rp + (pc->C1 - 1) * rowd, (size_t)(next >= 0 ? rowd * sizeof(double) : 0), next, rp + (pc->C0 - 1) * rowd,
+          (size_t)(prev >= 0 ? rowd * sizeof(double) : 0), prev};
+}
+static void exchange_rpart(ms_precond* pc) {
+  ms_problem* P = pc->prob;
+  Comm* c = P->ctx->comm.get();
+  if (!c || c->world == 1) return;
+  Xfer x[2];
+  rpart_xfers(pc, c, x);
+  c->sendrecv(x, 2, P->ctx->st);
 }
 
 // bitwise mode: the block partials of one dot product sit in their global
@@ -726,6 +740,64 @@ static void coarse_branch(ms_precond* pc, const double* r, const int* done, int 
   cudaEvent_t a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
   coarse_solve(pc, done, st);
   pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
+}
+
+// Multi-rank PCG apply with the collectives regrouped (5 communicator
+// calls per iteration instead of 7): the restriction partials were fused
+// into the residual update and exchanged together with the r halo, so the
+// restriction reduce runs before the level-1 sweeps, and the sweeps'
+// boundary solutions travel in the same group as the f0 (+ ||r||^2)
+// allreduce.
+static void precond_apply_dist_grouped(ms_precond* pc, const double* r, double* z, PcgScalars* sc,
+                                       double* beta_hist, int it, double* rr_hist) {
+  ms_problem* P = pc->prob;
+  ms_ctx* ctx = P->ctx;
+  const cudaStream_t st = ctx->st;
+  Prof& pf = ctx->prof;
+  Comm* c = ctx->comm.get();
+  const int* done = &sc->done;
+  const int ns = pc->s1 - pc->s0;
+  cudaEvent_t a = pf.begin(MS_PROF_RESTRICT, it, st);
+  MS_CUDA(cudaMemsetAsync(pc->f0.p, 0, pc->N_c * sizeof(double), st));
+  launch_restrict_reduce(pc->cd, pc->f0.p, done, st, pc->kc0, pc->kc1);
+  if (rr_hist)
+    MS_CUDA(cudaMemcpyAsync(pc->f0.p + pc->N_c, &P->sc.p->part[PART_RR], sizeof(double), cudaMemcpyDeviceToDevice,
+                            st));
+  pf.end(MS_PROF_RESTRICT, it, st, a);
+  if (ns > 0) {
+    a = pf.begin(MS_PROF_LEVEL1, it, st);
+    if (pc->dense)
+      launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
+    else
+      launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st,
+                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps);
+    pf.end(MS_PROF_LEVEL1, it, st, a);
+  }
+  Xfer yx[2];
+  ybuf_xfers(pc, c, yx);
+  c->allreduce_sendrecv(pc->f0.p, pc->N_c + (rr_hist ? 1 : 0), yx, ns > 0 ? 2 : 0, st);
+  if (rr_hist) {
+    MS_CUDA(cudaMemcpyAsync(&P->sc.p->part[PART_RR], pc->f0.p + pc->N_c, sizeof(double), cudaMemcpyDeviceToDevice,
+                            st));
+    launch_finalize(P->sc.p, PART_RR, rr_hist, st);
+  }
+  a = pf.begin(MS_PROF_COARSE_SOLVE, it, st);
+  coarse_solve(pc, done, st);
+  pf.end(MS_PROF_COARSE_SOLVE, it, st, a);
+  a = pf.begin(MS_PROF_COMBINE, it, st);
+  const bool bitwise = pc->bitwise;
+  if (bitwise) dist_zero_partials(P, pc->opts.Nx * pc->opts.Ny);
+  launch_combine(P->g, P->mask.p, pc->nsys > 0 ? &pc->l1 : nullptr, &pc->cd, pc->opts.Nx, pc->opts.Ny, pc->y0.p, r,
+                 z, sc, P->partials.p, beta_hist, st, pc->C0, pc->C1);
+  pf.end(MS_PROF_COMBINE, it, st, a);
+  Xfer x[4];
+  row_halo_xfers(P, c, z, 1, x);
+  if (bitwise) {
+    dist_reduce_bitwise(P, PART_RZ, pc->opts.Nx * pc->opts.Ny, combine_threads(), beta_hist, x, 4);
+  } else {
+    c->allreduce_sendrecv(&P->sc.p->part[PART_RZ], 1, x, 4, st);
+    launch_finalize(P->sc.p, PART_RZ, beta_hist, st);
+  }
 }
 
 // precond apply on full-layout r -> z (device); sc/partials/beta_hist for PCG mode
@@ -1870,11 +1942,22 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
         dist_reduce_bitwise(P, PART_RR, pc->opts.Nx * pc->opts.Ny, update_restrict_threads(pc->cd), P->hres.p);
       else if (!rr_in_f0)
         dist_finalize(P, PART_RR, P->hres.p);
-      // level-1 subdomains reach delta rows out; without a preconditioner the
-      // next matvec needs r (= z) on one halo row
-      exchange_rows(P, P->r.p, pc ? pc->halo_rows : 1);
+      // level-1 subdomains reach delta rows out (without a preconditioner the
+      // next matvec needs r (= z) on one halo row); the restriction partials
+      // of the boundary cell row travel in the same group
+      Comm* c = P->ctx->comm.get();
+      Xfer x[6];
+      row_halo_xfers(P, c, P->r.p, pc ? pc->halo_rows : 1, x);
+      int nx = 4;
+      if (fused) {
+        rpart_xfers(pc, c, x + 4);
+        nx = 6;
+      }
+      c->sendrecv(x, nx, st);
     }
-    if (pc) {
+    if (dist && fused) {
+      precond_apply_dist_grouped(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, i, rr_in_f0 ? P->hres.p : nullptr);
+    } else if (pc) {
       precond_apply_full(pc, P->r.p, P->z.p, P->sc.p, P->hbeta.p, i, fused, rr_in_f0 ? P->hres.p : nullptr);
     } else {
       a = pf.begin(MS_PROF_COMBINE, i, st);

@@ -240,3 +240,28 @@ def test_condition_estimate_helpers_follow_reference():
         assert lo == pytest.approx(w[0], rel=1e-10) and hi == pytest.approx(w[-1], rel=1e-12)
     assert K._ritz_extremes([], []) == (None, None)
     assert K._ritz_extremes([1.0, float("nan")], [0.5]) == (None, None)
+
+
+def test_parallel_reference_arm_reproduces_sequential_oracle():
+    """bench.py --impl reference runs the oracle on all host cores
+    (oracle/parallel_ref.py): the worker-split operator and the level-1 sum
+    are bit-identical to the sequential oracle (CSR rows unchanged; local
+    solutions added in the reference's subdomain order)."""
+    from oracle.parallel_ref import ParallelReference
+
+    spec = configs.config3(seed=0, n=128)
+    R = ParallelReference(spec, procs=3)
+    try:
+        prob = R.prob
+        rng = np.random.default_rng(4)
+        p = rng.standard_normal(R.n_free)
+        assert np.array_equal(R.matvec(p), prob.op.matrix @ p)
+        l1 = O.level1_solvers(prob.op, prob.mesh, O.block_rects(prob.mesh, spec.H, spec.delta), True)
+        z_seq = np.zeros(R.n_free)
+        for idx, solve in l1:
+            z_seq[idx] += solve(p[idx])
+        z_seq_full = z_seq + R.coarse.apply(p)  # coarse added last, as in schwarz.py:83
+        assert np.array_equal(R.apply(p), z_seq_full)
+        assert R.coarse_dim == sum(2 * m + 1 for m in R.info["mode_counts"])
+    finally:
+        R.close()
