@@ -448,6 +448,8 @@ def jitter_band(op, b, variant, level1, cop, blocks, tol, maxit, procs, x_ref, h
         "combined_banded_ebe_k0chol": lambda: run_op(ebe(np.arange(n_el)[::-1]), banded_level1(), cop),
     }
     names = list(_JIT)
+    if os.environ.get("JITTER_SUBSET"):  # long solves: a named subset of the perturbations
+        names = [n for n in names if n in os.environ["JITTER_SUBSET"].split(",")]
     with mp.get_context("fork").Pool(procs) as pool:
         res = dict(pool.map(_jitter_task, names))
     nb = np.linalg.norm(b)
@@ -563,9 +565,10 @@ def main():
         adapter_case(configs.config2(seed=0, eta=1e2, n=128, H=32, delta=2), "ref_config2_n128_eta1e2.npz")
         adapter_case(configs.config2(seed=0, eta=1e8, n=128, H=32, delta=2), "ref_config2_n128_eta1e8.npz")
         adapter_case(configs.config5(seed=0, step=3, n=128, H=32, delta=2), "ref_config5_n128_step3.npz")
-    if "cfg4s" in which:  # config 4's MBB recipe at 256 x 128 with the 32^2 blocks of the config (eta 1e9)
-        adapter_case(configs.config4(seed=0, nx=256, ny=128, H=32, delta=2, eta=1e9), "ref_config4_256x128.npz",
-                     procs=2)
+    if "cfg4s" in which:  # config 4's MBB recipe at 128 x 64 with the 32^2 blocks of the config (eta 1e9)
+        # (at 256 x 128 the reference does not reach 1e-8 within 5,000 iterations)
+        adapter_case(configs.config4(seed=0, nx=128, ny=64, H=32, delta=2, eta=1e9), "ref_config4_128x64.npz",
+                     maxit=20000, procs=2)
     if "cfg5seq" in which:  # three consecutive config-5 density steps at 64^2 (rebuild per step)
         for k in range(3):
             adapter_case(configs.config5(seed=1, step=k, n=64, H=16, delta=2), f"ref_config5_n64_step{k}.npz")

@@ -304,3 +304,47 @@ def test_strip_ranks_on_one_gpu_match_single_rank(world, bitwise, monkeypatch):
             assert np.allclose(resid, rep1.residuals, rtol=1e-9)
         assert np.linalg.norm(z - z1) <= 1e-12 * np.linalg.norm(z1)
         assert np.array_equal(x, res[0][0])
+
+
+def _apply_before_build_worker(rank, world, port, q):
+    sys.path.insert(0, str(ROOT))
+    _init(rank, world, port)
+    try:
+        from paper_2006_13387_b200 import ElasticityOperator, CoefficientField, build_fine_mesh, configs, dist as D
+
+        D.init_host_callbacks(0)
+        spec = configs.config1(seed=0)
+        mesh = build_fine_mesh(spec.nx, spec.ny)
+        op = ElasticityOperator(mesh, CoefficientField(spec.E, spec.nu, spec.E_min, spec.E_max), spec.free_dofs())
+        v = np.linspace(-1.0, 1.0, op.n_free)
+        q.put((rank, op @ v))  # no preconditioner yet: no strip ownership
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_operator_apply_before_any_preconditioner_two_ranks():
+    """with a communicator attached, `op @ v` before any
+    preconditioner exists (no strip ownership yet) must not index the empty
+    row tables; every rank computes all rows and gets the one-rank result."""
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("no CUDA device")
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_apply_before_build_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sys.path.insert(0, str(ROOT))
+    from paper_2006_13387_b200 import ElasticityOperator, CoefficientField, build_fine_mesh, configs
+
+    spec = configs.config1(seed=0)
+    mesh = build_fine_mesh(spec.nx, spec.ny)
+    op = ElasticityOperator(mesh, CoefficientField(spec.E, spec.nu, spec.E_min, spec.E_max), spec.free_dofs())
+    ref = op @ np.linspace(-1.0, 1.0, op.n_free)
+    for r in (0, 1):
+        assert np.array_equal(res[r], ref)
