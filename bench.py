@@ -503,6 +503,7 @@ def run_ours(args):
 PARITY_CASES = (("config1_64x64_d1", "ref_config1.npz"), ("config3_recipe_128x128", "ref_config3_n128.npz"),
                 ("config2_recipe_128x128_eta1e8", "ref_config2_n128_eta1e8.npz"),
                 ("config5_recipe_128x128_step3", "ref_config5_n128_step3.npz"),
+                ("config4_recipe_128x64_eta1e9", "ref_config4_128x64.npz"),
                 ("config2_512x512_eta1e2", "ref_config2_n512_eta100.npz"),
                 ("config2_512x512_eta1e4", "ref_config2_n512_eta10000.npz"),
                 ("config2_512x512_eta1e6", "ref_config2_n512_eta1e+06.npz"))

@@ -203,7 +203,8 @@ BASELINE_CASES = [("ref_config1.npz", "EH+Rot"), ("ref_mbb_64x32.npz", "EH+Rot")
                   ("ref_config2_n128_eta1e8.npz", "EH+Rot"),
                   ("ref_config5_n128_step3.npz", "EH+Rot"),
                   ("ref_config5_n64_step0.npz", "EH+Rot"), ("ref_config5_n64_step1.npz", "EH+Rot"),
-                  ("ref_config5_n64_step2.npz", "EH+Rot")]
+                  ("ref_config5_n64_step2.npz", "EH+Rot"),
+                  ("ref_config4_128x64.npz", "EH+Rot")]
 
 
 @pytest.mark.parametrize("coarse_solve", ["inverse", "cholesky"])
