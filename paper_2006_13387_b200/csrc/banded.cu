@@ -607,7 +607,6 @@ template <int T, int NR, bool PAD, class YMap>
 __device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int n, int bw, YMap ym, int lane,
                                                Ring& rg, double* __restrict__ xw,
                                                const CUtensorMap* map = nullptr, int col0 = 0) {
-  static_assert(kCh == 8, "4 lanes per chunk row");
   constexpr int kWin = 128;       // window rows (>= bw + kCh); stored twice so reads never wrap
   constexpr int kA = 8 * T;       // phase-A terms per lane: j = pc + 1 + g + 4 i <= 32 T
   constexpr int P = pad_slot_words<T>();
@@ -755,8 +754,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   } else {  // one factor copy: backward sweep by dot products over the column band
     double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD) +
                  (size_t)warp * 256 * NR;
-    band_sweep_dot<T, NR, PAD>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
-                               &mapc, col0);
+    if constexpr (kCh == 8)
+      band_sweep_dot<T, NR, PAD>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
+                                 &mapc, col0);
+    else
+      __trap();  // the dot-form sweep is laid out for 8-column stages
   }
 }
 
@@ -838,7 +840,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   pair_sync(pair);
   if (!Lr) {  // one factor copy: both backward sweeps by dot products over the column bands
     double* xw = smem_ring + ring_words + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw + (size_t)warp * 256 * NR;
-    if (role == 0)
+    if constexpr (kCh != 8) {
+      __trap();  // the dot-form sweep is laid out for 8-column stages
+    } else if (role == 0)
       band_sweep_dot<T, NR, PAD>(Lc + s.foff, nT, bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
                                  &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
     else  // bottom-local row k = natural n - 1 - k (its separator rows now hold x_S)
