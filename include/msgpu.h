@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MSGPU_ABI_VERSION 3
+#define MSGPU_ABI_VERSION 4
 
 enum {
   MS_OK = 0,
@@ -39,7 +39,8 @@ enum {
   MS_E_NOT_SPD = -2,   /* non-positive pivot in a Cholesky factor        -> ValueError   */
   MS_E_CUDA = -3,      /* CUDA runtime failure                           -> RuntimeError */
   MS_E_NOMEM = -4,     /* device allocation failed                       -> MemoryError  */
-  MS_E_STATE = -5      /* call out of order (e.g. apply before build)    -> RuntimeError */
+  MS_E_STATE = -5,     /* call out of order (e.g. apply before build)    -> RuntimeError */
+  MS_E_CALLBACK = -6   /* a host callback operator returned non-zero     -> the callback's own exception */
 };
 
 typedef struct ms_ctx ms_ctx;
@@ -118,6 +119,8 @@ typedef struct ms_precond_info {
   int level1_copies;     /* banded factor copies read per apply: 1 (column band, dot-form
                             backward sweep) or 2 (column + row band)                        */
   int n_subdomains_local; /* level-1 subdomains owned by this rank (all of them on one rank)    */
+  int level1_unit;       /* 1: unit-diagonal L D L^T level-1 factors (no pivot multiply on the
+                            sweeps' dependent chain), 0: Cholesky factors                      */
 } ms_precond_info;
 
 /* SolveReport (krylov.py:17-35); history arrays are caller-provided. */
@@ -247,6 +250,42 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms);
  * residuals (>= maxit+1), alphas (>= maxit), betas (>= maxit) may be NULL. */
 int ms_pcg_solve(ms_problem* prob, ms_precond* pc, const double* b, double tol, int maxit,
                  double* x, ms_report* rep, double* residuals, double* alphas, double* betas);
+
+/* ---- Generic PCG: the duck-typed seams of pcg_solve (ABI 4) -----------------
+ * The reference's pcg_solve accepts any sparse / dense matrix or callable as
+ * A and any object with .apply, callable or None as M (krylov.py:73-78, 90).
+ * ms_linop names one such operand: the Q1 problem, the two-level
+ * preconditioner, a CSR matrix held on the device (ms_csr: scipy.sparse and
+ * ndarray operands), or a host callback (callables / foreign .apply objects;
+ * `in` and `out` are host vectors of n doubles, return 0 or non-zero to abort
+ * with MS_E_CALLBACK).  The recurrence, its vectors and its dot products stay
+ * on the device; same stopping rule and histories as ms_pcg_solve. */
+typedef struct ms_csr ms_csr;
+typedef int (*ms_apply_fn)(void* user, const double* in, double* out, int64_t n);
+enum {
+  MS_LINOP_NONE = 0,     /* identity (M = None)                       */
+  MS_LINOP_PROBLEM = 1,  /* handle = ms_problem*  (op.matrix @ v)     */
+  MS_LINOP_PRECOND = 2,  /* handle = ms_precond*  (M.apply)           */
+  MS_LINOP_CSR = 3,      /* handle = ms_csr*      (A @ v)             */
+  MS_LINOP_CALLBACK = 4  /* fn(user, in, out, n) on host vectors      */
+};
+typedef struct ms_linop {
+  int kind;
+  void* handle;
+  ms_apply_fn fn;
+  void* user;
+} ms_linop;
+
+/* n x n CSR matrix (int64 row pointers, int32 column indices) copied to the device. */
+int ms_csr_create(ms_ctx* ctx, int64_t n, const int64_t* indptr, const int* indices,
+                  const double* data, ms_csr** out);
+int ms_csr_apply(ms_csr* A, const double* v, double* out); /* host or device vectors */
+int ms_csr_destroy(ms_csr* A);
+
+/* pcg_solve (krylov.py:81-134) for any A / M pair above; b and x host or device. */
+int ms_pcg_solve_generic(ms_ctx* ctx, int64_t n, const ms_linop* A, const ms_linop* M,
+                         const double* b, double tol, int maxit, double* x, ms_report* rep,
+                         double* residuals, double* alphas, double* betas);
 
 /* ---- Topology-optimisation caller --------------------
  * The per-design-step coefficient pipeline of the SIMP loop (topopt.py:123-216)

@@ -33,11 +33,21 @@ EXPORTS = (
     "ms_nccl_unique_id", "ms_ctx_attach_nccl", "ms_ctx_attach_callbacks", "ms_comm_selftest", "ms_strip_rows", "ms_copy", "ms_cache_trim",
     "ms_halo_plan", "ms_ctx_set_profiling_mask", "ms_filter_create", "ms_filter_destroy", "ms_filter_apply", "ms_filter_adjoint",
     "ms_problem_set_density", "ms_compliance_sensitivity", "ms_oc_update", "ms_dot", "ms_unit_element", "ms_dense_spd_solve",
+    "ms_csr_create", "ms_csr_apply", "ms_csr_destroy", "ms_pcg_solve_generic",
 )
 
 ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
 BROADCAST_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int)
 SENDRECV_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int)
+
+
+APPLY_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+MS_LINOP_NONE, MS_LINOP_PROBLEM, MS_LINOP_PRECOND, MS_LINOP_CSR, MS_LINOP_CALLBACK = range(5)
+
+
+class LinOp(C.Structure):
+    """ms_linop: one operand of ms_pcg_solve_generic."""
+    _fields_ = [("kind", C.c_int), ("handle", C.c_void_p), ("fn", APPLY_CB), ("user", C.c_void_p)]
 
 
 class CommCallbacks(C.Structure):
@@ -65,6 +75,7 @@ class PrecondInfo(C.Structure):
         ("max_eig_passes", C.c_int), ("mean_eig_passes", C.c_double), ("t_level1", C.c_double), ("t_eig", C.c_double),
         ("t_coarse", C.c_double), ("local_bytes", C.c_double), ("coarse_bytes", C.c_double),
         ("level1_twisted", C.c_int), ("level1_copies", C.c_int), ("n_subdomains_local", C.c_int),
+        ("level1_unit", C.c_int),
     ]
 
 
@@ -149,6 +160,11 @@ def load(path: str | os.PathLike | None = None):
         "ms_dot": (C.c_int, [vp, C.c_int64, vp, vp, dp]),
         "ms_unit_element": (C.c_int, [C.c_double, dp]),
         "ms_dense_spd_solve": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int]),
+        "ms_csr_create": (C.c_int, [vp, C.c_int64, i64p, ip, dp, C.POINTER(vp)]),
+        "ms_csr_apply": (C.c_int, [vp, vp, vp]),
+        "ms_csr_destroy": (C.c_int, [vp]),
+        "ms_pcg_solve_generic": (C.c_int, [vp, C.c_int64, C.POINTER(LinOp), C.POINTER(LinOp), vp, C.c_double,
+                                           C.c_int, vp, C.POINTER(Report), dp, dp, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -147,6 +147,63 @@ class ElasticityOperator:
 
     __matmul__ = apply
 
+    # scipy views of the assembled matrix (the reference's ``op.matrix`` is a
+    # CSR matrix, e.g. ``op.matrix.tocsc()`` for a direct solve): K is recovered
+    # from 18 operator applies on the GPU -- the Q1 stencil couples a node only
+    # to its 8 neighbours, so nodes of one colour (a mod 3, b mod 3) never share
+    # a row, and one apply per (colour, component) yields all their columns.
+    def tocsr(self):
+        import scipy.sparse as sp
+
+        if getattr(self, "_csr", None) is not None and self._csr_E is self.coeff:
+            return self._csr.copy()
+        mesh = self.mesh
+        nnx, nny = mesh.nx + 1, mesh.ny + 1
+        n_nodes = nnx * nny
+        a = np.tile(np.arange(nnx), nny)
+        b = np.repeat(np.arange(nny), nnx)
+        fidx = self.free_index()
+        rows, cols, vals = [], [], []
+        for comp in range(2):
+            for cb in range(3):
+                for ca in range(3):
+                    src_nodes = np.flatnonzero((a % 3 == ca) & (b % 3 == cb))
+                    src = fidx[comp * n_nodes + src_nodes]
+                    src_nodes, src = src_nodes[src >= 0], src[src >= 0]
+                    if src.size == 0:
+                        continue
+                    v = np.zeros(self.n_free)
+                    v[src] = 1.0
+                    q = self.expand(self.apply(v))
+                    # the source node of every row: the unique colour node within one step
+                    sa = a - ((a - ca) % 3) + np.where((a - ca) % 3 == 2, 3, 0)
+                    sb = b - ((b - cb) % 3) + np.where((b - cb) % 3 == 2, 3, 0)
+                    ok = (sa >= 0) & (sa < nnx) & (sb >= 0) & (sb < nny)
+                    snode = np.where(ok, sb * nnx + sa, 0)
+                    scol = np.where(ok, fidx[comp * n_nodes + snode], -1)
+                    for rc in range(2):
+                        r_full = rc * n_nodes + np.arange(n_nodes)
+                        r_free = fidx[r_full]
+                        val = q[r_full]
+                        keep = (r_free >= 0) & (scol >= 0) & (val != 0.0)
+                        rows.append(r_free[keep])
+                        cols.append(scol[keep])
+                        vals.append(val[keep])
+        K = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                          shape=(self.n_free, self.n_free))
+        K.sort_indices()
+        self._csr, self._csr_E = K, self.coeff
+        return K.copy()
+
+    def tocsc(self):
+        return self.tocsr().tocsc()
+
+    def toarray(self):
+        return self.tocsr().toarray()
+
+    def diagonal(self):
+        return self.tocsr().diagonal()
+
     def set_modulus(self, E):
         """Replace the per-element modulus in place (topopt.py:150-160); the
         same checks as CoefficientField (assembly.py:21-52) guard the copy."""
@@ -157,6 +214,7 @@ class ElasticityOperator:
             raise ValueError("element moduli must be positive")
         _lib.check(_lib.load().ms_problem_set_modulus(self.handle, C.c_void_p(E.ctypes.data)),
                    self._ctx.handle)
+        self._csr = None
 
     def set_density(self, rho_f, p, E_min, E_max):
         """E = simp_modulus(rho_f, p, E_min, E_max) computed on the device into the
@@ -167,6 +225,7 @@ class ElasticityOperator:
             raise ValueError("density field does not match mesh")
         _lib.check(_lib.load().ms_problem_set_density(self.handle, pp, float(p), float(E_min), float(E_max)),
                    self._ctx.handle)
+        self._csr = None
 
     def __del__(self):
         h = getattr(self, "handle", None)

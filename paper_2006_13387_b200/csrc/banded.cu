@@ -144,6 +144,10 @@ void launch_whole_node_check(const Grid& g, const uint8_t* mask, int* fail, cuda
 // level pivots of shifted singular pencils); stored so that the same sweeps
 // apply it: Lc holds the Schur column a_{k+j,k} with 1/d_k on the diagonal
 // (forward sweep -> D^-1 L^-1 b), Lr the unit factor l_{k+j,k} with 1.
+// ldl = 2: the same L D L^T of an SPD band (pivots must be positive) stored
+// for the UNIT sweeps: both bands hold the unit factor, Lc with 1/d_k on the
+// diagonal (applied once per row after the forward sweep), Lr with 1 -- the
+// sweeps' dependent chain is then shuffle + FMA per step, no multiply.
 __global__ void __launch_bounds__(256)
     k_band_potrf(const BandSys* __restrict__ sys, double* __restrict__ Lc,
                  double* __restrict__ Lr, int* fail, int ldl, double* __restrict__ schur) {
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(256)
   for (int k = 0; k < ne; ++k) {
     const int sk = k % S;
     double d = W[sk * S];
-    if (ldl ? !(d != 0.0 && isfinite(d)) : !(d > 0.0)) {
+    if (ldl == 1 ? !(d != 0.0 && isfinite(d)) : !(d > 0.0)) {
       bad = true;
       d = 1.0;
     }
@@ -184,7 +188,10 @@ __global__ void __launch_bounds__(256)
     const double lkk = ldl ? 1.0 : sqrt(d), inv = 1.0 / lkk;
     for (int j = threadIdx.x; j < S; j += blockDim.x) {
       double vc, vr;
-      if (ldl) {
+      if (ldl == 2) {
+        vr = (j == 0) ? 1.0 : W[sk * S + j] * invd;
+        vc = (j == 0) ? invd : vr;
+      } else if (ldl) {
         vc = (j == 0) ? invd : W[sk * S + j];
         vr = (j == 0) ? 1.0 : W[sk * S + j] * invd;
       } else {
@@ -369,7 +376,8 @@ __global__ void __launch_bounds__(kSolveWarps * 32)
 #define MS_L1_MINB 3  // register budget sized for >= 3 resident CTAs per SM (~128 registers)
 #endif
 constexpr int kCh = MS_TMA_CH;  // band columns per stage (divides 32)
-constexpr int kNst = MS_TMA_NST;  // stages per warp
+constexpr int kNst = MS_TMA_NST;  // default stages per warp (bandwidth-bound launches)
+constexpr int kMaxNst = 8;        // deepest ring a launch may ask for (latency-bound launches, pick_nst)
 constexpr int kTmaWarps = MS_TMA_WARPS;
 static_assert(32 % kCh == 0, "stage width must divide 32");
 
@@ -377,6 +385,7 @@ struct Ring {
   double* buf;     // kNst stages of `stage` words
   uint64_t* bar;   // kNst mbarriers
   int stage;       // words per stage (even)
+  int nst;         // stages of this launch (2..kMaxNst)
   uint32_t phase;  // parity bit per stage
 };
 
@@ -395,26 +404,27 @@ constexpr int kPadGuard = 32;
 
 // ring shared-memory header: kTmaWarps * kNst mbarriers, rounded to 16 words
 // (the stages stay 128-byte aligned)
-constexpr int kRingHeaderWords = (kTmaWarps * kNst + 15) & ~15;  // 128-byte aligned stages (TMA boxes)
+constexpr int kRingHeaderWords = (kTmaWarps * kMaxNst + 15) & ~15;  // 128-byte aligned stages (TMA boxes)
 
 // per-warp ring words: kNst stages (+ the zero guard of the padded layout)
-__host__ __device__ inline int ring_warp_words(int stage_words, bool pad) {
-  return kNst * stage_words + (pad ? kPadGuard : 0);
+__host__ __device__ inline int ring_warp_words(int stage_words, bool pad, int nst) {
+  return nst * stage_words + (pad ? kPadGuard : 0);
 }
 
-__device__ __forceinline__ void ring_init(Ring& rg, double* smem, int warp, int lane, int stage_words,
+__device__ __forceinline__ void ring_init(Ring& rg, double* smem, int warp, int lane, int stage_words, int nst,
                                           bool pad = false) {
-  rg.bar = reinterpret_cast<uint64_t*>(smem) + warp * kNst;
-  double* base = smem + kRingHeaderWords + (size_t)warp * ring_warp_words(stage_words, pad);
+  rg.nst = nst;
+  rg.bar = reinterpret_cast<uint64_t*>(smem) + warp * nst;
+  double* base = smem + kRingHeaderWords + (size_t)warp * ring_warp_words(stage_words, pad, nst);
   rg.buf = base + (pad ? kPadGuard : 0);
   rg.stage = stage_words;
   rg.phase = 0;
   if (pad) {  // guard and slot tails must read zero; the copies never touch them
-    for (int i = lane; i < ring_warp_words(stage_words, pad); i += 32) base[i] = 0.0;
+    for (int i = lane; i < ring_warp_words(stage_words, pad, nst); i += 32) base[i] = 0.0;
     __syncwarp();
   }
   if (lane == 0) {
-    for (int st = 0; st < kNst; ++st) mbar_init(rg.bar + st, 1);
+    for (int st = 0; st < nst; ++st) mbar_init(rg.bar + st, 1);
     mbar_fence_init();
   }
 }
@@ -439,30 +449,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 template <bool REV, int P>
-__device__ __forceinline__ void ring_issue_pad(Ring& rg, const CUtensorMap* map, int col0, int n, int c, int lane) {
+__device__ __forceinline__ void ring_issue_pad(Ring& rg, const CUtensorMap* map, int col0, int n, int c, int lane,
+                                               int st) {
   if (lane != 0) return;
   int start, cnt;
   chunk_cols(REV, n, c, start, cnt);
-  const int st = c % kNst;
   mbar_expect_tx(rg.bar + st, (uint32_t)(kCh * P * 8));
   tma_load_2d(rg.buf + (size_t)st * rg.stage, map, 0, col0 + start, rg.bar + st);
 }
 
 template <bool REV>
-__device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int S, int c) {
+__device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int S, int c, int st) {
   int start, cnt;
   chunk_cols(REV, n, c, start, cnt);
   const int64_t w0 = (int64_t)start * S;
   const int64_t a = w0 & ~(int64_t)1;  // 16-byte aligned source (L itself is)
   const uint32_t words = (uint32_t)((cnt * S + (int)(w0 - a) + 1) & ~1);
-  const int st = c % kNst;
   mbar_expect_tx(rg.bar + st, words * 8u);
   bulk_g2s(rg.buf + (size_t)st * rg.stage, L + a, words * 8u, rg.bar + st);
 }
 
 // ym(r): address of the NR values of the sweep's r-th row (r counts the
 // sweep's own steps, i.e. already reversed for REV)
-template <int T, int NR, bool REV, bool PAD, class YMap>
+template <int T, int NR, bool REV, bool PAD, bool UNIT = false, class YMap>
 __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw, YMap ym,
                                                 int lane, Ring& rg, const CUtensorMap* map = nullptr,
                                                 int col0 = 0) {
@@ -471,9 +480,9 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
   const int S = bw + 1;
   const int nch = (n + kCh - 1) / kCh;
   if (PAD) {
-    for (int c = 0; c < min(kNst, nch); ++c) ring_issue_pad<REV, P>(rg, map, col0, n, c, lane);
+    for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue_pad<REV, P>(rg, map, col0, n, c, lane, c);
   } else if (lane == 0) {
-    for (int c = 0; c < min(kNst, nch); ++c) ring_issue<REV>(rg, L, n, S, c);
+    for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue<REV>(rg, L, n, S, c, c);
   }
   auto yat = [&](int r, int c) -> double* { return ym(r) + c; };
 
@@ -489,6 +498,7 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
     rnext[c] = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane, c) : 0.0;
   }
 
+  int stc = 0;
   for (int k0 = 0; k0 < n; k0 += 32) {
 #pragma unroll
     for (int c = 0; c < NR; ++c) {
@@ -503,7 +513,8 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
 #pragma unroll 1
     for (int h = 0; h < 32 && k0 + h < n; h += kCh) {
       const int ch = (k0 + h) / kCh;
-      const int st = ch % kNst;
+      const int st = stc;  // ch % nst as a running counter (nst is a per-launch value)
+      stc = (stc + 1 == rg.nst) ? 0 : stc + 1;
       mbar_wait(rg.bar + st, (rg.phase >> st) & 1u);
       rg.phase ^= 1u << st;
       int start, cnt;
@@ -538,7 +549,7 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
             if (q < cnt) stepP(q, REV ? cnt - 1 - q : q);
         }
         __syncwarp();  // every lane is done with this stage before it is refilled
-        if (ch + kNst < nch) ring_issue_pad<REV, P>(rg, map, col0, n, ch + kNst, lane);
+        if (ch + rg.nst < nch) ring_issue_pad<REV, P>(rg, map, col0, n, ch + rg.nst, lane, st);
         continue;
       }
       const double* sb = rg.buf + (size_t)st * rg.stage + (int)(((int64_t)start * S) & 1);
@@ -561,7 +572,8 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
         if (lane == u) dsave = d;
 #pragma unroll
         for (int c = 0; c < NR; ++c) {
-          const double wk = __shfl_sync(0xffffffffu, acc[c][0] * d, u);
+          // UNIT: unit-diagonal factor, the pivot row's accumulator is final as it stands
+          const double wk = __shfl_sync(0xffffffffu, UNIT ? acc[c][0] : acc[c][0] * d, u);
 #pragma unroll
           for (int s = 0; s < R; ++s) acc[c][s] = fma(-m[s], wk, acc[c][s]);
         }
@@ -575,7 +587,7 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
           if (q < cnt) step(q);
       }
       __syncwarp();  // every lane is done with this stage before it is refilled
-      if (lane == 0 && ch + kNst < nch) ring_issue<REV>(rg, L, n, S, ch + kNst);
+      if (lane == 0 && ch + rg.nst < nch) ring_issue<REV>(rg, L, n, S, ch + rg.nst, st);
     }
     // slot 0 of lane L stopped changing at step L: it holds row k0+L's final
     // accumulator, and w = acc * (1/L_kk) exactly as the pivot step formed it
@@ -613,9 +625,9 @@ __device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int
   const int S = bw + 1;
   const int nch = (n + kCh - 1) / kCh;
   if (PAD) {
-    for (int c = 0; c < min(kNst, nch); ++c) ring_issue_pad<true, P>(rg, map, col0, n, c, lane);
+    for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue_pad<true, P>(rg, map, col0, n, c, lane, c);
   } else if (lane == 0) {
-    for (int c = 0; c < min(kNst, nch); ++c) ring_issue<true>(rg, L, n, S, c);
+    for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue<true>(rg, L, n, S, c, c);
   }
   for (int i = lane; i < 2 * kWin * NR; i += 32) xw[i] = 0.0;
   __syncwarp();
@@ -635,8 +647,10 @@ __device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int
 #pragma unroll
     for (int c = 0; c < NR; ++c) wnext[c] = ym(k0)[c];
   }
+  int stc = 0;
   for (int ch = 0; ch < nch; ++ch) {
-    const int st = ch % kNst;
+    const int st = stc;
+    stc = (stc + 1 == rg.nst) ? 0 : stc + 1;
     int start, cnt, pc;
     const int k = row_of(ch, start, cnt, pc);
     double wp[NR];
@@ -710,29 +724,29 @@ __device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int
     }
     __syncwarp();  // window writes visible; every lane done with the stage before it is refilled
     if (PAD) {
-      if (ch + kNst < nch) ring_issue_pad<true, P>(rg, map, col0, n, ch + kNst, lane);
-    } else if (lane == 0 && ch + kNst < nch) {
-      ring_issue<true>(rg, L, n, S, ch + kNst);
+      if (ch + rg.nst < nch) ring_issue_pad<true, P>(rg, map, col0, n, ch + rg.nst, lane, st);
+    } else if (lane == 0 && ch + rg.nst < nch) {
+      ring_issue<true>(rg, L, n, S, ch + rg.nst, st);
     }
   }
 }
 
 static int ring_stage_words(int max_bw) { return (kCh * (max_bw + 1) + 3) & ~1; }
 
-template <int T, int NR, bool PAD>
+template <int T, int NR, bool PAD, bool UNIT>
 __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_ring(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                     const double* __restrict__ Lr, const double* __restrict__ r,
                     double* __restrict__ ybuf, const int* done, int stage_words,
                     const __grid_constant__ CUtensorMap mapc, const __grid_constant__ CUtensorMap mapr,
-                    int fwd_only) {
+                    int fwd_only, int nst) {
   if (done && *(volatile const int*)done) return;
   extern __shared__ __align__(128) double smem_ring[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sid = blockIdx.x * kTmaWarps + warp;
   if (sid >= nsys) return;
   Ring rg;
-  ring_init(rg, smem_ring, warp, lane, stage_words, PAD);
+  ring_init(rg, smem_ring, warp, lane, stage_words, nst, PAD);
   const BandSys s = sys[sid];
   double* y = ybuf + s.yoff;
   for (int i = lane; i < s.n * NR; i += 32) {
@@ -744,15 +758,15 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   __syncwarp();
   const int n = s.n;
   const int col0 = PAD ? (int)(s.foff / (s.bw + 1)) : 0;  // the system's first column in the TMA view
-  band_sweep_ring<T, NR, false, PAD>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
+  band_sweep_ring<T, NR, false, PAD, UNIT>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
                                      &mapc, col0);
   if (fwd_only) return;  // the backward sweep follows in k_l1_bwd_window
   __syncwarp();
   if (Lr) {
-    band_sweep_ring<T, NR, true, PAD>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; },
+    band_sweep_ring<T, NR, true, PAD, UNIT>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; },
                                       lane, rg, &mapr, col0);
   } else {  // one factor copy: backward sweep by dot products over the column band
-    double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD) +
+    double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD, nst) +
                  (size_t)warp * 256 * NR;
     if constexpr (kCh == 8)
       band_sweep_dot<T, NR, PAD>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
@@ -771,13 +785,13 @@ __device__ __forceinline__ void pair_sync(int pair) {
   asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
 }
 
-template <int T, int NR, bool PAD>
+template <int T, int NR, bool PAD, bool UNIT>
 __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_twist(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                      const double* __restrict__ Lr, const double* __restrict__ Sinv,
                      const double* __restrict__ r, double* __restrict__ ybuf, const int* done, int stage_words,
                      int max_bw, const __grid_constant__ CUtensorMap mapc,
-                     const __grid_constant__ CUtensorMap mapr) {
+                     const __grid_constant__ CUtensorMap mapr, int nst) {
   static_assert(kTmaWarps % 2 == 0, "warp pairs");
   if (done && *(volatile const int*)done) return;
   extern __shared__ __align__(128) double smem_ring[];
@@ -786,8 +800,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   const int sid = blockIdx.x * (kTmaWarps / 2) + pair;
   if (sid >= nsys) return;  // both warps of a pair leave together
   Ring rg;
-  ring_init(rg, smem_ring, warp, lane, stage_words, PAD);
-  const size_t ring_words = kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD);
+  ring_init(rg, smem_ring, warp, lane, stage_words, nst, PAD);
+  const size_t ring_words = kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD, nst);
   double* sB = smem_ring + ring_words + (size_t)pair * 2 * NR * max_bw;  // bottom separator partials
   double* tS = sB + NR * max_bw;                                       // separator right-hand side
   const BandSys s = sys[sid];
@@ -807,11 +821,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   }
   __syncwarp();
   if (role == 0) {
-    band_sweep_ring<T, NR, false, PAD>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg,
+    band_sweep_ring<T, NR, false, PAD, UNIT>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg,
                                        &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
   } else {
     const int nb_own = nB - bw;
-    band_sweep_ring<T, NR, false, PAD>(
+    band_sweep_ring<T, NR, false, PAD, UNIT>(
         Lc + s.foffB, nB, bw,
         [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; }, lane, rg,
         &mapc, PAD ? (int)(s.foffB / (bw + 1)) : 0);
@@ -851,10 +865,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     return;
   }
   if (role == 0) {
-    band_sweep_ring<T, NR, true, PAD>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; },
+    band_sweep_ring<T, NR, true, PAD, UNIT>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; },
                                       lane, rg, &mapr, PAD ? (int)(s.foff / (bw + 1)) : 0);
   } else {
-    band_sweep_ring<T, NR, true, PAD>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane,
+    band_sweep_ring<T, NR, true, PAD, UNIT>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane,
                                       rg, &mapr, PAD ? (int)(s.foffB / (bw + 1)) : 0);
   }
 }
@@ -1005,8 +1019,34 @@ template <int T>
 static int ring_stage_words_t(int max_bw, bool pad) {
   return pad ? kCh * pad_slot_words<T>() : ring_stage_words(max_bw);
 }
-static size_t ring_bytes(int stage_words, bool pad) {
-  return ((size_t)kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, pad)) * sizeof(double);
+static size_t ring_bytes(int stage_words, bool pad, int nst) {
+  return ((size_t)kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, pad, nst)) * sizeof(double);
+}
+
+// Ring depth of a launch.  Launches of several waves are bandwidth-bound:
+// 2 stages keep 4 CTAs per SM resident (config 3: 1.94 ms vs 1.99 ms with
+// 3).  A launch that fits one wave is bound by its bytes in flight per warp
+// instead, so the shared memory its few CTAs leave free goes into deeper
+// rings (MS_L1_NST overrides; measured with the twisted kernel: config 2,
+// one CTA per SM, 0.207 / 0.197 / 0.181 / 0.180 ms at 2 / 3 / 4 / 6 stages;
+// config 3's 8-GPU strip, two CTAs per SM, 0.283 / 0.277 / 0.289 ms at
+// 2 / 3 / 4).
+static int pick_nst(int ctas, size_t stage_bytes_cta, size_t extra_bytes) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("MS_L1_NST");
+    env = e ? std::atoi(e) : -1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = div_up(ctas, sms);
+  int nst = env >= 2 ? env : (per_sm == 1 ? 4 : (per_sm == 2 ? 3 : kNst));
+  nst = std::min(nst, kMaxNst);
+  // the wave's CTAs must stay co-resident (227 KB per SM, 1 KB reserved per CTA)
+  const size_t budget = (size_t)227 * 1024 / std::max(1, std::min(per_sm, 4)) - 1024;
+  while (nst > 2 && kRingHeaderWords * sizeof(double) + extra_bytes + nst * stage_bytes_cta > budget) --nst;
+  return nst;
 }
 
 template <class K>
@@ -1024,31 +1064,37 @@ static const L1Maps& no_maps() {
   return m;
 }
 
-template <int T, int NR, bool PAD>
+template <int T, int NR, bool PAD, bool UNIT>
 static void solve_twist_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                           const double* Lr, const double* Sinv, const double* r, double* ybuf, const int* done,
                           cudaStream_t st, const L1Maps& maps) {
   const int sw = ring_stage_words_t<T>(max_bw, PAD);
-  const size_t smem = ring_bytes(sw, PAD) + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double) +
-                      (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));  // dot-sweep windows
+  const size_t extra = (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double) +
+                       (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));  // separator + dot-sweep windows
+  const int nst = pick_nst(div_up(nsys, kTmaWarps / 2), (size_t)kTmaWarps * sw * sizeof(double),
+                           extra + (PAD ? kTmaWarps * kPadGuard * sizeof(double) : 0));
+  const size_t smem = ring_bytes(sw, PAD, nst) + extra;
   static size_t configured[64] = {};
-  set_smem(k_l1_solve_twist<T, NR, PAD>, smem, configured);
-  { k_l1_solve_twist<T, NR, PAD><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
-      g, sys, nsys, Lc, Lr, Sinv, r, ybuf, done, sw, max_bw, maps.c, maps.r); ms_count_launch(); }
+  set_smem(k_l1_solve_twist<T, NR, PAD, UNIT>, smem, configured);
+  { k_l1_solve_twist<T, NR, PAD, UNIT><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, Sinv, r, ybuf, done, sw, max_bw, maps.c, maps.r, nst); ms_count_launch(); }
 }
 
-template <int T, int NR, bool PAD>
+template <int T, int NR, bool PAD, bool UNIT>
 static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                          const double* Lr, const double* r, double* ybuf, const int* done,
                          cudaStream_t st, const L1Maps& maps) {
   const int sw = ring_stage_words_t<T>(max_bw, PAD);
   // + the dot sweep's x windows (one factor copy)
-  const size_t smem = ring_bytes(sw, PAD) + (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));
+  const size_t extra = Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double);
+  const int nst = pick_nst(div_up(nsys, kTmaWarps), (size_t)kTmaWarps * sw * sizeof(double),
+                           extra + (PAD ? kTmaWarps * kPadGuard * sizeof(double) : 0));
+  const size_t smem = ring_bytes(sw, PAD, nst) + extra;
   static size_t configured[64] = {};  // per instantiation and device
-  set_smem(k_l1_solve_ring<T, NR, PAD>, smem, configured);
+  set_smem(k_l1_solve_ring<T, NR, PAD, UNIT>, smem, configured);
   const bool window = !Lr && NR == 1 && use_window_bwd();
-  { k_l1_solve_ring<T, NR, PAD><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
-      g, sys, nsys, Lc, Lr, r, ybuf, done, sw, maps.c, maps.r, window ? 1 : 0); ms_count_launch(); }
+  { k_l1_solve_ring<T, NR, PAD, UNIT><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
+      g, sys, nsys, Lc, Lr, r, ybuf, done, sw, maps.c, maps.r, window ? 1 : 0, nst); ms_count_launch(); }
   if (window) {
     const int nst = win_stages(max_bw), wsw = win_stage_words(max_bw);
     const size_t wsmem = ((size_t)win_header_words(nst) + (size_t)nst * wsw) * sizeof(double);
@@ -1118,22 +1164,29 @@ bool l1_ring_sweeps_enabled() { return use_ring_sweeps(); }
 template <int T, int NR>
 static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                     const double* Lr, const double* r, double* ybuf, const int* done, cudaStream_t st,
-                    const double* Sinv, bool ring_ok, const L1Maps* maps) {
+                    const double* Sinv, bool ring_ok, const L1Maps* maps, bool unit) {
   // padded TMA ring: elasticity bands with their tensor maps (uniform bw)
   const bool pad = NR == 1 && maps && maps->valid;
   const L1Maps& mp = pad ? *maps : no_maps();
+  // unit-diagonal factors: two-band ring sweeps without the padded layout only
+  if (unit && (pad || !Lr || !(Sinv || (use_ring_sweeps() && ring_ok))))
+    throw Error(-1, "unit-diagonal level-1 factors need the two-band ring sweeps");
   if (Sinv) {
     if (pad)
-      solve_twist_t<T, NR, NR == 1>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
+      solve_twist_t<T, NR, NR == 1, false>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
+    else if (unit)
+      solve_twist_t<T, NR, false, true>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
     else
-      solve_twist_t<T, NR, false>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
+      solve_twist_t<T, NR, false, false>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
     return;
   }
   if (use_ring_sweeps() && ring_ok) {
     if (pad)
-      solve_ring_t<T, NR, NR == 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
+      solve_ring_t<T, NR, NR == 1, false>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
+    else if (unit)
+      solve_ring_t<T, NR, false, true>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
     else
-      solve_ring_t<T, NR, false>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
+      solve_ring_t<T, NR, false, false>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
     return;
   }
   if (!Lr) throw Error(-1, "the register-prefetch level-1 sweeps need the row band (two factor copies)");
@@ -1143,7 +1196,8 @@ static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, con
 
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
-                     const int* done, cudaStream_t st, const double* Sinv, int min_bw, const L1Maps* maps) {
+                     const int* done, cudaStream_t st, const double* Sinv, int min_bw, const L1Maps* maps,
+                     bool unit) {
   if (nsys == 0) return;
   const int T = std::max(1, div_up(max_bw, 32));
   if (min_bw < 0) min_bw = max_bw;
@@ -1152,22 +1206,22 @@ void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, in
   if (Sinv && !ring_ok) throw Error(-1, "twisted level-1 needs every band wider than 32 (T - 1)");
   if (nrhs == 1) {
     switch (T) {
-      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 1: solve_t<1, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 2: solve_t<2, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 3: solve_t<3, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 4: solve_t<4, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 5: solve_t<5, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 6: solve_t<6, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 7: solve_t<7, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 8: solve_t<8, 1>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
       default: throw Error(-1, "level-1 band wider than 256 unsupported");
     }
   } else if (nrhs == 2) {
     switch (T) {
-      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
-      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps); break;
+      case 1: solve_t<1, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 2: solve_t<2, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 3: solve_t<3, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
+      case 4: solve_t<4, 2>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, Sinv, ring_ok, maps, unit); break;
       default: throw Error(-1, "heat level-1 band wider than 128 unsupported");
     }
   } else {

@@ -115,7 +115,7 @@ void make_band_map(CUtensorMap* map, const double* band, int64_t cols, int S, in
 void launch_l1_solve(const Grid& g, const BandSys* sys, int nsys, int max_bw, int nrhs,
                      const double* Lc, const double* Lr, const double* r, double* ybuf,
                      const int* done, cudaStream_t st, const double* Sinv = nullptr, int min_bw = -1,
-                     const L1Maps* maps = nullptr);
+                     const L1Maps* maps = nullptr, bool unit = false);
 bool ring_sweep_ok(int T, int min_bw);
 bool l1_ring_sweeps_enabled();  // false under MS_L1_SWEEP=reg
 bool l1_padded_ring_enabled();  // false under MS_L1_PAD=0

@@ -23,6 +23,7 @@
 #include "comm.cuh"
 #include "common.cuh"
 #include "eigen.cuh"
+#include "generic.cuh"
 #include "operator.cuh"
 #include "topopt.cuh"
 
@@ -121,6 +122,7 @@ void dev_free(void* p) {
 // above it the twisted kernel needs a second wave (measured at config 5,
 // 1,024 subdomains: twisted 2.52e9 vs plain 3.29e9 DOF-iter/s; config 2,
 // 256 subdomains: twisted 1.96e9 vs plain 1.35e9)
+constexpr bool kL1UnitDefault = true;  // 1-4% faster sweeps in every regime (config 2: 0.188 -> 0.180 ms, config 3: 1.94 -> 1.93 ms)
 static int twist_max_subdomains(int device) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -418,6 +420,7 @@ struct ms_precond {
   bool one_copy = false;  // plain banded level 1 with the column band only (dot-form backward sweep)
   bool bitwise = false;   // multi-rank results bit-identical to one rank (MS_DIST_BITWISE=1)
   bool pad = false;       // padded TMA ring (uniform bw), maps below
+  bool unit = false;      // unit-diagonal L D L^T level-1 factors (sweep chain without the pivot multiply)
   L1Maps maps;
   bool dense = false;  // MS_LOCAL_DENSE_INV: packed explicit inverses in Xinv
   int nrhs = 1;        // 2: heat level-1 (scalar factor applied to both blocks)
@@ -770,7 +773,7 @@ static void precond_apply_dist_grouped(ms_precond* pc, const double* r, double* 
       launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
     else
       launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st,
-                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps);
+                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps, pc->unit);
     pf.end(MS_PROF_LEVEL1, it, st, a);
   }
   Xfer yx[2];
@@ -837,7 +840,7 @@ static void precond_apply_full(ms_precond* pc, const double* r, double* z, PcgSc
       launch_l1_dense_apply(P->g, pc->sys.p + pc->s0, ns, pc->dense_nt, pc->Xinv.p, r, pc->ybuf.p, done, st);
     else
       launch_l1_solve(P->g, pc->sys.p + pc->s0, ns, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r, pc->ybuf.p, done, st,
-                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps);
+                      pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps, pc->unit);
     pf.end(MS_PROF_LEVEL1, it, st, a);
     if (dist) exchange_ybuf(pc);
   }
@@ -1317,6 +1320,16 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       pc->one_copy = !pc->dense && copies_env == 1 && l1_ring_sweeps_enabled() &&
                      ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
     }
+    // Unit-diagonal L D L^T factors (MS_L1_UNIT=0/1): the pivot multiply leaves
+    // the sweeps' dependent chain (shuffle + FMA per step instead of multiply +
+    // shuffle + FMA); two-band ring sweeps in the plain (non-padded) layout.
+    {
+      int unit_env = -1;
+      if (const char* e = getenv("MS_L1_UNIT")) unit_env = std::atoi(e);
+      const bool can = !pc->dense && !pc->one_copy && !pc->pad && l1_ring_sweeps_enabled() &&
+                       ring_sweep_ok(std::max(1, div_up(pc->max_bw, 32)), pc->min_bw);
+      pc->unit = can && (unit_env == 1 || (unit_env != 0 && kL1UnitDefault));
+    }
     if (pc->twisted) {
       // natural bands (assembly) -> top / bottom bands -> partial Cholesky of
       // both halves -> explicit inverse of the separator's Schur complement
@@ -1361,7 +1374,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
       half_d.upload(halves.data(), halves.size(), st);
       DBuf<double> schur;
       schur.alloc((size_t)2 * ns * mb2);
-      launch_band_potrf(half_d.p, 2 * ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st, 0, schur.p);
+      launch_band_potrf(half_d.p, 2 * ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st, pc->unit ? 2 : 0, schur.p);
       check_fail(fail, st, "level-1 subdomain matrix");
       launch_schur_inverse(pc->sys.p + pc->s0, ns, pc->max_bw, schur.p, pc->Sinv.p, fail.p, st);
       check_fail(fail, st, "level-1 subdomain separator");
@@ -1377,7 +1390,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
         pc->Lr.alloc(foff + 2);
         pc->Lr.zero(st);
       }
-      launch_band_potrf(pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st);
+      launch_band_potrf(pc->sys.p + pc->s0, ns, pc->max_bw, pc->Lc.p, pc->Lr.p, fail.p, st, pc->unit ? 2 : 0);
       check_fail(fail, st, "level-1 subdomain matrix");
     } else {
       launch_l1_assemble(g, P->ke, P->E.p, P->mask.p, pc->sys.p + pc->s0, ns, pc->Lc.p, st);
@@ -1423,6 +1436,7 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     pc->info.n_subdomains = pc->nsys;
     pc->info.level1_twisted = pc->twisted ? 1 : 0;
     pc->info.n_subdomains_local = pc->s1 - pc->s0;
+    pc->info.level1_unit = pc->unit ? 1 : 0;
     pc->info.level1_copies = pc->dense ? 0 : (pc->one_copy ? 1 : 2);
     pc->info.local_bytes = pc->dense ? (double)ns * packed_words(pc->dense_nt) * sizeof(double)
                                      : (double)(foff * (pc->one_copy ? 1 : 2) + (pc->twisted ? pc->Sinv.n : 0)) *
@@ -1800,7 +1814,7 @@ int ms_precond_bench(ms_precond* pc, int reps, double* ms) {
                               nullptr, st);
       else
         launch_l1_solve(g, pc->sys.p + pc->s0, pc->s1 - pc->s0, pc->max_bw, pc->nrhs, pc->Lc.p, pc->Lr.p, r,
-                        pc->ybuf.p, nullptr, st, pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps);
+                        pc->ybuf.p, nullptr, st, pc->twisted ? pc->Sinv.p : nullptr, pc->min_bw, &pc->maps, pc->unit);
     });
   if (pc->has_coarse) {
     ms[MS_BENCH_RESTRICT] = timeit([&] {
@@ -2032,6 +2046,235 @@ int ms_pcg_solve(ms_problem* P, ms_precond* pc, const double* b, double tol, int
     rep->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   }
   MS_API_END(P ? P->ctx : nullptr)
+}
+
+// ---------------------------------------------------------------------------
+// Generic PCG (the reference's duck-typed seams, krylov.py:73-78, 90):
+// any operator (the Q1 problem, a CSR matrix on the device, a host callback)
+// with any preconditioner (none, the two-level one, a host callback).  The
+// Krylov vectors, dot products and scalar recurrences stay on the device; a
+// callback sees host copies of its input / output.
+
+struct ms_csr {
+  ms_ctx* ctx = nullptr;
+  int64_t n = 0, nnz = 0;
+  DBuf<int64_t> indptr;
+  DBuf<int> indices;
+  DBuf<double> data, vin, vout;
+};
+
+int ms_csr_create(ms_ctx* ctx, int64_t n, const int64_t* indptr, const int* indices, const double* data,
+                  ms_csr** out) {
+  MS_API_BEGIN
+  if (!ctx || !indptr || !out || n < 1) throw Error(MS_E_INVALID, "null argument or empty matrix");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const int64_t nnz = indptr[n];
+  if (indptr[0] != 0 || nnz < 0 || (nnz > 0 && (!indices || !data)))
+    throw Error(MS_E_INVALID, "malformed CSR row pointers");
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] < indptr[i]) throw Error(MS_E_INVALID, "CSR row pointers must be non-decreasing");
+  for (int64_t e = 0; e < nnz; ++e)
+    if (indices[e] < 0 || indices[e] >= n) throw Error(MS_E_INVALID, "CSR column index out of range");
+  auto A = std::make_unique<ms_csr>();
+  A->ctx = ctx;
+  A->n = n;
+  A->nnz = nnz;
+  A->indptr.upload(indptr, n + 1, ctx->st);
+  A->indices.upload(indices, nnz, ctx->st);
+  A->data.upload(data, nnz, ctx->st);
+  MS_CUDA(cudaStreamSynchronize(ctx->st));
+  *out = A.release();
+  MS_API_END(ctx)
+}
+
+int ms_csr_destroy(ms_csr* A) {
+  if (!A) return MS_OK;
+  cudaSetDevice(A->ctx->device);
+  cudaStreamSynchronize(A->ctx->st);
+  delete A;
+  return MS_OK;
+}
+
+int ms_csr_apply(ms_csr* A, const double* v, double* out) {
+  MS_API_BEGIN
+  if (!A || !v || !out) throw Error(MS_E_INVALID, "null argument");
+  MS_CUDA(cudaSetDevice(A->ctx->device));
+  const cudaStream_t st = A->ctx->st;
+  const double* dv = v;
+  if (!is_device_ptr(v)) {
+    if (A->vin.n < (size_t)A->n) A->vin.alloc(A->n);
+    MS_CUDA(cudaMemcpyAsync(A->vin.p, v, A->n * sizeof(double), cudaMemcpyHostToDevice, st));
+    dv = A->vin.p;
+  }
+  double* dout = out;
+  const bool host_out = !is_device_ptr(out);
+  if (host_out) {
+    if (A->vout.n < (size_t)A->n) A->vout.alloc(A->n);
+    dout = A->vout.p;
+  }
+  launch_csr_spmv(A->n, A->nnz, A->indptr.p, A->indices.p, A->data.p, dv, dout, st);
+  if (host_out) MS_CUDA(cudaMemcpyAsync(out, dout, A->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  MS_API_END(A ? A->ctx : nullptr)
+}
+
+namespace {
+struct PinnedBuf {
+  double* p = nullptr;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(int64_t n) { MS_CUDA(cudaMallocHost(&p, n * sizeof(double))); }
+};
+
+// out = Op(in), both device vectors of length n
+void linop_apply(ms_ctx* ctx, const ms_linop* op, int64_t n, const double* in, double* out, PinnedBuf& hin,
+                 PinnedBuf& hout) {
+  const cudaStream_t st = ctx->st;
+  switch (op ? op->kind : MS_LINOP_NONE) {
+    case MS_LINOP_NONE:
+      MS_CUDA(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      break;
+    case MS_LINOP_PROBLEM: {
+      const int rc = ms_operator_apply(static_cast<ms_problem*>(op->handle), in, out);
+      if (rc != MS_OK) throw Error(rc, ctx->err.empty() ? "operator apply failed" : ctx->err);
+      break;
+    }
+    case MS_LINOP_PRECOND: {
+      const int rc = ms_precond_apply(static_cast<ms_precond*>(op->handle), in, out);
+      if (rc != MS_OK) throw Error(rc, ctx->err.empty() ? "preconditioner apply failed" : ctx->err);
+      break;
+    }
+    case MS_LINOP_CSR: {
+      ms_csr* A = static_cast<ms_csr*>(op->handle);
+      launch_csr_spmv(A->n, A->nnz, A->indptr.p, A->indices.p, A->data.p, in, out, st);
+      break;
+    }
+    case MS_LINOP_CALLBACK: {
+      if (!hin.p) hin.alloc(n);
+      if (!hout.p) hout.alloc(n);
+      MS_CUDA(cudaMemcpyAsync(hin.p, in, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      MS_CUDA(cudaStreamSynchronize(st));
+      const int rc = op->fn(op->user, hin.p, hout.p, n);
+      if (rc != 0) throw Error(MS_E_CALLBACK, "operator / preconditioner callback failed");
+      MS_CUDA(cudaMemcpyAsync(out, hout.p, n * sizeof(double), cudaMemcpyHostToDevice, st));
+      break;
+    }
+    default:
+      throw Error(MS_E_INVALID, "unknown ms_linop kind");
+  }
+}
+
+int64_t linop_dim(const ms_linop* op) {
+  if (!op) return -1;
+  switch (op->kind) {
+    case MS_LINOP_PROBLEM: return op->handle ? static_cast<ms_problem*>(op->handle)->n_free : -1;
+    case MS_LINOP_PRECOND: return op->handle ? static_cast<ms_precond*>(op->handle)->prob->n_free : -1;
+    case MS_LINOP_CSR: return op->handle ? static_cast<ms_csr*>(op->handle)->n : -1;
+    default: return -1;
+  }
+}
+}  // namespace
+
+int ms_pcg_solve_generic(ms_ctx* ctx, int64_t n, const ms_linop* A, const ms_linop* M, const double* b,
+                         double tol, int maxit, double* x, ms_report* rep, double* residuals, double* alphas,
+                         double* betas) {
+  MS_API_BEGIN
+  if (!ctx || !A || !b || !x || n < 1) throw Error(MS_E_INVALID, "null argument");
+  if (!(tol > 0.0 && tol < 1.0)) throw Error(MS_E_INVALID, "tolerance must be in (0, 1)");
+  if (maxit < 0) throw Error(MS_E_INVALID, "maxit must be >= 0");
+  if (A->kind == MS_LINOP_NONE || A->kind == MS_LINOP_PRECOND) throw Error(MS_E_INVALID, "A must be an operator");
+  if (M && M->kind != MS_LINOP_NONE && M->kind != MS_LINOP_PRECOND && M->kind != MS_LINOP_CALLBACK)
+    throw Error(MS_E_INVALID, "M must be none, a two-level preconditioner or a callback");
+  if ((A->kind == MS_LINOP_CALLBACK && !A->fn) || (M && M->kind == MS_LINOP_CALLBACK && !M->fn))
+    throw Error(MS_E_INVALID, "callback operator without a function");
+  for (const ms_linop* op : {A, M}) {
+    const int64_t d = linop_dim(op);
+    if (d >= 0 && d != n) throw Error(MS_E_INVALID, "operator dimension does not match the right-hand side");
+  }
+  if (ctx->world() > 1) throw Error(MS_E_INVALID, "the generic PCG runs on one rank");
+  MS_CUDA(cudaSetDevice(ctx->device));
+  const auto wall0 = std::chrono::steady_clock::now();
+  const long long launches0 = ms_launch_counter();
+  const cudaStream_t st = ctx->st;
+  const bool precond = M && M->kind != MS_LINOP_NONE;
+  DBuf<double> xd, r, p, z, q, partials, hres, halpha, hbeta;
+  DBuf<PcgScalars> sc;
+  xd.alloc(n);
+  r.alloc(n);
+  p.alloc(n);
+  q.alloc(n);
+  if (precond) z.alloc(n);
+  partials.alloc(reduce_blocks() + 8);
+  hres.alloc(maxit + 1);
+  halpha.alloc(std::max(maxit, 1));
+  hbeta.alloc(std::max(maxit, 1));
+  sc.alloc(1);
+  PinnedBuf hin, hout;
+  MS_CUDA(cudaMemcpyAsync(r.p, b, n * sizeof(double), cudaMemcpyDefault, st));  // r = b
+  xd.zero(st);
+  p.zero(st);
+  PcgScalars hs{};
+  hs.tol = tol;
+  hs.maxit = maxit;
+  hs.first = 1;
+  hs.done = maxit == 0 ? 1 : 0;
+  MS_CUDA(cudaMemcpyAsync(sc.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+  cudaEvent_t t0, t1;
+  MS_CUDA(cudaEventCreate(&t0));
+  MS_CUDA(cudaEventCreate(&t1));
+  MS_CUDA(cudaEventRecord(t0, st));
+  launch_init_norm(n, r.p, sc.p, partials.p, hres.p, st);
+  auto poll = [&]() {
+    MS_CUDA(cudaMemcpyAsync(&hs, sc.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    MS_CUDA(cudaStreamSynchronize(st));
+  };
+  // callbacks synchronise every iteration anyway; device-only operators are polled every 8
+  const bool host_side = A->kind == MS_LINOP_CALLBACK || (precond && M->kind == MS_LINOP_CALLBACK);
+  const int every = host_side ? 1 : 8;
+  poll();  // zero right-hand side: converged before the first apply
+  double* zp = precond ? z.p : r.p;
+  if (!hs.done) {
+    if (precond) linop_apply(ctx, M, n, r.p, z.p, hin, hout);
+    launch_rz(n, r.p, zp, sc.p, partials.p, hbeta.p, st);
+  }
+  int it = 0;
+  while (!hs.done && it < maxit) {
+    launch_direction(n, zp, p.p, sc.p, st);                       // p = z + beta p
+    linop_apply(ctx, A, n, p.p, q.p, hin, hout);                  // q = A p
+    launch_pq(n, p.p, q.p, sc.p, partials.p, halpha.p, st);       // alpha
+    launch_pcg_update(n, xd.p, p.p, r.p, q.p, sc.p, partials.p, hres.p, st);  // x, r, ||r||
+    ++it;
+    if (host_side) {
+      poll();
+      if (hs.converged) break;  // the reference leaves before the next M apply (krylov.py:121-123)
+    }
+    if (precond) linop_apply(ctx, M, n, r.p, z.p, hin, hout);
+    launch_rz(n, r.p, zp, sc.p, partials.p, hbeta.p, st);         // beta
+    if (!host_side && (it % every == 0 || it == maxit)) poll();
+  }
+  MS_CUDA(cudaEventRecord(t1, st));
+  poll();
+  MS_CUDA(cudaMemcpyAsync(x, xd.p, n * sizeof(double), cudaMemcpyDefault, st));
+  MS_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  MS_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  const int iters = hs.iter;
+  if (residuals) MS_CUDA(cudaMemcpy(residuals, hres.p, (iters + 1) * sizeof(double), cudaMemcpyDefault));
+  if (alphas && iters > 0) MS_CUDA(cudaMemcpy(alphas, halpha.p, iters * sizeof(double), cudaMemcpyDefault));
+  const int nbeta = hs.converged ? iters - 1 : iters;
+  if (betas && nbeta > 0) MS_CUDA(cudaMemcpy(betas, hbeta.p, nbeta * sizeof(double), cudaMemcpyDefault));
+  if (rep) {
+    rep->kernel_launches = ms_launch_counter() - launches0;
+    rep->iterations = iters;
+    rep->converged = hs.converged;
+    rep->final_residual = hs.res;
+    rep->t_solve = ms * 1e-3;
+    rep->t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  }
+  MS_API_END(ctx)
 }
 
 // ---------------------------------------------------------------------------

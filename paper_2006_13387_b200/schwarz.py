@@ -234,5 +234,6 @@ def build_preconditioner(tag, op, mesh, part, coeff, dirichlet_nodes, opts=None,
         "coarse_bytes": inf.coarse_bytes, "level1": level1, "level1_operator": variant.level1, "delta": delta, "local_solver": local_solver,
         "coarse_solve": coarse_solve, "level1_twisted": bool(inf.level1_twisted),
         "level1_copies": int(inf.level1_copies), "n_subdomains_local": int(inf.n_subdomains_local),
+        "level1_unit": int(inf.level1_unit),
     }
     return TwoLevelPreconditioner(variant, op, h, info)

@@ -583,6 +583,32 @@ def test_twisted_level1_matches_plain_sweeps(tag, rng, monkeypatch):
 
 @pytest.mark.parametrize("twist", ["0", "1"])
 @pytest.mark.parametrize("tag", ["EH+Rot", "HH+Rot"])
+def test_unit_diagonal_level1_matches_cholesky(tag, twist, rng, monkeypatch):
+    """Unit-diagonal L D L^T level-1 factors (the pivot multiply off the
+    sweeps' dependent chain) against the Cholesky factors of the same
+    subdomain matrices, plain and twisted: same local solves to round-off
+    (schwarz.py:97-109 / :112-140), same PCG solve."""
+    from paper_2006_13387_b200.solve import setup_spec
+
+    spec = configs.config1(seed=0, n=64, H=16, delta=2)
+    monkeypatch.setenv("MS_L1_TWIST", twist)
+    out = {}
+    for unit in ("0", "1"):
+        monkeypatch.setenv("MS_L1_UNIT", unit)
+        mesh, op, l1 = setup_spec(spec, tag)
+        assert l1.info["level1_unit"] == int(unit)
+        out[unit] = (op, l1)
+    for _ in range(3):
+        v = rng.standard_normal(out["1"][0].n_free)
+        za, zb = out["0"][1].apply(v), out["1"][1].apply(v)
+        assert rel(zb, za) <= 1e-9, rel(zb, za)
+    x1, r1 = G.pcg_solve(out["1"][0], spec.rhs(), out["1"][1], tol=1e-8, maxit=5000)
+    x0, r0 = G.pcg_solve(out["0"][0], spec.rhs(), out["0"][1], tol=1e-8, maxit=5000)
+    assert r1.converged and r0.converged and rel(x1, x0) <= 1e-7
+
+
+@pytest.mark.parametrize("twist", ["0", "1"])
+@pytest.mark.parametrize("tag", ["EH+Rot", "HH+Rot"])
 def test_one_copy_level1_matches_two_copy(tag, twist, rng, monkeypatch):
     """One factor copy (backward sweep by dot products over the column band)
     against the column + row band sweeps, plain and twisted: same local
