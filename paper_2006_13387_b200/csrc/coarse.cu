@@ -569,6 +569,194 @@ __global__ void __launch_bounds__(kCombineThreads, MS_CB_MINB)
   }
 }
 
+// Same combine for the implicit (non-vector) basis with the level-1 cover
+// metadata of the cell staged once per CTA: the per-node chain cover table ->
+// subdomain extents -> local-vector offset -> y (three dependent global loads
+// per node above) becomes shared-memory lookups plus the y load itself, and NU
+// nodes per thread are in flight.  Same values, same summation order per
+// thread as k_combine<false> (bitwise identical z and r.z).
+constexpr int kCellMax = 72;  // largest cell side (nodes) the staged tables hold
+template <int NU>
+__global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
+    k_combine2(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, CoarseDev cd, int has_coarse, int Nx, int Ny,
+               int J0, const double* __restrict__ y0, const double* __restrict__ r, double* __restrict__ z,
+               PcgScalars* sc, double* partials, double* beta_hist) {
+  if (sc && sc->done) return;
+  __shared__ double sred[kCombineThreads / 32];
+  __shared__ int4 sx[2 * kCellMax], sy[2 * kCellMax];  // per column / row and cover: (I, lo, len, -)
+  __shared__ int64_t syoff[16];                        // yoff of (Jmin + dj, Imin + di)
+  const int64_t nn = g.n_nodes;
+  const int ci = blockIdx.x, cj = J0 + blockIdx.y;
+  const int mx = g.nx / Nx, my = g.ny / Ny;
+  const int a_lo = ci * mx, a_hi = (ci == Nx - 1) ? g.nx : a_lo + mx - 1;
+  const int b_lo = cj * my, b_hi = (cj == Ny - 1) ? g.ny : b_lo + my - 1;
+  const int w = a_hi - a_lo + 1, hgt = b_hi - b_lo + 1;
+  bool cok[4];
+  int ck[4], cns[4];
+  int64_t cpo[4];
+  __shared__ double cy[4][2 * kMaxModes + 1];
+  const int NL = has_coarse ? cd.NLx * cd.NLy : 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int I = ci + (c & 1), J = cj + (c >> 1);
+    cok[c] = has_coarse && I >= 1 && I <= Nx - 1 && J >= 1 && J <= Ny - 1;
+    ck[c] = cok[c] ? (J - 1) * (Nx - 1) + (I - 1) : 0;
+    cns[c] = cok[c] ? __ldg(cd.nsel + ck[c]) : 0;
+    cpo[c] = cok[c] ? __ldg(cd.psioff + ck[c]) : 0;
+  }
+  if (threadIdx.x < 4 * (2 * kMaxModes + 1)) {
+    const int c = threadIdx.x / (2 * kMaxModes + 1), m = threadIdx.x % (2 * kMaxModes + 1);
+    double v = 0.0;
+    if (cok[c]) {
+      if (m < 2 * cns[c])
+        v = y0[__ldg(cd.hoff + ck[c]) + m];
+      else if (m == 2 * kMaxModes && cd.enrich)
+        v = y0[cd.roff + ck[c]];
+    }
+    cy[c][m] = v;
+  }
+  // cover tables of the cell's columns and rows; covers are listed in
+  // ascending block order, so the first cover of the first column / row is
+  // the smallest block index of the cell
+  // (the first COVERED column / row: clamped boundary nodes may have no cover)
+  int Imin = -1, Jmin = -1;
+  for (int a = a_lo; a <= a_hi && Imin < 0; ++a) Imin = __ldg(l1.xcov + a * 4);
+  for (int b = b_lo; b <= b_hi && Jmin < 0; ++b) Jmin = __ldg(l1.ycov + b * 4);
+  for (int t = threadIdx.x; t < 2 * (w + hgt); t += kCombineThreads) {
+    const bool isx = t < 2 * w;
+    const int u = isx ? t : t - 2 * w;
+    const int pos = (isx ? a_lo : b_lo) + (u >> 1);
+    const int B = __ldg((isx ? l1.xcov : l1.ycov) + pos * 4 + (u & 1));
+    int4 e = make_int4(B, 0, 1, 0);
+    if (B >= 0) {
+      e.y = __ldg((isx ? l1.xlo : l1.ylo) + B);
+      e.z = __ldg((isx ? l1.xlen : l1.ylen) + B);
+    }
+    (isx ? sx : sy)[u] = e;
+  }
+  if (threadIdx.x >= 64 && threadIdx.x < 80) {
+    const int dj = (threadIdx.x - 64) >> 2, di = (threadIdx.x - 64) & 3;
+    const int J = Jmin + dj, I = Imin + di;
+    syoff[threadIdx.x - 64] = (Imin >= 0 && Jmin >= 0 && J < l1.NbY && I < l1.NbX) ? __ldg(l1.yoff + J * l1.NbX + I) : 0;
+  }
+  __syncthreads();
+  double dot = 0.0;
+  const int total = w * hgt;
+  for (int t0 = threadIdx.x; t0 < total; t0 += NU * kCombineThreads) {
+    int a[NU], b[NU];
+    int64_t n[NU];
+    bool ok[NU];
+    double2 v[NU][2][2], c4a[NU], c4b[NU], p4a[NU], p4b[NU];
+    double rx[NU], ry[NU];
+    uint8_t mk[NU][2];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int t = t0 + u * kCombineThreads;
+      ok[u] = t < total;
+      const int tt = ok[u] ? t : 0;
+      const int lb = tt / w, la = tt - lb * w;
+      b[u] = b_lo + lb;
+      a[u] = a_lo + la;
+      n[u] = (int64_t)b[u] * g.nnx + a[u];
+#pragma unroll
+      for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti) {
+          const int4 ex = sx[2 * la + ti], ey = sy[2 * lb + tj];
+          v[u][tj][ti] = make_double2(0.0, 0.0);
+          if (ok[u] && ey.x >= 0 && ex.x >= 0) {
+            const int ln = (ex.z <= ey.z) ? (b[u] - ey.y) * ex.z + (a[u] - ex.y) : (a[u] - ex.y) * ey.z + (b[u] - ey.y);
+            const int dj = ey.x - Jmin, di = ex.x - Imin;
+            const int64_t off = (dj >= 0 && dj < 4 && di >= 0 && di < 4) ? syoff[dj * 4 + di]
+                                                                         : __ldg(l1.yoff + ey.x * l1.NbX + ex.x);
+            v[u][tj][ti] = __ldg(reinterpret_cast<const double2*>(l1.ybuf + off + 2 * ln));
+          }
+        }
+      c4a[u] = c4b[u] = p4a[u] = p4b[u] = make_double2(0.0, 0.0);
+      if (has_coarse && ok[u]) {
+        const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n[u];
+        const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n[u];
+        c4a[u] = __ldg(c2);
+        c4b[u] = __ldg(c2 + 1);
+        p4a[u] = __ldg(p2);
+        p4b[u] = __ldg(p2 + 1);
+      }
+      mk[u][0] = ok[u] ? mask[n[u]] : 0;
+      mk[u][1] = ok[u] ? mask[n[u] + nn] : 0;
+      rx[u] = (sc && ok[u]) ? r[n[u]] : 0.0;
+      ry[u] = (sc && ok[u]) ? r[n[u] + nn] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      if (!ok[u]) continue;
+      double zx = 0.0, zy = 0.0;
+#pragma unroll
+      for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti) {
+          zx += v[u][tj][ti].x;
+          zy += v[u][tj][ti].y;
+        }
+      if (has_coarse) {
+        double cxs = 0.0, cys = 0.0;
+        const double ch4[4] = {c4a[u].x, c4a[u].y, c4b[u].x, c4b[u].y};
+        const double ps4[4] = {p4a[u].x, p4a[u].y, p4b[u].x, p4b[u].y};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (!cok[c]) continue;
+          const int I = ci + (c & 1), J = cj + (c >> 1);
+          cxs += ps4[c] * cy[c][0];
+          cys += ps4[c] * cy[c][1];
+          if (cns[c] > 1) {  // rare: extra modes from the per-centre store
+            const int ln = (a[u] - (I - 1) * cd.mex) + (b[u] - (J - 1) * cd.mey) * cd.NLx;
+            const double* ps = cd.psi + cpo[c] + ln;
+            for (int m = 1; m < cns[c]; ++m) {
+              const double vv = ch4[c] * __ldg(ps + (int64_t)m * NL);
+              cxs += vv * cy[c][2 * m];
+              cys += vv * cy[c][2 * m + 1];
+            }
+          }
+          if (cd.enrich) {
+            double ex, ey;
+            rot_xy(cd, I, J, a[u], b[u], ex, ey);
+            cxs += __dmul_rn(ch4[c], ex) * cy[c][2 * kMaxModes];
+            cys += __dmul_rn(ch4[c], ey) * cy[c][2 * kMaxModes];
+          }
+        }
+        zx += cxs;
+        zy += cys;
+      }
+      zx = mk[u][0] ? zx : 0.0;
+      zy = mk[u][1] ? zy : 0.0;
+      z[n[u]] = zx;
+      z[n[u] + nn] = zy;
+      if (sc) dot += zx * rx[u] + zy * ry[u];
+    }
+  }
+  if (!sc) return;
+  const double bs = block_sum(dot, sred);
+  double tot;
+  if (grid_reduce_dist(bs, partials, (J0 + blockIdx.y) * gridDim.x + blockIdx.x, sc->dist && sc->bitwise,
+                       &sc->tickets[2], &tot, sred)) {
+    if (threadIdx.x == 0) {
+      if (sc->dist)
+        sc->part[PART_RZ] = tot;
+      else
+        fin_beta(sc, tot, beta_hist);
+    }
+  }
+}
+
+static int combine_variant() {
+  static int v = [] {
+    // A/B knob: 0 = per-node cover lookups, 1 / 2 = staged tables with 1 / 2 nodes per thread in flight
+    // (config 3 in the PCG loop: 0.139 / 0.133 / 0.201 ms -- two nodes in flight spill at 3 CTAs per SM)
+    const char* e = getenv("MS_COMBINE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 int combine_threads() { return kCombineThreads; }
 
 void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const CoarseDev* cd,
@@ -579,7 +767,15 @@ void launch_combine(const Grid& g, const uint8_t* mask, const L1Dev* l1, const C
   if (l1) l1v = *l1;
   if (cd) cdv = *cd;
   if (J1 < 0) J1 = Ny;
-  if (cd && cd->vec)
+  const int cell_w = g.nx / Nx + 1, cell_h = g.ny / Ny + 1;
+  if (l1 && !(cd && cd->vec) && combine_variant() > 0 && cell_w <= kCellMax && cell_h <= kCellMax) {
+    if (combine_variant() == 1)
+      { k_combine2<1><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, cdv, cd ? 1 : 0, Nx, Ny, J0, y0, r, z,
+                                                                    sc, partials, beta_hist); ms_count_launch(); }
+    else
+      { k_combine2<2><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, cdv, cd ? 1 : 0, Nx, Ny, J0, y0, r, z,
+                                                                    sc, partials, beta_hist); ms_count_launch(); }
+  } else if (cd && cd->vec)
     { k_combine<true><<<dim3(Nx, J1 - J0), kCombineThreads, 0, st>>>(g, mask, l1v, l1 ? 1 : 0, cdv, 1, Nx, Ny, J0,
                                                                    y0, r, z, sc, partials, beta_hist); ms_count_launch(); }
   else

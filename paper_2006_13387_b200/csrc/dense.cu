@@ -537,56 +537,181 @@ void dense_spd_inverse(int N, const double* A, double* packed_inv, double* work,
 // ---------------------------------------------------------------------------
 // packed-tile SYMV (batch 1): per tile, u = X_IJ f_J (-> y_I) and, off the
 // diagonal, v = X_IJ^T f_I (-> y_J); partials are reduced in a fixed order.
+// Each CTA streams kSymvTilesPerCta consecutive tiles, the next tile's 32 KB
+// loaded into registers while the current one is reduced (one short-lived CTA
+// per tile left the loads of a tile exposed: 143 us for config 3's 584 MB).
+constexpr int kSymvTilesPerCta = 8;
+
 __global__ void __launch_bounds__(256)
     k_symv_tiles(int N, int nt, const double* __restrict__ X, const double* __restrict__ f,
-                 double* __restrict__ part, const int* done, int64_t t_begin) {
+                 double* __restrict__ part, const int* done, int64_t t_begin, int64_t t_end) {
   if (done && *(volatile const int*)done) return;
-  __shared__ double sv[16][T + 1];
-  const int64_t t = t_begin + blockIdx.x;
-  int i, j;
-  tile_ij(t, i, j);
+  __shared__ double sv[2][16][T + 1];
+  const int64_t t0 = t_begin + (int64_t)blockIdx.x * kSymvTilesPerCta;
+  const int64_t t1 = t0 + kSymvTilesPerCta < t_end ? t0 + kSymvTilesPerCta : t_end;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const double* Xt = X + t * T * T;
-  double fj[4], fi[4];
+  double2 cur[8], nxt[8];
+  auto load = [&](int64_t t, double2(&dst)[8]) {
+    const double* Xt = X + t * T * T;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int cj = j * T + tx * 4 + q, ri = i * T + ty * 4 + q;
-    fj[q] = cj < N ? f[cj] : 0.0;
-    fi[q] = ri < N ? f[ri] : 0.0;
-  }
-  double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
+      dst[2 * rr] = __ldg(row);
+      dst[2 * rr + 1] = __ldg(row + 1);
+    }
+  };
+  load(t0, cur);
+  int i, j;
+  tile_ij(t0, i, j);
+  for (int64_t t = t0; t < t1; ++t) {
+    if (t + 1 < t1) load(t + 1, nxt);
+    double fj[4], fi[4];
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
-    const double2 x01 = __ldg(row), x23 = __ldg(row + 1);
-    u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
-    v[0] += x01.x * fi[rr];
-    v[1] += x01.y * fi[rr];
-    v[2] += x23.x * fi[rr];
-    v[3] += x23.y * fi[rr];
-  }
+    for (int q = 0; q < 4; ++q) {
+      const int cj = j * T + tx * 4 + q, ri = i * T + ty * 4 + q;
+      fj[q] = cj < N ? f[cj] : 0.0;
+      fi[q] = ri < N ? f[ri] : 0.0;
+    }
+    double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2 x01 = cur[2 * rr], x23 = cur[2 * rr + 1];
+      u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
+      v[0] += x01.x * fi[rr];
+      v[1] += x01.y * fi[rr];
+      v[2] += x23.x * fi[rr];
+      v[3] += x23.y * fi[rr];
+    }
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
-  }
-  double* pu = part + t * 2 * T;
-  double* pv = pu + T;
-  if (tx == 0) {
+    for (int rr = 0; rr < 4; ++rr) {
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) pu[ty * 4 + rr] = u[rr];
-  }
-  if (i != j) {
+      for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
+    }
+    double* pu = part + t * 2 * T;
+    double* pv = pu + T;
+    if (tx == 0) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) sv[ty][tx * 4 + q] = v[q];
+      for (int rr = 0; rr < 4; ++rr) pu[ty * 4 + rr] = u[rr];
+    }
+    // the staging buffer alternates, so one barrier per tile (every tile, also
+    // the diagonal ones that stage nothing) orders a buffer's readers before
+    // its next writers
+    double(*sb)[T + 1] = sv[(t - t0) & 1];
+    if (i != j) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sb[ty][tx * 4 + q] = v[q];
+    }
     __syncthreads();
-    if (threadIdx.x < T) {
+    if (i != j && threadIdx.x < T) {
       double s = 0.0;
 #pragma unroll
-      for (int g = 0; g < 16; ++g) s += sv[g][threadIdx.x];
+      for (int g = 0; g < 16; ++g) s += sb[g][threadIdx.x];
       pv[threadIdx.x] = s;
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+    if (++j > i) {  // next tile of the packed lower-triangular order
+      ++i;
+      j = 0;
+    }
   }
+}
+
+// The same tile products with the tiles streamed by the bulk-copy (TMA)
+// engine: a tile is 32 KB of contiguous packed storage, so one cp.async.bulk
+// per tile fills a shared-memory stage; 2 CTAs per SM x kSymvStages tiles in
+// flight, each CTA a contiguous range of tiles.  Per-thread arithmetic and
+// the partial layout are those of k_symv_tiles (bitwise the same y).
+constexpr int kSymvStages = 3;
+
+__global__ void __launch_bounds__(256, 2)
+    k_symv_bulk(int N, int nt, const double* __restrict__ X, const double* __restrict__ f,
+                double* __restrict__ part, const int* done, int64_t t_begin, int64_t t_end, int per) {
+  if (done && *(volatile const int*)done) return;
+  extern __shared__ __align__(128) double stage[];  // kSymvStages tiles, then the mbarriers
+  __shared__ double sv[2][16][T + 1];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + kSymvStages * T * T);
+  const int64_t t0 = t_begin + (int64_t)blockIdx.x * per;
+  const int64_t t1 = t0 + per < t_end ? t0 + per : t_end;
+  if (t0 >= t1) return;
+  constexpr uint32_t kTileBytes = T * T * sizeof(double);
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < kSymvStages; ++s2) mbar_init(bar + s2, 1);
+    mbar_fence_init();
+    for (int s2 = 0; s2 < kSymvStages && t0 + s2 < t1; ++s2) {
+      mbar_expect_tx(bar + s2, kTileBytes);
+      bulk_g2s(stage + s2 * T * T, X + (t0 + s2) * T * T, kTileBytes, bar + s2);
+    }
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  int i, j;
+  tile_ij(t0, i, j);
+  int st = 0;
+  uint32_t phase = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    double fj[4], fi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cj = j * T + tx * 4 + q, ri = i * T + ty * 4 + q;
+      fj[q] = cj < N ? f[cj] : 0.0;
+      fi[q] = ri < N ? f[ri] : 0.0;
+    }
+    mbar_wait(bar + st, (phase >> st) & 1u);
+    phase ^= 1u << st;
+    const double* Xt = stage + st * T * T;
+    double u[4], v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double2* row = reinterpret_cast<const double2*>(Xt + (ty * 4 + rr) * T + tx * 4);
+      const double2 x01 = row[0], x23 = row[1];
+      u[rr] = x01.x * fj[0] + x01.y * fj[1] + x23.x * fj[2] + x23.y * fj[3];
+      v[0] += x01.x * fi[rr];
+      v[1] += x01.y * fi[rr];
+      v[2] += x23.x * fi[rr];
+      v[3] += x23.y * fi[rr];
+    }
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) u[rr] += __shfl_xor_sync(0xffffffffu, u[rr], o);
+    }
+    double* pu = part + t * 2 * T;
+    double* pv = pu + T;
+    if (tx == 0) {
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) pu[ty * 4 + rr] = u[rr];
+    }
+    double(*sb)[T + 1] = sv[(t - t0) & 1];
+    if (i != j) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sb[ty][tx * 4 + q] = v[q];
+    }
+    __syncthreads();  // every thread has read the stage; the v staging is complete
+    if (threadIdx.x == 0 && t + kSymvStages < t1) {
+      mbar_expect_tx(bar + st, kTileBytes);
+      bulk_g2s(stage + st * T * T, X + (t + kSymvStages) * T * T, kTileBytes, bar + st);
+    }
+    if (i != j && threadIdx.x < T) {
+      double s = 0.0;
+#pragma unroll
+      for (int g = 0; g < 16; ++g) s += sb[g][threadIdx.x];
+      pv[threadIdx.x] = s;
+    }
+    st = (st + 1 == kSymvStages) ? 0 : st + 1;
+    if (++j > i) {
+      ++i;
+      j = 0;
+    }
+  }
+}
+
+static int symv_variant() {
+  static int v = [] {
+    const char* e = getenv("MS_SYMV");  // A/B knob: 0 = register-prefetch tiles, 1 = bulk-copy stages
+    return e ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 // y_I = sum_J u(I,J) + sum_{I'>I} v(I',I): 8 groups of 64 threads split the
@@ -620,8 +745,23 @@ void launch_symv_packed(int N, const double* X, const double* f, double* y, doub
   if (N == 0) return;
   const int nt = div_up(N, T);
   if (t_end < 0) t_end = packed_tiles(nt);
-  if (t_end > t_begin)
-    { k_symv_tiles<<<(unsigned)(t_end - t_begin), 256, 0, st>>>(N, nt, X, f, part, done, t_begin); ms_count_launch(); }
+  if (t_end > t_begin && symv_variant() == 1) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntile = t_end - t_begin;
+    const int ctas = (int)std::min<int64_t>(ntile, 2 * sms);
+    const int per = div_up(ntile, ctas);
+    const size_t smem = (size_t)kSymvStages * T * T * sizeof(double) + kSymvStages * sizeof(uint64_t);
+    static bool configured[64] = {};
+    if (dev >= 64 || !configured[dev]) {
+      MS_CUDA(cudaFuncSetAttribute(k_symv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (dev < 64) configured[dev] = true;
+    }
+    { k_symv_bulk<<<div_up(ntile, per), 256, smem, st>>>(N, nt, X, f, part, done, t_begin, t_end, per); ms_count_launch(); }
+  } else if (t_end > t_begin)
+    { k_symv_tiles<<<(unsigned)div_up(t_end - t_begin, kSymvTilesPerCta), 256, 0, st>>>(N, nt, X, f, part, done,
+                                                                                         t_begin, t_end); ms_count_launch(); }
   { k_symv_reduce<<<nt, T * kRedGroups, 0, st>>>(N, nt, part, y, done, t_begin, t_end); ms_count_launch(); }
   MS_CUDA(cudaGetLastError());
 }
