@@ -19,7 +19,20 @@ $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared $(OBJ) -o $@ -ldl
 	@cat build/ptxas/*.log > /tmp/ptxas.log
 
+# bounds-checked variant (device-side asserts, -DMS_BOUNDS_CHECK) for tests/test_gpu_bounds.py
+CHK_OBJ := $(patsubst paper_2006_13387_b200/csrc/%.cu,build/check/%.o,$(SRC))
+CHK_LIB := build/check/libmsgpu_check.so
+
+build/check/%.o: paper_2006_13387_b200/csrc/%.cu $(HDR)
+	@mkdir -p build/check
+	$(NVCC) $(ARCH) $(NVFLAGS) -DMS_BOUNDS_CHECK -c $< -o $@ 2> build/check/$*.log || (cat build/check/$*.log; false)
+
+$(CHK_LIB): $(CHK_OBJ)
+	$(NVCC) $(ARCH) -shared $(CHK_OBJ) -o $@ -ldl
+
+check: $(CHK_LIB)
+
 clean:
 	rm -f $(LIB) $(OBJ)
 
-.PHONY: all clean
+.PHONY: all check clean

@@ -465,6 +465,9 @@ __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int
   const int64_t w0 = (int64_t)start * S;
   const int64_t a = w0 & ~(int64_t)1;  // 16-byte aligned source (L itself is)
   const uint32_t words = (uint32_t)((cnt * S + (int)(w0 - a) + 1) & ~1);
+  MS_BCHECK(st >= 0 && st < rg.nst && cnt >= 1 && start >= 0 && start + cnt <= n);
+  MS_BCHECK((int)words <= rg.stage);                          // the chunk fits its shared-memory stage
+  MS_BCHECK(a >= 0 && a + (int64_t)words <= (int64_t)n * S + 2);  // and stays inside the system's band (+ slack)
   mbar_expect_tx(rg.bar + st, words * 8u);
   bulk_g2s(rg.buf + (size_t)st * rg.stage, L + a, words * 8u, rg.bar + st);
 }
@@ -753,6 +756,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     const int ln = i >> 1, c = i & 1;
     int a, b;
     band_node_of(s, ln, a, b);
+    MS_BCHECK(a >= 0 && a <= g.nx && b >= 0 && b <= g.ny);
     y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
   }
   __syncwarp();
@@ -806,6 +810,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   double* tS = sB + NR * max_bw;                                       // separator right-hand side
   const BandSys s = sys[sid];
   const int n = s.n, bw = s.bw, m = s.m, nT = m + bw, nB = n - m;
+  MS_BCHECK(bw >= 1 && bw <= max_bw && m >= 1 && nT <= n && nB >= bw && nst >= 2 && nst <= kMaxNst);
   double* y = ybuf + s.yoff;
   // gather R_s r: top warp rows [0, nT), bottom warp rows [nT, n) and zero separator partials
   {
@@ -814,6 +819,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
       const int ln = NR == 1 ? (i >> 1) : (i >> 1), c = i & 1;
       int a, b;
       band_node_of(s, ln, a, b);
+      MS_BCHECK(a >= 0 && a <= g.nx && b >= 0 && b <= g.ny);
       y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
     }
     if (role)
@@ -919,6 +925,7 @@ __global__ void __launch_bounds__(32, 4)
     const int64_t w0 = (int64_t)start * S;
     const int64_t a = w0 & ~(int64_t)1;
     const uint32_t words = (uint32_t)((cnt * S + (int)(w0 - a) + 1) & ~1);
+    MS_BCHECK((int)words <= stage_words && a >= 0 && a + (int64_t)words <= (int64_t)n * S + 2);
     const int st = c % nst;
     mbar_expect_tx(bar + st, words * 8u);
     bulk_g2s(buf + (size_t)st * stage_words, L + a, words * 8u, bar + st);

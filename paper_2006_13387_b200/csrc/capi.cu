@@ -567,6 +567,20 @@ static HaloPlan halo_plan(int lo, int hi, int ny, int k, int rank, int world) {
   return h;
 }
 
+// every non-empty send / receive segment of a transfer list must lie inside
+// the buffer it addresses (host-side, always on: a wrong strip or halo plan
+// fails here instead of corrupting a neighbour's rows)
+static void check_xfers(const Xfer* x, int n, const void* base, size_t bytes, const char* what) {
+  const char* lo = static_cast<const char*>(base);
+  const char* hi = lo + bytes;
+  for (int i = 0; i < n; ++i) {
+    const char* s = static_cast<const char*>(x[i].s);
+    const char* r = static_cast<const char*>(x[i].r);
+    if ((x[i].sb && (s < lo || s + x[i].sb > hi)) || (x[i].rb && (r < lo || r + x[i].rb > hi)))
+      throw Error(MS_E_STATE, std::string(what) + ": transfer " + std::to_string(i) + " leaves its buffer");
+  }
+}
+
 // the 4 transfers of a k-row halo of both planes with the neighbouring strips
 static void row_halo_xfers(ms_problem* P, Comm* c, double* v, int k, Xfer x[4]) {
   const HaloPlan h = halo_plan(P->b_lo, row_hi(P), P->g.ny, k, c->rank, c->world);
@@ -577,6 +591,7 @@ static void row_halo_xfers(ms_problem* P, Comm* c, double* v, int k, Xfer x[4]) 
       x[plane * 2 + q] = {base + h.send_lo[q] * rowb, (size_t)(h.send_n[q] * rowb), h.dst[q],
                           base + h.recv_lo[q] * rowb, (size_t)(h.recv_n[q] * rowb), h.src[q]};
   }
+  check_xfers(x, 4, v, (size_t)2 * P->g.n_nodes * sizeof(double), "row halo");
 }
 
 // exchange k node rows of both planes with the neighbouring strips
@@ -633,6 +648,7 @@ static void ybuf_xfers(ms_precond* pc, Comm* c, Xfer x[2]) {
   double* y = pc->ybuf.p;
   x[0] = {y + o_first, (size_t)(prev >= 0 ? b_first : 0), prev, y + o_nf, (size_t)b_nf, next};
   x[1] = {y + o_last, (size_t)(next >= 0 ? b_last : 0), next, y + o_pl, (size_t)b_pl, prev};
+  check_xfers(x, 2, y, pc->ybuf.n * sizeof(double), "level-1 boundary solutions");
 }
 
 // restriction partials of the cell row below my lowest centre row (prev's last)
@@ -646,6 +662,7 @@ static void rpart_xfers(ms_precond* pc, Comm* c, Xfer x[2]) {
   x[0] = {nullptr, 0, -1, nullptr, 0, -1};
   x[1] = {rp + (pc->C1 - 1) * rowd, (size_t)(next >= 0 ? rowd * sizeof(double) : 0), next, rp + (pc->C0 - 1) * rowd,
           (size_t)(prev >= 0 ? rowd * sizeof(double) : 0), prev};
+  check_xfers(x, 2, rp, pc->rpart.n * sizeof(double), "restriction partials");
 }
 static void exchange_rpart(ms_precond* pc) {
   ms_problem* P = pc->prob;

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(TPB, MINB)
       b[u] = b_lo + tt / w;
       a[u] = a_lo + tt - (tt / w) * w;
       n[u] = (int64_t)b[u] * g.nnx + a[u];
+      MS_BCHECK(a[u] >= 0 && a[u] <= g.nx && b[u] >= 0 && b[u] <= g.ny && n[u] < nn);
       rx[u] = ok[u] ? r[n[u]] : 0.0;
       ry[u] = ok[u] ? r[n[u] + nn] : 0.0;
       if (UPD) {
@@ -666,6 +667,8 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
           v[u][tj][ti] = make_double2(0.0, 0.0);
           if (ok[u] && ey.x >= 0 && ex.x >= 0) {
             const int ln = (ex.z <= ey.z) ? (b[u] - ey.y) * ex.z + (a[u] - ex.y) : (a[u] - ex.y) * ey.z + (b[u] - ey.y);
+            MS_BCHECK(ex.x < l1.NbX && ey.x < l1.NbY && a[u] >= ex.y && a[u] < ex.y + ex.z && b[u] >= ey.y &&
+                      b[u] < ey.y + ey.z && ln >= 0 && ln < ex.z * ey.z);
             const int dj = ey.x - Jmin, di = ex.x - Imin;
             const int64_t off = (dj >= 0 && dj < 4 && di >= 0 && di < 4) ? syoff[dj * 4 + di]
                                                                          : __ldg(l1.yoff + ey.x * l1.NbX + ex.x);

@@ -126,6 +126,27 @@ __device__ __forceinline__ bool grid_reduce_dist(double blockval, double* partia
   return grid_reduce_last(blockval, partials, ticket, out, sh);
 }
 
+// ---- device-side bounds checks (compute-sanitizer is not available on the GPU pool) ----
+// `make check` builds build/check/libmsgpu_check.so with -DMS_BOUNDS_CHECK: the
+// index computations of the ring / halo / gather code assert their ranges and
+// trap with a message; tests/test_gpu_bounds.py runs every level-1 layout and
+// the multi-rank strips through that library.  Compiled out of the product build.
+#ifdef MS_BOUNDS_CHECK
+#include <cstdio>
+#define MS_BCHECK(cond)                                                                        \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("msgpu bounds check failed: %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                               \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define MS_BCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // ---- bulk async copy (TMA engine, 1-D) + mbarrier helpers (sm_90+/sm_100a) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

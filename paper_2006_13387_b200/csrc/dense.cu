@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(256, 2)
   const int64_t t0 = t_begin + (int64_t)blockIdx.x * per;
   const int64_t t1 = t0 + per < t_end ? t0 + per : t_end;
   if (t0 >= t1) return;
+  MS_BCHECK(t0 >= 0 && t1 <= (int64_t)nt * (nt + 1) / 2);  // the CTA's tile range lies in the packed matrix
   constexpr uint32_t kTileBytes = T * T * sizeof(double);
   if (threadIdx.x == 0) {
     for (int s2 = 0; s2 < kSymvStages; ++s2) mbar_init(bar + s2, 1);

@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
     const int b = b0 + ty * MV_RPT + r;
     if (a <= g.nx && b >= b_lo - 1 && b <= b_hi + 1 && b <= g.ny) {
       const int64_t n = (int64_t)b * g.nnx + a;
+      MS_BCHECK(a >= 0 && b >= 0 && n < nn);
       const bool own = b >= b_lo && b <= b_hi;
       const double ox = mask[n] ? qx[r] : 0.0;
       const double oy = mask[n + nn] ? qy[r] : 0.0;
