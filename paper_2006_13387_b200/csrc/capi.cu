@@ -433,7 +433,8 @@ struct ms_precond {
   CoarseDev cd{};
   DBuf<int> nsel, hoff;
   DBuf<int64_t> psioff;
-  DBuf<double> psi, chi, K0inv, f0, y0, part, evals, K0keep, chi4, psi4, rpart;
+  DBuf<double> psi, chi, K0inv, f0, y0, part, evals, K0keep, chi4, psi4, rpart, psi0c;
+  DBuf<int> chi_src;
   // MS_COARSE_CHOLESKY: packed factor L (in K0inv), inverses of its diagonal
   // tiles, the forward-sweep result and the blocked-TRSV tickets/flags
   bool coarse_factor = false;
@@ -1674,6 +1675,27 @@ int ms_precond_build(ms_problem* P, const ms_precond_opts* o, ms_precond** out) 
     cd.chi4 = pc->chi4.p;
     cd.psi4 = pc->psi4.p;
     cd.rpart = pc->rpart.p;
+    // constant mode 0 per centre (pure Neumann neighbourhoods): their cells
+    // rebuild psi4 = chi4 * value instead of reading it (MS_PSI0_CONST=0: off)
+    cd.psi0c = nullptr;
+    cd.chi_src = nullptr;
+    {
+      // cells with bitwise identical chi4 records read one shared copy (MS_CHI_DEDUP=0: off)
+      const char* e = getenv("MS_CHI_DEDUP");
+      if (!cd.vec && !(e && std::atoi(e) == 0)) {
+        pc->chi_src.alloc((size_t)o->Nx * o->Ny);
+        launch_chi_dedup(g, cd, pc->chi_src.p, st);
+        cd.chi_src = pc->chi_src.p;
+      }
+    }
+    {
+      const char* e = getenv("MS_PSI0_CONST");
+      if (!cd.vec && !(e && std::atoi(e) == 0)) {
+        pc->psi0c.alloc(nc);
+        launch_psi0_const(cd, pc->psi0c.p, st);
+        cd.psi0c = pc->psi0c.p;
+      }
+    }
     // K0 = R0 A R0^T, symmetrised, inverted
     const int N = pc->N_c;
     DBuf<double> K0;

@@ -133,6 +133,92 @@ void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double
   MS_CUDA(cudaGetLastError());
 }
 
+__global__ void __launch_bounds__(256) k_psi0_const(CoarseDev cd, double* __restrict__ psi0c) {
+  const int k = blockIdx.x, NL = cd.NLx * cd.NLy;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  if (cd.nsel[k] < 1) {  // no mode stored for this centre (CTA-uniform)
+    if (threadIdx.x == 0) psi0c[k] = nan;
+    return;
+  }
+  const double* ps = cd.psi + cd.psioff[k];
+  const double v0 = ps[0];
+  int same = 1;
+  for (int i = threadIdx.x; i < NL; i += blockDim.x) same &= (ps[i] == v0) ? 1 : 0;
+  same = __syncthreads_and(same);
+  if (threadIdx.x == 0) psi0c[k] = same ? v0 : nan;
+}
+
+void launch_psi0_const(const CoarseDev& cd, double* psi0c, cudaStream_t st) {
+  if (cd.n_centers == 0 || cd.vec) return;
+  { k_psi0_const<<<cd.n_centers, 256, 0, st>>>(cd, psi0c); ms_count_launch(); }
+  MS_CUDA(cudaGetLastError());
+}
+
+// cell (ci, cj): node range and size (the last cell row / column owns the far boundary nodes)
+__device__ __forceinline__ void cell_box(const Grid& g, int Nx, int Ny, int ci, int cj, int& a_lo, int& b_lo, int& w,
+                                         int& hgt) {
+  const int mx = g.nx / Nx, my = g.ny / Ny;
+  a_lo = ci * mx;
+  b_lo = cj * my;
+  w = ((ci == Nx - 1) ? g.nx : a_lo + mx - 1) - a_lo + 1;
+  hgt = ((cj == Ny - 1) ? g.ny : b_lo + my - 1) - b_lo + 1;
+}
+
+__global__ void __launch_bounds__(256) k_chi_dedup(Grid g, CoarseDev cd, int* __restrict__ chi_src) {
+  const int ci = blockIdx.x, cj = blockIdx.y, Nx = cd.Nx, Ny = cd.Ny;
+  // class representative: same position class per axis (first / interior / last)
+  const int ri = (ci == 0 || ci == Nx - 1) ? ci : 1, rj = (cj == 0 || cj == Ny - 1) ? cj : 1;
+  int a_lo, b_lo, w, hgt, ra, rb, rw, rh;
+  cell_box(g, Nx, Ny, ci, cj, a_lo, b_lo, w, hgt);
+  cell_box(g, Nx, Ny, ri, rj, ra, rb, rw, rh);
+  int same = (rw == w && rh == hgt) ? 1 : 0;
+  if (same && (ri != ci || rj != cj)) {
+    for (int t = threadIdx.x; t < w * hgt; t += blockDim.x) {
+      const int lb = t / w, la = t - lb * w;
+      const int64_t n = (int64_t)(b_lo + lb) * g.nnx + a_lo + la, m = (int64_t)(rb + lb) * g.nnx + ra + la;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        same &= (__double_as_longlong(cd.chi4[n * 4 + c]) == __double_as_longlong(cd.chi4[m * 4 + c])) ? 1 : 0;
+    }
+  }
+  same = __syncthreads_and(same);
+  if (threadIdx.x == 0) chi_src[cj * Nx + ci] = same ? rj * Nx + ri : cj * Nx + ci;
+}
+
+void launch_chi_dedup(const Grid& g, const CoarseDev& cd, int* chi_src, cudaStream_t st) {
+  if (cd.n_centers == 0 || cd.vec) return;
+  { k_chi_dedup<<<dim3(cd.Nx, cd.Ny), 256, 0, st>>>(g, cd, chi_src); ms_count_launch(); }
+  MS_CUDA(cudaGetLastError());
+}
+
+// origin of the cell whose chi4 records this cell reads (CTA-uniform)
+__device__ __forceinline__ void chi_origin(const Grid& g, const CoarseDev& cd, int ci, int cj, int a_lo, int b_lo,
+                                           int& ca, int& cb) {
+  ca = a_lo;
+  cb = b_lo;
+  if (cd.chi_src) {
+    const int src = __ldg(cd.chi_src + cj * cd.Nx + ci);
+    int w, hgt;
+    cell_box(g, cd.Nx, cd.Ny, src % cd.Nx, src / cd.Nx, ca, cb, w, hgt);
+  }
+}
+
+// mode-0 values of a cell's 4 corner centres when all of them are constant
+// (then psi4 = chi4 * value needs no table read); CTA-uniform
+__device__ __forceinline__ bool cell_psi0_const(const CoarseDev& cd, const bool cok[4], int ci, int cj, double pv0[4]) {
+  bool all = cd.psi0c != nullptr;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    pv0[c] = 0.0;
+    if (all && cok[c]) {
+      const int I = ci + (c & 1), J = cj + (c >> 1);
+      pv0[c] = __ldg(cd.psi0c + (J - 1) * (cd.Nx - 1) + (I - 1));
+      all = pv0[c] == pv0[c];  // NaN: mode 0 of this centre is not constant
+    }
+  }
+  return all;
+}
+
 // ---------------------------------------------------------------------------
 // Cell-tiled restriction, optionally fused with the PCG residual update.
 // One CTA per coarse cell accumulates, for each of its <= 4 corner centres,
@@ -178,6 +264,10 @@ __global__ void __launch_bounds__(TPB, MINB)
     cok[c] = has_coarse && I >= 1 && I <= Nx - 1 && J >= 1 && J <= Ny - 1;
     cns[c] = cok[c] ? __ldg(cd.nsel + (J - 1) * (Nx - 1) + (I - 1)) : 0;
   }
+  double pv0[4];
+  const bool pconst = !VEC && has_coarse && cell_psi0_const(cd, cok, ci, cj, pv0);
+  int cha = a_lo, chb = b_lo;  // origin of the cell whose chi4 records are read (bitwise identical ones)
+  if (!VEC && has_coarse) chi_origin(g, cd, ci, cj, a_lo, b_lo, cha, chb);
   double acc[13];
 #pragma unroll
   for (int v = 0; v < 13; ++v) acc[v] = 0.0;  // [4 corners][x, y, rot] + ||r||^2
@@ -211,12 +301,15 @@ __global__ void __launch_bounds__(TPB, MINB)
       }
       c4[u][0] = c4[u][1] = p4[u][0] = p4[u][1] = make_double2(0.0, 0.0);
       if (!VEC && has_coarse && ok[u]) {
-        const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n[u];
+        const int64_t nc4 = (int64_t)(chb + (b[u] - b_lo)) * g.nnx + cha + (a[u] - a_lo);
+        const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * nc4;
         const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n[u];
         c4[u][0] = __ldg(c2);
         c4[u][1] = __ldg(c2 + 1);
-        p4[u][0] = __ldg(p2);
-        p4[u][1] = __ldg(p2 + 1);
+        if (!pconst) {
+          p4[u][0] = __ldg(p2);
+          p4[u][1] = __ldg(p2 + 1);
+        }
       }
     }
 #pragma unroll
@@ -234,7 +327,11 @@ __global__ void __launch_bounds__(TPB, MINB)
       }
       if (!VEC && has_coarse) {
         const double ch4[4] = {c4[u][0].x, c4[u][0].y, c4[u][1].x, c4[u][1].y};
-        const double ps4[4] = {p4[u][0].x, p4[u][0].y, p4[u][1].x, p4[u][1].y};
+        double ps4[4] = {p4[u][0].x, p4[u][0].y, p4[u][1].x, p4[u][1].y};
+        if (pconst) {  // the table's own product (k_node_tables)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ps4[c] = __dmul_rn(ch4[c], pv0[c]);
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int I = ci + (c & 1), J = cj + (c >> 1);
@@ -616,6 +713,10 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
     }
     cy[c][m] = v;
   }
+  double pv0[4];
+  const bool pconst = has_coarse && cell_psi0_const(cd, cok, ci, cj, pv0);
+  int cha = a_lo, chb = b_lo;
+  if (has_coarse) chi_origin(g, cd, ci, cj, a_lo, b_lo, cha, chb);
   // cover tables of the cell's columns and rows; covers are listed in
   // ascending block order, so the first cover of the first column / row is
   // the smallest block index of the cell
@@ -677,12 +778,15 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
         }
       c4a[u] = c4b[u] = p4a[u] = p4b[u] = make_double2(0.0, 0.0);
       if (has_coarse && ok[u]) {
-        const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * n[u];
+        const int64_t nc4 = (int64_t)(chb + lb) * g.nnx + cha + la;
+        const double2* c2 = reinterpret_cast<const double2*>(cd.chi4) + 2 * nc4;
         const double2* p2 = reinterpret_cast<const double2*>(cd.psi4) + 2 * n[u];
         c4a[u] = __ldg(c2);
         c4b[u] = __ldg(c2 + 1);
-        p4a[u] = __ldg(p2);
-        p4b[u] = __ldg(p2 + 1);
+        if (!pconst) {
+          p4a[u] = __ldg(p2);
+          p4b[u] = __ldg(p2 + 1);
+        }
       }
       mk[u][0] = ok[u] ? mask[n[u]] : 0;
       mk[u][1] = ok[u] ? mask[n[u] + nn] : 0;
@@ -703,7 +807,11 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
       if (has_coarse) {
         double cxs = 0.0, cys = 0.0;
         const double ch4[4] = {c4a[u].x, c4a[u].y, c4b[u].x, c4b[u].y};
-        const double ps4[4] = {p4a[u].x, p4a[u].y, p4b[u].x, p4b[u].y};
+        double ps4[4] = {p4a[u].x, p4a[u].y, p4b[u].x, p4b[u].y};
+        if (pconst) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ps4[c] = __dmul_rn(ch4[c], pv0[c]);
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (!cok[c]) continue;
@@ -751,13 +859,11 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
 }
 
 static int combine_variant() {
-  static int v = [] {
-    // A/B knob: 0 = per-node cover lookups, 1 / 2 = staged tables with 1 / 2 nodes per thread in flight
-    // (config 3 in the PCG loop: 0.139 / 0.133 / 0.201 ms -- two nodes in flight spill at 3 CTAs per SM)
-    const char* e = getenv("MS_COMBINE");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
+  // A/B knob, read per launch (tests toggle it): 0 = per-node cover lookups, 1 / 2 = staged tables with 1 / 2
+  // nodes per thread in flight (config 3 in the PCG loop: 0.139 / 0.133 / 0.201 ms -- two nodes in flight
+  // spill at 3 CTAs per SM)
+  const char* e = getenv("MS_COMBINE");
+  return e ? atoi(e) : 1;
 }
 
 int combine_threads() { return kCombineThreads; }

@@ -45,6 +45,18 @@ struct CoarseDev {
   // centres (ci + (c&1), cj + (c>>1)), c = 0..3, J-major; zero where invalid
   const double* chi4;     // [n_nodes][4] chi of the corner centres
   const double* psi4;     // [n_nodes][4] chi * psi (mode 0) of the corner centres
+  // per centre: the value of mode 0 when it is the constant vector (pure
+  // Neumann neighbourhoods: the locked exact kernel of the heat pencil), NaN
+  // otherwise.  A cell whose corner centres all have one skips the psi4
+  // records: psi4 = chi4 * value, the product the table holds (nullptr: off)
+  const double* psi0c;
+  // per coarse cell: the cell whose chi4 records are bitwise identical to
+  // this one's (itself when none of its class is).  On a uniform coarse grid
+  // with exactly representable h every interior cell shares one 32 KB block
+  // of records (likewise each edge class), which then lives in L2: the cell
+  // kernels read chi4 through this map and move no DRAM bytes for it
+  // (nullptr: off)
+  const int* chi_src;
   double* rpart;          // [Nx*Ny cells][4][2*kMaxModes+1] restriction partials
 };
 
@@ -54,6 +66,11 @@ constexpr int kSlots = 2 * kMaxModes + 1;  // heat x/y per mode + rotation
 // node-major chi4 / psi4 from the per-centre tables
 void launch_node_tables(const Grid& g, const CoarseDev& cd, double* chi4, double* psi4,
                         cudaStream_t st);
+// chi_src[cell] = the class representative (interior / edge / corner cell, 9 classes) when this
+// cell's chi4 block equals it bit for bit, else the cell itself
+void launch_chi_dedup(const Grid& g, const CoarseDev& cd, int* chi_src, cudaStream_t st);
+// psi0c[k] = the constant value of centre k's mode 0, NaN when it is not constant
+void launch_psi0_const(const CoarseDev& cd, double* psi0c, cudaStream_t st);
 
 // fused x += alpha p, r -= alpha q, ||r||^2 -> convergence, and restriction
 // partial sums per coarse cell; then f0 = sum of the 4 cell partials per centre

@@ -12,6 +12,7 @@
 // and L^-T L^-1 (lauum); every tile kernel takes the batch index from
 // blockIdx.y and works on packed lower tiles.
 #include <algorithm>
+#include <cstdlib>
 
 #include "dense.cuh"
 
@@ -708,11 +709,9 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 static int symv_variant() {
-  static int v = [] {
-    const char* e = getenv("MS_SYMV");  // A/B knob: 0 = register-prefetch tiles, 1 = bulk-copy stages
-    return e ? atoi(e) : 1;
-  }();
-  return v;
+  // A/B knob, read per launch (tests toggle it): 0 = register-prefetch tiles, 1 = bulk-copy stages
+  const char* e = getenv("MS_SYMV");
+  return e ? atoi(e) : 1;
 }
 
 // y_I = sum_J u(I,J) + sum_{I'>I} v(I',I): 8 groups of 64 threads split the

@@ -71,6 +71,7 @@ CASES = [
     ("dense-inverses", {"CASE_DENSE": "1"}),
     ("cholesky-coarse", {"CASE_CHOL": "1"}),
     ("combine-per-node", {"MS_COMBINE": "0"}),
+    ("no-table-sharing", {"MS_CHI_DEDUP": "0", "MS_PSI0_CONST": "0"}),
     ("symv-register-tiles", {"MS_SYMV": "0"}),
     ("strip-mesh", {"CASE_SHAPE": "strip"}),
     ("mbb-mesh", {"CASE_SHAPE": "mbb"}),

@@ -581,6 +581,29 @@ def test_twisted_level1_matches_plain_sweeps(tag, rng, monkeypatch):
     assert v @ pre.apply(w) == pytest.approx(w @ pre.apply(v), rel=1e-9)
 
 
+@pytest.mark.parametrize("knob", ["MS_PSI0_CONST", "MS_CHI_DEDUP", "MS_COMBINE", "MS_SYMV"])
+def test_byte_saving_variants_are_bitwise_identical(knob, rng, monkeypatch):
+    """The restriction / combine / coarse-SYMV variants that move fewer bytes
+    or move them differently -- psi4 rebuilt from chi4 and the constant first
+    mode of pure-Neumann neighbourhoods, cover metadata staged per cell, tiles
+    streamed by bulk copies -- keep the arithmetic of the kernels they replace:
+    same z bit for bit, same PCG iterates (schwarz.py:76-84)."""
+    from paper_2006_13387_b200.solve import setup_spec
+
+    spec = configs.config3(seed=0, n=128)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv(knob, mode)
+        mesh, op, pre = setup_spec(spec)
+        out[mode] = (op, pre)
+    for _ in range(3):
+        v = rng.standard_normal(out["0"][0].n_free)
+        assert np.array_equal(out["0"][1].apply(v), out["1"][1].apply(v))
+    xa, ra = G.pcg_solve(out["0"][0], spec.rhs(), out["0"][1], tol=1e-8, maxit=300)
+    xb, rb = G.pcg_solve(out["1"][0], spec.rhs(), out["1"][1], tol=1e-8, maxit=300)
+    assert ra.iterations == rb.iterations and np.array_equal(xa, xb) and ra.residuals == rb.residuals
+
+
 @pytest.mark.parametrize("twist", ["0", "1"])
 @pytest.mark.parametrize("tag", ["EH+Rot", "HH+Rot"])
 def test_unit_diagonal_level1_matches_cholesky(tag, twist, rng, monkeypatch):
