@@ -235,6 +235,9 @@ constexpr int kCellThreads = 256;
 #ifndef MS_CB_MINB
 #define MS_CB_MINB 6
 #endif
+#ifndef MS_CB2_MINB
+#define MS_CB2_MINB 5
+#endif
 #ifndef MS_CR2_TPB
 #define MS_CR2_TPB 128
 #endif
@@ -675,7 +678,7 @@ __global__ void __launch_bounds__(kCombineThreads, MS_CB_MINB)
 // thread as k_combine<false> (bitwise identical z and r.z).
 constexpr int kCellMax = 72;  // largest cell side (nodes) the staged tables hold
 template <int NU>
-__global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
+__global__ void __launch_bounds__(kCombineThreads, NU == 1 ? MS_CB2_MINB : 3)
     k_combine2(Grid g, const uint8_t* __restrict__ mask, L1Dev l1, CoarseDev cd, int has_coarse, int Nx, int Ny,
                int J0, const double* __restrict__ y0, const double* __restrict__ r, double* __restrict__ z,
                PcgScalars* sc, double* partials, double* beta_hist) {
@@ -744,6 +747,7 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
   __syncthreads();
   double dot = 0.0;
   const int total = w * hgt;
+  const unsigned wmagic = 0xFFFFFFFFu / (unsigned)w + 1u;  // floor(t / w) = umulhi(t, wmagic) for t * w < 2^32
   for (int t0 = threadIdx.x; t0 < total; t0 += NU * kCombineThreads) {
     int a[NU], b[NU];
     int64_t n[NU];
@@ -756,7 +760,7 @@ __global__ void __launch_bounds__(kCombineThreads, NU == 1 ? 5 : 3)
       const int t = t0 + u * kCombineThreads;
       ok[u] = t < total;
       const int tt = ok[u] ? t : 0;
-      const int lb = tt / w, la = tt - lb * w;
+      const int lb = (int)__umulhi((unsigned)tt, wmagic), la = tt - lb * w;  // tt / w (exact: tt * w < 2^32)
       b[u] = b_lo + lb;
       a[u] = a_lo + la;
       n[u] = (int64_t)b[u] * g.nnx + a[u];

@@ -6,6 +6,7 @@
 // constrained dofs are held at exactly zero by a byte mask, which makes the
 // full-layout Krylov recurrence identical to the reference's free-dof one.
 #include <algorithm>
+#include <cstdlib>
 
 #include "operator.cuh"
 
@@ -215,6 +216,169 @@ __global__ void __launch_bounds__(MV_TX* MV_TY, MS_MV_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// PCG-mode matvec with the tile loads of the NEXT tile in flight while the
+// current one is computed: each CTA handles kMv2Tiles vertically adjacent
+// 32 x 16 tiles; all their z / p_old / E tiles are requested up front as
+// asynchronous global -> shared copies (cp.async, zero-filled outside the
+// domain) into separate buffers, so the second tile's loads overlap the
+// first tile's stencil.  (k_matvec above shows 25% of its stall samples at
+// the barrier behind its tile loads and 33% on the loads themselves.)  Node
+// -> thread mapping, per-thread arithmetic, the per-tile block sums and their
+// partial slots are those of k_matvec: q, p and p.q are bitwise the same.
+// One rank only (the strips of a multi-rank run keep k_matvec).
+constexpr int kMv2Tiles = 2;
+constexpr int kMv2PT = (MV_NY + 2) * (MV_TX + 2);
+constexpr int kMv2ET = (MV_NY + 1) * (MV_TX + 1);
+constexpr int kMv2Buf = 4 * kMv2PT + kMv2ET + 1;  // z(2) + p_old(2) + E, doubles per tile buffer
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(MV_TX* MV_TY, 4)
+    k_matvec2(Grid g, KeParam ke, const double* __restrict__ E, const uint8_t* __restrict__ mask,
+              const double* __restrict__ z, const double* __restrict__ p_old, double* __restrict__ p_new,
+              double* __restrict__ q, PcgScalars* sc, double* partials, double* alpha_hist, int tiles_y) {
+  if (sc->done) return;
+  extern __shared__ double mv2[];
+  __shared__ double sred[MV_TX * MV_TY / 32];
+  __shared__ bool am_last;
+  const int tid = threadIdx.x;
+  const int a0 = blockIdx.x * MV_TX;
+  const double beta = sc->beta;
+  const int64_t nn = g.n_nodes;
+  typedef double (*PTile)[MV_NY + 2][MV_TX + 2];
+  typedef double (*ETile)[MV_TX + 1];
+#pragma unroll
+  for (int k = 0; k < kMv2Tiles; ++k) {
+    const int tyk = blockIdx.y * kMv2Tiles + k;
+    if (tyk < tiles_y) {
+      double* buf = mv2 + k * kMv2Buf;
+      PTile sz = reinterpret_cast<PTile>(buf);
+      PTile so = reinterpret_cast<PTile>(buf + 2 * kMv2PT);
+      ETile sE = reinterpret_cast<ETile>(buf + 4 * kMv2PT);
+      const int b0 = tyk * MV_NY;
+      for (int t = tid; t < kMv2PT; t += MV_TX * MV_TY) {
+        const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
+        const int a = a0 + lx - 1, b = b0 + ly - 1;
+        const bool ok = a >= 0 && a <= g.nx && b >= 0 && b <= g.ny;
+        const int64_t n = ok ? (int64_t)b * g.nnx + a : 0;
+        cp_async8(&so[0][ly][lx], p_old + n, ok);
+        cp_async8(&so[1][ly][lx], p_old + n + nn, ok);
+        cp_async8(&sz[0][ly][lx], z + n, ok);
+        cp_async8(&sz[1][ly][lx], z + n + nn, ok);
+      }
+      for (int t = tid; t < kMv2ET; t += MV_TX * MV_TY) {
+        const int ly = t / (MV_TX + 1), lx = t - ly * (MV_TX + 1);
+        const int i = a0 + lx - 1, j = b0 + ly - 1;
+        const bool ok = i >= 0 && i < g.nx && j >= 0 && j < g.ny;
+        cp_async8(&sE[ly][lx], E + (ok ? (int64_t)j * g.nx + i : 0), ok);
+      }
+    }
+    cp_async_commit();
+  }
+  const int tx = tid % MV_TX, ty = tid / MV_TX;
+  const int X = tx + 1;
+  const int Y0 = ty * MV_RPT + 1;
+  const int dxs[4] = {0, -1, -1, 0};
+  const int dys[4] = {0, 0, -1, -1};
+#pragma unroll
+  for (int k = 0; k < kMv2Tiles; ++k) {
+    const int tyk = blockIdx.y * kMv2Tiles + k;
+    if (tyk >= tiles_y) break;  // CTA-uniform
+    if (k == 0)
+      cp_async_wait_group<kMv2Tiles - 1>();
+    else
+      cp_async_wait_group<0>();
+    double* buf = mv2 + k * kMv2Buf;
+    PTile sp = reinterpret_cast<PTile>(buf);  // z in place -> p
+    PTile so = reinterpret_cast<PTile>(buf + 2 * kMv2PT);
+    ETile sE = reinterpret_cast<ETile>(buf + 4 * kMv2PT);
+    // p = z + beta p_old on the entries this thread copied itself (its own copies are complete)
+    for (int t = tid; t < kMv2PT; t += MV_TX * MV_TY) {
+      const int ly = t / (MV_TX + 2), lx = t - ly * (MV_TX + 2);
+      sp[0][ly][lx] = sp[0][ly][lx] + beta * so[0][ly][lx];
+      sp[1][ly][lx] = sp[1][ly][lx] + beta * so[1][ly][lx];
+    }
+    __syncthreads();
+    const int b0 = tyk * MV_NY;
+    double qx[MV_RPT], qy[MV_RPT];
+#pragma unroll
+    for (int r = 0; r < MV_RPT; ++r) qx[r] = qy[r] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double kx[8], ky[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        kx[m] = ke.k[c * 8 + m];
+        ky[m] = ke.k[(4 + c) * 8 + m];
+      }
+      const int ex = X + dxs[c];
+#pragma unroll
+      for (int r = 0; r < MV_RPT; ++r) {
+        const int ey = Y0 + r + dys[c];
+        const double Ee = sE[ey][ex];
+        const double u0 = sp[0][ey][ex], u1 = sp[0][ey][ex + 1], u2 = sp[0][ey + 1][ex + 1],
+                     u3 = sp[0][ey + 1][ex];
+        const double v0 = sp[1][ey][ex], v1 = sp[1][ey][ex + 1], v2 = sp[1][ey + 1][ex + 1],
+                     v3 = sp[1][ey + 1][ex];
+        const double sx = kx[0] * u0 + kx[1] * u1 + kx[2] * u2 + kx[3] * u3 + kx[4] * v0 +
+                          kx[5] * v1 + kx[6] * v2 + kx[7] * v3;
+        const double sy = ky[0] * u0 + ky[1] * u1 + ky[2] * u2 + ky[3] * u3 + ky[4] * v0 +
+                          ky[5] * v1 + ky[6] * v2 + ky[7] * v3;
+        qx[r] += Ee * sx;
+        qy[r] += Ee * sy;
+      }
+    }
+    double dot = 0.0;
+    const int a = a0 + tx;
+#pragma unroll
+    for (int r = 0; r < MV_RPT; ++r) {
+      const int b = b0 + ty * MV_RPT + r;
+      if (a <= g.nx && b <= g.ny) {
+        const int64_t n = (int64_t)b * g.nnx + a;
+        MS_BCHECK(n < nn);
+        const double ox = mask[n] ? qx[r] : 0.0;
+        const double oy = mask[n + nn] ? qy[r] : 0.0;
+        q[n] = ox;
+        q[n + nn] = oy;
+        const double px = sp[0][Y0 + r][X], py = sp[1][Y0 + r][X];
+        p_new[n] = px;
+        p_new[n + nn] = py;
+        dot += px * ox + py * oy;
+      }
+    }
+    const double bs = block_sum(dot, sred);
+    if (tid == 0) partials[blockIdx.x + gridDim.x * tyk] = bs;  // the tile's slot in k_matvec's grid
+  }
+  // last CTA sums the per-tile partials in k_matvec's order
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(&sc->tickets[0], 1u);
+    am_last = (t == gridDim.x * gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  const double tot = reduce_partials_fixed(partials, gridDim.x * (unsigned)tiles_y, sred);
+  if (tid == 0) {
+    sc->tickets[0] = 0u;
+    fin_alpha(sc, tot, alpha_hist);
+  }
+}
+
+static int matvec_variant() {
+  // A/B knob, read per launch: 0 = k_matvec (register-staged tile loads, default), 1 = k_matvec2 (two tiles
+  // per CTA, asynchronous copies of the second tile in flight behind the first tile's stencil).  Measured at
+  // config 3 in the PCG loop: 0.096 ms vs 0.103 ms -- the 8-byte cp.async copies (the 2,049-double rows are
+  // not 16-byte multiples) cost more issue slots than the overlap returns, so the variant stays opt-in.
+  const char* e = getenv("MS_MATVEC");
+  return e ? atoi(e) : 0;
+}
+
 int matvec_partial_slots(const Grid& g) { return div_up(g.nx + 1, MV_TX) * (g.ny / MV_NY + 1); }
 int matvec_threads() { return MV_TX * MV_TY; }
 
@@ -234,6 +398,22 @@ void launch_matvec(const Grid& g, const KeParam& ke, const double* E, const uint
                    PcgScalars* sc, double* partials, double* alpha_hist, cudaStream_t st,
                    int b_lo, int b_hi) {
   if (b_hi < 0) b_hi = g.ny;
+  if (mode == MV_PCG && b_lo == 0 && b_hi == g.ny && matvec_variant() == 1) {
+    const int tiles_y = g.ny / MV_NY + 1;
+    const size_t smem = (size_t)kMv2Tiles * kMv2Buf * sizeof(double);
+    static bool configured[64] = {};
+    int dev = 0;
+    MS_CUDA(cudaGetDevice(&dev));
+    if (dev >= 64 || !configured[dev]) {
+      MS_CUDA(cudaFuncSetAttribute(k_matvec2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (dev < 64) configured[dev] = true;
+    }
+    dim3 grid2(div_up(g.nx + 1, MV_TX), div_up(tiles_y, kMv2Tiles));
+    { k_matvec2<<<grid2, MV_TX * MV_TY, smem, st>>>(g, ke, E, mask, z, p_old, p_new, q, sc, partials, alpha_hist,
+                                                    tiles_y); ms_count_launch(); }
+    MS_CUDA(cudaGetLastError());
+    return;
+  }
   const int ty0 = std::max(0, b_lo - 1) / MV_NY, ty1 = std::min(g.ny, b_hi + 1) / MV_NY;
   dim3 grid(div_up(g.nx + 1, MV_TX), ty1 - ty0 + 1);
   { k_matvec<<<grid, MV_TX * MV_TY, 0, st>>>(g, ke, E, mask, z, p_old, p_new, q, mode, sc, partials,

@@ -581,7 +581,7 @@ def test_twisted_level1_matches_plain_sweeps(tag, rng, monkeypatch):
     assert v @ pre.apply(w) == pytest.approx(w @ pre.apply(v), rel=1e-9)
 
 
-@pytest.mark.parametrize("knob", ["MS_PSI0_CONST", "MS_CHI_DEDUP", "MS_COMBINE", "MS_SYMV"])
+@pytest.mark.parametrize("knob", ["MS_PSI0_CONST", "MS_CHI_DEDUP", "MS_COMBINE", "MS_SYMV", "MS_MATVEC"])
 def test_byte_saving_variants_are_bitwise_identical(knob, rng, monkeypatch):
     """The restriction / combine / coarse-SYMV variants that move fewer bytes
     or move them differently -- psi4 rebuilt from chi4 and the constant first
