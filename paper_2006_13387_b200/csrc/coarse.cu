@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   // NU nodes per thread in flight: all their loads are issued before the first
   // is consumed; per-node arithmetic and accumulation order do not depend on NU.
   const int total = w * hgt;
+  const unsigned wmagic = 0xFFFFFFFFu / (unsigned)w + 1u;
   for (int t0 = threadIdx.x; t0 < total; t0 += NU * TPB) {
     int a[NU], b[NU];
     int64_t n[NU];
@@ -288,8 +289,9 @@ __global__ void __launch_bounds__(TPB, MINB)
       const int t = t0 + u * TPB;
       ok[u] = t < total;
       const int tt = ok[u] ? t : 0;
-      b[u] = b_lo + tt / w;
-      a[u] = a_lo + tt - (tt / w) * w;
+      const int lbu = (int)__umulhi((unsigned)tt, wmagic);  // tt / w (exact: tt * w < 2^32)
+      b[u] = b_lo + lbu;
+      a[u] = a_lo + tt - lbu * w;
       n[u] = (int64_t)b[u] * g.nnx + a[u];
       MS_BCHECK(a[u] >= 0 && a[u] <= g.nx && b[u] >= 0 && b[u] <= g.ny && n[u] < nn);
       rx[u] = ok[u] ? r[n[u]] : 0.0;
