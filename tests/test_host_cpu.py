@@ -59,7 +59,8 @@ def _c_layout(struct, fields):
 
 @pytest.mark.parametrize("cls,struct", [(_lib.PrecondOpts, "ms_precond_opts"),
                                         (_lib.PrecondInfo, "ms_precond_info"),
-                                        (_lib.Report, "ms_report")])
+                                        (_lib.Report, "ms_report"),
+                                        (_lib.LinOp, "ms_linop")])
 def test_struct_layouts_match_header(cls, struct):
     # every field offset and the size of the ctypes mirror equal the C layout
     import ctypes as C
@@ -67,6 +68,25 @@ def test_struct_layouts_match_header(cls, struct):
     names = [f for f, _ in cls._fields_]
     got = [getattr(cls, f).offset for f in names] + [C.sizeof(cls)]
     assert got == _c_layout(struct, names)
+
+
+def test_duck_typed_operands_map_to_linops():
+    # the reference's pcg_solve operands (krylov.py:73-78, 90) classify without touching the GPU:
+    # callables -> host-callback linops, wrong types -> TypeError, bad tolerance -> ValueError
+    from paper_2006_13387_b200 import krylov
+
+    cb = krylov._HostCallback(lambda v: 2.0 * v)
+    lo = cb.linop()
+    assert lo.kind == _lib.MS_LINOP_CALLBACK and lo.handle is None
+    src = np.arange(4.0)
+    dst = np.empty(4)
+    assert cb.cb(None, _lib.dptr(src), _lib.dptr(dst), 4) == 0 and np.array_equal(dst, 2.0 * src)
+    bad = krylov._HostCallback(lambda v: v[:2])  # wrong shape: carried as an error, status 1
+    assert bad.cb(None, _lib.dptr(src), _lib.dptr(dst), 4) == 1 and isinstance(bad.error, ValueError)
+    with pytest.raises(ValueError):
+        G.pcg_solve(lambda v: v, np.ones(3), tol=2.0)
+    with pytest.raises(TypeError):
+        krylov._as_linops("not an operator", None)
 
 
 def test_unit_element_bitwise_equals_reference():
@@ -166,7 +186,14 @@ def test_product_path_has_no_cpu_fallback(tmp_path):
         G.build_preconditioner("XX", object(), mesh, part, coeff, [])
     assert set(G.GPU_VARIANTS) == set(G.VARIANTS)
     with pytest.raises(TypeError):
-        G.pcg_solve(np.eye(3), np.ones(3))
+        G.pcg_solve("not an operator", np.ones(3))
+    # a foreign matrix is a valid operand (krylov.py:90) and runs on the GPU: without one the
+    # solve fails loudly instead of falling back to a host loop
+    import torch
+
+    if not torch.cuda.is_available():
+        with pytest.raises(_lib.MsError):
+            G.pcg_solve(np.eye(3), np.ones(3))
 
 
 def test_topopt_host_pieces():
