@@ -432,9 +432,9 @@ __device__ __forceinline__ void ring_init(Ring& rg, double* smem, int warp, int 
 
 
 // first physical column and count of chunk c (steps [c kCh, c kCh + cnt))
-__device__ __forceinline__ void chunk_cols(bool rev, int n, int c, int& start, int& cnt) {
-  const int k0 = c * kCh;
-  cnt = min(kCh, n - k0);
+__device__ __forceinline__ void chunk_cols(bool rev, int n, int c, int& start, int& cnt, int ch = kCh) {
+  const int k0 = c * ch;
+  cnt = min(ch, n - k0);
   start = rev ? n - k0 - cnt : k0;
 }
 
@@ -458,10 +458,10 @@ __device__ __forceinline__ void ring_issue_pad(Ring& rg, const CUtensorMap* map,
   tma_load_2d(rg.buf + (size_t)st * rg.stage, map, 0, col0 + start, rg.bar + st);
 }
 
-template <bool REV>
+template <bool REV, int CH = kCh>
 __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int S, int c, int st) {
   int start, cnt;
-  chunk_cols(REV, n, c, start, cnt);
+  chunk_cols(REV, n, c, start, cnt, CH);
   const int64_t w0 = (int64_t)start * S;
   const int64_t a = w0 & ~(int64_t)1;  // 16-byte aligned source (L itself is)
   const uint32_t words = (uint32_t)((cnt * S + (int)(w0 - a) + 1) & ~1);
@@ -474,18 +474,25 @@ __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int
 
 // ym(r): address of the NR values of the sweep's r-th row (r counts the
 // sweep's own steps, i.e. already reversed for REV)
-template <int T, int NR, bool REV, bool PAD, bool UNIT = false, class YMap>
+// CH: band columns per ring stage.  8 for bandwidth-bound launches (more
+// resident CTAs); 16 when the launch fits one wave: the per-chunk work --
+// mbarrier wait, warp sync, lane 0 re-arming the stage and issuing the next
+// bulk copy -- sits on the warp's dependent stream, and halving the chunk
+// count took config 2's twisted level 1 from 0.180 to 0.156 ms (32 columns
+// per stage spill: 0.32 ms).
+template <int T, int NR, bool REV, bool PAD, bool UNIT = false, int CH = kCh, class YMap>
 __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw, YMap ym,
                                                 int lane, Ring& rg, const CUtensorMap* map = nullptr,
                                                 int col0 = 0) {
   constexpr int R = T + 1;
   constexpr int P = pad_slot_words<T>();
   const int S = bw + 1;
-  const int nch = (n + kCh - 1) / kCh;
+  static_assert(32 % CH == 0 && (!PAD || CH == kCh), "stage width must divide 32; padded TMA boxes are kCh wide");
+  const int nch = (n + CH - 1) / CH;
   if (PAD) {
     for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue_pad<REV, P>(rg, map, col0, n, c, lane, c);
   } else if (lane == 0) {
-    for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue<REV>(rg, L, n, S, c, c);
+    for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue<REV, CH>(rg, L, n, S, c, c);
   }
   auto yat = [&](int r, int c) -> double* { return ym(r) + c; };
 
@@ -514,14 +521,14 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
 #pragma unroll
     for (int c = 0; c < NR; ++c) yfin[c] = 0.0;
 #pragma unroll 1
-    for (int h = 0; h < 32 && k0 + h < n; h += kCh) {
-      const int ch = (k0 + h) / kCh;
+    for (int h = 0; h < 32 && k0 + h < n; h += CH) {
+      const int ch = (k0 + h) / CH;
       const int st = stc;  // ch % nst as a running counter (nst is a per-launch value)
       stc = (stc + 1 == rg.nst) ? 0 : stc + 1;
       mbar_wait(rg.bar + st, (rg.phase >> st) & 1u);
       rg.phase ^= 1u << st;
       int start, cnt;
-      chunk_cols(REV, n, ch, start, cnt);
+      chunk_cols(REV, n, ch, start, cnt, CH);
       if (PAD) {
         // slot q of the stage = column start + q; this lane's coefficient of
         // step q (u = h + q) sits at slot(q) + lane - u
@@ -543,12 +550,12 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
             for (int s2 = 0; s2 < R; ++s2) acc[c][s2] = fma(-m[s2], wk, acc[c][s2]);
           }
         };
-        if (cnt == kCh) {
+        if (cnt == CH) {
 #pragma unroll
-          for (int q = 0; q < kCh; ++q) stepP(q, REV ? kCh - 1 - q : q);
+          for (int q = 0; q < CH; ++q) stepP(q, REV ? CH - 1 - q : q);
         } else {
 #pragma unroll
-          for (int q = 0; q < kCh; ++q)
+          for (int q = 0; q < CH; ++q)
             if (q < cnt) stepP(q, REV ? cnt - 1 - q : q);
         }
         __syncwarp();  // every lane is done with this stage before it is refilled
@@ -581,16 +588,16 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
           for (int s = 0; s < R; ++s) acc[c][s] = fma(-m[s], wk, acc[c][s]);
         }
       };
-      if (cnt == kCh) {
+      if (cnt == CH) {
 #pragma unroll
-        for (int q = 0; q < kCh; ++q) step(q);
+        for (int q = 0; q < CH; ++q) step(q);
       } else {
 #pragma unroll
-        for (int q = 0; q < kCh; ++q)
+        for (int q = 0; q < CH; ++q)
           if (q < cnt) step(q);
       }
       __syncwarp();  // every lane is done with this stage before it is refilled
-      if (lane == 0 && ch + rg.nst < nch) ring_issue<REV>(rg, L, n, S, ch + rg.nst, st);
+      if (lane == 0 && ch + rg.nst < nch) ring_issue<REV, CH>(rg, L, n, S, ch + rg.nst, st);
     }
     // slot 0 of lane L stopped changing at step L: it holds row k0+L's final
     // accumulator, and w = acc * (1/L_kk) exactly as the pivot step formed it
@@ -734,9 +741,9 @@ __device__ __forceinline__ void band_sweep_dot(const double* __restrict__ L, int
   }
 }
 
-static int ring_stage_words(int max_bw) { return (kCh * (max_bw + 1) + 3) & ~1; }
+static int ring_stage_words(int max_bw, int ch = kCh) { return (ch * (max_bw + 1) + 3) & ~1; }
 
-template <int T, int NR, bool PAD, bool UNIT>
+template <int T, int NR, bool PAD, bool UNIT, int CH>
 __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_ring(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                     const double* __restrict__ Lr, const double* __restrict__ r,
@@ -762,17 +769,17 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   __syncwarp();
   const int n = s.n;
   const int col0 = PAD ? (int)(s.foff / (s.bw + 1)) : 0;  // the system's first column in the TMA view
-  band_sweep_ring<T, NR, false, PAD, UNIT>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
+  band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
                                      &mapc, col0);
   if (fwd_only) return;  // the backward sweep follows in k_l1_bwd_window
   __syncwarp();
   if (Lr) {
-    band_sweep_ring<T, NR, true, PAD, UNIT>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; },
+    band_sweep_ring<T, NR, true, PAD, UNIT, CH>(Lr + s.foff, n, s.bw, [&](int r) { return y + (int64_t)(n - 1 - r) * NR; },
                                       lane, rg, &mapr, col0);
   } else {  // one factor copy: backward sweep by dot products over the column band
     double* xw = smem_ring + kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, PAD, nst) +
                  (size_t)warp * 256 * NR;
-    if constexpr (kCh == 8)
+    if constexpr (kCh == 8 && CH == kCh)
       band_sweep_dot<T, NR, PAD>(Lc + s.foff, n, s.bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
                                  &mapc, col0);
     else
@@ -789,7 +796,7 @@ __device__ __forceinline__ void pair_sync(int pair) {
   asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
 }
 
-template <int T, int NR, bool PAD, bool UNIT>
+template <int T, int NR, bool PAD, bool UNIT, int CH>
 __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     k_l1_solve_twist(Grid g, const BandSys* __restrict__ sys, int nsys, const double* __restrict__ Lc,
                      const double* __restrict__ Lr, const double* __restrict__ Sinv,
@@ -827,11 +834,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   }
   __syncwarp();
   if (role == 0) {
-    band_sweep_ring<T, NR, false, PAD, UNIT>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg,
+    band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg,
                                        &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
   } else {
     const int nb_own = nB - bw;
-    band_sweep_ring<T, NR, false, PAD, UNIT>(
+    band_sweep_ring<T, NR, false, PAD, UNIT, CH>(
         Lc + s.foffB, nB, bw,
         [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; }, lane, rg,
         &mapc, PAD ? (int)(s.foffB / (bw + 1)) : 0);
@@ -860,7 +867,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   pair_sync(pair);
   if (!Lr) {  // one factor copy: both backward sweeps by dot products over the column bands
     double* xw = smem_ring + ring_words + (size_t)(kTmaWarps / 2) * 2 * NR * max_bw + (size_t)warp * 256 * NR;
-    if constexpr (kCh != 8) {
+    if constexpr (kCh != 8 || CH != kCh) {
       __trap();  // the dot-form sweep is laid out for 8-column stages
     } else if (role == 0)
       band_sweep_dot<T, NR, PAD>(Lc + s.foff, nT, bw, [&](int k) { return y + (int64_t)k * NR; }, lane, rg, xw,
@@ -871,10 +878,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
     return;
   }
   if (role == 0) {
-    band_sweep_ring<T, NR, true, PAD, UNIT>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; },
+    band_sweep_ring<T, NR, true, PAD, UNIT, CH>(Lr + s.foff, nT, bw, [&](int q) { return y + (int64_t)(nT - 1 - q) * NR; },
                                       lane, rg, &mapr, PAD ? (int)(s.foff / (bw + 1)) : 0);
   } else {
-    band_sweep_ring<T, NR, true, PAD, UNIT>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane,
+    band_sweep_ring<T, NR, true, PAD, UNIT, CH>(Lr + s.foffB, nB, bw, [&](int q) { return y + (int64_t)(m + q) * NR; }, lane,
                                       rg, &mapr, PAD ? (int)(s.foffB / (bw + 1)) : 0);
   }
 }
@@ -1023,8 +1030,27 @@ __global__ void __launch_bounds__(32, 4)
 
 // ring shared memory of a launch: header + per-warp rings (+ extras)
 template <int T>
-static int ring_stage_words_t(int max_bw, bool pad) {
-  return pad ? kCh * pad_slot_words<T>() : ring_stage_words(max_bw);
+static int ring_stage_words_t(int max_bw, bool pad, int ch = kCh) {
+  return pad ? kCh * pad_slot_words<T>() : ring_stage_words(max_bw, ch);
+}
+
+// 16-column ring stages for launches of at most one CTA per SM, 8 otherwise
+// (MS_L1_CH=8 / 16 forces one): see band_sweep_ring.  At two CTAs per SM the
+// two widths measure the same (config 3's 8-GPU strip twisted: 0.277 ms with
+// 3 x 8 or 2 x 16 columns; its 4-GPU strip plain: within run-to-run noise).
+constexpr int kChWide = 16;
+static bool wide_chunks(int ctas) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("MS_L1_CH");
+    env = e ? std::atoi(e) : -1;
+  }
+  if (env == kCh) return false;
+  if (env == kChWide) return true;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return ctas <= sms;
 }
 static size_t ring_bytes(int stage_words, bool pad, int nst) {
   return ((size_t)kRingHeaderWords + (size_t)kTmaWarps * ring_warp_words(stage_words, pad, nst)) * sizeof(double);
@@ -1071,36 +1097,36 @@ static const L1Maps& no_maps() {
   return m;
 }
 
-template <int T, int NR, bool PAD, bool UNIT>
+template <int T, int NR, bool PAD, bool UNIT, int CH = kCh>
 static void solve_twist_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                           const double* Lr, const double* Sinv, const double* r, double* ybuf, const int* done,
                           cudaStream_t st, const L1Maps& maps) {
-  const int sw = ring_stage_words_t<T>(max_bw, PAD);
+  const int sw = ring_stage_words_t<T>(max_bw, PAD, CH);
   const size_t extra = (size_t)(kTmaWarps / 2) * 2 * NR * max_bw * sizeof(double) +
                        (Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double));  // separator + dot-sweep windows
   const int nst = pick_nst(div_up(nsys, kTmaWarps / 2), (size_t)kTmaWarps * sw * sizeof(double),
                            extra + (PAD ? kTmaWarps * kPadGuard * sizeof(double) : 0));
   const size_t smem = ring_bytes(sw, PAD, nst) + extra;
   static size_t configured[64] = {};
-  set_smem(k_l1_solve_twist<T, NR, PAD, UNIT>, smem, configured);
-  { k_l1_solve_twist<T, NR, PAD, UNIT><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
+  set_smem(k_l1_solve_twist<T, NR, PAD, UNIT, CH>, smem, configured);
+  { k_l1_solve_twist<T, NR, PAD, UNIT, CH><<<div_up(nsys, kTmaWarps / 2), kTmaWarps * 32, smem, st>>>(
       g, sys, nsys, Lc, Lr, Sinv, r, ybuf, done, sw, max_bw, maps.c, maps.r, nst); ms_count_launch(); }
 }
 
-template <int T, int NR, bool PAD, bool UNIT>
+template <int T, int NR, bool PAD, bool UNIT, int CH = kCh>
 static void solve_ring_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, const double* Lc,
                          const double* Lr, const double* r, double* ybuf, const int* done,
                          cudaStream_t st, const L1Maps& maps) {
-  const int sw = ring_stage_words_t<T>(max_bw, PAD);
+  const int sw = ring_stage_words_t<T>(max_bw, PAD, CH);
   // + the dot sweep's x windows (one factor copy)
   const size_t extra = Lr ? 0 : (size_t)kTmaWarps * 256 * NR * sizeof(double);
   const int nst = pick_nst(div_up(nsys, kTmaWarps), (size_t)kTmaWarps * sw * sizeof(double),
                            extra + (PAD ? kTmaWarps * kPadGuard * sizeof(double) : 0));
   const size_t smem = ring_bytes(sw, PAD, nst) + extra;
   static size_t configured[64] = {};  // per instantiation and device
-  set_smem(k_l1_solve_ring<T, NR, PAD, UNIT>, smem, configured);
+  set_smem(k_l1_solve_ring<T, NR, PAD, UNIT, CH>, smem, configured);
   const bool window = !Lr && NR == 1 && use_window_bwd();
-  { k_l1_solve_ring<T, NR, PAD, UNIT><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
+  { k_l1_solve_ring<T, NR, PAD, UNIT, CH><<<div_up(nsys, kTmaWarps), kTmaWarps * 32, smem, st>>>(
       g, sys, nsys, Lc, Lr, r, ybuf, done, sw, maps.c, maps.r, window ? 1 : 0, nst); ms_count_launch(); }
   if (window) {
     const int nst = win_stages(max_bw), wsw = win_stage_words(max_bw);
@@ -1181,6 +1207,9 @@ static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, con
   if (Sinv) {
     if (pad)
       solve_twist_t<T, NR, NR == 1, false>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
+    else if (unit && T <= 4 && wide_chunks(div_up(nsys, kTmaWarps / 2)))
+      solve_twist_t<T, NR, false, true, (T <= 4 ? kChWide : kCh)>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st,
+                                                                  mp);
     else if (unit)
       solve_twist_t<T, NR, false, true>(g, sys, nsys, max_bw, Lc, Lr, Sinv, r, ybuf, done, st, mp);
     else
@@ -1190,6 +1219,8 @@ static void solve_t(const Grid& g, const BandSys* sys, int nsys, int max_bw, con
   if (use_ring_sweeps() && ring_ok) {
     if (pad)
       solve_ring_t<T, NR, NR == 1, false>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
+    else if (unit && T <= 4 && wide_chunks(div_up(nsys, kTmaWarps)))
+      solve_ring_t<T, NR, false, true, (T <= 4 ? kChWide : kCh)>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
     else if (unit)
       solve_ring_t<T, NR, false, true>(g, sys, nsys, max_bw, Lc, Lr, r, ybuf, done, st, mp);
     else
