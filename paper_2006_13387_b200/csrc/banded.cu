@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32)
 #define MS_L1_MINB 3  // register budget sized for >= 3 resident CTAs per SM (~128 registers)
 #endif
 constexpr int kCh = MS_TMA_CH;  // band columns per stage (divides 32)
+constexpr int kChWide = 16;    // per stage for launches of at most one CTA per SM (wide_chunks)
 constexpr int kNst = MS_TMA_NST;  // default stages per warp (bandwidth-bound launches)
 constexpr int kMaxNst = 8;        // deepest ring a launch may ask for (latency-bound launches, pick_nst)
 constexpr int kTmaWarps = MS_TMA_WARPS;
@@ -479,7 +480,8 @@ __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int
 // mbarrier wait, warp sync, lane 0 re-arming the stage and issuing the next
 // bulk copy -- sits on the warp's dependent stream, and halving the chunk
 // count took config 2's twisted level 1 from 0.180 to 0.156 ms (32 columns
-// per stage spill: 0.32 ms).
+// per stage spill: 0.32 ms).  (Software-pipelining the steps -- step q + 1's
+// loads issued inside step q's shuffle shadow -- measured the same, 0.159 ms.)
 template <int T, int NR, bool REV, bool PAD, bool UNIT = false, int CH = kCh, class YMap>
 __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw, YMap ym,
                                                 int lane, Ring& rg, const CUtensorMap* map = nullptr,
@@ -1038,7 +1040,6 @@ static int ring_stage_words_t(int max_bw, bool pad, int ch = kCh) {
 // (MS_L1_CH=8 / 16 forces one): see band_sweep_ring.  At two CTAs per SM the
 // two widths measure the same (config 3's 8-GPU strip twisted: 0.277 ms with
 // 3 x 8 or 2 x 16 columns; its 4-GPU strip plain: within run-to-run noise).
-constexpr int kChWide = 16;
 static bool wide_chunks(int ctas) {
   static int env = -2;
   if (env == -2) {
