@@ -1,4 +1,5 @@
-# round-2 validation + profiles: smoke, full GPU suite, default bench, config sweep, launch list, ncu --set full pages (csv only: .ncu-rep stay in /tmp)
+# Round validation + profiles (run on the GPU box from the repo root: gpurun -- bash tools/gpucmd_validate_and_profile.sh):
+# smoke, full GPU suite, default bench, config sweep, launch list, ncu --set full pages (csv only: .ncu-rep stay in /tmp)
 mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo exit=$? >> gpurun_out/smoke.log
 timeout 3000 python -m pytest tests -m gpu -q -rs > gpurun_out/pytest_gpu.log 2>&1; echo exit=$? >> gpurun_out/pytest_gpu.log
