@@ -197,3 +197,25 @@ def test_two_level_preconditioner_on_a_foreign_matrix(G, O):
     assert abs(rg.iterations - rf.iterations) <= 1 and abs(rh.iterations - rf.iterations) <= 1
     assert np.linalg.norm(xg - xf) <= 1e-7 * np.linalg.norm(xf)
     assert np.linalg.norm(xh - xf) <= 1e-7 * np.linalg.norm(xf)
+
+
+def test_device_tensors_through_the_generic_path(G):
+    """b as a float64 CUDA tensor with a CSR operand: x comes back as a CUDA
+    tensor (nothing but the callback operands crosses PCIe); the CSR operator
+    itself applies to host and device vectors."""
+    import torch
+
+    from paper_2006_13387_b200.krylov import CsrOperator
+
+    A, b = spd(80, 21, 300.0)
+    op = CsrOperator(A)
+    v = np.random.default_rng(4).standard_normal(80)
+    assert np.allclose(op @ v, A @ v, rtol=0, atol=1e-12 * np.abs(A @ v).max())
+    vd = torch.from_numpy(v).cuda()
+    assert np.allclose((op @ vd).cpu().numpy(), A @ v, rtol=0, atol=1e-12 * np.abs(A @ v).max())
+    xh, rh = G.pcg_solve(op, b, tol=1e-10)
+    xd, rd = G.pcg_solve(op, torch.from_numpy(b).cuda(), tol=1e-10)
+    assert isinstance(xd, torch.Tensor) and xd.is_cuda
+    assert rd.iterations == rh.iterations and np.array_equal(xd.cpu().numpy(), xh)
+    with pytest.raises(ValueError):
+        CsrOperator(sp.csr_matrix(np.ones((3, 4))))

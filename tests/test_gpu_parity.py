@@ -590,11 +590,13 @@ def test_byte_saving_variants_are_bitwise_identical(knob, rng, monkeypatch):
     same z bit for bit, same PCG iterates (schwarz.py:76-84)."""
     from paper_2006_13387_b200.solve import setup_spec
 
-    spec = configs.config3(seed=0, n=128)
+    # config 2 at eta 1e8: several modes per centre (the extra-mode paths run), channels to the clamped edge
+    spec = configs.config2(seed=0, eta=1e8, n=128)
     out = {}
     for mode in ("0", "1"):
         monkeypatch.setenv(knob, mode)
         mesh, op, pre = setup_spec(spec)
+        assert max(pre.mode_counts) >= 3
         out[mode] = (op, pre)
     for _ in range(3):
         v = rng.standard_normal(out["0"][0].n_free)
