@@ -506,10 +506,11 @@ PARITY_CASES = (("config1_64x64_d1", "ref_config1.npz"), ("config3_recipe_128x12
                 ("config4_recipe_128x64_eta1e9", "ref_config4_128x64.npz"),
                 ("config2_512x512_eta1e2", "ref_config2_n512_eta100.npz"),
                 ("config2_512x512_eta1e4", "ref_config2_n512_eta10000.npz"),
-                ("config2_512x512_eta1e6", "ref_config2_n512_eta1e+06.npz"))
+                ("config2_512x512_eta1e6", "ref_config2_n512_eta1e+06.npz"),
+                ("config2_512x512_eta1e8", "ref_config2_n512_eta1e+08.npz"))
 # full-size fixtures keep no E / load (regenerated by the seeded generator)
 FULLSIZE_SPECS = {"ref_config2_n512_eta100.npz": (2, 1e2), "ref_config2_n512_eta10000.npz": (2, 1e4),
-                  "ref_config2_n512_eta1e+06.npz": (2, 1e6)}
+                  "ref_config2_n512_eta1e+06.npz": (2, 1e6), "ref_config2_n512_eta1e+08.npz": (2, 1e8)}
 
 
 def iters_vs_reference():

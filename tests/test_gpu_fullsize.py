@@ -212,7 +212,7 @@ def test_fullsize_mode_counts_every_neighbourhood(case):
 
 
 @pytest.mark.parametrize("coarse_solve", ["inverse", "cholesky"])
-@pytest.mark.parametrize("eta", ["100", "10000", "1e+06"])
+@pytest.mark.parametrize("eta", ["100", "10000", "1e+06", "1e+08"])
 def test_fullsize_config2_solve_against_reference(eta, coarse_solve):
     """BASELINE config 2 at its full 512^2 size (525,312 dofs): the reference's
     own converged solve of each contrast (make_golden.py cfg2full, with its
