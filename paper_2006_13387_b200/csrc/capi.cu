@@ -2230,6 +2230,13 @@ int ms_pcg_solve_generic(ms_ctx* ctx, int64_t n, const ms_linop* A, const ms_lin
   for (const ms_linop* op : {A, M}) {
     const int64_t d = linop_dim(op);
     if (d >= 0 && d != n) throw Error(MS_E_INVALID, "operator dimension does not match the right-hand side");
+    // native operands run on their own context's stream: it must be the solve's
+    const ms_ctx* oc = !op || !op->handle ? ctx
+                       : op->kind == MS_LINOP_PROBLEM ? static_cast<ms_problem*>(op->handle)->ctx
+                       : op->kind == MS_LINOP_PRECOND ? static_cast<ms_precond*>(op->handle)->prob->ctx
+                       : op->kind == MS_LINOP_CSR ? static_cast<ms_csr*>(op->handle)->ctx
+                                                  : ctx;
+    if (oc != ctx) throw Error(MS_E_INVALID, "operand created on another context");
   }
   if (ctx->world() > 1) throw Error(MS_E_INVALID, "the generic PCG runs on one rank");
   MS_CUDA(cudaSetDevice(ctx->device));
