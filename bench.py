@@ -437,6 +437,11 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    read_only_gbs = None
+    try:
+        read_only_gbs = float(json.loads((ROOT / "profiles" / "r02_read_bw.json").read_text())["read_gbs"])
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
@@ -459,6 +464,11 @@ def run_ours(args):
                      "achieved": l1_gbs, "peak": hbm, "unit": "GB/s", "frac": l1_gbs / hbm,
                      "traffic": traffic, "bytes_per_launch": l1_bytes, "ms_per_launch": l1_ms,
                      "peak_kind": pk_kind,
+                     "peak_note": ("peak = the driver's COPY figure (read + write, MEASURED_PEAKS.json); this kernel is "
+                                   "98% reads, and read-only HBM measures higher (profiles/r02_read_bw.json, torch.sum "
+                                   "over 8 GiB): frac_read_only uses that figure, so frac can approach 1 on a box "
+                                   "that holds higher clocks than the one the copy figure was taken on"),
+                     "peak_read_only": read_only_gbs, "frac_read_only": (l1_gbs / read_only_gbs if read_only_gbs else None),
                      "iteration_model": {"B_iter_bytes": B_iter, "terms": terms, "achieved_GBs": iter_gbs,
                                          "frac": iter_gbs / hbm},
                      "kernel_ms_per_launch": per, "kernel_share": share,
