@@ -79,6 +79,9 @@ def test_callable_preconditioner_and_callable_operator(G, O):
 def test_dense_ndarray_operand_and_two_by_two_condition(G):
     _, rep = G.pcg_solve(np.diag([1.0, 4.0]), np.array([1.0, 1.0]), tol=1e-12)
     assert G.estimate_condition(rep) == pytest.approx(4.0, rel=1e-6)
+    # the 'None' variant's IdentityPreconditioner is the same solve as M = None
+    _, rep_id = G.pcg_solve(np.diag([1.0, 4.0]), np.array([1.0, 1.0]), G.IdentityPreconditioner(), tol=1e-12)
+    assert rep_id.iterations == rep.iterations and rep_id.residuals == rep.residuals
 
 
 def test_condition_estimate_scale_invariant_and_monotone(G):
