@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "banded.cuh"
 
@@ -482,10 +483,16 @@ __device__ __forceinline__ void ring_issue(Ring& rg, const double* L, int n, int
 // count took config 2's twisted level 1 from 0.180 to 0.156 ms (32 columns
 // per stage spill: 0.32 ms).  (Software-pipelining the steps -- step q + 1's
 // loads issued inside step q's shuffle shadow -- measured the same, 0.159 ms.)
-template <int T, int NR, bool REV, bool PAD, bool UNIT = false, int CH = kCh, class YMap>
+struct NoInput {};  // the sweep reads its right-hand side where it writes its result
+
+// rd(r, c): value of the sweep's input row r, right-hand side c, when it is not
+// stored at ym(r) yet -- the forward sweeps gather R_s r from the global vector
+// as they go (one value per lane and 32 steps) instead of a separate gather
+// pass that writes y and reads it back.
+template <int T, int NR, bool REV, bool PAD, bool UNIT = false, int CH = kCh, class YMap, class RMap = NoInput>
 __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, int n, int bw, YMap ym,
                                                 int lane, Ring& rg, const CUtensorMap* map = nullptr,
-                                                int col0 = 0) {
+                                                int col0 = 0, RMap rd = RMap{}) {
   constexpr int R = T + 1;
   constexpr int P = pad_slot_words<T>();
   const int S = bw + 1;
@@ -497,6 +504,12 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
     for (int c = 0; c < min(rg.nst, nch); ++c) ring_issue<REV, CH>(rg, L, n, S, c, c);
   }
   auto yat = [&](int r, int c) -> double* { return ym(r) + c; };
+  auto input = [&](int r, int c) -> double {
+    if constexpr (std::is_same<RMap, NoInput>::value)
+      return *yat(r, c);
+    else
+      return rd(r, c);
+  };
 
   double acc[NR][R], rnext[NR];
 #pragma unroll
@@ -504,10 +517,10 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
 #pragma unroll
     for (int s = 0; s < R - 1; ++s) {
       const int r = 32 * s + lane;
-      acc[c][s] = r < n ? *yat(r, c) : 0.0;
+      acc[c][s] = r < n ? input(r, c) : 0.0;
     }
     acc[c][R - 1] = 0.0;
-    rnext[c] = (32 * (R - 1) + lane < n) ? *yat(32 * (R - 1) + lane, c) : 0.0;
+    rnext[c] = (32 * (R - 1) + lane < n) ? input(32 * (R - 1) + lane, c) : 0.0;
   }
 
   int stc = 0;
@@ -516,7 +529,7 @@ __device__ __forceinline__ void band_sweep_ring(const double* __restrict__ L, in
     for (int c = 0; c < NR; ++c) {
       acc[c][R - 1] = rnext[c];
       const int r = k0 + 32 * R + lane;
-      rnext[c] = r < n ? *yat(r, c) : 0.0;
+      rnext[c] = r < n ? input(r, c) : 0.0;
     }
     double dsave = 0.0;  // 1/L_kk of this lane's row of the block
     double yfin[NR];     // PAD: the row's final value, captured at its pivot step
@@ -761,18 +774,20 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   ring_init(rg, smem_ring, warp, lane, stage_words, nst, PAD);
   const BandSys s = sys[sid];
   double* y = ybuf + s.yoff;
-  for (int i = lane; i < s.n * NR; i += 32) {
-    const int ln = i >> 1, c = i & 1;
-    int a, b;
-    band_node_of(s, ln, a, b);
-    MS_BCHECK(a >= 0 && a <= g.nx && b >= 0 && b <= g.ny);
-    y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
-  }
-  __syncwarp();
   const int n = s.n;
+  const int64_t nn = g.n_nodes;
+  // R_s r, gathered by the forward sweep itself: entry i = row * NR + c of the
+  // subdomain's node-interleaved vector is component i & 1 of local node i >> 1
+  auto gather = [&](int row, int c) -> double {
+    const int i = row * NR + c;
+    int a, b;
+    band_node_of(s, i >> 1, a, b);
+    MS_BCHECK(a >= 0 && a <= g.nx && b >= 0 && b <= g.ny);
+    return __ldg(r + (i & 1) * nn + (int64_t)b * g.nnx + a);
+  };
   const int col0 = PAD ? (int)(s.foff / (s.bw + 1)) : 0;  // the system's first column in the TMA view
-  band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, n, s.bw, [&](int r) { return y + (int64_t)r * NR; }, lane, rg,
-                                     &mapc, col0);
+  band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, n, s.bw, [&](int q) { return y + (int64_t)q * NR; }, lane,
+                                               rg, &mapc, col0, gather);
   if (fwd_only) return;  // the backward sweep follows in k_l1_bwd_window
   __syncwarp();
   if (Lr) {
@@ -821,29 +836,41 @@ __global__ void __launch_bounds__(kTmaWarps * 32, MS_L1_MINB)
   const int n = s.n, bw = s.bw, m = s.m, nT = m + bw, nB = n - m;
   MS_BCHECK(bw >= 1 && bw <= max_bw && m >= 1 && nT <= n && nB >= bw && nst >= 2 && nst <= kMaxNst);
   double* y = ybuf + s.yoff;
-  // gather R_s r: top warp rows [0, nT), bottom warp rows [nT, n) and zero separator partials
-  {
+  // R_s r is gathered by the forward sweeps themselves (top warp: rows [0, nT)
+  // incl. the separator's; bottom warp: its own rows [nT, n) in reverse, its
+  // separator rows start from zero and end as the partials -L_SB y_B in sB)
+  const int64_t nn = g.n_nodes;
+  auto gather = [&](int row, int c) -> double {
+    const int i = row * NR + c;
+    int a, b;
+    band_node_of(s, i >> 1, a, b);
+    MS_BCHECK(a >= 0 && a <= g.nx && b >= 0 && b <= g.ny);
+    return __ldg(r + (i & 1) * nn + (int64_t)b * g.nnx + a);
+  };
+  const int nb_own = nB - bw;
+  auto ymB = [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; };
+  if constexpr (CH == kChWide) {
+    // latency-bound launches (one warp per scheduler): a separate gather pass
+    // keeps the index arithmetic off the sweeps' in-order stream (config 2:
+    // 0.157 ms vs 0.162 ms with the gather inside the sweeps)
     const int i0 = role ? nT * NR : 0, i1 = role ? n * NR : nT * NR;
-    for (int i = i0 + lane; i < i1; i += 32) {
-      const int ln = NR == 1 ? (i >> 1) : (i >> 1), c = i & 1;
-      int a, b;
-      band_node_of(s, ln, a, b);
-      MS_BCHECK(a >= 0 && a <= g.nx && b >= 0 && b <= g.ny);
-      y[i] = r[c * g.n_nodes + (int64_t)b * g.nnx + a];
-    }
+    for (int i = i0 + lane; i < i1; i += 32) y[i] = gather(i / NR, i % NR);
     if (role)
       for (int i = lane; i < NR * bw; i += 32) sB[i] = 0.0;
-  }
-  __syncwarp();
-  if (role == 0) {
-    band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane, rg,
-                                       &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
+    __syncwarp();
+    if (role == 0)
+      band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; },
+                                                   lane, rg, &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0);
+    else
+      band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foffB, nB, bw, ymB, lane, rg, &mapc,
+                                                   PAD ? (int)(s.foffB / (bw + 1)) : 0);
+  } else if (role == 0) {
+    band_sweep_ring<T, NR, false, PAD, UNIT, CH>(Lc + s.foff, nT, bw, [&](int q) { return y + (int64_t)q * NR; }, lane,
+                                                 rg, &mapc, PAD ? (int)(s.foff / (bw + 1)) : 0, gather);
   } else {
-    const int nb_own = nB - bw;
     band_sweep_ring<T, NR, false, PAD, UNIT, CH>(
-        Lc + s.foffB, nB, bw,
-        [&](int q) { return q < nb_own ? y + (int64_t)(n - 1 - q) * NR : sB + (q - nb_own) * NR; }, lane, rg,
-        &mapc, PAD ? (int)(s.foffB / (bw + 1)) : 0);
+        Lc + s.foffB, nB, bw, ymB, lane, rg, &mapc, PAD ? (int)(s.foffB / (bw + 1)) : 0,
+        [&](int q, int c) -> double { return q < nb_own ? gather(n - 1 - q, c) : 0.0; });
   }
   pair_sync(pair);
   // separator: t = (r_S - L_ST y_T) + (- L_SB y_B); x_S = Sinv t
